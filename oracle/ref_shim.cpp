@@ -1,0 +1,219 @@
+// ref_shim.cpp -- extern "C" shim over the UNMODIFIED reference headers.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/build_ref.sh compiles this file against
+// /root/reference/proj/include (header-only library; no reference sources
+// are copied into this repo) into oracle/_ref/libccgref.so, which the tests
+// use to pin the C restatement (oracle/ccg_oracle.c) and to make the golden
+// fixtures, and which bench.py times as the reference CPU baseline.
+//
+// Entry points mirror the reference API:
+//   ccg_solve      coopcg/solvers.hpp:329-333
+//   parallel_ccg   coopcg/parallel.hpp:76-111
+//   mccg_solve     coopcg/solvers.hpp:338-342
+//   cg_solve       coopcg/solvers.hpp:388-530
+//   make_problem   coopcg/problem.hpp:234-246
+//   matvec_block / gram / solve_small / numerical_rank  coopcg/dense_ops.hpp
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <exception>
+#include <vector>
+
+#include "coopcg/parallel.hpp"
+#include "coopcg/problem.hpp"
+#include "coopcg/solvers.hpp"
+
+extern "C" {
+#include "ccg_oracle.h"
+}
+
+using namespace coopcg;
+
+namespace {
+
+int status_code(TerminalStatus s) {
+    switch (s) {
+    case TerminalStatus::Converged: return ORC_STATUS_CONVERGED;
+    case TerminalStatus::RankCollapse: return ORC_STATUS_RANK_COLLAPSE;
+    case TerminalStatus::MaxIterations: return ORC_STATUS_MAX_ITERATIONS;
+    }
+    return -1;
+}
+
+template <class F>
+int guarded(orc_trace* tr, F&& f) {
+    try {
+        f();
+        return ORC_OK;
+    } catch (const SpdViolationError& e) {
+        std::snprintf(tr->error_msg, sizeof tr->error_msg, "%s", e.what());
+        return ORC_E_SPD_VIOLATION;
+    } catch (const NumericalBreakdownError& e) {
+        std::snprintf(tr->error_msg, sizeof tr->error_msg, "%s", e.what());
+        return ORC_E_NUMERICAL_BREAKDOWN;
+    } catch (const DimensionError& e) {
+        std::snprintf(tr->error_msg, sizeof tr->error_msg, "%s", e.what());
+        return ORC_E_DIMENSION;
+    } catch (const std::exception& e) {
+        std::snprintf(tr->error_msg, sizeof tr->error_msg, "%s", e.what());
+        return 9;
+    }
+}
+
+void fill_trace(const SolveTrace<double>& t, int n, orc_trace* tr) {
+    tr->status = status_code(t.status);
+    tr->converged_agent = t.converged_agent;
+    tr->iterations = t.iteration_count();
+    tr->loop_wall_ns = t.loop_wall_ns;
+    const int p0 = t.initial_residual_norms.empty() ? 0 : (int)t.initial_residual_norms.size();
+    for (int k = 0; k < tr->iterations && k < tr->capacity; ++k) {
+        const auto& rec = t.iterations[(size_t)k];
+        // Norms are stored per ORIGINAL agent id so restricted (mccg) traces
+        // keep a fixed p-wide row; inactive agents are NaN.
+        if (tr->residual_norms) {
+            for (int j = 0; j < p0; ++j) tr->residual_norms[(size_t)k * p0 + j] = __builtin_nan("");
+            for (int s = 0; s < rec.active_agents; ++s)
+                tr->residual_norms[(size_t)k * p0 + rec.agents[(size_t)s]] = rec.residual_norms[(size_t)s];
+        }
+        if (tr->minres) tr->minres[k] = rec.minres;
+        if (tr->wall_ns) tr->wall_ns[k] = rec.wall_ns;
+    }
+    if (tr->initial_residual_norms)
+        std::copy(t.initial_residual_norms.begin(), t.initial_residual_norms.end(), tr->initial_residual_norms);
+    tr->initial_minres = t.initial_minres;
+    if (tr->final_x) {
+        // final_x is n x (surviving agents), column-major; scatter by agent id.
+        for (int s = 0; s < t.final_x.cols(); ++s) {
+            auto c = t.final_x.col(s);
+            std::copy(c.begin(), c.end(), tr->final_x + (size_t)t.active_agents[(size_t)s] * n);
+        }
+    }
+    if (tr->final_residual_norms) {
+        for (size_t s = 0; s < t.final_residual_norms.size(); ++s)
+            tr->final_residual_norms[t.active_agents[s]] = t.final_residual_norms[s];
+    }
+    tr->final_minres = t.final_minres;
+}
+
+SpdMatrix<double> make_A(int n, const double* A) {
+    return SpdMatrix<double>(n, std::vector<double>(A, A + (size_t)n * n), SpdCheck::skip);
+}
+
+} // namespace
+
+extern "C" {
+
+/// algo: 0 = ccg_solve, 1 = parallel_ccg (p OpenMP threads), 2 = mccg_solve.
+int ref_block_solve(int algo, int n, int p, const double* A, const double* b, const double* X0,
+                    const orc_opts* o, orc_trace* tr) {
+    tr->error_msg[0] = '\0';
+    return guarded(tr, [&] {
+        auto Am = make_A(n, A);
+        std::vector<double> bv(b, b + n);
+        DenseBlock<double> x0(n, p);
+        for (int j = 0; j < p; ++j)
+            for (int i = 0; i < n; ++i) x0(i, j) = X0[(size_t)j * n + i];
+        SolveOptions<double> opts;
+        opts.tol = o->tol;
+        opts.max_iters = o->max_iters;
+        opts.recompute_residual_every = o->recompute_residual_every;
+        opts.rank_rel_tol = o->rank_rel_tol;
+        SolveTrace<double> t;
+        if (algo == 0) t = ccg_solve(Am, bv, x0, opts);
+        else if (algo == 1) t = parallel_ccg(Am, bv, x0, opts, p);
+        else t = mccg_solve(Am, bv, x0, opts);
+        fill_trace(t, n, tr);
+    });
+}
+
+int ref_cg_solve(int n, const double* A, const double* b, const double* x0, const orc_opts* o,
+                 orc_trace* tr) {
+    tr->error_msg[0] = '\0';
+    return guarded(tr, [&] {
+        auto Am = make_A(n, A);
+        std::vector<double> bv(b, b + n), xv(x0, x0 + n);
+        SolveOptions<double> opts;
+        opts.tol = o->tol;
+        opts.max_iters = o->max_iters;
+        opts.recompute_residual_every = o->recompute_residual_every;
+        opts.rank_rel_tol = o->rank_rel_tol;
+        auto t = cg_solve(Am, bv, xv, opts);
+        fill_trace(t, n, tr);
+    });
+}
+
+/// The reference's own problem family (random_spd + rhs/starts, float mode).
+int ref_make_problem(int n, int p, double cond, unsigned long long seed, double* A, double* b,
+                     double* X0) {
+    try {
+        ProblemSpec spec;
+        spec.n = n;
+        spec.p = p;
+        spec.cond = cond;
+        spec.seed = seed;
+        auto inst = make_problem<double>(spec);
+        std::copy(inst.A.entries().begin(), inst.A.entries().end(), A);
+        std::copy(inst.b.begin(), inst.b.end(), b);
+        for (int j = 0; j < p; ++j) {
+            auto c = inst.X0.col(j);
+            std::copy(c.begin(), c.end(), X0 + (size_t)j * n);
+        }
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
+void ref_matvec_block(int n, int p, const double* A, const double* D, double* out) {
+    auto Am = make_A(n, A);
+    DenseBlock<double> d(n, p);
+    for (int j = 0; j < p; ++j)
+        for (int i = 0; i < n; ++i) d(i, j) = D[(size_t)j * n + i];
+    auto q = matvec_block(Am, d);
+    for (int j = 0; j < p; ++j) {
+        auto c = q.col(j);
+        std::copy(c.begin(), c.end(), out + (size_t)j * n);
+    }
+}
+
+void ref_gram(int n, int p, const double* D, const double* AD, double* raw, double* sym) {
+    DenseBlock<double> d(n, p), ad(n, p);
+    for (int j = 0; j < p; ++j)
+        for (int i = 0; i < n; ++i) {
+            d(i, j) = D[(size_t)j * n + i];
+            ad(i, j) = AD[(size_t)j * n + i];
+        }
+    auto r = gram_raw(d, ad);
+    auto s = gram(d, ad);
+    std::copy(r.data().begin(), r.data().end(), raw);
+    std::copy(s.data().begin(), s.data().end(), sym);
+}
+
+/// Returns 0 on success, 1 on SingularMatrixError.
+int ref_solve_small(int p, const double* M, int q, const double* B, double* X) {
+    SmallSpd<double> m(p);
+    std::copy(M, M + (size_t)p * p, m.data().begin());
+    DenseBlock<double> bb(p, q);
+    for (int j = 0; j < q; ++j)
+        for (int i = 0; i < p; ++i) bb(i, j) = B[(size_t)j * p + i];
+    try {
+        auto x = solve_small(m, bb);
+        for (int j = 0; j < q; ++j)
+            for (int i = 0; i < p; ++i) X[(size_t)j * p + i] = x(i, j);
+        return 0;
+    } catch (const SingularMatrixError&) {
+        return 1;
+    }
+}
+
+int ref_numerical_rank(int n, int p, const double* D, double tol, int* columns) {
+    DenseBlock<double> d(n, p);
+    for (int j = 0; j < p; ++j)
+        for (int i = 0; i < n; ++i) d(i, j) = D[(size_t)j * n + i];
+    auto r = numerical_rank(d, tol);
+    if (columns)
+        std::copy(r.columns.begin(), r.columns.end(), columns);
+    return r.rank;
+}
+
+} // extern "C"
