@@ -1,0 +1,166 @@
+/*
+ * coopcg_gpu.h -- C ABI of the B200-native cooperative-CG hot path.
+ *
+ * Drop-in boundary for the reference's solver entry point
+ *   template<ScalarField S> SolveTrace<S> ccg_solve(const SpdMatrix<S>&,
+ *       const Vec<S>&, const DenseBlock<S>&, const SolveOptions<S>& = {})
+ *   (/root/reference/proj/include/coopcg/solvers.hpp:329-333)
+ * and its OpenMP twin parallel_ccg (coopcg/parallel.hpp:76-111).  The
+ * reference's executor policy (drive<S,Exec>, solvers.hpp:259-262) is per-slot
+ * and host-memory based, so the GPU backend plugs in at solver level: the C++
+ * header include/coopcg/gpu_ccg.hpp wraps these functions into
+ *   coopcg::gpu_ccg(A, b, X0, opts, gpu_opts) -> SolveTrace<double>
+ * with ccg_solve's semantics; INTEGRATION.md shows the binding.
+ *
+ * No C++ or torch types cross this boundary: plain pointers, sizes, PODs.
+ * Every function returns an int code (coopcg_err); the context keeps the last
+ * message (coopcg_gpu_last_error).  Contexts are independent: no global
+ * mutable state, one CUDA stream per context (reentrant per context, like the
+ * reference's concurrent independent solves, tests/test_parallel.cpp:190-204).
+ *
+ * Layouts at the boundary are the reference's: A row-major n x n
+ * (coopcg/dense.hpp:101-170); X0 / final_x column-major n x p DenseBlock
+ * (dense.hpp:35-38).  Device layouts are private.
+ */
+#ifndef COOPCG_GPU_H
+#define COOPCG_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COOPCG_GPU_ABI_VERSION 1
+#define COOPCG_GPU_MAX_P 32
+
+/* Error codes; map to the reference exception hierarchy (errors.hpp:11-41). */
+enum coopcg_err {
+    COOPCG_OK = 0,
+    COOPCG_E_DIMENSION = 1,            /* DimensionError */
+    COOPCG_E_SPD_VIOLATION = 2,        /* SpdViolationError */
+    COOPCG_E_NUMERICAL_BREAKDOWN = 3,  /* NumericalBreakdownError */
+    COOPCG_E_SINGULAR = 4,             /* SingularMatrixError */
+    COOPCG_E_INVALID = 5,              /* bad argument (null pointer, bad enum) */
+    COOPCG_E_STATE = 6,                /* call out of order (e.g. run before A set) */
+    COOPCG_E_CUDA = 10                 /* CUDA runtime error; message has details */
+};
+
+/* TerminalStatus (trace.hpp:13-17). */
+enum coopcg_status {
+    COOPCG_CONVERGED = 0,
+    COOPCG_RANK_COLLAPSE = 1,
+    COOPCG_MAX_ITERATIONS = 2
+};
+
+/* Arithmetic modes.  EXACT reproduces the reference's
+ * floating-point operation order bit for bit; FAST reorders (DFMA/DMMA,
+ * tree reductions, Cholesky) for the roofline. */
+enum coopcg_arith { COOPCG_ARITH_EXACT = 0, COOPCG_ARITH_FAST = 1 };
+
+/* On-device matrix generators. */
+enum coopcg_matrix_kind { COOPCG_MATRIX_DIAGDOM = 0, COOPCG_MATRIX_HOUSEHOLDER = 1 };
+enum coopcg_vector_kind { COOPCG_VEC_UNIFORM = 0, COOPCG_VEC_NORMAL = 1 };
+
+/* SolveOptions<double> (trace.hpp:74-88). keep_history / x_star are not
+ * carried by the ABI (verification-only fields of the reference). */
+typedef struct {
+    double tol;                   /* absolute threshold on ||r_j||_2 (block_cg.hpp:283-289) */
+    int max_iters;                /* -1 => 2n (solvers.hpp:18-23) */
+    int recompute_residual_every; /* -1 => 50; 0 disables (solvers.hpp:25-35) */
+    double rank_rel_tol;          /* numerical_rank tolerance, reference default 1e-10 */
+} coopcg_opts;
+
+/* SolveTrace<double> (trace.hpp:46-71), caller-allocated arrays.
+ * Any array pointer may be NULL to skip that output. */
+typedef struct {
+    int capacity;                   /* rows the per-iteration arrays can hold */
+    double* residual_norms;         /* [capacity * p]; row k = IterationRecord::residual_norms */
+    double* minres;                 /* [capacity] */
+    uint64_t* wall_ns;              /* [capacity]; device clock, per iteration */
+    double* initial_residual_norms; /* [p] */
+    double* final_x;                /* [n * p], column-major (DenseBlock) */
+    double* final_residual_norms;   /* [p], true recomputation ||A x_j - b|| */
+    /* outputs */
+    int status;                     /* coopcg_status */
+    int converged_agent;            /* -1 unless converged */
+    int iterations;                 /* IterationRecord count */
+    double initial_minres;
+    double final_minres;
+    uint64_t loop_wall_ns;          /* sum of wall_ns (solvers.hpp:145) */
+    int exact_rank_checks;          /* diagnostics: certificate fell back to exact MGS */
+} coopcg_trace;
+
+/* Per-kernel timing of the last run, from CUDA events on the context stream. */
+typedef struct {
+    int matvec_launches;            /* A.D launches timed in the last run */
+    double matvec_ms_total;         /* sum of their event durations */
+    double run_ms;                  /* event time of the whole last run (setup..finalize) */
+    double loop_ms;                 /* event time of the iteration loop only */
+    long long kernel_launches;      /* kernels this library launched in the last run */
+} coopcg_timing;
+
+typedef struct coopcg_gpu_ctx coopcg_gpu_ctx;
+
+/* Library version / build information, e.g. "coopcg_gpu 1 sm_100a". */
+const char* coopcg_gpu_version(void);
+
+/* Create a context for an n x n system with p agents on CUDA `device`.
+ * Owns the rows [row_begin, row_end) of A (row_begin = 0, row_end = n for a
+ * single-GPU solve).  1 <= p < n, p <= COOPCG_GPU_MAX_P. */
+int coopcg_gpu_create(int n, int p, int device, int arith, coopcg_gpu_ctx** out);
+int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, int row_end,
+                            coopcg_gpu_ctx** out);
+int coopcg_gpu_destroy(coopcg_gpu_ctx* ctx);
+
+/* Copy the last error message (NUL-terminated, truncated to len).  With
+ * ctx == NULL: the calling thread's last coopcg_gpu_create* failure. */
+int coopcg_gpu_last_error(const coopcg_gpu_ctx* ctx, char* buf, size_t len);
+
+/* Load this context's row block of A: rows [row_begin, row_end) of the
+ * row-major n x n matrix, i.e. (row_end - row_begin) x n doubles, host memory. */
+int coopcg_gpu_set_A(coopcg_gpu_ctx* ctx, const double* A_rows);
+/* Generate A on the device.  DIAGDOM ignores m, kappa.
+ * HOUSEHOLDER needs the full matrix on this device (single-GPU contexts). */
+int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double kappa);
+/* Download this context's row block of A (row-major), for verification. */
+int coopcg_gpu_get_A(coopcg_gpu_ctx* ctx, double* A_rows);
+
+/* Host-side generators for b and X0. */
+int coopcg_gen_rhs(int n, int kind, uint64_t seed, double* b);
+int coopcg_gen_starts(int n, int p, uint64_t seed, double* X0_colmajor);
+/* Host part of the Householder generator: reflector vectors V (m x n) and
+ * the spectrum lambda (n). */
+int coopcg_gen_householder_factors(int n, int m, double kappa, uint64_t seed, double* V,
+                                   double* lambda);
+
+/* Upload b (n) and X0 (n x p column-major) into the context. */
+int coopcg_gpu_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0_colmajor);
+/* Run ccg_solve on the resident A, b, X0; fill `trace` (may be NULL). */
+int coopcg_gpu_run(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* trace);
+/* The drop-in: upload + run + copy-out, host buffers in and out. */
+int coopcg_gpu_solve(coopcg_gpu_ctx* ctx, const double* b, const double* X0_colmajor,
+                     const coopcg_opts* opts, coopcg_trace* trace);
+
+int coopcg_gpu_timing(const coopcg_gpu_ctx* ctx, coopcg_timing* out);
+/* The context's CUDA stream (cudaStream_t), so callers can record events on
+ * the stream the kernels run on. */
+void* coopcg_gpu_stream(const coopcg_gpu_ctx* ctx);
+
+/* ---- kernel-level entry points (parity tests of the building blocks) ----
+ * All take host buffers and run on the context's device/stream. */
+/* out = A_rows . D  (D n x p column-major; out (row_end-row_begin) x p column-major) */
+int coopcg_gpu_matvec_block(coopcg_gpu_ctx* ctx, const double* D_colmajor, double* out_colmajor);
+/* numerical_rank of an n x p column-major block (dense_ops.hpp:104-157). */
+int coopcg_gpu_numerical_rank(coopcg_gpu_ctx* ctx, const double* D_colmajor, double tol,
+                              int* rank);
+/* Same; force_exact != 0 skips the Gram certificate and always runs the
+ * exact column-pivoted MGS restatement (tests of both paths). */
+int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D_colmajor, double tol,
+                                 int force_exact, int* rank);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COOPCG_GPU_H */

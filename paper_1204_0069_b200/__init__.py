@@ -1,0 +1,28 @@
+"""B200-native hot path of cooperative conjugate gradient (cCG, arXiv 1204.0069).
+
+Drop-in for the reference's ``ccg_solve`` (coopcg/solvers.hpp:329-333): the
+per-iteration block CG update -- Q = A.D with the Gram reductions, the p x p
+step solves for alpha and beta, and the X/R/D updates -- runs as hand-written
+sm_100a CUDA kernels behind the C ABI in ``include/coopcg_gpu.h``.
+"""
+from .solver import (  # noqa: F401
+    CudaError,
+    DimensionError,
+    Error,
+    GpuContext,
+    GpuOptions,
+    IterationRecord,
+    NumericalBreakdownError,
+    SingularMatrixError,
+    SolveOptions,
+    SolveTrace,
+    SpdViolationError,
+    TerminalStatus,
+    ccg_solve,
+    gen_householder_factors,
+    gen_rhs,
+    gen_starts,
+    iteration_mults,
+    library_version,
+)
+from .configs import CONFIGS, make_problem_on_device  # noqa: F401

@@ -1,0 +1,84 @@
+"""ctypes declarations of the C ABI in include/coopcg_gpu.h.
+
+This is the binding a maintainer of a Python caller would write (the same
+shape as INTEGRATION.md's cgo/ctypes stubs).  The library must exist: there is
+no CPU fallback anywhere in the product path -- a missing or unloadable .so
+raises immediately.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from . import build as _build
+
+LIB_PATH = _build.LIB
+
+
+class coopcg_opts(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iters", C.c_int),
+                ("recompute_residual_every", C.c_int), ("rank_rel_tol", C.c_double)]
+
+
+class coopcg_trace(C.Structure):
+    _fields_ = [("capacity", C.c_int),
+                ("residual_norms", C.POINTER(C.c_double)),
+                ("minres", C.POINTER(C.c_double)),
+                ("wall_ns", C.POINTER(C.c_uint64)),
+                ("initial_residual_norms", C.POINTER(C.c_double)),
+                ("final_x", C.POINTER(C.c_double)),
+                ("final_residual_norms", C.POINTER(C.c_double)),
+                ("status", C.c_int), ("converged_agent", C.c_int), ("iterations", C.c_int),
+                ("initial_minres", C.c_double), ("final_minres", C.c_double),
+                ("loop_wall_ns", C.c_uint64), ("exact_rank_checks", C.c_int)]
+
+
+class coopcg_timing(C.Structure):
+    _fields_ = [("matvec_launches", C.c_int), ("matvec_ms_total", C.c_double),
+                ("run_ms", C.c_double), ("loop_ms", C.c_double),
+                ("kernel_launches", C.c_longlong)]
+
+
+# Every symbol include/coopcg_gpu.h declares: (name, restype, argtypes).
+_VP = C.c_void_p
+_I = C.c_int
+SIGNATURES = [
+    ("coopcg_gpu_version", C.c_char_p, []),
+    ("coopcg_gpu_create", _I, [_I, _I, _I, _I, C.POINTER(_VP)]),
+    ("coopcg_gpu_create_shard", _I, [_I, _I, _I, _I, _I, _I, C.POINTER(_VP)]),
+    ("coopcg_gpu_destroy", _I, [_VP]),
+    ("coopcg_gpu_last_error", _I, [_VP, C.c_char_p, C.c_size_t]),
+    ("coopcg_gpu_set_A", _I, [_VP, _VP]),
+    ("coopcg_gpu_gen_A", _I, [_VP, _I, C.c_uint64, _I, C.c_double]),
+    ("coopcg_gpu_get_A", _I, [_VP, _VP]),
+    ("coopcg_gen_rhs", _I, [_I, _I, C.c_uint64, _VP]),
+    ("coopcg_gen_starts", _I, [_I, _I, C.c_uint64, _VP]),
+    ("coopcg_gen_householder_factors", _I, [_I, _I, C.c_double, C.c_uint64, _VP, _VP]),
+    ("coopcg_gpu_upload", _I, [_VP, _VP, _VP]),
+    ("coopcg_gpu_run", _I, [_VP, C.POINTER(coopcg_opts), C.POINTER(coopcg_trace)]),
+    ("coopcg_gpu_solve", _I, [_VP, _VP, _VP, C.POINTER(coopcg_opts), C.POINTER(coopcg_trace)]),
+    ("coopcg_gpu_timing", _I, [_VP, C.POINTER(coopcg_timing)]),
+    ("coopcg_gpu_stream", _VP, [_VP]),
+    ("coopcg_gpu_matvec_block", _I, [_VP, _VP, _VP]),
+    ("coopcg_gpu_numerical_rank", _I, [_VP, _VP, C.c_double, C.POINTER(_I)]),
+    ("coopcg_gpu_numerical_rank_ex", _I, [_VP, _VP, C.c_double, _I, C.POINTER(_I)]),
+]
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load the CUDA library (fails loudly if it is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(
+                f"CUDA library {LIB_PATH} is missing; build it with "
+                "`python -m paper_1204_0069_b200.build` (there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, res, args in SIGNATURES:
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib

@@ -1,0 +1,114 @@
+// common.cuh -- shared device definitions for the cCG hot path (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace coopcg_gpu {
+
+constexpr int kMaxP = 32;
+
+// Offsets into the per-context "small" array (p x p grids stored with row
+// stride P, per-agent vectors of length P).  Row-major like the reference's
+// gram/rhs/alpha/beta grids (block_cg.hpp:45-46).
+struct SmallLayout {
+    int P;
+    __host__ __device__ int raw() const { return 0; }
+    __host__ __device__ int rhs_a() const { return P * P; }
+    __host__ __device__ int rhs_b() const { return 2 * P * P; }
+    __host__ __device__ int alpha() const { return 3 * P * P; }
+    __host__ __device__ int beta() const { return 4 * P * P; }
+    __host__ __device__ int nsq_d() const { return 5 * P * P; }
+    __host__ __device__ int nsq_r() const { return 5 * P * P + P; }
+    __host__ __device__ int nsq_f() const { return 5 * P * P + 2 * P; }
+    __host__ __device__ int norm() const { return 5 * P * P + 3 * P; }
+    __host__ __device__ int mgs() const { return 5 * P * P + 4 * P; } // P values
+    __host__ __device__ int total() const { return 5 * P * P + 5 * P; }
+};
+
+// Device control block: the coordinator state of DriverControl
+// (block_cg.hpp:106-125) plus the factorisation shared by the alpha and beta
+// solves (the reference re-factors the same Gram matrix per agent, with
+// identical results; SURVEY §8a notes).
+struct Ctl {
+    int stop;             // every kernel becomes a no-op once set
+    int status;           // coopcg_status
+    int err;              // coopcg_err raised inside the loop (SPD violation)
+    int err_iter;
+    int k;                // current iteration index
+    int iterations;       // IterationRecords written
+    int converged_agent;
+    int need_exact_rank;  // rank certificate inconclusive -> exact MGS this iteration
+    int force_exact;      // tests: always run the exact MGS
+    int exact_rank_checks;
+    int rank_result;
+    int perm[kMaxP];
+    double lu[kMaxP * kMaxP];
+    unsigned long long t_last;
+    // options (SolveOptions)
+    double tol;
+    double rank_rel_tol;
+    int max_iters;
+    int p;
+    int P;
+    int pad_;
+};
+
+// One sequential dot-product chain (kernels.hpp:20-26):
+// out = (neg ? -1 : 1) * sum_k S[sx][k][a] * S[sy][k][b], k ascending.
+struct ChainDesc {
+    uint8_t sx, a, sy, b;
+    uint16_t out;
+    uint8_t neg, pad;
+};
+
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+
+// ---- mbarrier + bulk async copy (TMA 1-D) helpers --------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@!P1 bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// Global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0,
+// both addresses 16-byte aligned).
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// Exact reference arithmetic: one rounding per operation, no contraction.
+__device__ __forceinline__ double mac_exact(double acc, double a, double b) {
+    return __dadd_rn(acc, __dmul_rn(a, b));
+}
+__device__ __forceinline__ double msub_exact(double acc, double a, double b) {
+    return __dsub_rn(acc, __dmul_rn(a, b));
+}
+
+} // namespace coopcg_gpu

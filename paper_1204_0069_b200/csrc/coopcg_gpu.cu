@@ -1,0 +1,793 @@
+// coopcg_gpu.cu -- host driver + C ABI of the B200-native cCG hot path.
+//
+// The driver reproduces the reference's drive() loop (coopcg/solvers.hpp:
+// 259-283) on one CUDA stream: setup (stage_setup + setup_coordinator),
+// then per iteration
+//   ad_exact (Q = A D) -> chains (D^T Q, -R^T D, |D|^2) -> solve_alpha ->
+//   update (R, X | X then R = A X - b) -> chains (-R^T Q, |R|^2) ->
+//   solve_beta (+ record + convergence) -> direction (Dn = R + D beta^T,
+//   Gram partials) -> rank_end (certificate / exact MGS, status, k++)
+// and finalize_trace.  The coordinator decisions live on the device (Ctl):
+// once a stop condition is reached every later kernel is a no-op, so the host
+// enqueues iterations in chunks and only reads a small control snapshot per
+// chunk (no per-iteration host round trip).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/coopcg_gpu.h"
+#include "common.cuh"
+#include "exact_kernels.cuh"
+#include "gen_kernels.cuh"
+
+using namespace coopcg_gpu;
+
+namespace {
+
+constexpr int kChainT = 64;
+constexpr int kAdT = 32;
+constexpr int kAdS = 4;
+constexpr int kChunkMax = 16;
+constexpr int kMaxParts = 296;  // 2 x 148 SMs
+
+int round_up(int x, int m) { return (x + m - 1) / m * m; }
+int pad_cols(int p) {
+    int P = 4;
+    while (P < p) P *= 2;
+    return P;
+}
+
+struct AdConfig {
+    int BR = 64;
+    int CPT = 4;
+};
+
+}  // namespace
+
+struct coopcg_gpu_ctx {
+    int n = 0, p = 0, P = 0, device = 0, arith = 0;
+    int row0 = 0, row1 = 0, n_loc = 0, ld = 0;
+    bool a_ready = false, inputs_ready = false;
+    cudaStream_t stream = nullptr;
+    std::string msg;
+
+    double* At = nullptr;
+    double* X = nullptr;
+    double* R = nullptr;
+    double* Dblk[2] = {nullptr, nullptr};
+    double* Q = nullptr;
+    double* S = nullptr;
+    double* V = nullptr;  // MGS working copy
+    double* b = nullptr;
+    double* small = nullptr;
+    double* partials = nullptr;
+    double* init_norms = nullptr;  // P + 1
+    double* final_norms = nullptr; // P + 1
+    Ctl* ctl = nullptr;
+    Ctl* ctl_host = nullptr;  // pinned snapshots [2]
+    ChainDesc* descs = nullptr;
+    int desc_off[4] = {0, 0, 0, 0};
+    int desc_cnt[4] = {0, 0, 0, 0};
+    double* tr_norms = nullptr;
+    double* tr_minres = nullptr;
+    unsigned long long* tr_wall = nullptr;
+    int tr_capacity = 0;
+    double* stage = nullptr;  // host<->device staging, n * P doubles
+    size_t stage_elems = 0;
+
+    AdConfig ad;
+    int nparts = 0;
+
+    std::vector<cudaEvent_t> mv_ev;  // [2 * 2 * kChunkMax]
+    cudaEvent_t ev_run0 = nullptr, ev_run1 = nullptr, ev_loop0 = nullptr, ev_loop1 = nullptr;
+    cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
+    coopcg_timing timing{};
+    long long launches = 0;  // kernels launched since the last run started
+};
+
+namespace {
+
+thread_local std::string g_create_error;  // last coopcg_gpu_create* failure (ctx == NULL)
+
+int fail(coopcg_gpu_ctx* c, int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    std::vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) c->msg = buf;
+    else g_create_error = buf;
+    return code;
+}
+
+#define CK(call)                                                                                 \
+    do {                                                                                         \
+        cudaError_t e_ = (call);                                                                 \
+        if (e_ != cudaSuccess)                                                                   \
+            return fail(ctx, COOPCG_E_CUDA, "%s failed: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                     \
+    } while (0)
+
+#define CKL()                                                                                   \
+    do {                                                                                        \
+        cudaError_t e_ = cudaGetLastError();                                                    \
+        if (e_ != cudaSuccess)                                                                  \
+            return fail(ctx, COOPCG_E_CUDA, "kernel launch failed: %s (%s:%d)", cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                                    \
+    } while (0)
+
+// ---- A.D launcher: template dispatch on (P, CPT, BR) -------------------------
+template <int P, int CPT, int BR>
+size_t ad_smem() {
+    return static_cast<size_t>(kAdS) * kAdT * (BR + P) * sizeof(double) + kAdS * sizeof(uint64_t);
+}
+
+template <int P, int CPT, int BR>
+cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
+    auto kern = ad_exact_kernel<P, CPT, BR, kAdT, kAdS>;
+    const size_t smem = ad_smem<P, CPT, BR>();
+    static bool attr_done[64] = {};
+    const int dev = ctx->device & 63;
+    if (!attr_done[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_done[dev] = true;
+    }
+    dim3 grid((ctx->n_loc + BR - 1) / BR);
+    dim3 block(BR * (P / CPT));
+    kern<<<grid, block, smem, ctx->stream>>>(ctx->At, ctx->ld, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p,
+                                             stop);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+
+template <int P, int CPT>
+cudaError_t ad_launch_br(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
+    switch (ctx->ad.BR) {
+    case 32: return ad_launch_t<P, CPT, 32>(ctx, src, dst, b, stop);
+    case 64: return ad_launch_t<P, CPT, 64>(ctx, src, dst, b, stop);
+    default: return ad_launch_t<P, CPT, 128>(ctx, src, dst, b, stop);
+    }
+}
+
+cudaError_t ad_launch(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
+    switch (ctx->P) {
+    case 4: return ad_launch_br<4, 2>(ctx, src, dst, b, stop);
+    case 8: return ad_launch_br<8, 4>(ctx, src, dst, b, stop);
+    case 16: return ad_launch_br<16, 8>(ctx, src, dst, b, stop);
+    default: return ad_launch_br<32, 8>(ctx, src, dst, b, stop);
+    }
+}
+
+AdConfig pick_ad_config(int n_loc, int P) {
+    AdConfig c;
+    if (n_loc >= 2 * 148 * 128) c.BR = 128;
+    else if (n_loc >= 148 * 64) c.BR = 64;
+    else c.BR = 32;
+    // P=32 with BR=128 -> 512 threads, 160 KB ring: one CTA per SM.
+    c.CPT = (P == 4) ? 2 : (P == 8 ? 4 : 8);
+    return c;
+}
+
+// ---- chain launcher ---------------------------------------------------------
+enum ChainPhase { kPhSetup = 0, kPhGram = 1, kPhBeta = 2, kPhFinal = 3 };
+
+cudaError_t chains_launch(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
+                          int nsrc, const int* stop) {
+    const int cnt = ctx->desc_cnt[phase];
+    const size_t smem = 2ull * nsrc * kChainT * ctx->P * sizeof(double) + 2 * sizeof(uint64_t);
+    dim3 grid((cnt + 63) / 64);
+    chain_kernel<kChainT><<<grid, 64, smem, ctx->stream>>>(s0, s1, s2, nsrc, ctx->n, ctx->P,
+                                                           ctx->descs + ctx->desc_off[phase], cnt, ctx->small, stop);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+
+void build_descs(int p, int P, std::vector<ChainDesc>& all, int off[4], int cnt[4]) {
+    const SmallLayout L{P};
+    auto add = [&](int sx, int a, int sy, int b, int out, int neg) {
+        ChainDesc d;
+        d.sx = (uint8_t)sx;
+        d.a = (uint8_t)a;
+        d.sy = (uint8_t)sy;
+        d.b = (uint8_t)b;
+        d.out = (uint16_t)out;
+        d.neg = (uint8_t)neg;
+        d.pad = 0;
+        all.push_back(d);
+    };
+    // setup: |R_i|^2 (stage_setup, block_cg.hpp:140)        srcs: 0=R
+    off[kPhSetup] = (int)all.size();
+    for (int i = 0; i < p; ++i) add(0, i, 0, i, L.nsq_r() + i, 0);
+    cnt[kPhSetup] = (int)all.size() - off[kPhSetup];
+    // gram: raw(i,j) = D_i.Q_j; rhs_a(i,j) = -R_i.D_j; |D_i|^2   srcs: 0=D 1=Q 2=R
+    off[kPhGram] = (int)all.size();
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j < p; ++j) add(0, i, 1, j, L.raw() + i * P + j, 0);
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j < p; ++j) add(2, i, 0, j, L.rhs_a() + i * P + j, 1);
+    for (int i = 0; i < p; ++i) add(0, i, 0, i, L.nsq_d() + i, 0);
+    cnt[kPhGram] = (int)all.size() - off[kPhGram];
+    // beta: rhs_b(i,j) = -R_i.Q_j; |R_i|^2                    srcs: 0=R 1=Q
+    off[kPhBeta] = (int)all.size();
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j < p; ++j) add(0, i, 1, j, L.rhs_b() + i * P + j, 1);
+    for (int i = 0; i < p; ++i) add(0, i, 0, i, L.nsq_r() + i, 0);
+    cnt[kPhBeta] = (int)all.size() - off[kPhBeta];
+    // final: |A x_j - b|^2                                    srcs: 0=S
+    off[kPhFinal] = (int)all.size();
+    for (int i = 0; i < p; ++i) add(0, i, 0, i, L.nsq_f() + i, 0);
+    cnt[kPhFinal] = (int)all.size() - off[kPhFinal];
+}
+
+size_t rank_smem(int P) { return 2ull * kRankTile * P * sizeof(double) + 2 * sizeof(uint64_t); }
+
+int grid_for(size_t elems, int block) {
+    size_t g = (elems + block - 1) / block;
+    return (int)std::min<size_t>(g, 148ull * 16);
+}
+
+int destroy_impl(coopcg_gpu_ctx* ctx) {
+    if (!ctx) return COOPCG_OK;
+    cudaSetDevice(ctx->device);
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    cudaFree(ctx->At);
+    cudaFree(ctx->X);
+    cudaFree(ctx->R);
+    cudaFree(ctx->Dblk[0]);
+    cudaFree(ctx->Dblk[1]);
+    cudaFree(ctx->Q);
+    cudaFree(ctx->S);
+    cudaFree(ctx->V);
+    cudaFree(ctx->b);
+    cudaFree(ctx->small);
+    cudaFree(ctx->partials);
+    cudaFree(ctx->init_norms);
+    cudaFree(ctx->final_norms);
+    cudaFree(ctx->ctl);
+    cudaFree(ctx->descs);
+    cudaFree(ctx->tr_norms);
+    cudaFree(ctx->tr_minres);
+    cudaFree(ctx->tr_wall);
+    cudaFree(ctx->stage);
+    if (ctx->ctl_host) cudaFreeHost(ctx->ctl_host);
+    for (auto e : ctx->mv_ev) cudaEventDestroy(e);
+    cudaEvent_t evs[] = {ctx->ev_run0, ctx->ev_run1, ctx->ev_loop0, ctx->ev_loop1, ctx->ev_chunk[0], ctx->ev_chunk[1]};
+    for (auto e : evs)
+        if (e) cudaEventDestroy(e);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    return COOPCG_OK;
+}
+
+int ensure_trace_capacity(coopcg_gpu_ctx* ctx, int cap) {
+    if (cap <= ctx->tr_capacity) return COOPCG_OK;
+    cudaFree(ctx->tr_norms);
+    cudaFree(ctx->tr_minres);
+    cudaFree(ctx->tr_wall);
+    ctx->tr_norms = nullptr;
+    ctx->tr_minres = nullptr;
+    ctx->tr_wall = nullptr;
+    CK(cudaMalloc(&ctx->tr_norms, sizeof(double) * (size_t)cap * ctx->p));
+    CK(cudaMalloc(&ctx->tr_minres, sizeof(double) * (size_t)cap));
+    CK(cudaMalloc(&ctx->tr_wall, sizeof(unsigned long long) * (size_t)cap));
+    ctx->tr_capacity = cap;
+    return COOPCG_OK;
+}
+
+// Host part of the generators, shared by the C ABI.
+uint64_t host_draw(uint64_t key, uint64_t c) { return mix64(key + c * kGolden); }
+double host_unit(uint64_t x) { return (double)(x >> 11) * 0x1.0p-53; }
+double host_uniform_pm1(uint64_t key, uint64_t c) {
+    volatile double u = host_unit(host_draw(key, c));
+    volatile double t = 2.0 * u;
+    return -1.0 + t;
+}
+double host_normal(uint64_t key, uint64_t t) {
+    double u1 = host_unit(host_draw(key, 2 * t + 1));
+    double u2 = host_unit(host_draw(key, 2 * t + 2));
+    if (u1 <= 0.0) u1 = 0x1.0p-53;
+    volatile double l = -2.0 * std::log(u1);
+    const double r = std::sqrt(l);
+    const double two_pi = 6.283185307179586476925286766559;
+    volatile double ang = two_pi * u2;
+    volatile double cs = std::cos(ang);
+    return r * cs;
+}
+
+}  // namespace
+
+// =============================================================================
+// C ABI
+// =============================================================================
+extern "C" {
+
+const char* coopcg_gpu_version(void) { return "coopcg_gpu 1 sm_100a exact"; }
+
+int coopcg_gpu_last_error(const coopcg_gpu_ctx* ctx, char* buf, size_t len) {
+    if (!buf || len == 0) return COOPCG_E_INVALID;
+    const char* m = ctx ? ctx->msg.c_str() : g_create_error.c_str();
+    std::snprintf(buf, len, "%s", m);
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, int row_end,
+                            coopcg_gpu_ctx** out) {
+    if (!out) return COOPCG_E_INVALID;
+    *out = nullptr;
+    g_create_error.clear();
+    if (n < 2 || p < 1 || p >= n)
+        return fail(nullptr, COOPCG_E_DIMENSION, "solver: need 1 <= p < n starting columns");  // solvers.hpp:300-306
+    if (p > COOPCG_GPU_MAX_P) return fail(nullptr, COOPCG_E_DIMENSION, "p > %d agents", COOPCG_GPU_MAX_P);
+    if (row_begin < 0 || row_end > n || row_begin >= row_end)
+        return fail(nullptr, COOPCG_E_DIMENSION, "bad row block [%d, %d) of %d", row_begin, row_end, n);
+    if (arith != COOPCG_ARITH_EXACT && arith != COOPCG_ARITH_FAST)
+        return fail(nullptr, COOPCG_E_INVALID, "unknown arith mode %d", arith);
+    auto* ctx = new coopcg_gpu_ctx();
+    ctx->n = n;
+    ctx->p = p;
+    ctx->P = pad_cols(p);
+    ctx->device = device;
+    ctx->arith = arith;
+    ctx->row0 = row_begin;
+    ctx->row1 = row_end;
+    ctx->n_loc = row_end - row_begin;
+    ctx->ld = round_up(ctx->n_loc, 128);
+    ctx->ad = pick_ad_config(ctx->n_loc, ctx->P);
+    auto bail = [&](int code) {
+        g_create_error = ctx->msg;
+        destroy_impl(ctx);
+        return code;
+    };
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        fail(ctx, COOPCG_E_CUDA, "cudaSetDevice(%d): %s", device, cudaGetErrorString(e));
+        return bail(COOPCG_E_CUDA);
+    }
+    const size_t blk = (size_t)n * ctx->P;
+#define CKC(call)                                                                         \
+    do {                                                                                  \
+        cudaError_t e_ = (call);                                                          \
+        if (e_ != cudaSuccess) {                                                          \
+            fail(ctx, COOPCG_E_CUDA, "%s failed: %s", #call, cudaGetErrorString(e_));     \
+            return bail(COOPCG_E_CUDA);                                                   \
+        }                                                                                 \
+    } while (0)
+    CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CKC(cudaMalloc(&ctx->At, sizeof(double) * (size_t)n * ctx->ld));
+    CKC(cudaMemsetAsync(ctx->At, 0, sizeof(double) * (size_t)n * ctx->ld, ctx->stream));
+    double** blocks[] = {&ctx->X, &ctx->R, &ctx->Dblk[0], &ctx->Dblk[1], &ctx->Q, &ctx->S, &ctx->V};
+    for (double** bp : blocks) {
+        CKC(cudaMalloc(bp, sizeof(double) * blk));
+        CKC(cudaMemsetAsync(*bp, 0, sizeof(double) * blk, ctx->stream));
+    }
+    CKC(cudaMalloc(&ctx->b, sizeof(double) * n));
+    const SmallLayout L{ctx->P};
+    CKC(cudaMalloc(&ctx->small, sizeof(double) * L.total()));
+    CKC(cudaMemsetAsync(ctx->small, 0, sizeof(double) * L.total(), ctx->stream));
+    ctx->nparts = kMaxParts;
+    CKC(cudaMalloc(&ctx->partials, sizeof(double) * kMaxParts * 528));
+    CKC(cudaMalloc(&ctx->init_norms, sizeof(double) * (ctx->P + 1)));
+    CKC(cudaMalloc(&ctx->final_norms, sizeof(double) * (ctx->P + 1)));
+    CKC(cudaMalloc(&ctx->ctl, sizeof(Ctl)));
+    CKC(cudaHostAlloc(&ctx->ctl_host, 2 * sizeof(Ctl), cudaHostAllocDefault));
+    std::vector<ChainDesc> descs;
+    build_descs(p, ctx->P, descs, ctx->desc_off, ctx->desc_cnt);
+    CKC(cudaMalloc(&ctx->descs, sizeof(ChainDesc) * descs.size()));
+    CKC(cudaMemcpyAsync(ctx->descs, descs.data(), sizeof(ChainDesc) * descs.size(), cudaMemcpyHostToDevice,
+                        ctx->stream));
+    ctx->stage_elems = std::max<size_t>(blk, (size_t)n * 64);
+    CKC(cudaMalloc(&ctx->stage, sizeof(double) * ctx->stage_elems));
+    ctx->mv_ev.resize(2 * 2 * kChunkMax);
+    for (auto& ev : ctx->mv_ev) CKC(cudaEventCreate(&ev));
+    CKC(cudaEventCreate(&ctx->ev_run0));
+    CKC(cudaEventCreate(&ctx->ev_run1));
+    CKC(cudaEventCreate(&ctx->ev_loop0));
+    CKC(cudaEventCreate(&ctx->ev_loop1));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_chunk[0], cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_chunk[1], cudaEventDisableTiming));
+    // dynamic shared-memory opt-ins
+    CKC(cudaFuncSetAttribute(chain_kernel<kChainT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(2ull * 3 * kChainT * 32 * sizeof(double) + 64)));
+    CKC(cudaFuncSetAttribute(rank_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)rank_smem(32)));
+    CKC(cudaStreamSynchronize(ctx->stream));
+#undef CKC
+    *out = ctx;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_create(int n, int p, int device, int arith, coopcg_gpu_ctx** out) {
+    return coopcg_gpu_create_shard(n, p, device, arith, 0, n, out);
+}
+
+int coopcg_gpu_destroy(coopcg_gpu_ctx* ctx) { return destroy_impl(ctx); }
+
+int coopcg_gpu_set_A(coopcg_gpu_ctx* ctx, const double* A_rows) {
+    if (!ctx || !A_rows) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    const int n = ctx->n;
+    // Stage row chunks (pinned bounce is implicit in cudaMemcpy from pageable).
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>(ctx->stage_elems / n, 4096));
+    for (int r0 = 0; r0 < ctx->n_loc; r0 += chunk) {
+        const int rows = std::min(chunk, ctx->n_loc - r0);
+        CK(cudaMemcpyAsync(ctx->stage, A_rows + (size_t)r0 * n, sizeof(double) * (size_t)rows * n,
+                           cudaMemcpyHostToDevice, ctx->stream));
+        dim3 grid((n + 31) / 32, (rows + 31) / 32);
+        transpose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->stage, rows, n, ctx->At, ctx->ld, r0);
+        CKL();
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->a_ready = true;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_get_A(coopcg_gpu_ctx* ctx, double* A_rows) {
+    if (!ctx || !A_rows) return COOPCG_E_INVALID;
+    if (!ctx->a_ready) return fail(ctx, COOPCG_E_STATE, "A not set");
+    CK(cudaSetDevice(ctx->device));
+    const int n = ctx->n;
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>(ctx->stage_elems / n, 4096));
+    for (int r0 = 0; r0 < ctx->n_loc; r0 += chunk) {
+        const int rows = std::min(chunk, ctx->n_loc - r0);
+        dim3 grid((n + 31) / 32, (rows + 31) / 32);
+        untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->ld, r0, rows, n, ctx->stage);
+        CKL();
+        CK(cudaMemcpyAsync(A_rows + (size_t)r0 * n, ctx->stage, sizeof(double) * (size_t)rows * n,
+                           cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return COOPCG_OK;
+}
+
+int coopcg_gen_householder_factors(int n, int m, double kappa, uint64_t seed, double* V, double* lambda) {
+    if (n < 2 || m < 0 || (!V && m > 0) || !lambda) return COOPCG_E_INVALID;
+    for (int i = 0; i < n; ++i) lambda[i] = std::pow(kappa, (double)i / (double)(n - 1));
+    for (int r = 0; r < m; ++r) {
+        const uint64_t key = stream_key(seed, 102, (uint64_t)r);
+        for (int i = 0; i < n; ++i) V[(size_t)r * n + i] = host_normal(key, (uint64_t)i);
+    }
+    return COOPCG_OK;
+}
+
+int coopcg_gen_rhs(int n, int kind, uint64_t seed, double* b) {
+    if (n < 1 || !b) return COOPCG_E_INVALID;
+    const uint64_t key = stream_key(seed, 3, (uint64_t)n);
+    for (int i = 0; i < n; ++i)
+        b[i] = (kind == COOPCG_VEC_UNIFORM) ? host_uniform_pm1(key, (uint64_t)i + 1) : host_normal(key, (uint64_t)i);
+    return COOPCG_OK;
+}
+
+int coopcg_gen_starts(int n, int p, uint64_t seed, double* X0) {
+    if (n < 1 || p < 1 || !X0) return COOPCG_E_INVALID;
+    const uint64_t key = stream_key(seed, 4, (uint64_t)n);
+    for (int i = 0; i < n; ++i) X0[i] = 0.0;
+    for (int j = 1; j < p; ++j)
+        for (int i = 0; i < n; ++i)
+            X0[(size_t)j * n + i] = host_uniform_pm1(key, (uint64_t)j * (uint64_t)n + (uint64_t)i + 1);
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double kappa) {
+    if (!ctx) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    const int n = ctx->n;
+    if (kind == COOPCG_MATRIX_DIAGDOM) {
+        const uint64_t key = stream_key(seed, 101, (uint64_t)n);
+        gen_dd_offdiag_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->ld, n, ctx->n_loc, ctx->row0, key);
+        CKL();
+        gen_dd_diag_kernel<<<(ctx->n_loc + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->ld, n, ctx->n_loc,
+                                                                             ctx->row0);
+        CKL();
+    } else if (kind == COOPCG_MATRIX_HOUSEHOLDER) {
+        if (ctx->n_loc != n) return fail(ctx, COOPCG_E_INVALID, "Householder generation needs the full matrix");
+        if (m < 0) return COOPCG_E_INVALID;
+        std::vector<double> V((size_t)std::max(m, 1) * n), lam(n);
+        coopcg_gen_householder_factors(n, m, kappa, seed, V.data(), lam.data());
+        double *dV = nullptr, *dl = nullptr, *dw = nullptr, *dt = nullptr;
+        CK(cudaMalloc(&dV, sizeof(double) * V.size()));
+        CK(cudaMalloc(&dl, sizeof(double) * n));
+        CK(cudaMalloc(&dw, sizeof(double) * n));
+        CK(cudaMalloc(&dt, sizeof(double) * 2));
+        CK(cudaMemcpyAsync(dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+        hh_init_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->ld, n, dl);
+        CKL();
+        for (int r = m - 1; r >= 0; --r) {
+            const double* v = dV + (size_t)r * n;
+            hh_w_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->ld, n, v, dw);
+            hh_scalars_kernel<<<1, 32, 0, ctx->stream>>>(n, v, dw, dt);
+            hh_update_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->ld, n, v, dw, dt);
+            CKL();
+        }
+        CK(cudaStreamSynchronize(ctx->stream));
+        cudaFree(dV);
+        cudaFree(dl);
+        cudaFree(dw);
+        cudaFree(dt);
+    } else {
+        return fail(ctx, COOPCG_E_INVALID, "unknown matrix kind %d", kind);
+    }
+    CK(cudaStreamSynchronize(ctx->stream));
+    ctx->a_ready = true;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0) {
+    if (!ctx || !b || !X0) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    CK(cudaMemcpyAsync(ctx->b, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->stage, X0, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, ctx->stream));
+    colmajor_to_rowmajor_kernel<<<grid_for((size_t)n * P, 256), 256, 0, ctx->stream>>>(ctx->stage, ctx->X, n, p, P);
+    CKL();
+    ctx->inputs_ready = true;
+    return COOPCG_OK;
+}
+
+static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* trace) {
+    if (!ctx->a_ready) return fail(ctx, COOPCG_E_STATE, "A not set (coopcg_gpu_set_A / coopcg_gpu_gen_A)");
+    if (!ctx->inputs_ready) return fail(ctx, COOPCG_E_STATE, "b / X0 not uploaded");
+    if (ctx->n_loc != ctx->n)
+        return fail(ctx, COOPCG_E_STATE, "sharded contexts are driven by the multi-GPU orchestrator");
+    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    coopcg_opts o{0.0, -1, -1, 1e-10};
+    if (opts) o = *opts;
+    const int max_iters = o.max_iters >= 0 ? o.max_iters : 2 * n;      // solvers.hpp:18-23
+    const int every = o.recompute_residual_every >= 0 ? o.recompute_residual_every : 50;
+    if (int rc = ensure_trace_capacity(ctx, std::max(max_iters, 1))) return rc;
+    cudaStream_t st = ctx->stream;
+
+    Ctl h{};
+    h.stop = 0;
+    h.status = COOPCG_MAX_ITERATIONS;
+    h.err = 0;
+    h.k = 0;
+    h.iterations = 0;
+    h.converged_agent = -1;
+    h.tol = o.tol;
+    h.rank_rel_tol = o.rank_rel_tol;
+    h.max_iters = max_iters;
+    h.p = p;
+    h.P = P;
+    std::memcpy(&ctx->ctl_host[0], &h, sizeof(Ctl));
+    CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_host[0], sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    int* stop = &ctx->ctl->stop;
+    const SmallLayout L{P};
+
+    ctx->launches = 0;
+    CK(cudaEventRecord(ctx->ev_run0, st));
+    // ---- setup: stage_setup + setup_coordinator (solvers.hpp:263-264) ----
+    CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, nullptr));
+    CK(cudaMemcpyAsync(ctx->Dblk[0], ctx->R, sizeof(double) * (size_t)n * P, cudaMemcpyDeviceToDevice, st));
+    CK(chains_launch(ctx, kPhSetup, ctx->R, nullptr, nullptr, 1, nullptr));
+    setup_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->init_norms);
+    CKL();
+    ++ctx->launches;
+    const int rows_per_tile = 256 / P;
+    const int dgrid = std::min(ctx->nparts, (n + rows_per_tile - 1) / rows_per_tile);
+    direction_kernel<<<dgrid, 256, 0, st>>>(nullptr, ctx->Dblk[0], nullptr, nullptr, n, p, P, ctx->partials, stop);
+    CKL();
+    ++ctx->launches;
+    rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[0], ctx->V, n, ctx->ctl, 1);
+    CKL();
+    ++ctx->launches;
+    CK(cudaEventRecord(ctx->ev_loop0, st));
+
+    // ---- main loop, enqueued in chunks; device-side stop makes extras no-ops ----
+    // One host read after setup (the setup coordinator may already stop).
+    CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    bool stopped = ctx->ctl_host[0].stop != 0;
+    int k_host = 0;
+    int chunk_id = 0;
+    double mv_total = 0.0;
+    int mv_count = 0;
+    int chunk_iters[2] = {0, 0};
+    int chunk_k0[2] = {0, 0};
+    int pending[2];
+    int npending = 0;
+    auto read_chunk = [&](int c) -> int {
+        const int slot = c & 1;
+        CK(cudaEventSynchronize(ctx->ev_chunk[slot]));
+        const Ctl& snap = ctx->ctl_host[slot];
+        for (int u = 0; u < chunk_iters[slot]; ++u) {
+            const int kk = chunk_k0[slot] + u;
+            if (kk >= snap.iterations) break;  // launches after the stop were no-ops
+            float ms = 0.f;
+            if (cudaEventElapsedTime(&ms, ctx->mv_ev[(slot * kChunkMax + u) * 2],
+                                     ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1]) == cudaSuccess) {
+                mv_total += ms;
+                ++mv_count;
+            }
+        }
+        if (snap.stop) stopped = true;
+        return COOPCG_OK;
+    };
+    int chunk = 4;
+    while (!stopped && k_host < max_iters) {
+        if (npending == 2) {
+            if (int rc = read_chunk(pending[0])) return rc;
+            pending[0] = pending[1];
+            npending = 1;
+            if (stopped) break;
+        }
+        const int slot = chunk_id & 1;
+        const int U = std::min(chunk, max_iters - k_host);
+        chunk_iters[slot] = U;
+        chunk_k0[slot] = k_host;
+        for (int u = 0; u < U; ++u, ++k_host) {
+            double* D = ctx->Dblk[k_host & 1];
+            double* Dn = ctx->Dblk[(k_host + 1) & 1];
+            CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2], st));
+            CK(ad_launch(ctx, D, ctx->Q, nullptr, stop));
+            CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1], st));
+            CK(chains_launch(ctx, kPhGram, D, ctx->Q, ctx->R, 3, stop));
+            solve_alpha_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl);
+            CKL();
+    ++ctx->launches;
+            const bool recompute = every > 0 && (k_host + 1) % every == 0;  // solvers.hpp:33-35
+            update_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->R, ctx->X, ctx->Q, D, ctx->small, n, p,
+                                                                        P, recompute ? 1 : 0, stop);
+            CKL();
+    ++ctx->launches;
+            if (recompute) CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, stop));
+            CK(chains_launch(ctx, kPhBeta, ctx->R, ctx->Q, nullptr, 2, stop));
+            solve_beta_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
+                                                ctx->tr_capacity);
+            CKL();
+    ++ctx->launches;
+            direction_kernel<<<dgrid, 256, 0, st>>>(ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop);
+            CKL();
+    ++ctx->launches;
+            rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, Dn, ctx->V, n, ctx->ctl, 0);
+            CKL();
+    ++ctx->launches;
+        }
+        CK(cudaMemcpyAsync(&ctx->ctl_host[slot], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CK(cudaEventRecord(ctx->ev_chunk[slot], st));
+        pending[npending++] = chunk_id;
+        ++chunk_id;
+        chunk = std::min(kChunkMax, chunk * 2);
+    }
+    for (int q = 0; q < npending; ++q)
+        if (int rc = read_chunk(pending[q])) return rc;
+    CK(cudaEventRecord(ctx->ev_loop1, st));
+
+    // ---- finalize_trace (solvers.hpp:188-210) ----
+    CK(ad_launch(ctx, ctx->X, ctx->S, ctx->b, nullptr));
+    CK(chains_launch(ctx, kPhFinal, ctx->S, nullptr, nullptr, 1, nullptr));
+    final_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->final_norms);
+    CKL();
+    ++ctx->launches;
+    CK(cudaEventRecord(ctx->ev_run1, st));
+    CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const Ctl& fin = ctx->ctl_host[0];
+
+    float run_ms = 0.f, loop_ms = 0.f;
+    CK(cudaEventElapsedTime(&run_ms, ctx->ev_run0, ctx->ev_run1));
+    CK(cudaEventElapsedTime(&loop_ms, ctx->ev_loop0, ctx->ev_loop1));
+    ctx->timing.run_ms = run_ms;
+    ctx->timing.loop_ms = loop_ms;
+    ctx->timing.matvec_ms_total = mv_total;
+    ctx->timing.matvec_launches = mv_count;
+    ctx->timing.kernel_launches = ctx->launches;
+
+    if (trace) {
+        const int iters = fin.iterations;
+        trace->status = fin.status;
+        trace->converged_agent = fin.converged_agent;
+        trace->iterations = iters;
+        trace->exact_rank_checks = fin.exact_rank_checks;
+        const int cap = std::min(iters, trace->capacity);
+        std::vector<unsigned long long> wall(std::max(iters, 1));
+        if (iters > 0) CK(cudaMemcpy(wall.data(), ctx->tr_wall, sizeof(unsigned long long) * iters, cudaMemcpyDeviceToHost));
+        uint64_t total = 0;
+        for (int k = 0; k < iters; ++k) total += wall[k];
+        trace->loop_wall_ns = total;
+        if (cap > 0) {
+            if (trace->residual_norms)
+                CK(cudaMemcpy(trace->residual_norms, ctx->tr_norms, sizeof(double) * (size_t)cap * p,
+                              cudaMemcpyDeviceToHost));
+            if (trace->minres) CK(cudaMemcpy(trace->minres, ctx->tr_minres, sizeof(double) * cap, cudaMemcpyDeviceToHost));
+            if (trace->wall_ns) std::memcpy(trace->wall_ns, wall.data(), sizeof(uint64_t) * cap);
+        }
+        std::vector<double> tmp(P + 1);
+        CK(cudaMemcpy(tmp.data(), ctx->init_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
+        if (trace->initial_residual_norms) std::memcpy(trace->initial_residual_norms, tmp.data(), sizeof(double) * p);
+        trace->initial_minres = tmp[p];
+        CK(cudaMemcpy(tmp.data(), ctx->final_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
+        if (trace->final_residual_norms) std::memcpy(trace->final_residual_norms, tmp.data(), sizeof(double) * p);
+        trace->final_minres = tmp[p];
+        if (trace->final_x) {
+            rowmajor_to_colmajor_kernel<<<grid_for((size_t)n * p, 256), 256, 0, st>>>(ctx->X, ctx->stage, n, p, P);
+            CKL();
+    ++ctx->launches;
+            CK(cudaMemcpyAsync(trace->final_x, ctx->stage, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+        }
+    }
+    if (fin.err == COOPCG_E_SPD_VIOLATION)
+        return fail(ctx, COOPCG_E_SPD_VIOLATION, "nonpositive direction energy d^T A d at iteration %d",
+                    fin.err_iter);  // solvers.hpp:111-115
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_run(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* trace) {
+    if (!ctx) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    return run_impl(ctx, opts, trace);
+}
+
+int coopcg_gpu_solve(coopcg_gpu_ctx* ctx, const double* b, const double* X0, const coopcg_opts* opts,
+                     coopcg_trace* trace) {
+    if (int rc = coopcg_gpu_upload(ctx, b, X0)) return rc;
+    return coopcg_gpu_run(ctx, opts, trace);
+}
+
+int coopcg_gpu_timing(const coopcg_gpu_ctx* ctx, coopcg_timing* out) {
+    if (!ctx || !out) return COOPCG_E_INVALID;
+    *out = ctx->timing;
+    return COOPCG_OK;
+}
+
+void* coopcg_gpu_stream(const coopcg_gpu_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+
+int coopcg_gpu_matvec_block(coopcg_gpu_ctx* ctx, const double* D, double* out) {
+    if (!ctx || !D || !out) return COOPCG_E_INVALID;
+    if (!ctx->a_ready) return fail(ctx, COOPCG_E_STATE, "A not set");
+    CK(cudaSetDevice(ctx->device));
+    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    cudaStream_t st = ctx->stream;
+    CK(cudaMemcpyAsync(ctx->stage, D, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, st));
+    colmajor_to_rowmajor_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->stage, ctx->Dblk[0], n, p, P);
+    CKL();
+    CK(ad_launch(ctx, ctx->Dblk[0], ctx->Q, nullptr, nullptr));
+    rowmajor_to_colmajor_kernel<<<grid_for((size_t)ctx->n_loc * p, 256), 256, 0, st>>>(
+        ctx->Q + (size_t)ctx->row0 * P, ctx->stage, ctx->n_loc, p, P);
+    CKL();
+    CK(cudaMemcpyAsync(out, ctx->stage, sizeof(double) * (size_t)ctx->n_loc * p, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D, double tol, int force_exact, int* rank) {
+    if (!ctx || !D || !rank) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    cudaStream_t st = ctx->stream;
+    Ctl h{};
+    h.p = p;
+    h.P = P;
+    h.rank_rel_tol = tol;
+    h.max_iters = 1;
+    h.force_exact = force_exact;
+    std::memcpy(&ctx->ctl_host[0], &h, sizeof(Ctl));
+    CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_host[0], sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->stage, D, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, st));
+    colmajor_to_rowmajor_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->stage, ctx->Dblk[1], n, p, P);
+    CKL();
+    const int rows_per_tile = 256 / P;
+    const int dgrid = std::min(ctx->nparts, (n + rows_per_tile - 1) / rows_per_tile);
+    direction_kernel<<<dgrid, 256, 0, st>>>(nullptr, ctx->Dblk[1], nullptr, nullptr, n, p, P, ctx->partials, nullptr);
+    CKL();
+    rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[1], ctx->V, n, ctx->ctl, 2);
+    CKL();
+    CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *rank = ctx->ctl_host[0].rank_result;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_numerical_rank(coopcg_gpu_ctx* ctx, const double* D, double tol, int* rank) {
+    return coopcg_gpu_numerical_rank_ex(ctx, D, tol, 0, rank);
+}
+
+}  // extern "C"

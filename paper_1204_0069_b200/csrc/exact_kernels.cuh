@@ -1,0 +1,856 @@
+// exact_kernels.cuh -- bit-exact cCG iteration kernels for sm_100a.
+//
+// "Exact" = every output scalar is produced by the same sequence of IEEE
+// double operations as the reference CPU solver (coopcg/kernels.hpp:13-16:
+// ascending-index accumulation from +0.0, one rounding per multiply and per
+// add -- the reference forbids FMA contraction, CMakeLists.txt:25).  Only
+// the assignment of independent chains to threads differs.  Every multiply /
+// add below is an explicit __dmul_rn / __dadd_rn so ptxas cannot contract.
+#pragma once
+#include "common.cuh"
+
+namespace coopcg_gpu {
+
+// ---------------------------------------------------------------------------
+// (1) Q = A . D, the hot kernel.
+//
+// Reference: kernels::matvec_col (kernels.hpp:28-34) per column via
+// stage_matvec (block_cg.hpp:146-151): Q[i][j] = sum_k A[i][k] * D[k][j], k
+// ascending.  The reference streams A p times per iteration (once per
+// agent); here A is streamed ONCE for all p columns.
+//
+// Device layout: A is stored k-major ("At[k][i] = A[i][k]", leading
+// dimension ld >= local rows), so the k-th step of 32 consecutive row chains
+// reads 256 contiguous bytes.  A CTA owns BR rows and all P columns split
+// into P/CPT groups of CPT columns per thread; its A tiles (T k-rows x BR
+// rows) and D tiles (T x P) stream through an S-stage shared-memory ring
+// filled by bulk async copies (cp.async.bulk, TMA 1-D) that complete on
+// mbarriers.  Each thread runs CPT independent sequential chains.
+//
+// Epilogue (sub_b != 0): Y = acc - b (block_cg.hpp:132-138 / :236-241
+// `r[row] -= b[row]`), used for R0 = A X0 - b, the periodic residual
+// recomputation and the final true residual (solvers.hpp:188-210).
+template <int P, int CPT, int BR, int T, int S>
+__global__ void __launch_bounds__(BR*(P / CPT))
+    ad_exact_kernel(const double* __restrict__ At, int ld, int n, int n_loc, int row0,
+                    const double* __restrict__ D, double* __restrict__ Y,
+                    const double* __restrict__ b, int p, const int* __restrict__ stop) {
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* As = reinterpret_cast<double*>(smem_raw);
+    double* Ds = As + S * T * BR;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Ds + S * T * P);
+
+    const int tid = threadIdx.x;
+    const int r = tid % BR;
+    const int g = tid / BR;
+    const int warp = tid >> 5, lane = tid & 31;
+    const int i0 = blockIdx.x * BR;
+    const int ntiles = (n + T - 1) / T;
+
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    auto issue = [&](int t) {
+        const int s = t % S;
+        const int k0 = t * T;
+        const int rows = min(T, n - k0);
+        if (lane == 0)
+            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
+        __syncwarp();
+        for (int kk = lane; kk < rows; kk += 32)
+            bulk_g2s(As + (s * T + kk) * BR, At + static_cast<size_t>(k0 + kk) * ld + i0, BR * 8u,
+                     &full[s]);
+        if (lane == 0)
+            bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
+                     &full[s]);
+    };
+
+    if (warp == 0) {
+        for (int t = 0; t < S - 1 && t < ntiles; ++t) issue(t);
+    }
+
+    double acc[CPT];
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
+
+    for (int t = 0; t < ntiles; ++t) {
+        const int s = t % S;
+        if (warp == 0 && t + S - 1 < ntiles) issue(t + S - 1);
+        mbar_wait(&full[s], static_cast<uint32_t>(t / S) & 1u);
+        const double* a_t = As + s * T * BR + r;
+        const double* d_t = Ds + s * T * P + g * CPT;
+        const int rows = min(T, n - t * T);
+        if (rows == T) {
+#pragma unroll 4
+            for (int kk = 0; kk < T; ++kk) {
+                const double a = a_t[kk * BR];
+                const double2* d2 = reinterpret_cast<const double2*>(d_t + kk * P);
+#pragma unroll
+                for (int c = 0; c < CPT / 2; ++c) {
+                    const double2 dv = d2[c];
+                    acc[2 * c] = mac_exact(acc[2 * c], a, dv.x);
+                    acc[2 * c + 1] = mac_exact(acc[2 * c + 1], a, dv.y);
+                }
+            }
+        } else {
+            for (int kk = 0; kk < rows; ++kk) {
+                const double a = a_t[kk * BR];
+                const double2* d2 = reinterpret_cast<const double2*>(d_t + kk * P);
+#pragma unroll
+                for (int c = 0; c < CPT / 2; ++c) {
+                    const double2 dv = d2[c];
+                    acc[2 * c] = mac_exact(acc[2 * c], a, dv.x);
+                    acc[2 * c + 1] = mac_exact(acc[2 * c + 1], a, dv.y);
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    const int il = i0 + r;
+    if (il < n_loc) {
+        const int row = row0 + il;
+        double* y = Y + static_cast<size_t>(row) * P + g * CPT;
+        const double bb = (b != nullptr) ? b[row] : 0.0;
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            const int col = g * CPT + c;
+            double v = 0.0;
+            if (col < p) v = (b != nullptr) ? __dsub_rn(acc[c], bb) : acc[c];
+            y[c] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// (2) Sequential dot-product chains: Gram rows, step right-hand sides and
+// norms (block_cg.hpp:153-160, :214-216, :262-264, :275-276; kernels.hpp:20-26).
+// Each chain is one thread walking k = 0..n-1 in order; tiles of T rows of
+// up to three n x P row-major source blocks stream through a double-buffered
+// shared-memory ring (bulk async copies).  64 chains per CTA keeps the
+// per-step shared-memory traffic under the 9-cycle DADD latency.
+template <int T>
+__global__ void __launch_bounds__(64)
+    chain_kernel(const double* __restrict__ s0, const double* __restrict__ s1,
+                 const double* __restrict__ s2, int nsrc, int n, int P,
+                 const ChainDesc* __restrict__ descs, int nchains, double* __restrict__ out,
+                 const int* __restrict__ stop) {
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* buf = reinterpret_cast<double*>(smem_raw);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(buf + 2 * nsrc * T * P);
+    const int tid = threadIdx.x;
+    const int c = blockIdx.x * blockDim.x + tid;
+    const bool active = c < nchains;
+    ChainDesc d{0, 0, 0, 0, 0, 0, 0};
+    if (active) d = descs[c];
+    const double* srcs[3] = {s0, s1, s2};
+    const int ntiles = (n + T - 1) / T;
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int t) {
+        if (tid == 0) {
+            const int rows = min(T, n - t * T);
+            const uint32_t bytes = static_cast<uint32_t>(rows) * P * 8u;
+            mbar_arrive_expect_tx(&bar[t & 1], bytes * nsrc);
+            for (int s = 0; s < nsrc; ++s)
+                bulk_g2s(buf + ((t & 1) * nsrc + s) * T * P, srcs[s] + static_cast<size_t>(t) * T * P, bytes,
+                         &bar[t & 1]);
+        }
+    };
+    issue(0);
+    double acc = 0.0;
+    for (int t = 0; t < ntiles; ++t) {
+        if (t + 1 < ntiles) issue(t + 1);
+        mbar_wait(&bar[t & 1], static_cast<uint32_t>(t >> 1) & 1u);
+        const double* xs = buf + ((t & 1) * nsrc + d.sx) * T * P + d.a;
+        const double* ys = buf + ((t & 1) * nsrc + d.sy) * T * P + d.b;
+        const int rows = min(T, n - t * T);
+        if (rows == T) {
+#pragma unroll 16
+            for (int kk = 0; kk < T; ++kk) acc = mac_exact(acc, xs[kk * P], ys[kk * P]);
+        } else {
+            for (int kk = 0; kk < rows; ++kk) acc = mac_exact(acc, xs[kk * P], ys[kk * P]);
+        }
+        __syncthreads();
+    }
+    if (active) out[d.out] = d.neg ? -acc : acc;
+}
+
+// ---------------------------------------------------------------------------
+// (3) Small p x p solves on one warp.
+//
+// lu_factor (kernels.hpp:61-95): partial pivoting, largest |.| with the
+// lowest row index on ties; fails when the pivot is not above
+// floor = max|M| * 1e-14 (block_cg.hpp:180-190).  Lane i owns row i during
+// elimination; every element sees the reference's update sequence.
+// lu_solve_vec (kernels.hpp:97-115): lane i solves agent i's row.
+struct WarpLU {
+    double m[kMaxP][kMaxP + 1];
+    double y[kMaxP][kMaxP + 1];
+    double x[kMaxP][kMaxP + 1];
+};
+
+// Pivot search with the reference's sequential semantics
+// (`if (cand > best)` scanning i = k+1.. from best = |a_kk|): the first index
+// holding the maximum non-NaN value; a NaN at the diagonal always fails.
+__device__ __forceinline__ int warp_pivot(double cand, int lane, int k, int p, bool* ok, double floor) {
+    double v = (lane >= k && lane < p && !isnan(cand)) ? cand : -1.0;
+    int idx = (lane >= k && lane < p) ? lane : 1 << 30;
+    for (int off = 16; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, off);
+        const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
+        if (ov > v || (ov == v && oi < idx)) {
+            v = ov;
+            idx = oi;
+        }
+    }
+    const double diag = __shfl_sync(0xffffffffu, cand, k);
+    double best = isnan(diag) ? diag : v;
+    if (isnan(diag)) idx = k;
+    *ok = (best > floor);
+    return idx;
+}
+
+__device__ bool warp_lu_factor(WarpLU& w, int* perm, int p, double floor) {
+    const int lane = threadIdx.x & 31;
+    if (lane < p) perm[lane] = lane;
+    __syncwarp();
+    for (int k = 0; k < p; ++k) {
+        const double cand = (lane < p) ? fabs(w.m[lane][k]) : 0.0;
+        bool ok;
+        const int piv = warp_pivot(cand, lane, k, p, &ok, floor);
+        if (!ok) return false;
+        if (piv != k) {
+            if (lane < p) {
+                const double t = w.m[k][lane];
+                w.m[k][lane] = w.m[piv][lane];
+                w.m[piv][lane] = t;
+            }
+            if (lane == 0) {
+                const int t = perm[k];
+                perm[k] = perm[piv];
+                perm[piv] = t;
+            }
+        }
+        __syncwarp();
+        if (lane > k && lane < p) {
+            const double mult = __ddiv_rn(w.m[lane][k], w.m[k][k]);
+            w.m[lane][k] = mult;
+            for (int j = k + 1; j < p; ++j) w.m[lane][j] = msub_exact(w.m[lane][j], mult, w.m[k][j]);
+        }
+        __syncwarp();
+    }
+    return true;
+}
+
+// Lane `lane` solves L U x = P rhs for its own right-hand side.
+__device__ void warp_lu_solve_row(WarpLU& w, const int* perm, int p, const double* rhs, double* xout) {
+    const int i_ = threadIdx.x & 31;
+    if (i_ >= p) return;
+    double* y = w.y[i_];
+    double* x = w.x[i_];
+    for (int i = 0; i < p; ++i) {
+        double acc = rhs[perm[i]];
+        for (int j = 0; j < i; ++j) acc = msub_exact(acc, w.m[i][j], y[j]);
+        y[i] = acc;
+    }
+    for (int i = p - 1; i >= 0; --i) {
+        double acc = y[i];
+        for (int j = i + 1; j < p; ++j) acc = msub_exact(acc, w.m[i][j], x[j]);
+        x[i] = __ddiv_rn(acc, w.m[i][i]);
+    }
+    for (int j = 0; j < p; ++j) xout[j] = x[j];
+}
+
+// stage_gram_finalize + stage_alpha (block_cg.hpp:165-218), one warp.
+__global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ small, Ctl* ctl) {
+    if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
+    __shared__ WarpLU w;
+    __shared__ int perm[kMaxP];
+    const int lane = threadIdx.x;
+    const int p = ctl->p, P = ctl->P;
+    const SmallLayout L{P};
+    const double* raw = small + L.raw();
+    // M(i,j) = (raw(i,j) + raw(j,i)) / 2.0
+    double maxabs = 0.0;
+    for (int idx = lane; idx < p * p; idx += 32) {
+        const int i = idx / p, j = idx % p;
+        const double v = __ddiv_rn(__dadd_rn(raw[i * P + j], raw[j * P + i]), 2.0);
+        w.m[i][j] = v;
+        const double a = fabs(v);
+        maxabs = (maxabs < a) ? a : maxabs;
+    }
+    // std::max over all entries ignores NaN in this formulation; order-free.
+    for (int off = 16; off > 0; off >>= 1) {
+        const double o = __shfl_xor_sync(0xffffffffu, maxabs, off);
+        maxabs = (maxabs < o) ? o : maxabs;
+    }
+    __syncwarp();
+    const double floor = __dmul_rn(maxabs, 1e-14);
+    // SPD guard (block_cg.hpp:196-202): nonpositive d_i^T A d_i with d_i != 0.
+    bool bad = false;
+    if (lane < p) bad = !(w.m[lane][lane] > 0.0) && (small[L.nsq_d() + lane] > 0.0);
+    if (__any_sync(0xffffffffu, bad)) {
+        if (lane == 0) {
+            ctl->err = 2;  // COOPCG_E_SPD_VIOLATION
+            ctl->err_iter = ctl->k;
+            ctl->stop = 1;
+        }
+        return;
+    }
+    if (!warp_lu_factor(w, perm, p, floor)) {
+        if (lane == 0) {
+            ctl->status = 1;  // RankCollapse (solvers.hpp:117-123)
+            ctl->stop = 1;
+        }
+        return;
+    }
+    __syncwarp();
+    double xr[kMaxP];
+    if (lane < p) {
+        warp_lu_solve_row(w, perm, p, small + L.rhs_a() + lane * P, xr);
+        for (int j = 0; j < P; ++j) small[L.alpha() + lane * P + j] = (j < p) ? xr[j] : 0.0;
+    }
+    // Keep the factorisation for the beta solve (same M, same pivots).
+    for (int idx = lane; idx < p * p; idx += 32) ctl->lu[idx] = w.m[idx / p][idx % p];
+    if (lane < p) ctl->perm[lane] = perm[lane];
+}
+
+// stage_beta (block_cg.hpp:248-266) + the norms of stage_direction_and_norms
+// (:275-276) + the record / convergence part of end_of_iteration
+// (solvers.hpp:125-154).  One warp.
+__global__ void __launch_bounds__(32)
+    solve_beta_kernel(double* __restrict__ small, Ctl* ctl, double* __restrict__ tr_norms,
+                      double* __restrict__ tr_minres, unsigned long long* __restrict__ tr_wall, int capacity) {
+    if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
+    __shared__ WarpLU w;
+    __shared__ int perm[kMaxP];
+    __shared__ double norms[kMaxP];
+    const int lane = threadIdx.x;
+    const int p = ctl->p, P = ctl->P;
+    const SmallLayout L{P};
+    for (int idx = lane; idx < p * p; idx += 32) w.m[idx / p][idx % p] = ctl->lu[idx];
+    if (lane < p) perm[lane] = ctl->perm[lane];
+    __syncwarp();
+    double xr[kMaxP];
+    if (lane < p) {
+        warp_lu_solve_row(w, perm, p, small + L.rhs_b() + lane * P, xr);
+        for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? xr[j] : 0.0;
+        norms[lane] = __dsqrt_rn(small[L.nsq_r() + lane]);
+        small[L.norm() + lane] = norms[lane];
+    }
+    __syncwarp();
+    if (lane == 0) {
+        const unsigned long long now = globaltimer_ns();
+        const int k = ctl->k;
+        double m = norms[0];
+        int slot = -1;
+        for (int j = 0; j < p; ++j) {
+            m = (norms[j] < m) ? norms[j] : m;  // std::min (block_cg.hpp:297-303)
+            if (slot < 0 && norms[j] <= ctl->tol) slot = j;
+        }
+        if (k < capacity) {
+            for (int j = 0; j < p; ++j) tr_norms[static_cast<size_t>(k) * p + j] = norms[j];
+            tr_minres[k] = m;
+            tr_wall[k] = now - ctl->t_last;
+        }
+        ctl->t_last = now;
+        ctl->iterations = k + 1;
+        if (slot >= 0) {
+            ctl->status = 0;  // Converged
+            ctl->converged_agent = slot;
+            ctl->stop = 1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// (4) Elementwise block updates (kernels.hpp:36-49 combine_columns:
+// dest = base + sum_j coeff[j] * B(:, j), j ascending).  One thread per
+// (row, agent) element; the coefficient grid is staged with stride P+1.
+//
+// mode 0: R_i += sum_j alpha_ij Q_j ; X_i += sum_j alpha_ij D_j (recurrence)
+// mode 1: X_i += sum_j alpha_ij D_j only (recompute iterations: R is then
+//         recomputed as A X - b by ad_exact_kernel; block_cg.hpp:222-244)
+// mode 2: Dn_i = R_i + sum_j beta_ij D_j (block_cg.hpp:270-273), plus the
+//         fast (reordered) Gram partials Dn^T Dn used by the rank certificate.
+__global__ void __launch_bounds__(256)
+    update_kernel(double* __restrict__ R, double* __restrict__ X, const double* __restrict__ Q,
+                  const double* __restrict__ D, const double* __restrict__ small, int n, int p, int P,
+                  int mode, const int* __restrict__ stop) {
+    if (*reinterpret_cast<volatile const int*>(stop)) return;
+    __shared__ double coef[kMaxP * (kMaxP + 1)];
+    const SmallLayout L{P};
+    for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) {
+        const int i = idx / p, j = idx % p;
+        coef[i * (kMaxP + 1) + j] = small[L.alpha() + i * P + j];
+    }
+    __syncthreads();
+    const size_t total = static_cast<size_t>(n) * P;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int i = static_cast<int>(e % P);
+        if (i >= p) continue;
+        const size_t rowoff = e - i;
+        const double* a = coef + i * (kMaxP + 1);
+        if (mode == 0) {
+            double acc = R[e];
+            for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], Q[rowoff + j]);
+            R[e] = acc;
+        }
+        double acc = X[e];
+        for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], D[rowoff + j]);
+        X[e] = acc;
+    }
+}
+
+// Dn = R + D beta^T, plus per-CTA partial Grams of Dn for the rank
+// certificate (pairs i <= j < p).  Rows are processed in tiles of 256/P.
+__global__ void __launch_bounds__(256)
+    direction_kernel(const double* __restrict__ R, const double* __restrict__ D, double* __restrict__ Dn,
+                     const double* __restrict__ small, int n, int p, int P, double* __restrict__ partials,
+                     const int* __restrict__ stop) {
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
+    __shared__ double coef[kMaxP * (kMaxP + 1)];
+    __shared__ double tile[256];
+    const SmallLayout L{P};
+    const int tid = threadIdx.x;
+    const bool with_beta = (small != nullptr);
+    if (with_beta)
+        for (int idx = tid; idx < p * p; idx += blockDim.x) {
+            const int i = idx / p, j = idx % p;
+            coef[i * (kMaxP + 1) + j] = small[L.beta() + i * P + j];
+        }
+    const int npairs = p * (p + 1) / 2;
+    int pi[3], pj[3];
+    double part[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        int t = tid + q * 256;
+        pi[q] = -1;
+        pj[q] = -1;
+        if (t < npairs) {
+            int i = 0;
+            while (t >= p - i) {
+                t -= p - i;
+                ++i;
+            }
+            pi[q] = i;
+            pj[q] = i + t;
+        }
+    }
+    __syncthreads();
+    const int rows_per_tile = 256 / P;
+    const int ntiles = (n + rows_per_tile - 1) / rows_per_tile;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int row = t * rows_per_tile + tid / P;
+        const int i = tid % P;
+        double v = 0.0;
+        if (row < n) {
+            const size_t e = static_cast<size_t>(row) * P + i;
+            if (i < p) {
+                if (with_beta) {
+                    double acc = R[e];
+                    const double* a = coef + i * (kMaxP + 1);
+                    const size_t rowoff = e - i;
+                    for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], D[rowoff + j]);
+                    v = acc;
+                    Dn[e] = v;
+                } else {
+                    v = D[e];
+                }
+            } else if (with_beta) {
+                Dn[e] = 0.0;
+            }
+        }
+        tile[tid] = v;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            if (pi[q] >= 0) {
+                double s = part[q];
+                for (int rr = 0; rr < rows_per_tile; ++rr)
+                    s = fma(tile[rr * P + pi[q]], tile[rr * P + pj[q]], s);
+                part[q] = s;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+        if (pi[q] >= 0) partials[static_cast<size_t>(blockIdx.x) * npairs + tid + q * 256] = part[q];
+}
+
+// ---------------------------------------------------------------------------
+// (5) Rank check of the direction block (solvers.hpp:156-162 calls
+// numerical_rank(Dnext, rank_rel_tol), dense_ops.hpp:104-157) and the rest of
+// end_of_iteration.  A certificate first: from G = Dn^T Dn (fast partials),
+// normalise to unit diagonal, Cholesky, and bound lambda_min(G^) >=
+// 1/||L^-1||_F^2.  Every pivot of column-pivoted MGS is >= sigma_min(Dn)^2 >=
+// lambda_min(G^) * min_j G_jj while the first pivot is max_j G_jj, so if
+// lambda_lower * min/max clears the rank tolerance by a wide margin MGS
+// reports full rank.  Otherwise the exact MGS restatement runs (same op order
+// as the reference) and its rank is used.  One CTA of 1024 threads.
+struct RankScratch {
+    double g[kMaxP][kMaxP + 1];
+    double l[kMaxP][kMaxP + 1];
+    double wi[kMaxP][kMaxP + 1];
+    double vals[kMaxP];
+    double coefs[kMaxP];
+    int used[kMaxP];
+    int ok;
+    int best;
+    double best_sq;
+    int rank;
+    int brk;
+};
+
+template <int T>
+__device__ void cta_exact_chains(const double* __restrict__ V, int n, int P, int nact, const int* xcol,
+                                 const int* ycol, double* outv, double* buf, uint64_t* bar, int& phase_ctr) {
+    // Chains: thread c < nact computes sum_k V[k][xcol[c]] * V[k][ycol[c]].
+    const int tid = threadIdx.x;
+    const int ntiles = (n + T - 1) / T;
+    double acc = 0.0;
+    const int xc = (tid < nact) ? xcol[tid] : 0;
+    const int yc = (tid < nact) ? ycol[tid] : 0;
+    auto issue = [&](int t) {
+        if (tid == 0) {
+            const int rows = min(T, n - t * T);
+            const uint32_t bytes = static_cast<uint32_t>(rows) * P * 8u;
+            const int slot = (phase_ctr + t) & 1;
+            mbar_arrive_expect_tx(&bar[slot], bytes);
+            bulk_g2s(buf + slot * T * P, V + static_cast<size_t>(t) * T * P, bytes, &bar[slot]);
+        }
+    };
+    issue(0);
+    for (int t = 0; t < ntiles; ++t) {
+        if (t + 1 < ntiles) issue(t + 1);
+        const int use = phase_ctr + t;
+        mbar_wait(&bar[use & 1], static_cast<uint32_t>(use >> 1) & 1u);
+        if (tid < nact) {
+            const double* tl = buf + (use & 1) * T * P;
+            const int rows = min(T, n - t * T);
+            for (int kk = 0; kk < rows; ++kk) acc = mac_exact(acc, tl[kk * P + xc], tl[kk * P + yc]);
+        }
+        __syncthreads();
+    }
+    phase_ctr += ntiles;
+    if (tid < nact) outv[tid] = acc;
+    __syncthreads();
+}
+
+constexpr int kRankTile = 64;
+
+// mode 0: end of iteration k; mode 1: setup (rank of D0, then max_iters==0);
+// mode 2: rank only (kernel-level entry point).
+__global__ void __launch_bounds__(1024)
+    rank_end_kernel(const double* __restrict__ partials, int nparts, const double* __restrict__ Dn,
+                    double* __restrict__ V, int n, Ctl* ctl, int mode) {
+    if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int p = ctl->p, P = ctl->P;
+    double* buf = reinterpret_cast<double*>(smem_raw);  // 2 * kRankTile * P
+    uint64_t* bar = reinterpret_cast<uint64_t*>(buf + 2 * kRankTile * P);
+    __shared__ RankScratch rs;
+    __shared__ int xcol[kMaxP], ycol[kMaxP];
+    const int tid = threadIdx.x;
+    const int npairs = p * (p + 1) / 2;
+    // 1. fixed-order reduction of the partial Grams
+    for (int q = tid; q < npairs; q += blockDim.x) {
+        double s = 0.0;
+        for (int b = 0; b < nparts; ++b) s += partials[static_cast<size_t>(b) * npairs + q];
+        int t = q, i = 0;
+        while (t >= p - i) {
+            t -= p - i;
+            ++i;
+        }
+        rs.g[i][i + t] = s;
+        rs.g[i + t][i] = s;
+    }
+    __syncthreads();
+    // 2. certificate on warp 0
+    if (tid < 32) {
+        const int lane = tid;
+        double dmin = 0, dmax = 0;
+        bool good = true;
+        for (int j = 0; j < p; ++j) {
+            const double dj = rs.g[j][j];
+            if (!(dj > 0.0) || !isfinite(dj)) good = false;
+            if (j == 0 || dj < dmin) dmin = dj;
+            if (j == 0 || dj > dmax) dmax = dj;
+        }
+        if (good) {
+            if (lane < p)
+                for (int j = 0; j < p; ++j) rs.l[lane][j] = rs.g[lane][j] / sqrt(rs.g[lane][lane] * rs.g[j][j]);
+            __syncwarp();
+            // Cholesky, lane owns row
+            for (int k = 0; k < p && good; ++k) {
+                if (lane == k) {
+                    double s = rs.l[k][k];
+                    for (int m = 0; m < k; ++m) s -= rs.l[k][m] * rs.l[k][m];
+                    rs.vals[k] = (s > 0.0 && isfinite(s)) ? sqrt(s) : -1.0;
+                    rs.l[k][k] = rs.vals[k];
+                }
+                __syncwarp();
+                if (!(rs.vals[k] > 0.0)) good = false;
+                if (good && lane > k && lane < p) {
+                    double s = rs.l[lane][k];
+                    for (int m = 0; m < k; ++m) s -= rs.l[lane][m] * rs.l[k][m];
+                    rs.l[lane][k] = s / rs.l[k][k];
+                }
+                __syncwarp();
+            }
+            double fro = 0.0;
+            if (good && lane < p) {
+                // column `lane` of L^-1
+                const int j = lane;
+                for (int i = 0; i < p; ++i) rs.wi[i][j] = 0.0;
+                rs.wi[j][j] = 1.0 / rs.l[j][j];
+                fro = rs.wi[j][j] * rs.wi[j][j];
+                for (int i = j + 1; i < p; ++i) {
+                    double s = 0.0;
+                    for (int m = j; m < i; ++m) s += rs.l[i][m] * rs.wi[m][j];
+                    rs.wi[i][j] = -s / rs.l[i][i];
+                    fro += rs.wi[i][j] * rs.wi[i][j];
+                }
+            }
+            for (int off = 16; off > 0; off >>= 1) fro += __shfl_xor_sync(0xffffffffu, fro, off);
+            if (good) {
+                const double lam_lower = 1.0 / fro;
+                const double tol = ctl->rank_rel_tol;
+                const double thr = fmax(1e-6, tol * tol * 1e6);
+                good = isfinite(lam_lower) && lam_lower > 1e-6 && lam_lower * (dmin / dmax) > thr;
+            }
+        }
+        if (lane == 0) rs.ok = good ? 1 : 0;
+    }
+    __syncthreads();
+    int rank = p;
+    if (!rs.ok || ctl->force_exact) {
+        // 3. exact column-pivoted MGS (dense_ops.hpp:104-157) on a working copy.
+        if (tid == 0) {
+            ctl->exact_rank_checks += 1;
+            mbar_init(&bar[0], 1);
+            mbar_init(&bar[1], 1);
+            fence_mbar_init();
+        }
+        const size_t total = static_cast<size_t>(n) * P;
+        for (size_t e = tid; e < total; e += blockDim.x) V[e] = Dn[e];
+        if (tid < kMaxP) rs.used[tid] = 0;
+        if (tid == 0) rs.rank = 0;
+        __threadfence_block();
+        __syncthreads();
+        int phase_ctr = 0;
+        double max_pivot_sq = 0.0;
+        const double tol = ctl->rank_rel_tol;
+        const double tol_sq = __dmul_rn(tol, tol);
+        for (int step = 0; step < p; ++step) {
+            // squared norms of unused columns
+            if (tid == 0) {
+                int a = 0;
+                for (int j = 0; j < p; ++j)
+                    if (!rs.used[j]) {
+                        xcol[a] = j;
+                        ycol[a] = j;
+                        ++a;
+                    }
+                rs.best = a;  // temporarily: number of active chains
+            }
+            __syncthreads();
+            const int nact = rs.best;
+            __syncthreads();
+            // make V writes visible to the async (bulk copy) proxy
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            __syncthreads();
+            cta_exact_chains<kRankTile>(V, n, P, nact, xcol, ycol, rs.vals, buf, bar, phase_ctr);
+            if (tid == 0) {
+                int best = -1;
+                double best_sq = 0.0;
+                for (int a = 0; a < nact; ++a) {
+                    const double nsq = rs.vals[a];
+                    if (best < 0 || nsq > best_sq) {
+                        best = xcol[a];
+                        best_sq = nsq;
+                    }
+                }
+                if (step == 0) max_pivot_sq = best_sq;
+                rs.brk = !(best_sq > __dmul_rn(tol_sq, max_pivot_sq));
+                if (!rs.brk) {
+                    rs.used[best] = 1;
+                    rs.rank += 1;
+                }
+                rs.best = best;
+                rs.best_sq = best_sq;
+            }
+            __syncthreads();
+            if (rs.brk) break;
+            // projections: coef_j = dot(q, c_j) / qsq for unused j
+            const int qb = rs.best;
+            const double qsq = rs.best_sq;
+            if (tid == 0) {
+                int a = 0;
+                for (int j = 0; j < p; ++j)
+                    if (!rs.used[j]) {
+                        xcol[a] = qb;
+                        ycol[a] = j;
+                        ++a;
+                    }
+                rs.brk = a;
+            }
+            __syncthreads();
+            const int nproj = rs.brk;
+            __syncthreads();
+            if (nproj == 0) break;
+            cta_exact_chains<kRankTile>(V, n, P, nproj, xcol, ycol, rs.vals, buf, bar, phase_ctr);
+            if (tid < nproj) rs.coefs[tid] = __ddiv_rn(rs.vals[tid], qsq);
+            __syncthreads();
+            // c[i] -= coef * q[i]
+            for (size_t e = tid; e < static_cast<size_t>(n) * nproj; e += blockDim.x) {
+                const int a = static_cast<int>(e % nproj);
+                const size_t row = e / nproj;
+                const int j = ycol[a];
+                V[row * P + j] = msub_exact(V[row * P + j], rs.coefs[a], V[row * P + qb]);
+            }
+            __threadfence_block();
+            __syncthreads();
+            if (tid == 0) rs.brk = 0;
+            __syncthreads();
+        }
+        rank = rs.rank;
+    }
+    if (tid == 0) {
+        ctl->rank_result = rank;
+        if (mode == 0) {
+            if (rank < p) {
+                ctl->status = 1;  // RankCollapse (solvers.hpp:157-161)
+                ctl->stop = 1;
+            } else if (ctl->k + 1 >= ctl->max_iters) {
+                ctl->status = 2;  // MaxIterations (solvers.hpp:177-181)
+                ctl->stop = 1;
+            } else {
+                ctl->k += 1;
+            }
+        } else if (mode == 1) {
+            if (rank < p) {
+                ctl->status = 1;  // setup_coordinator, solvers.hpp:83-85
+                ctl->stop = 1;
+            } else if (ctl->max_iters == 0) {
+                ctl->status = 2;  // solvers.hpp:95-98
+                ctl->stop = 1;
+            }
+            ctl->t_last = globaltimer_ns();
+        }
+    }
+}
+
+// Setup coordinator part 1 (solvers.hpp:55-82): initial norms, minres and
+// the tolerance check.  One warp.
+__global__ void setup_norms_kernel(double* __restrict__ small, Ctl* ctl, double* __restrict__ init_norms) {
+    const int lane = threadIdx.x;
+    const int p = ctl->p;
+    const SmallLayout L{ctl->P};
+    if (lane < p) {
+        const double v = __dsqrt_rn(small[L.nsq_r() + lane]);
+        small[L.norm() + lane] = v;
+        init_norms[lane] = v;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        const double* nv = small + L.norm();
+        double m = nv[0];
+        int slot = -1;
+        for (int j = 0; j < p; ++j) {
+            m = (nv[j] < m) ? nv[j] : m;
+            if (slot < 0 && nv[j] <= ctl->tol) slot = j;
+        }
+        init_norms[p] = m;
+        if (slot >= 0) {
+            ctl->status = 0;
+            ctl->converged_agent = slot;
+            ctl->stop = 1;
+        }
+        ctl->t_last = globaltimer_ns();
+    }
+}
+
+// finalize_trace (solvers.hpp:188-210): final_residual_norms = ||A x_j - b||.
+__global__ void final_norms_kernel(const double* __restrict__ small, const Ctl* ctl, double* __restrict__ out) {
+    const int lane = threadIdx.x;
+    const int p = ctl->p;
+    const SmallLayout L{ctl->P};
+    if (lane < p) out[lane] = __dsqrt_rn(small[L.nsq_f() + lane]);
+    __syncwarp();
+    if (lane == 0) {
+        double m = out[0];
+        for (int j = 1; j < p; ++j) m = (out[j] < m) ? out[j] : m;  // std::min_element
+        out[p] = m;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Layout helpers.
+// host DenseBlock (n x p column-major) <-> device row-major n x P, zero padded.
+__global__ void colmajor_to_rowmajor_kernel(const double* __restrict__ src, double* __restrict__ dst, int n,
+                                            int p, int P) {
+    const size_t total = static_cast<size_t>(n) * P;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int j = static_cast<int>(e % P);
+        const size_t k = e / P;
+        dst[e] = (j < p) ? src[static_cast<size_t>(j) * n + k] : 0.0;
+    }
+}
+__global__ void rowmajor_to_colmajor_kernel(const double* __restrict__ src, double* __restrict__ dst, int n,
+                                            int p, int P) {
+    const size_t total = static_cast<size_t>(n) * p;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t k = e % n;
+        const int j = static_cast<int>(e / n);
+        dst[e] = src[k * P + j];
+    }
+}
+// rows [c0, c0+rows) of a row-major n-wide matrix (staging) -> At[k][c0+i].
+__global__ void transpose_rows_kernel(const double* __restrict__ stage, int rows, int n, double* __restrict__ At,
+                                      int ld, int c0) {
+    __shared__ double tile[32][33];
+    const int bx = blockIdx.x * 32;  // k
+    const int by = blockIdx.y * 32;  // local row
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int i = by + yy, k = bx + threadIdx.x;
+        tile[yy][threadIdx.x] = (i < rows && k < n) ? stage[static_cast<size_t>(i) * n + k] : 0.0;
+    }
+    __syncthreads();
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int k = bx + yy, i = by + threadIdx.x;
+        if (k < n && i < rows) At[static_cast<size_t>(k) * ld + c0 + i] = tile[threadIdx.x][yy];
+    }
+}
+__global__ void untranspose_rows_kernel(const double* __restrict__ At, int ld, int c0, int rows, int n,
+                                        double* __restrict__ stage) {
+    __shared__ double tile[32][33];
+    const int bx = blockIdx.x * 32;  // k
+    const int by = blockIdx.y * 32;  // local row
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int k = bx + yy, i = by + threadIdx.x;
+        tile[yy][threadIdx.x] = (k < n && i < rows) ? At[static_cast<size_t>(k) * ld + c0 + i] : 0.0;
+    }
+    __syncthreads();
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int i = by + yy, k = bx + threadIdx.x;
+        if (i < rows && k < n) stage[static_cast<size_t>(i) * n + k] = tile[threadIdx.x][yy];
+    }
+}
+
+} // namespace coopcg_gpu

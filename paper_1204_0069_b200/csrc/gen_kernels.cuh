@@ -1,0 +1,117 @@
+// gen_kernels.cuh -- on-device generators for the BASELINE inputs.
+//
+// The reference has no generator for the BASELINE configs; these follow the
+// spec in DESIGN.md §3 built on the reference's counter-based SplitMix64
+// streams (coopcg/rng.hpp:16-20, :35-48, :80-87).  Every value is a pure
+// function of (seed, element index) or a sequential chain with the
+// specified order, so the GPU bytes equal the host oracle's bytes
+// (tests/test_gen.py).  A is written in the k-major device layout
+// At[k][i - row0] = A(i, k) for the context's rows i.
+#pragma once
+#include "common.cuh"
+
+namespace coopcg_gpu {
+
+constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t id, uint64_t extra) {
+    return mix64(seed ^ mix64(id ^ mix64(extra)));
+}
+__device__ __forceinline__ double uniform_pm1_dev(uint64_t key, uint64_t c) {
+    const uint64_t x = mix64(key + c * kGolden);
+    const double u = __dmul_rn(__ull2double_rn(x >> 11), 0x1.0p-53);
+    return __dadd_rn(-1.0, __dmul_rn(2.0, u));
+}
+
+// Off-diagonal entries of the diagonally dominant matrix: A_ij = A_ji =
+// (B_lo,hi + B_hi,lo) / 2 with B_ij ~ U[-1,1] at counter i*n + j + 1.
+__global__ void gen_dd_offdiag_kernel(double* __restrict__ At, int ld, int n, int n_loc, int row0, uint64_t key) {
+    const size_t total = static_cast<size_t>(n) * n_loc;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int il = static_cast<int>(e % n_loc);
+        const uint64_t k = e / n_loc;
+        const uint64_t i = static_cast<uint64_t>(row0 + il);
+        double v = 0.0;
+        if (k != i) {
+            const uint64_t lo = k < i ? k : i, hi = k < i ? i : k;
+            const uint64_t un = static_cast<uint64_t>(n);
+            const double u1 = uniform_pm1_dev(key, lo * un + hi + 1);
+            const double u2 = uniform_pm1_dev(key, hi * un + lo + 1);
+            v = __dmul_rn(__dadd_rn(u1, u2), 0.5);
+        }
+        At[k * ld + il] = v;
+    }
+}
+
+// Diagonal: A_ii = (sum_{j != i, ascending} |A_ij|) + 1.  One chain per row,
+// reading At[j][i] (coalesced across consecutive rows).
+__global__ void gen_dd_diag_kernel(double* __restrict__ At, int ld, int n, int n_loc, int row0) {
+    const int il = blockIdx.x * blockDim.x + threadIdx.x;
+    if (il >= n_loc) return;
+    const int i = row0 + il;
+    double acc = 0.0;
+    const double* col = At + il;
+#pragma unroll 8
+    for (int j = 0; j < n; ++j) {
+        const double a = fabs(col[static_cast<size_t>(j) * ld]);
+        if (j != i) acc = __dadd_rn(acc, a);
+    }
+    At[static_cast<size_t>(i) * ld + il] = __dadd_rn(acc, 1.0);
+}
+
+// Householder construction (single-GPU contexts hold the full matrix):
+// M = diag(lambda); for r = m-1 .. 0: M <- H_r M H_r with
+//   s = v.v, w = M v, c = v.w, t1 = 2/s, t2 = (4 c)/(s s),
+//   M_ij <- (M_ij - t1 (v_i w_j + w_i v_j)) + t2 (v_i v_j)
+// (every sum sequential ascending, one rounding per op).
+__global__ void hh_init_kernel(double* __restrict__ At, int ld, int n, const double* __restrict__ lambda) {
+    const size_t total = static_cast<size_t>(n) * ld;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const size_t k = e / ld;
+        const size_t i = e % ld;
+        At[e] = (i == k) ? lambda[i] : 0.0;
+    }
+}
+__global__ void hh_w_kernel(const double* __restrict__ At, int ld, int n, const double* __restrict__ v,
+                            double* __restrict__ w) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double acc = 0.0;
+    const double* col = At + i;
+#pragma unroll 8
+    for (int k = 0; k < n; ++k) acc = mac_exact(acc, col[static_cast<size_t>(k) * ld], v[k]);
+    w[i] = acc;
+}
+__global__ void hh_scalars_kernel(int n, const double* __restrict__ v, const double* __restrict__ w,
+                                  double* __restrict__ t12) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double s = 0.0, c = 0.0;
+    for (int k = 0; k < n; ++k) s = mac_exact(s, v[k], v[k]);
+    for (int k = 0; k < n; ++k) c = mac_exact(c, v[k], w[k]);
+    t12[0] = __ddiv_rn(2.0, s);
+    t12[1] = __ddiv_rn(__dmul_rn(4.0, c), __dmul_rn(s, s));
+}
+__global__ void hh_update_kernel(double* __restrict__ At, int ld, int n, const double* __restrict__ v,
+                                 const double* __restrict__ w, const double* __restrict__ t12) {
+    const double t1 = t12[0], t2 = t12[1];
+    const size_t total = static_cast<size_t>(n) * ld;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int k = static_cast<int>(e / ld);
+        const int i = static_cast<int>(e % ld);
+        if (i >= n) continue;
+        // element (i, k); the expression is symmetric in (i, k) bit for bit.
+        const double q = __dadd_rn(__dmul_rn(v[i], w[k]), __dmul_rn(w[i], v[k]));
+        const double m1 = __dsub_rn(At[e], __dmul_rn(t1, q));
+        At[e] = __dadd_rn(m1, __dmul_rn(t2, __dmul_rn(v[i], v[k])));
+    }
+}
+
+} // namespace coopcg_gpu

@@ -1,0 +1,339 @@
+"""Host-side mirror of the reference solver API over the CUDA C ABI.
+
+Reference interface mirrored (names, argument meaning, error behaviour):
+  * ``ccg_solve(A, b, X0, opts)``      coopcg/solvers.hpp:329-333
+  * ``SolveOptions``                   coopcg/trace.hpp:74-88
+  * ``SolveTrace`` / ``IterationRecord`` coopcg/trace.hpp:33-71
+  * ``TerminalStatus``                 coopcg/trace.hpp:13-29
+  * exceptions                         coopcg/errors.hpp:11-41
+  * mult counting convention           coopcg/workplan.hpp:26-59
+
+Everything numeric runs in the CUDA library (``_capi``); this module only
+marshals host buffers.  There is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional
+
+import numpy as np
+
+from . import _capi
+
+
+# ---- errors (errors.hpp:11-41) ------------------------------------------------
+class Error(RuntimeError):
+    """Base class for all library errors (errors.hpp:15-18)."""
+
+
+class DimensionError(Error):
+    pass
+
+
+class SingularMatrixError(Error):
+    pass
+
+
+class SpdViolationError(Error):
+    pass
+
+
+class NumericalBreakdownError(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+_ERRORS = {1: DimensionError, 2: SpdViolationError, 3: NumericalBreakdownError,
+           4: SingularMatrixError, 5: Error, 6: Error, 10: CudaError}
+
+
+class TerminalStatus(enum.IntEnum):
+    Converged = 0
+    RankCollapse = 1
+    MaxIterations = 2
+
+    def __str__(self) -> str:  # to_string (trace.hpp:19-29)
+        return {0: "converged", 1: "rank-collapse", 2: "max-iterations"}[int(self)]
+
+
+@dataclass
+class SolveOptions:
+    tol: float = 0.0
+    max_iters: int = -1
+    recompute_residual_every: int = -1
+    rank_rel_tol: float = 1e-10
+
+    def to_c(self) -> _capi.coopcg_opts:
+        o = _capi.coopcg_opts()
+        o.tol = float(self.tol)
+        o.max_iters = int(self.max_iters)
+        o.recompute_residual_every = int(self.recompute_residual_every)
+        o.rank_rel_tol = float(self.rank_rel_tol)
+        return o
+
+
+@dataclass
+class GpuOptions:
+    device: int = 0
+    arith: str = "exact"  # "exact" (bit-identical to the reference) | "fast"
+
+
+@dataclass
+class IterationRecord:
+    k: int
+    active_agents: int
+    agents: List[int]
+    residual_norms: np.ndarray
+    minres: float
+    mults: int
+    mults_per_worker: List[int]
+    wall_ns: int
+
+
+@dataclass
+class SolveTrace:
+    iterations: List[IterationRecord]
+    status: TerminalStatus
+    converged_agent: int
+    final_x: np.ndarray  # (n, p)
+    active_agents: List[int]
+    initial_residual_norms: np.ndarray
+    initial_minres: float
+    final_residual_norms: np.ndarray
+    final_minres: float
+    setup_mults: int
+    loop_wall_ns: int
+    barriers_per_iteration: int = 0
+    residual_norms: np.ndarray = field(default=None)  # (iterations, p)
+    minres: np.ndarray = field(default=None)
+    wall_ns: np.ndarray = field(default=None)
+    exact_rank_checks: int = 0
+
+    def iteration_count(self) -> int:
+        return len(self.iterations)
+
+
+def _lu_mults(p: int) -> int:
+    return p * (p + 1) * (2 * p + 1) // 6
+
+
+def iteration_mults(n: int, p: int, recompute: bool) -> int:
+    """Per-worker counted multiplications of one iteration (workplan.hpp:693-715)."""
+    resid = n * n if recompute else n * p
+    return n * n + 5 * n * p + resid + 2 * _lu_mults(p)
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _check(ctx_handle, rc: int) -> None:
+    if rc == 0:
+        return
+    buf = C.create_string_buffer(512)
+    if ctx_handle is not None:
+        _capi.lib().coopcg_gpu_last_error(ctx_handle, buf, 512)
+    msg = buf.value.decode() or f"coopcg error code {rc}"
+    raise _ERRORS.get(rc, Error)(msg)
+
+
+_ARITH = {"exact": 0, "fast": 1}
+
+
+class GpuContext:
+    """One solver context on one GPU (owns device memory and a CUDA stream).
+
+    ``row_begin``/``row_end`` select a row block of A for sharded multi-GPU
+    solves (see ``paper_1204_0069_b200.sharded``); the default is the whole
+    matrix.
+    """
+
+    def __init__(self, n: int, p: int, device: int = 0, arith: str = "exact",
+                 row_begin: int = 0, row_end: Optional[int] = None):
+        L = _capi.lib()
+        self.n, self.p, self.device, self.arith = n, p, device, arith
+        self.row_begin = row_begin
+        self.row_end = n if row_end is None else row_end
+        h = C.c_void_p()
+        if arith not in _ARITH:
+            raise Error(f"unknown arith mode {arith!r}")
+        rc = L.coopcg_gpu_create_shard(n, p, device, _ARITH[arith], self.row_begin, self.row_end,
+                                       C.byref(h))
+        if rc != 0:
+            buf = C.create_string_buffer(512)
+            L.coopcg_gpu_last_error(None, buf, 512)
+            raise _ERRORS.get(rc, Error)(buf.value.decode() or f"create failed ({rc})")
+        self._h = h
+        self._timing = _capi.coopcg_timing()
+
+    # -- lifecycle --
+    def close(self) -> None:
+        if getattr(self, "_h", None):
+            _capi.lib().coopcg_gpu_destroy(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- the matrix --
+    def set_A(self, A_rows: np.ndarray) -> None:
+        A_rows = np.ascontiguousarray(A_rows, dtype=np.float64)
+        if A_rows.shape != (self.row_end - self.row_begin, self.n):
+            raise DimensionError("SpdMatrix: entry grid does not match dimension")
+        _check(self._h, _capi.lib().coopcg_gpu_set_A(self._h, A_rows.ctypes.data))
+
+    def gen_A(self, kind: str, seed: int, m: int = 0, kappa: float = 1.0) -> None:
+        k = {"diagdom": 0, "householder": 1}[kind]
+        _check(self._h, _capi.lib().coopcg_gpu_gen_A(self._h, k, seed, m, kappa))
+
+    def get_A(self) -> np.ndarray:
+        out = np.empty((self.row_end - self.row_begin, self.n))
+        _check(self._h, _capi.lib().coopcg_gpu_get_A(self._h, out.ctypes.data))
+        return out
+
+    # -- inputs / solve --
+    def upload(self, b: np.ndarray, X0: np.ndarray) -> None:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        X0 = np.asarray(X0, dtype=np.float64)
+        if b.shape != (self.n,) or X0.shape != (self.n, self.p):
+            raise DimensionError("solver: operand shapes do not match the system matrix")
+        X0c = np.ascontiguousarray(X0.T)  # DenseBlock column-major
+        _check(self._h, _capi.lib().coopcg_gpu_upload(self._h, b.ctypes.data, X0c.ctypes.data))
+
+    def run(self, opts: Optional[SolveOptions] = None, want_x: bool = True) -> SolveTrace:
+        opts = opts or SolveOptions()
+        n, p = self.n, self.p
+        cap = max(opts.max_iters if opts.max_iters >= 0 else 2 * n, 1)
+        norms = np.zeros((cap, p))
+        minres = np.zeros(cap)
+        wall = np.zeros(cap, dtype=np.uint64)
+        init = np.zeros(p)
+        fres = np.zeros(p)
+        fx = np.zeros((p, n)) if want_x else None
+        tr = _capi.coopcg_trace()
+        tr.capacity = cap
+        tr.residual_norms = _dp(norms)
+        tr.minres = _dp(minres)
+        tr.wall_ns = wall.ctypes.data_as(C.POINTER(C.c_uint64))
+        tr.initial_residual_norms = _dp(init)
+        tr.final_residual_norms = _dp(fres)
+        tr.final_x = _dp(fx) if want_x else C.POINTER(C.c_double)()
+        co = opts.to_c()
+        rc = _capi.lib().coopcg_gpu_run(self._h, C.byref(co), C.byref(tr))
+        _check(self._h, rc)
+        _capi.lib().coopcg_gpu_timing(self._h, C.byref(self._timing))
+        return self._make_trace(tr, norms, minres, wall, init, fres, fx, opts)
+
+    def _make_trace(self, tr, norms, minres, wall, init, fres, fx, opts) -> SolveTrace:
+        n, p = self.n, self.p
+        it = tr.iterations
+        every = opts.recompute_residual_every if opts.recompute_residual_every >= 0 else 50
+        recs = []
+        for k in range(it):
+            rc = every > 0 and (k + 1) % every == 0
+            m = iteration_mults(n, p, rc)
+            recs.append(IterationRecord(k=k, active_agents=p, agents=list(range(p)),
+                                        residual_norms=norms[k].copy(), minres=float(minres[k]),
+                                        mults=m, mults_per_worker=[m] * p, wall_ns=int(wall[k])))
+        return SolveTrace(iterations=recs, status=TerminalStatus(tr.status),
+                          converged_agent=tr.converged_agent,
+                          final_x=(fx.T.copy() if fx is not None else None),
+                          active_agents=list(range(p)), initial_residual_norms=init,
+                          initial_minres=tr.initial_minres, final_residual_norms=fres,
+                          final_minres=tr.final_minres, setup_mults=n * n,
+                          loop_wall_ns=int(tr.loop_wall_ns), residual_norms=norms[:it].copy(),
+                          minres=minres[:it].copy(), wall_ns=wall[:it].copy(),
+                          exact_rank_checks=tr.exact_rank_checks)
+
+    def solve(self, b, X0, opts: Optional[SolveOptions] = None) -> SolveTrace:
+        self.upload(b, X0)
+        return self.run(opts)
+
+    def timing(self) -> dict:
+        t = self._timing
+        return {"matvec_launches": t.matvec_launches, "matvec_ms_total": t.matvec_ms_total,
+                "run_ms": t.run_ms, "loop_ms": t.loop_ms, "kernel_launches": t.kernel_launches}
+
+    def stream_handle(self) -> int:
+        """cudaStream_t of this context (for events on the launching stream)."""
+        return int(_capi.lib().coopcg_gpu_stream(self._h) or 0)
+
+    # -- kernel-level entry points --
+    def matvec_block(self, D: np.ndarray) -> np.ndarray:
+        D = np.asarray(D, dtype=np.float64)
+        if D.shape != (self.n, self.p):
+            raise DimensionError("matvec_block: row count does not match matrix dimension")
+        Dc = np.ascontiguousarray(D.T)
+        out = np.zeros((self.p, self.row_end - self.row_begin))
+        _check(self._h, _capi.lib().coopcg_gpu_matvec_block(self._h, Dc.ctypes.data, out.ctypes.data))
+        return out.T.copy()
+
+    def numerical_rank(self, D: np.ndarray, tol: float, force_exact: bool = False) -> int:
+        D = np.asarray(D, dtype=np.float64)
+        if D.shape != (self.n, self.p):
+            raise DimensionError("numerical_rank: shape")
+        Dc = np.ascontiguousarray(D.T)
+        r = C.c_int()
+        _check(self._h, _capi.lib().coopcg_gpu_numerical_rank_ex(self._h, Dc.ctypes.data, tol,
+                                                                 1 if force_exact else 0, C.byref(r)))
+        return r.value
+
+
+def ccg_solve(A: np.ndarray, b: np.ndarray, X0: np.ndarray, opts: Optional[SolveOptions] = None,
+              gpu: Optional[GpuOptions] = None) -> SolveTrace:
+    """Cooperative block CG on the GPU with ccg_solve's semantics
+    (coopcg/solvers.hpp:325-333).  A is (n, n), b (n,), X0 (n, p)."""
+    gpu = gpu or GpuOptions()
+    A = np.asarray(A, dtype=np.float64)
+    X0 = np.asarray(X0, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    if A.ndim != 2 or A.shape[0] != A.shape[1]:
+        raise DimensionError("SpdMatrix: entry grid does not match dimension")
+    n = A.shape[0]
+    if b.shape != (n,) or X0.ndim != 2 or X0.shape[0] != n:
+        raise DimensionError("solver: operand shapes do not match the system matrix")
+    p = X0.shape[1]
+    if p < 1 or p >= n:
+        raise DimensionError("solver: need 1 <= p < n starting columns")
+    with GpuContext(n, p, gpu.device, gpu.arith) as ctx:
+        ctx.set_A(A)
+        return ctx.solve(b, X0, opts)
+
+
+# ---- host generators for b, X0 -------------------------------
+def gen_rhs(n: int, kind: str, seed: int) -> np.ndarray:
+    b = np.zeros(n)
+    _check(None, _capi.lib().coopcg_gen_rhs(n, 0 if kind == "uniform" else 1, seed, b.ctypes.data))
+    return b
+
+
+def gen_starts(n: int, p: int, seed: int) -> np.ndarray:
+    X0c = np.zeros((p, n))
+    _check(None, _capi.lib().coopcg_gen_starts(n, p, seed, X0c.ctypes.data))
+    return X0c.T.copy()
+
+
+def gen_householder_factors(n: int, m: int, kappa: float, seed: int):
+    V = np.zeros((max(m, 1), n))
+    lam = np.zeros(n)
+    _check(None, _capi.lib().coopcg_gen_householder_factors(n, m, kappa, seed, V.ctypes.data,
+                                                              lam.ctypes.data))
+    return V[:m], lam
+
+
+def library_version() -> str:
+    return _capi.lib().coopcg_gpu_version().decode()

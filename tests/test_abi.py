@@ -1,0 +1,95 @@
+"""The C-ABI library builds for sm_100a, loads, and exports every symbol
+include/coopcg_gpu.h declares (no GPU needed: no compute calls here)."""
+import ctypes as C
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "coopcg_gpu.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(coopcg_[A-Za-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1204_0069_b200 import _capi
+    lib = _capi.lib()
+    names = declared_functions()
+    assert len(names) >= 15
+    for name in names:
+        assert hasattr(lib, name), name
+    assert {s[0] for s in _capi.SIGNATURES} == set(names), "ctypes table out of sync with header"
+
+
+def test_library_is_sm100a():
+    from paper_1204_0069_b200 import build
+    out = subprocess.run(["cuobjdump", "--list-elf", build.LIB], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_exact_kernels_have_no_fma_contraction():
+    """The exact-mode hot kernels must compile to separate DMUL/DADD (the
+    reference builds with -ffp-contract=off, CMakeLists.txt:25)."""
+    from paper_1204_0069_b200 import build
+    out = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    func = None
+    bad = {}
+    for line in out.stdout.splitlines():
+        m = re.search(r"Function : (\S+)", line)
+        if m:
+            func = m.group(1)
+        elif func and ("ad_exact_kernel" in func or "chain_kernel" in func or "update_kernel" in func) \
+                and "DFMA" in line:
+            bad[func] = bad.get(func, 0) + 1
+    assert not bad, bad
+    assert "UBLKCP" in out.stdout  # bulk async copies (TMA 1-D) are in the SASS
+
+
+def test_version_and_create_error_without_gpu():
+    from paper_1204_0069_b200 import _capi, solver
+    lib = _capi.lib()
+    assert lib.coopcg_gpu_version().decode().startswith("coopcg_gpu")
+    with pytest.raises(solver.DimensionError):
+        solver.GpuContext(10, 10)
+    with pytest.raises(solver.DimensionError):
+        solver.GpuContext(100, 33)
+
+
+def test_host_generators_match_oracle(po):
+    import paper_1204_0069_b200 as m
+    for kind in ("uniform", "normal"):
+        assert np.array_equal(m.gen_rhs(257, kind, 9), po.gen_rhs(257, kind, 9))
+    assert np.array_equal(m.gen_starts(100, 5, 3), po.gen_starts(100, 5, 3))
+    V, lam = m.gen_householder_factors(90, 4, 1e6, 8)
+    V2, lam2 = po.gen_householder_factors(90, 4, 1e6, 8)
+    assert np.array_equal(V, V2) and np.array_equal(lam, lam2)
+
+
+def test_python_api_validates_shapes():
+    import paper_1204_0069_b200 as m
+    with pytest.raises(m.DimensionError):
+        m.ccg_solve(np.eye(4), np.ones(4), np.zeros((4, 4)))
+    with pytest.raises(m.DimensionError):
+        m.ccg_solve(np.eye(4), np.ones(3), np.zeros((4, 2)))
+    with pytest.raises(m.DimensionError):
+        m.ccg_solve(np.ones((4, 3)), np.ones(4), np.zeros((4, 2)))
+
+
+def test_mult_counting_matches_workplan():
+    # count_iteration_mults (workplan.hpp:711-715)
+    from paper_1204_0069_b200 import iteration_mults
+    for n, p in ((100, 3), (4096, 4), (7, 1)):
+        assert iteration_mults(n, p, False) == n * n + 6 * n * p + p * (p + 1) * (2 * p + 1) // 3
+        assert iteration_mults(n, p, True) == 2 * n * n + 5 * n * p + p * (p + 1) * (2 * p + 1) // 3

@@ -1,0 +1,89 @@
+"""The oracle (plain-C restatement of ccg_solve) is pinned against the
+reference: the golden fixtures the reference produced (tests/golden/, made by
+make_golden.py from oracle/_ref) and, where the reference shim is built, a
+direct bit-for-bit comparison on fresh seeded inputs."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden_names, load_golden
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+def assert_trace_equal(t, z):
+    assert t.rc == int(z["rc"])
+    if t.rc != 0:
+        return
+    assert t.status == str(z["status"])
+    assert t.iterations == int(z["iterations"])
+    assert t.converged_agent == int(z["converged_agent"])
+    # bitwise: per-iteration per-agent norms, minres, final X, true residuals
+    assert np.array_equal(t.residual_norms, z["residual_norms"])
+    assert np.array_equal(t.minres, z["minres"])
+    assert np.array_equal(t.initial_residual_norms, z["initial_residual_norms"])
+    assert np.array_equal(t.final_x, z["final_x"])
+    assert np.array_equal(t.final_residual_norms, z["final_residual_norms"])
+    assert t.final_minres == float(z["final_minres"])
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_oracle_matches_reference_golden(po, name):
+    A, z = load_golden(name)
+    assert _sha(A) == str(z["A_sha256"]), "generator drifted from the pinned bytes"
+    t = po.oracle_ccg(A, z["b"], z["X0"], tol=float(z["tol"]), max_iters=int(z["max_iters"]),
+                      recompute=int(z["recompute"]))
+    assert_trace_equal(t, z)
+
+
+@pytest.mark.skipif(not __import__("pyoracle").ref_available(), reason="reference shim not built")
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_oracle_matches_reference_live(po, seed):
+    rng = np.random.default_rng(seed)
+    n, p = int(rng.integers(40, 160)), int(rng.integers(1, 7))
+    A, b, X0 = po.ref_make_problem(n, p, float(10 ** rng.uniform(1, 4)), seed)
+    a = po.oracle_ccg(A, b, X0, tol=1e-9)
+    r = po.ref_solve(A, b, X0, tol=1e-9)
+    assert a.status == r.status and a.iterations == r.iterations
+    assert np.array_equal(a.residual_norms, r.residual_norms)
+    assert np.array_equal(a.final_x, r.final_x)
+    pr = po.ref_solve(A, b, X0, tol=1e-9, algo="parallel")  # parallel_ccg == ccg_solve bitwise
+    assert np.array_equal(pr.final_x, r.final_x) and np.array_equal(pr.residual_norms, r.residual_norms)
+
+
+@pytest.mark.skipif(not __import__("pyoracle").ref_available(), reason="reference shim not built")
+def test_oracle_kernels_match_reference(po):
+    import ctypes as C
+    rng = np.random.default_rng(5)
+    n, p = 70, 5
+    A, _, _ = po.ref_make_problem(n, p, 100.0, 9)
+    D = rng.uniform(-1, 1, (n, p))
+    Dc = np.ascontiguousarray(D.T)
+    o1 = np.zeros((p, n))
+    o2 = np.zeros((p, n))
+    po.oracle_lib().orc_matvec_block(A.ctypes.data, n, Dc.ctypes.data, p, o1.ctypes.data)
+    po.ref_lib().ref_matvec_block(n, p, A.ctypes.data, Dc.ctypes.data, o2.ctypes.data)
+    assert np.array_equal(o1, o2)
+    # numerical_rank: full, (v, 2v, w), zero block (tests/test_dense.cpp:246-291)
+    for blk in (D, np.stack([D[:, 0], 2 * D[:, 0], D[:, 1]], 1), np.zeros((n, 3))):
+        assert po.numerical_rank(blk, 1e-10) [0] == po.numerical_rank(blk, 1e-10, lib="ref")[0]
+
+
+def test_generators_are_symmetric_and_spd(po):
+    A = po.gen_diagdom(64, 3)
+    assert np.array_equal(A, A.T)
+    assert np.all(np.diag(A) > np.sum(np.abs(A), 1) - np.diag(A))
+    H = po.gen_householder(48, 4, 1e3, 3)
+    assert np.array_equal(H, H.T)
+    ev = np.linalg.eigvalsh(H)
+    assert ev.min() > 0.5 and ev.max() < 1.1e3
+
+
+def test_degenerate_x0_rank_collapse(po):
+    A = po.gen_diagdom(100, 1)
+    b = po.gen_rhs(100, "uniform", 1)
+    t = po.oracle_ccg(A, b, np.zeros((100, 3)), tol=1e-10)
+    assert t.status == "rank-collapse" and t.iterations == 0
