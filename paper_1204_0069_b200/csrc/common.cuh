@@ -61,6 +61,14 @@ struct ChainDesc {
     uint8_t neg, pad;
 };
 
+// Device layout of A ("panels"): the context's local rows are cut into panels
+// of BR consecutive rows; panel q stores A(q*BR + r, k) at
+// ((q * n) + k) * BR + r.  One k-row of a panel is BR contiguous doubles and a
+// T x BR stage tile of the A.D kernel is one contiguous block (one bulk copy).
+__host__ __device__ __forceinline__ size_t ap_idx(int n, int brs, int k, int il) {
+    return ((static_cast<size_t>(il >> brs) * n + k) << brs) | static_cast<size_t>(il & ((1 << brs) - 1));
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -92,6 +100,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // Global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0,
 // both addresses 16-byte aligned).

@@ -30,13 +30,11 @@ using namespace coopcg_gpu;
 
 namespace {
 
-constexpr int kChainT = 64;
 constexpr int kAdT = 32;
 constexpr int kAdS = 4;
 constexpr int kChunkMax = 16;
 constexpr int kMaxParts = 296;  // 2 x 148 SMs
 
-int round_up(int x, int m) { return (x + m - 1) / m * m; }
 int pad_cols(int p) {
     int P = 4;
     while (P < p) P *= 2;
@@ -52,7 +50,8 @@ struct AdConfig {
 
 struct coopcg_gpu_ctx {
     int n = 0, p = 0, P = 0, device = 0, arith = 0;
-    int row0 = 0, row1 = 0, n_loc = 0, ld = 0;
+    int row0 = 0, row1 = 0, n_loc = 0, brs = 6, npanels = 0;
+    size_t ap_elems = 0;
     bool a_ready = false, inputs_ready = false;
     cudaStream_t stream = nullptr;
     std::string msg;
@@ -125,7 +124,7 @@ int fail(coopcg_gpu_ctx* c, int code, const char* fmt, ...) {
 // ---- A.D launcher: template dispatch on (P, CPT, BR) -------------------------
 template <int P, int CPT, int BR>
 size_t ad_smem() {
-    return static_cast<size_t>(kAdS) * kAdT * (BR + P) * sizeof(double) + kAdS * sizeof(uint64_t);
+    return static_cast<size_t>(kAdS) * kAdT * (BR + P) * sizeof(double) + 2 * kAdS * sizeof(uint64_t);
 }
 
 template <int P, int CPT, int BR>
@@ -140,9 +139,8 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
         attr_done[dev] = true;
     }
     dim3 grid((ctx->n_loc + BR - 1) / BR);
-    dim3 block(BR * (P / CPT));
-    kern<<<grid, block, smem, ctx->stream>>>(ctx->At, ctx->ld, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p,
-                                             stop);
+    dim3 block(32 + BR * (P / CPT));
+    kern<<<grid, block, smem, ctx->stream>>>(ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop);
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -151,8 +149,7 @@ template <int P, int CPT>
 cudaError_t ad_launch_br(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
     switch (ctx->ad.BR) {
     case 32: return ad_launch_t<P, CPT, 32>(ctx, src, dst, b, stop);
-    case 64: return ad_launch_t<P, CPT, 64>(ctx, src, dst, b, stop);
-    default: return ad_launch_t<P, CPT, 128>(ctx, src, dst, b, stop);
+    default: return ad_launch_t<P, CPT, 64>(ctx, src, dst, b, stop);
     }
 }
 
@@ -167,10 +164,10 @@ cudaError_t ad_launch(coopcg_gpu_ctx* ctx, const double* src, double* dst, const
 
 AdConfig pick_ad_config(int n_loc, int P) {
     AdConfig c;
-    if (n_loc >= 2 * 148 * 128) c.BR = 128;
-    else if (n_loc >= 148 * 64) c.BR = 64;
-    else c.BR = 32;
-    // P=32 with BR=128 -> 512 threads, 160 KB ring: one CTA per SM.
+    // Measured sweep (tools/probe/ad_probe.cu, profiles/): T=32, S=4 rings;
+    // P=4: 2 cols/thread (7.1 TB/s at n=16384), P=8: 4 (5.0 TB/s),
+    // P=16/32: 8 (FP64-issue bound in exact mode, ~12 of 18 T instr/s).
+    c.BR = (n_loc >= 148 * 64) ? 64 : 32;
     c.CPT = (P == 4) ? 2 : (P == 8 ? 4 : 8);
     return c;
 }
@@ -178,15 +175,35 @@ AdConfig pick_ad_config(int n_loc, int P) {
 // ---- chain launcher ---------------------------------------------------------
 enum ChainPhase { kPhSetup = 0, kPhGram = 1, kPhBeta = 2, kPhFinal = 3 };
 
-cudaError_t chains_launch(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
-                          int nsrc, const int* stop) {
+template <int P, int T, int S>
+cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
+                            int nsrc, const int* stop) {
+    auto kern = chain_kernel<P, T, S>;
+    const size_t smem_max = (size_t)S * 3 * T * P * sizeof(double) + 2 * S * sizeof(uint64_t);
+    static bool attr_done[64] = {};
+    const int dev = ctx->device & 63;
+    if (!attr_done[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+        if (e != cudaSuccess) return e;
+        attr_done[dev] = true;
+    }
     const int cnt = ctx->desc_cnt[phase];
-    const size_t smem = 2ull * nsrc * kChainT * ctx->P * sizeof(double) + 2 * sizeof(uint64_t);
-    dim3 grid((cnt + 63) / 64);
-    chain_kernel<kChainT><<<grid, 64, smem, ctx->stream>>>(s0, s1, s2, nsrc, ctx->n, ctx->P,
-                                                           ctx->descs + ctx->desc_off[phase], cnt, ctx->small, stop);
+    const size_t smem = (size_t)S * nsrc * T * P * sizeof(double) + 2 * S * sizeof(uint64_t);
+    kern<<<(cnt + 63) / 64, 96, smem, ctx->stream>>>(s0, s1, s2, nsrc, ctx->n, ctx->descs + ctx->desc_off[phase],
+                                                     cnt, ctx->small, stop);
     ++ctx->launches;
     return cudaGetLastError();
+}
+
+// ~96 KB rings: P=4: 3 x 256 rows; P=8: 4 x 128; P=16: 4 x 64; P=32: 4 x 32.
+cudaError_t chains_launch(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
+                          int nsrc, const int* stop) {
+    switch (ctx->P) {
+    case 4: return chains_launch_t<4, 256, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 8: return chains_launch_t<8, 128, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 16: return chains_launch_t<16, 64, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
+    default: return chains_launch_t<32, 32, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
+    }
 }
 
 void build_descs(int p, int P, std::vector<ChainDesc>& all, int off[4], int cnt[4]) {
@@ -338,8 +355,10 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     ctx->row0 = row_begin;
     ctx->row1 = row_end;
     ctx->n_loc = row_end - row_begin;
-    ctx->ld = round_up(ctx->n_loc, 128);
     ctx->ad = pick_ad_config(ctx->n_loc, ctx->P);
+    ctx->brs = (ctx->ad.BR == 32) ? 5 : 6;
+    ctx->npanels = (ctx->n_loc + ctx->ad.BR - 1) / ctx->ad.BR;
+    ctx->ap_elems = (size_t)ctx->npanels * n * ctx->ad.BR;
     auto bail = [&](int code) {
         g_create_error = ctx->msg;
         destroy_impl(ctx);
@@ -360,8 +379,8 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         }                                                                                 \
     } while (0)
     CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    CKC(cudaMalloc(&ctx->At, sizeof(double) * (size_t)n * ctx->ld));
-    CKC(cudaMemsetAsync(ctx->At, 0, sizeof(double) * (size_t)n * ctx->ld, ctx->stream));
+    CKC(cudaMalloc(&ctx->At, sizeof(double) * ctx->ap_elems));
+    CKC(cudaMemsetAsync(ctx->At, 0, sizeof(double) * ctx->ap_elems, ctx->stream));
     double** blocks[] = {&ctx->X, &ctx->R, &ctx->Dblk[0], &ctx->Dblk[1], &ctx->Q, &ctx->S, &ctx->V};
     for (double** bp : blocks) {
         CKC(cudaMalloc(bp, sizeof(double) * blk));
@@ -382,7 +401,7 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     CKC(cudaMalloc(&ctx->descs, sizeof(ChainDesc) * descs.size()));
     CKC(cudaMemcpyAsync(ctx->descs, descs.data(), sizeof(ChainDesc) * descs.size(), cudaMemcpyHostToDevice,
                         ctx->stream));
-    ctx->stage_elems = std::max<size_t>(blk, (size_t)n * 64);
+    ctx->stage_elems = std::max<size_t>(blk, (size_t)n * 128);
     CKC(cudaMalloc(&ctx->stage, sizeof(double) * ctx->stage_elems));
     ctx->mv_ev.resize(2 * 2 * kChunkMax);
     for (auto& ev : ctx->mv_ev) CKC(cudaEventCreate(&ev));
@@ -393,8 +412,6 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     CKC(cudaEventCreateWithFlags(&ctx->ev_chunk[0], cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_chunk[1], cudaEventDisableTiming));
     // dynamic shared-memory opt-ins
-    CKC(cudaFuncSetAttribute(chain_kernel<kChainT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)(2ull * 3 * kChainT * 32 * sizeof(double) + 64)));
     CKC(cudaFuncSetAttribute(rank_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)rank_smem(32)));
     CKC(cudaStreamSynchronize(ctx->stream));
@@ -420,7 +437,7 @@ int coopcg_gpu_set_A(coopcg_gpu_ctx* ctx, const double* A_rows) {
         CK(cudaMemcpyAsync(ctx->stage, A_rows + (size_t)r0 * n, sizeof(double) * (size_t)rows * n,
                            cudaMemcpyHostToDevice, ctx->stream));
         dim3 grid((n + 31) / 32, (rows + 31) / 32);
-        transpose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->stage, rows, n, ctx->At, ctx->ld, r0);
+        transpose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->stage, rows, n, ctx->At, ctx->brs, r0);
         CKL();
     }
     CK(cudaStreamSynchronize(ctx->stream));
@@ -437,7 +454,7 @@ int coopcg_gpu_get_A(coopcg_gpu_ctx* ctx, double* A_rows) {
     for (int r0 = 0; r0 < ctx->n_loc; r0 += chunk) {
         const int rows = std::min(chunk, ctx->n_loc - r0);
         dim3 grid((n + 31) / 32, (rows + 31) / 32);
-        untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->ld, r0, rows, n, ctx->stage);
+        untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->brs, r0, rows, n, ctx->stage);
         CKL();
         CK(cudaMemcpyAsync(A_rows + (size_t)r0 * n, ctx->stage, sizeof(double) * (size_t)rows * n,
                            cudaMemcpyDeviceToHost, ctx->stream));
@@ -480,9 +497,10 @@ int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double
     const int n = ctx->n;
     if (kind == COOPCG_MATRIX_DIAGDOM) {
         const uint64_t key = stream_key(seed, 101, (uint64_t)n);
-        gen_dd_offdiag_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->ld, n, ctx->n_loc, ctx->row0, key);
+        gen_dd_offdiag_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->brs, n, ctx->n_loc, ctx->row0, key,
+                                                                 ctx->ap_elems);
         CKL();
-        gen_dd_diag_kernel<<<(ctx->n_loc + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->ld, n, ctx->n_loc,
+        gen_dd_diag_kernel<<<(ctx->n_loc + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->brs, n, ctx->n_loc,
                                                                              ctx->row0);
         CKL();
     } else if (kind == COOPCG_MATRIX_HOUSEHOLDER) {
@@ -497,13 +515,13 @@ int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double
         CK(cudaMalloc(&dt, sizeof(double) * 2));
         CK(cudaMemcpyAsync(dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-        hh_init_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->ld, n, dl);
+        hh_init_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->brs, n, dl, ctx->ap_elems);
         CKL();
         for (int r = m - 1; r >= 0; --r) {
             const double* v = dV + (size_t)r * n;
-            hh_w_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->ld, n, v, dw);
+            hh_w_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->brs, n, v, dw);
             hh_scalars_kernel<<<1, 32, 0, ctx->stream>>>(n, v, dw, dt);
-            hh_update_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->ld, n, v, dw, dt);
+            hh_update_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->brs, n, v, dw, dt, ctx->ap_elems);
             CKL();
         }
         CK(cudaStreamSynchronize(ctx->stream));

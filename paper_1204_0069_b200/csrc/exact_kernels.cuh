@@ -19,83 +19,120 @@ namespace coopcg_gpu {
 // ascending.  The reference streams A p times per iteration (once per
 // agent); here A is streamed ONCE for all p columns.
 //
-// Device layout: A is stored k-major ("At[k][i] = A[i][k]", leading
-// dimension ld >= local rows), so the k-th step of 32 consecutive row chains
-// reads 256 contiguous bytes.  A CTA owns BR rows and all P columns split
-// into P/CPT groups of CPT columns per thread; its A tiles (T k-rows x BR
-// rows) and D tiles (T x P) stream through an S-stage shared-memory ring
-// filled by bulk async copies (cp.async.bulk, TMA 1-D) that complete on
-// mbarriers.  Each thread runs CPT independent sequential chains.
+// Device layout: A is stored in panels of BR rows (common.cuh ap_idx): a
+// panel holds A(i, k) for its BR rows at k*BR + r, so the k-th step of 32
+// consecutive row chains reads 256 contiguous bytes and a T x BR stage tile
+// is ONE contiguous block.  A CTA owns one panel and all P columns split
+// into P/CPT groups of CPT columns per thread; its A tiles and D tiles
+// (T x P) stream through an S-stage shared-memory ring filled by bulk async
+// copies (cp.async.bulk, TMA 1-D: one copy for A, one for D per stage)
+// completing on mbarriers.  Each thread runs CPT independent sequential chains.
 //
 // Epilogue (sub_b != 0): Y = acc - b (block_cg.hpp:132-138 / :236-241
 // `r[row] -= b[row]`), used for R0 = A X0 - b, the periodic residual
 // recomputation and the final true residual (solvers.hpp:188-210).
 template <int P, int CPT, int BR, int T, int S>
-__global__ void __launch_bounds__(BR*(P / CPT))
-    ad_exact_kernel(const double* __restrict__ At, int ld, int n, int n_loc, int row0,
+__global__ void __launch_bounds__(32 + BR*(P / CPT))
+    ad_exact_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
                     const double* __restrict__ b, int p, const int* __restrict__ stop) {
+    constexpr int kConsumerWarps = BR * (P / CPT) / 32;
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);
     double* Ds = As + S * T * BR;
     uint64_t* full = reinterpret_cast<uint64_t*>(Ds + S * T * P);
+    uint64_t* empty = full + S;
 
-    const int tid = threadIdx.x;
-    const int r = tid % BR;
-    const int g = tid / BR;
-    const int warp = tid >> 5, lane = tid & 31;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int i0 = blockIdx.x * BR;
     const int ntiles = (n + T - 1) / T;
+    const double* panel = Ap + static_cast<size_t>(blockIdx.x) * n * BR;
 
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
         fence_mbar_init();
     }
     __syncthreads();
 
-    auto issue = [&](int t) {
-        const int s = t % S;
-        const int k0 = t * T;
-        const int rows = min(T, n - k0);
-        if (lane == 0)
-            mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
-        __syncwarp();
-        for (int kk = lane; kk < rows; kk += 32)
-            bulk_g2s(As + (s * T + kk) * BR, At + static_cast<size_t>(k0 + kk) * ld + i0, BR * 8u,
-                     &full[s]);
-        if (lane == 0)
-            bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
-                     &full[s]);
-    };
-
     if (warp == 0) {
-        for (int t = 0; t < S - 1 && t < ntiles; ++t) issue(t);
+        // Producer: one lane streams the A panel tiles and the D tiles.
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = 0; t < ntiles; ++t) {
+                if (t >= S) mbar_wait(&empty[s], ph ^ 1u);
+                const int k0 = t * T;
+                const int rows = min(T, n - k0);
+                mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
+                bulk_g2s(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
+                         static_cast<uint32_t>(rows) * BR * 8u, &full[s]);
+                bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
+                         &full[s]);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
     }
 
+    const int tid = threadIdx.x - 32;
+    const int r = tid % BR;
+    const int g = tid / BR;
     double acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
 
+    int s = 0;
+    uint32_t phase = 0;
     for (int t = 0; t < ntiles; ++t) {
-        const int s = t % S;
-        if (warp == 0 && t + S - 1 < ntiles) issue(t + S - 1);
-        mbar_wait(&full[s], static_cast<uint32_t>(t / S) & 1u);
+        mbar_wait(&full[s], phase);
         const double* a_t = As + s * T * BR + r;
         const double* d_t = Ds + s * T * P + g * CPT;
         const int rows = min(T, n - t * T);
         if (rows == T) {
-#pragma unroll 4
-            for (int kk = 0; kk < T; ++kk) {
-                const double a = a_t[kk * BR];
-                const double2* d2 = reinterpret_cast<const double2*>(d_t + kk * P);
+            // Register software pipeline: the products of a batch of U k-steps
+            // are formed, the next batch's shared-memory loads are issued, and
+            // only then the dependent DADD chains run (k ascending per column).
+            constexpr int U = (CPT >= 8) ? 2 : 4;
+            static_assert(T % U == 0, "T must be a multiple of U");
+            double av[U];
+            double2 dv[U][CPT / 2];
 #pragma unroll
-                for (int c = 0; c < CPT / 2; ++c) {
-                    const double2 dv = d2[c];
-                    acc[2 * c] = mac_exact(acc[2 * c], a, dv.x);
-                    acc[2 * c + 1] = mac_exact(acc[2 * c + 1], a, dv.y);
+            for (int u = 0; u < U; ++u) {
+                av[u] = a_t[u * BR];
+#pragma unroll
+                for (int c = 0; c < CPT / 2; ++c) dv[u][c] = reinterpret_cast<const double2*>(d_t + u * P)[c];
+            }
+#pragma unroll
+            for (int kb = 0; kb < T; kb += U) {
+                double prod[U][CPT];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int c = 0; c < CPT / 2; ++c) {
+                        prod[u][2 * c] = __dmul_rn(av[u], dv[u][c].x);
+                        prod[u][2 * c + 1] = __dmul_rn(av[u], dv[u][c].y);
+                    }
+                if (kb + U < T) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        av[u] = a_t[(kb + U + u) * BR];
+#pragma unroll
+                        for (int c = 0; c < CPT / 2; ++c)
+                            dv[u][c] = reinterpret_cast<const double2*>(d_t + (kb + U + u) * P)[c];
+                    }
                 }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) acc[c] = __dadd_rn(acc[c], prod[u][c]);
             }
         } else {
             for (int kk = 0; kk < rows; ++kk) {
@@ -109,7 +146,12 @@ __global__ void __launch_bounds__(BR*(P / CPT))
                 }
             }
         }
-        __syncthreads();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) {
+            s = 0;
+            phase ^= 1u;
+        }
     }
 
     const int il = i0 + r;
@@ -130,58 +172,110 @@ __global__ void __launch_bounds__(BR*(P / CPT))
 // ---------------------------------------------------------------------------
 // (2) Sequential dot-product chains: Gram rows, step right-hand sides and
 // norms (block_cg.hpp:153-160, :214-216, :262-264, :275-276; kernels.hpp:20-26).
-// Each chain is one thread walking k = 0..n-1 in order; tiles of T rows of
-// up to three n x P row-major source blocks stream through a double-buffered
-// shared-memory ring (bulk async copies).  64 chains per CTA keeps the
-// per-step shared-memory traffic under the 9-cycle DADD latency.
-template <int T>
-__global__ void __launch_bounds__(64)
+// Each chain is one thread walking k = 0..n-1 in order (a DADD latency chain,
+// ~9 cycles per step).  Tiles of T rows of up to three n x P row-major source
+// blocks stream through an S-stage shared-memory ring (bulk async copies) so
+// S-1 tiles are in flight while the chains consume one.  64 chains per CTA
+// keeps the per-step shared-memory traffic under the DADD latency.
+//
+// Warp-specialised: warp 0 is the producer (one lane issues the bulk copies,
+// waiting on per-stage "empty" barriers); warps 1..W consume, one chain per
+// thread, and release each stage with one arrive per warp.
+template <int P, int T, int S>
+__global__ void __launch_bounds__(96)
     chain_kernel(const double* __restrict__ s0, const double* __restrict__ s1,
-                 const double* __restrict__ s2, int nsrc, int n, int P,
+                 const double* __restrict__ s2, int nsrc, int n,
                  const ChainDesc* __restrict__ descs, int nchains, double* __restrict__ out,
                  const int* __restrict__ stop) {
+    static_assert(T % 16 == 0, "tile rows must be a multiple of the batch");
+    constexpr int kConsumerWarps = 2;
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* buf = reinterpret_cast<double*>(smem_raw);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(buf + 2 * nsrc * T * P);
+    uint64_t* full = reinterpret_cast<uint64_t*>(buf + static_cast<size_t>(S) * nsrc * T * P);
+    uint64_t* empty = full + S;
     const int tid = threadIdx.x;
-    const int c = blockIdx.x * blockDim.x + tid;
-    const bool active = c < nchains;
-    ChainDesc d{0, 0, 0, 0, 0, 0, 0};
-    if (active) d = descs[c];
-    const double* srcs[3] = {s0, s1, s2};
+    const int warp = tid >> 5, lane = tid & 31;
     const int ntiles = (n + T - 1) / T;
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
         fence_mbar_init();
     }
     __syncthreads();
-    auto issue = [&](int t) {
-        if (tid == 0) {
-            const int rows = min(T, n - t * T);
-            const uint32_t bytes = static_cast<uint32_t>(rows) * P * 8u;
-            mbar_arrive_expect_tx(&bar[t & 1], bytes * nsrc);
-            for (int s = 0; s < nsrc; ++s)
-                bulk_g2s(buf + ((t & 1) * nsrc + s) * T * P, srcs[s] + static_cast<size_t>(t) * T * P, bytes,
-                         &bar[t & 1]);
+    if (warp == 0) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = 0; t < ntiles; ++t) {
+                if (t >= S) mbar_wait(&empty[s], ph ^ 1u);
+                const int rows = min(T, n - t * T);
+                const uint32_t bytes = static_cast<uint32_t>(rows) * P * 8u;
+                mbar_arrive_expect_tx(&full[s], bytes * nsrc);
+                double* dst = buf + static_cast<size_t>(s) * nsrc * T * P;
+                bulk_g2s(dst, s0 + static_cast<size_t>(t) * T * P, bytes, &full[s]);
+                if (nsrc > 1) bulk_g2s(dst + T * P, s1 + static_cast<size_t>(t) * T * P, bytes, &full[s]);
+                if (nsrc > 2) bulk_g2s(dst + 2 * T * P, s2 + static_cast<size_t>(t) * T * P, bytes, &full[s]);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
         }
-    };
-    issue(0);
+        return;
+    }
+    const int c = blockIdx.x * (kConsumerWarps * 32) + (tid - 32);
+    const bool active = c < nchains;
+    ChainDesc d{0, 0, 0, 0, 0, 0, 0};
+    if (active) d = descs[c];
     double acc = 0.0;
+    const int xoff = d.sx * T * P + d.a;
+    const int yoff = d.sy * T * P + d.b;
+    int s = 0;
+    uint32_t phase = 0;
     for (int t = 0; t < ntiles; ++t) {
-        if (t + 1 < ntiles) issue(t + 1);
-        mbar_wait(&bar[t & 1], static_cast<uint32_t>(t >> 1) & 1u);
-        const double* xs = buf + ((t & 1) * nsrc + d.sx) * T * P + d.a;
-        const double* ys = buf + ((t & 1) * nsrc + d.sy) * T * P + d.b;
-        const int rows = min(T, n - t * T);
-        if (rows == T) {
-#pragma unroll 16
-            for (int kk = 0; kk < T; ++kk) acc = mac_exact(acc, xs[kk * P], ys[kk * P]);
+        mbar_wait(&full[s], phase);
+        const double* base = buf + static_cast<size_t>(s) * nsrc * T * P;
+        const double* xs = base + xoff;
+        const double* ys = base + yoff;
+        if (t * T + T <= n) {
+            // Batches of 16 products; the next batch's loads are in flight
+            // while this batch's 16 dependent DADDs retire (k ascending).
+            constexpr int U = 16;
+            double xv[U], yv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                xv[u] = xs[u * P];
+                yv[u] = ys[u * P];
+            }
+#pragma unroll
+            for (int kb = 0; kb < T; kb += U) {
+                double prod[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) prod[u] = __dmul_rn(xv[u], yv[u]);
+                if (kb + U < T) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        xv[u] = xs[(kb + U + u) * P];
+                        yv[u] = ys[(kb + U + u) * P];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, prod[u]);
+            }
         } else {
+            const int rows = n - t * T;
             for (int kk = 0; kk < rows; ++kk) acc = mac_exact(acc, xs[kk * P], ys[kk * P]);
         }
-        __syncthreads();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) {
+            s = 0;
+            phase ^= 1u;
+        }
     }
     if (active) out[d.out] = d.neg ? -acc : acc;
 }
@@ -253,8 +347,9 @@ __device__ bool warp_lu_factor(WarpLU& w, int* perm, int p, double floor) {
     return true;
 }
 
-// Lane `lane` solves L U x = P rhs for its own right-hand side.
-__device__ void warp_lu_solve_row(WarpLU& w, const int* perm, int p, const double* rhs, double* xout) {
+// Lane `lane` solves L U x = P rhs for its own right-hand side; writes the
+// p solution entries to xout and zeroes xout[p..P).
+__device__ void warp_lu_solve_row(WarpLU& w, const int* perm, int p, int P, const double* rhs, double* xout) {
     const int i_ = threadIdx.x & 31;
     if (i_ >= p) return;
     double* y = w.y[i_];
@@ -269,7 +364,7 @@ __device__ void warp_lu_solve_row(WarpLU& w, const int* perm, int p, const doubl
         for (int j = i + 1; j < p; ++j) acc = msub_exact(acc, w.m[i][j], x[j]);
         x[i] = __ddiv_rn(acc, w.m[i][i]);
     }
-    for (int j = 0; j < p; ++j) xout[j] = x[j];
+    for (int j = 0; j < P; ++j) xout[j] = (j < p) ? x[j] : 0.0;
 }
 
 // stage_gram_finalize + stage_alpha (block_cg.hpp:165-218), one warp.
@@ -316,11 +411,7 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
         return;
     }
     __syncwarp();
-    double xr[kMaxP];
-    if (lane < p) {
-        warp_lu_solve_row(w, perm, p, small + L.rhs_a() + lane * P, xr);
-        for (int j = 0; j < P; ++j) small[L.alpha() + lane * P + j] = (j < p) ? xr[j] : 0.0;
-    }
+    if (lane < p) warp_lu_solve_row(w, perm, p, P, small + L.rhs_a() + lane * P, small + L.alpha() + lane * P);
     // Keep the factorisation for the beta solve (same M, same pivots).
     for (int idx = lane; idx < p * p; idx += 32) ctl->lu[idx] = w.m[idx / p][idx % p];
     if (lane < p) ctl->perm[lane] = perm[lane];
@@ -342,10 +433,8 @@ __global__ void __launch_bounds__(32)
     for (int idx = lane; idx < p * p; idx += 32) w.m[idx / p][idx % p] = ctl->lu[idx];
     if (lane < p) perm[lane] = ctl->perm[lane];
     __syncwarp();
-    double xr[kMaxP];
     if (lane < p) {
-        warp_lu_solve_row(w, perm, p, small + L.rhs_b() + lane * P, xr);
-        for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? xr[j] : 0.0;
+        warp_lu_solve_row(w, perm, p, P, small + L.rhs_b() + lane * P, small + L.beta() + lane * P);
         norms[lane] = __dsqrt_rn(small[L.nsq_r() + lane]);
         small[L.norm() + lane] = norms[lane];
     }
@@ -566,19 +655,34 @@ __global__ void __launch_bounds__(1024)
     __shared__ int xcol[kMaxP], ycol[kMaxP];
     const int tid = threadIdx.x;
     const int npairs = p * (p + 1) / 2;
-    // 1. fixed-order reduction of the partial Grams
-    for (int q = tid; q < npairs; q += blockDim.x) {
+    // 1. fixed-order reduction of the partial Grams: `lanes_per_pair` threads
+    // sum strided subsets of the CTA partials, combined in a fixed order.
+    {
+        __shared__ double red[1024];
+        const int lpp = max(1, min(32, static_cast<int>(blockDim.x) / max(npairs, 1)));
+        const int q = tid / lpp, sub = tid % lpp;
         double s = 0.0;
-        for (int b = 0; b < nparts; ++b) s += partials[static_cast<size_t>(b) * npairs + q];
-        int t = q, i = 0;
-        while (t >= p - i) {
-            t -= p - i;
-            ++i;
+        if (q < npairs)
+            for (int b = sub; b < nparts; b += lpp) s += partials[static_cast<size_t>(b) * npairs + q];
+        red[tid] = s;
+        __syncthreads();
+        for (int qq = tid; qq < npairs; qq += blockDim.x) {
+            double tot = 0.0;
+            if (lpp * npairs <= static_cast<int>(blockDim.x)) {
+                for (int j = 0; j < lpp; ++j) tot += red[qq * lpp + j];
+            } else {
+                for (int b = 0; b < nparts; ++b) tot += partials[static_cast<size_t>(b) * npairs + qq];
+            }
+            int t = qq, i = 0;
+            while (t >= p - i) {
+                t -= p - i;
+                ++i;
+            }
+            rs.g[i][i + t] = tot;
+            rs.g[i + t][i] = tot;
         }
-        rs.g[i][i + t] = s;
-        rs.g[i + t][i] = s;
+        __syncthreads();
     }
-    __syncthreads();
     // 2. certificate on warp 0
     if (tid < 32) {
         const int lane = tid;
@@ -591,8 +695,11 @@ __global__ void __launch_bounds__(1024)
             if (j == 0 || dj > dmax) dmax = dj;
         }
         if (good) {
+            // sqrt(g_ii) * sqrt(g_jj): the product g_ii * g_jj underflows in the
+            // post-convergence tail (entries ~1e-80, Gram ~1e-160).
             if (lane < p)
-                for (int j = 0; j < p; ++j) rs.l[lane][j] = rs.g[lane][j] / sqrt(rs.g[lane][lane] * rs.g[j][j]);
+                for (int j = 0; j < p; ++j)
+                    rs.l[lane][j] = rs.g[lane][j] / (sqrt(rs.g[lane][lane]) * sqrt(rs.g[j][j]));
             __syncwarp();
             // Cholesky, lane owns row
             for (int k = 0; k < p && good; ++k) {
@@ -629,8 +736,12 @@ __global__ void __launch_bounds__(1024)
             if (good) {
                 const double lam_lower = 1.0 / fro;
                 const double tol = ctl->rank_rel_tol;
-                const double thr = fmax(1e-6, tol * tol * 1e6);
-                good = isfinite(lam_lower) && lam_lower > 1e-6 && lam_lower * (dmin / dmax) > thr;
+                // Every MGS pivot^2 >= lambda_min(G^) * min_j G_jj and the first
+                // pivot^2 = max_j G_jj; MGS accepts while pivot^2 > tol^2 * first.
+                // Demand lambda_lower(G^) > 1e-6 (well above the ~n*eps error of
+                // the reordered Gram) and a 1e4 margin over tol^2.
+                good = isfinite(lam_lower) && lam_lower > 1e-6 &&
+                       lam_lower * (dmin / dmax) > tol * tol * 1e4 && dmin > 1e-280;
             }
         }
         if (lane == 0) rs.ok = good ? 1 : 0;
@@ -821,9 +932,9 @@ __global__ void rowmajor_to_colmajor_kernel(const double* __restrict__ src, doub
         dst[e] = src[k * P + j];
     }
 }
-// rows [c0, c0+rows) of a row-major n-wide matrix (staging) -> At[k][c0+i].
-__global__ void transpose_rows_kernel(const double* __restrict__ stage, int rows, int n, double* __restrict__ At,
-                                      int ld, int c0) {
+// rows [c0, c0+rows) of a row-major n-wide matrix (staging) -> panels.
+__global__ void transpose_rows_kernel(const double* __restrict__ stage, int rows, int n, double* __restrict__ Ap,
+                                      int brs, int c0) {
     __shared__ double tile[32][33];
     const int bx = blockIdx.x * 32;  // k
     const int by = blockIdx.y * 32;  // local row
@@ -834,17 +945,17 @@ __global__ void transpose_rows_kernel(const double* __restrict__ stage, int rows
     __syncthreads();
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
         const int k = bx + yy, i = by + threadIdx.x;
-        if (k < n && i < rows) At[static_cast<size_t>(k) * ld + c0 + i] = tile[threadIdx.x][yy];
+        if (k < n && i < rows) Ap[ap_idx(n, brs, k, c0 + i)] = tile[threadIdx.x][yy];
     }
 }
-__global__ void untranspose_rows_kernel(const double* __restrict__ At, int ld, int c0, int rows, int n,
+__global__ void untranspose_rows_kernel(const double* __restrict__ Ap, int brs, int c0, int rows, int n,
                                         double* __restrict__ stage) {
     __shared__ double tile[32][33];
     const int bx = blockIdx.x * 32;  // k
     const int by = blockIdx.y * 32;  // local row
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
         const int k = bx + yy, i = by + threadIdx.x;
-        tile[yy][threadIdx.x] = (k < n && i < rows) ? At[static_cast<size_t>(k) * ld + c0 + i] : 0.0;
+        tile[yy][threadIdx.x] = (k < n && i < rows) ? Ap[ap_idx(n, brs, k, c0 + i)] : 0.0;
     }
     __syncthreads();
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {

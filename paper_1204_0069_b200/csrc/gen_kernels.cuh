@@ -5,8 +5,8 @@
 // streams (coopcg/rng.hpp:16-20, :35-48, :80-87).  Every value is a pure
 // function of (seed, element index) or a sequential chain with the
 // specified order, so the GPU bytes equal the host oracle's bytes
-// (tests/test_gen.py).  A is written in the k-major device layout
-// At[k][i - row0] = A(i, k) for the context's rows i.
+// (tests/test_gpu_parity.py).  A is written in the panel layout of
+// common.cuh (ap_idx) for the context's rows.
 #pragma once
 #include "common.cuh"
 
@@ -30,39 +30,42 @@ __device__ __forceinline__ double uniform_pm1_dev(uint64_t key, uint64_t c) {
 
 // Off-diagonal entries of the diagonally dominant matrix: A_ij = A_ji =
 // (B_lo,hi + B_hi,lo) / 2 with B_ij ~ U[-1,1] at counter i*n + j + 1.
-__global__ void gen_dd_offdiag_kernel(double* __restrict__ At, int ld, int n, int n_loc, int row0, uint64_t key) {
-    const size_t total = static_cast<size_t>(n) * n_loc;
+__global__ void gen_dd_offdiag_kernel(double* __restrict__ Ap, int brs, int n, int n_loc, int row0, uint64_t key,
+                                      size_t total) {
+    const int BR = 1 << brs;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int il = static_cast<int>(e % n_loc);
-        const uint64_t k = e / n_loc;
-        const uint64_t i = static_cast<uint64_t>(row0 + il);
+        const size_t panel = e / (static_cast<size_t>(n) << brs);
+        const size_t rem = e - panel * (static_cast<size_t>(n) << brs);
+        const uint64_t k = rem >> brs;
+        const int il = static_cast<int>(panel * BR + (rem & (BR - 1)));
         double v = 0.0;
-        if (k != i) {
+        const uint64_t i = static_cast<uint64_t>(row0 + il);
+        if (il < n_loc && k != i) {
             const uint64_t lo = k < i ? k : i, hi = k < i ? i : k;
             const uint64_t un = static_cast<uint64_t>(n);
             const double u1 = uniform_pm1_dev(key, lo * un + hi + 1);
             const double u2 = uniform_pm1_dev(key, hi * un + lo + 1);
             v = __dmul_rn(__dadd_rn(u1, u2), 0.5);
         }
-        At[k * ld + il] = v;
+        Ap[e] = v;
     }
 }
 
 // Diagonal: A_ii = (sum_{j != i, ascending} |A_ij|) + 1.  One chain per row,
-// reading At[j][i] (coalesced across consecutive rows).
-__global__ void gen_dd_diag_kernel(double* __restrict__ At, int ld, int n, int n_loc, int row0) {
+// reading the row's panel column (coalesced across consecutive rows).
+__global__ void gen_dd_diag_kernel(double* __restrict__ Ap, int brs, int n, int n_loc, int row0) {
     const int il = blockIdx.x * blockDim.x + threadIdx.x;
     if (il >= n_loc) return;
     const int i = row0 + il;
     double acc = 0.0;
-    const double* col = At + il;
+    const double* col = Ap + ap_idx(n, brs, 0, il);
 #pragma unroll 8
     for (int j = 0; j < n; ++j) {
-        const double a = fabs(col[static_cast<size_t>(j) * ld]);
+        const double a = fabs(col[static_cast<size_t>(j) << brs]);
         if (j != i) acc = __dadd_rn(acc, a);
     }
-    At[static_cast<size_t>(i) * ld + il] = __dadd_rn(acc, 1.0);
+    Ap[ap_idx(n, brs, i, il)] = __dadd_rn(acc, 1.0);
 }
 
 // Householder construction (single-GPU contexts hold the full matrix):
@@ -70,23 +73,26 @@ __global__ void gen_dd_diag_kernel(double* __restrict__ At, int ld, int n, int n
 //   s = v.v, w = M v, c = v.w, t1 = 2/s, t2 = (4 c)/(s s),
 //   M_ij <- (M_ij - t1 (v_i w_j + w_i v_j)) + t2 (v_i v_j)
 // (every sum sequential ascending, one rounding per op).
-__global__ void hh_init_kernel(double* __restrict__ At, int ld, int n, const double* __restrict__ lambda) {
-    const size_t total = static_cast<size_t>(n) * ld;
+__global__ void hh_init_kernel(double* __restrict__ Ap, int brs, int n, const double* __restrict__ lambda,
+                               size_t total) {
+    const int BR = 1 << brs;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t k = e / ld;
-        const size_t i = e % ld;
-        At[e] = (i == k) ? lambda[i] : 0.0;
+        const size_t panel = e / (static_cast<size_t>(n) << brs);
+        const size_t rem = e - panel * (static_cast<size_t>(n) << brs);
+        const size_t k = rem >> brs;
+        const size_t i = panel * BR + (rem & (BR - 1));
+        Ap[e] = (i == k && i < static_cast<size_t>(n)) ? lambda[i] : 0.0;
     }
 }
-__global__ void hh_w_kernel(const double* __restrict__ At, int ld, int n, const double* __restrict__ v,
+__global__ void hh_w_kernel(const double* __restrict__ Ap, int brs, int n, const double* __restrict__ v,
                             double* __restrict__ w) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc = 0.0;
-    const double* col = At + i;
+    const double* col = Ap + ap_idx(n, brs, 0, i);
 #pragma unroll 8
-    for (int k = 0; k < n; ++k) acc = mac_exact(acc, col[static_cast<size_t>(k) * ld], v[k]);
+    for (int k = 0; k < n; ++k) acc = mac_exact(acc, col[static_cast<size_t>(k) << brs], v[k]);
     w[i] = acc;
 }
 __global__ void hh_scalars_kernel(int n, const double* __restrict__ v, const double* __restrict__ w,
@@ -98,19 +104,21 @@ __global__ void hh_scalars_kernel(int n, const double* __restrict__ v, const dou
     t12[0] = __ddiv_rn(2.0, s);
     t12[1] = __ddiv_rn(__dmul_rn(4.0, c), __dmul_rn(s, s));
 }
-__global__ void hh_update_kernel(double* __restrict__ At, int ld, int n, const double* __restrict__ v,
-                                 const double* __restrict__ w, const double* __restrict__ t12) {
+__global__ void hh_update_kernel(double* __restrict__ Ap, int brs, int n, const double* __restrict__ v,
+                                 const double* __restrict__ w, const double* __restrict__ t12, size_t total) {
     const double t1 = t12[0], t2 = t12[1];
-    const size_t total = static_cast<size_t>(n) * ld;
+    const int BR = 1 << brs;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int k = static_cast<int>(e / ld);
-        const int i = static_cast<int>(e % ld);
+        const size_t panel = e / (static_cast<size_t>(n) << brs);
+        const size_t rem = e - panel * (static_cast<size_t>(n) << brs);
+        const int k = static_cast<int>(rem >> brs);
+        const int i = static_cast<int>(panel * BR + (rem & (BR - 1)));
         if (i >= n) continue;
         // element (i, k); the expression is symmetric in (i, k) bit for bit.
         const double q = __dadd_rn(__dmul_rn(v[i], w[k]), __dmul_rn(w[i], v[k]));
-        const double m1 = __dsub_rn(At[e], __dmul_rn(t1, q));
-        At[e] = __dadd_rn(m1, __dmul_rn(t2, __dmul_rn(v[i], v[k])));
+        const double m1 = __dsub_rn(Ap[e], __dmul_rn(t1, q));
+        Ap[e] = __dadd_rn(m1, __dmul_rn(t2, __dmul_rn(v[i], v[k])));
     }
 }
 

@@ -1,0 +1,65 @@
+// Sweep ad_exact_kernel configurations at the cfg-2 shape (n=16384, P=8) and
+// others: time per launch (CUDA events, A = 2.15 GB > L2).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../../paper_1204_0069_b200/csrc -o ad_probe ad_probe.cu
+#include <cstdio>
+#include "exact_kernels.cuh"
+
+using namespace coopcg_gpu;
+
+template <int P, int CPT, int BR, int T, int S>
+void run(const double* Ap, int n, const double* D, double* Y, int p) {
+    auto k = ad_exact_kernel<P, CPT, BR, T, S>;
+    size_t smem = (size_t)S * T * (BR + P) * 8 + 2 * S * 8;
+    if (smem > 227 * 1024) return;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    dim3 grid((n + BR - 1) / BR), block(32 + BR * (P / CPT));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k<<<grid, block, smem>>>(Ap, n, n, 0, D, Y, nullptr, p, nullptr);
+    cudaEventRecord(e0);
+    const int reps = 5;
+    for (int r = 0; r < reps; ++r) k<<<grid, block, smem>>>(Ap, n, n, 0, D, Y, nullptr, p, nullptr);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= reps;
+    cudaError_t e = cudaGetLastError();
+    std::printf("n=%6d P=%2d CPT=%d BR=%3d T=%3d S=%d smem=%6zu : %8.3f ms  %7.1f GB/s  %5.2f TF/s %s\n", n, P, CPT, BR,
+                T, S, smem, ms, 8.0 * n * n / (ms * 1e-3) / 1e9, 2.0 * n * n * p / (ms * 1e-3) / 1e12,
+                e == cudaSuccess ? "" : cudaGetErrorString(e));
+}
+
+int main(int argc, char** argv) {
+    const int n = 16384;
+    double *Ap, *D, *Y;
+    cudaMalloc(&Ap, (size_t)n * n * 8 + (size_t)128 * n * 8);
+    cudaMalloc(&D, (size_t)n * 32 * 8);
+    cudaMalloc(&Y, (size_t)n * 32 * 8);
+    cudaMemset(Ap, 0, (size_t)n * n * 8);
+    cudaMemset(D, 0, (size_t)n * 32 * 8);
+    // P = 8 (cfg 2)
+    run<8, 8, 64, 32, 4>(Ap, n, D, Y, 8);
+    run<8, 4, 64, 32, 4>(Ap, n, D, Y, 8);
+    run<8, 2, 64, 32, 4>(Ap, n, D, Y, 8);
+    run<8, 4, 32, 32, 4>(Ap, n, D, Y, 8);
+    run<8, 8, 32, 32, 4>(Ap, n, D, Y, 8);
+    run<8, 4, 128, 32, 4>(Ap, n, D, Y, 8);
+    run<8, 2, 128, 32, 4>(Ap, n, D, Y, 8);
+    run<8, 4, 64, 64, 4>(Ap, n, D, Y, 8);
+    run<8, 4, 64, 16, 6>(Ap, n, D, Y, 8);
+    run<8, 4, 64, 32, 8>(Ap, n, D, Y, 8);
+    run<8, 2, 64, 32, 6>(Ap, n, D, Y, 8);
+    run<8, 2, 32, 64, 4>(Ap, n, D, Y, 8);
+    // P = 4 / 16 / 32 at the same n (per-byte behaviour)
+    run<4, 2, 64, 32, 4>(Ap, n, D, Y, 4);
+    run<4, 4, 64, 32, 4>(Ap, n, D, Y, 4);
+    run<16, 8, 64, 32, 4>(Ap, n, D, Y, 16);
+    run<16, 4, 64, 32, 4>(Ap, n, D, Y, 16);
+    run<16, 8, 128, 32, 4>(Ap, n, D, Y, 16);
+    run<32, 8, 64, 32, 4>(Ap, n, D, Y, 32);
+    run<32, 8, 128, 32, 3>(Ap, n, D, Y, 32);
+    run<32, 4, 64, 32, 4>(Ap, n, D, Y, 32);
+    return 0;
+}
