@@ -69,6 +69,39 @@ __host__ __device__ __forceinline__ size_t ap_idx(int n, int brs, int k, int il)
     return ((static_cast<size_t>(il >> brs) * n + k) << brs) | static_cast<size_t>(il & ((1 << brs) - 1));
 }
 
+// Which device layout a context uses for A: exact contexts use the panel
+// layout above; fast contexts use [r][kk] tiles (fast_kernels.cuh).
+struct ALay {
+    int fast;    // 0 panels (BR = 1 << brs), 1 fast tiles (64 x 36)
+    int brs;
+    int ntiles;  // fast: ceil(n / 36)
+};
+constexpr int kFastBRc = 64, kFastTc = 36;
+__host__ __device__ __forceinline__ size_t a_idx(const ALay& L, int n, int k, int il) {
+    if (!L.fast) return ap_idx(n, L.brs, k, il);
+    const int q = il / kFastBRc, r = il % kFastBRc, t = k / kFastTc, kk = k % kFastTc;
+    return ((static_cast<size_t>(q) * L.ntiles + t) * kFastBRc + r) * kFastTc + kk;
+}
+// storage index -> (k, il); the caller checks k < n and il < n_loc.
+__host__ __device__ __forceinline__ void a_decode(const ALay& L, int n, size_t e, int& k, int& il) {
+    if (!L.fast) {
+        const int BR = 1 << L.brs;
+        const size_t per = static_cast<size_t>(n) << L.brs;
+        const size_t panel = e / per, rem = e - panel * per;
+        k = static_cast<int>(rem >> L.brs);
+        il = static_cast<int>(panel * BR + (rem & (BR - 1)));
+    } else {
+        const int kk = static_cast<int>(e % kFastTc);
+        const size_t rest = e / kFastTc;
+        const int r = static_cast<int>(rest % kFastBRc);
+        const size_t rest2 = rest / kFastBRc;
+        const int t = static_cast<int>(rest2 % L.ntiles);
+        const size_t q = rest2 / L.ntiles;
+        k = t * kFastTc + kk;
+        il = static_cast<int>(q * kFastBRc + r);
+    }
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -112,6 +145,43 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
+}
+
+// Fixed-order reduction of per-CTA partial vectors inside one CTA:
+//   out[o] = sum_b part[b * stride + off + o * ostride],  o < nout.
+// lpp threads per output each sum a strided subset with 8 independent loads in
+// flight, then the lpp sub-sums are added in a fixed order (deterministic).
+// `red` needs blockDim.x doubles of shared memory; all threads must call.
+__device__ inline void cta_reduce_fixed(const double* __restrict__ part, int nparts, size_t stride, int off,
+                                        int ostride, int nout, double* out, double* red) {
+    const int nt = blockDim.x, tid = threadIdx.x;
+    int lpp = nt / (nout > 0 ? nout : 1);
+    lpp = lpp < 1 ? 1 : (lpp > 32 ? 32 : lpp);
+    const int per_pass = nt / lpp;
+    for (int base = 0; base < nout; base += per_pass) {
+        const int o = base + tid / lpp, sub = tid % lpp;
+        double s = 0.0;
+        if (tid / lpp < per_pass && o < nout) {
+            const double* src = part + off + static_cast<size_t>(o) * ostride;
+            int b = sub;
+            for (; b + 7 * lpp < nparts; b += 8 * lpp) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = src[static_cast<size_t>(b + u * lpp) * stride];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) s += v[u];
+            }
+            for (; b < nparts; b += lpp) s += src[static_cast<size_t>(b) * stride];
+        }
+        red[tid] = s;
+        __syncthreads();
+        if (tid < per_pass && base + tid < nout) {
+            double t = 0.0;
+            for (int j = 0; j < lpp; ++j) t += red[tid * lpp + j];
+            out[base + tid] = t;
+        }
+        __syncthreads();
+    }
 }
 
 // Exact reference arithmetic: one rounding per operation, no contraction.

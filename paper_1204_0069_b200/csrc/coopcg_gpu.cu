@@ -25,6 +25,7 @@
 #include "common.cuh"
 #include "exact_kernels.cuh"
 #include "gen_kernels.cuh"
+#include "fast_kernels.cuh"
 
 using namespace coopcg_gpu;
 
@@ -52,6 +53,12 @@ struct coopcg_gpu_ctx {
     int n = 0, p = 0, P = 0, device = 0, arith = 0;
     int row0 = 0, row1 = 0, n_loc = 0, brs = 6, npanels = 0;
     size_t ap_elems = 0;
+    ALay lay{0, 6, 0};
+    // fast mode work decomposition (ad_fast_kernel): units = panels x kchunks
+    int f_kchunks = 1, f_tpc = 1, f_units = 0, f_grid = 0, f_rgrid = 0, f_ugrid = 0;
+    double* qpart = nullptr;     // kchunks x n_loc x P
+    double* gpart = nullptr;     // rgrid x 4 P^2 (row-pass Gram partials)
+    double* npart = nullptr;     // ugrid x P (norm partials)
     bool a_ready = false, inputs_ready = false;
     cudaStream_t stream = nullptr;
     std::string msg;
@@ -162,6 +169,71 @@ cudaError_t ad_launch(coopcg_gpu_ctx* ctx, const double* src, double* dst, const
     }
 }
 
+// ---- fast-mode launchers ------------------------------------------------------
+template <int P>
+size_t fast_ad_smem() {
+    return (size_t)kFastS * (kFastBR * kFastT + kFastT * P) * sizeof(double) + 2 * kFastS * sizeof(uint64_t);
+}
+template <int P>
+cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
+    auto kern = ad_fast_kernel<P>;
+    static bool attr_done[64] = {};
+    const int dev = ctx->device & 63;
+    if (!attr_done[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_ad_smem<P>());
+        if (e != cudaSuccess) return e;
+        attr_done[dev] = true;
+    }
+    kern<<<ctx->f_grid, 96, fast_ad_smem<P>(), ctx->stream>>>(ctx->At, ctx->n, ctx->n_loc, ctx->lay.ntiles, src,
+                                                              ctx->qpart, ctx->f_kchunks, ctx->f_tpc, ctx->f_units,
+                                                              stop);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+cudaError_t fast_ad(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
+    switch (ctx->P) {
+    case 8: return fast_ad_t<8>(ctx, src, stop);
+    case 16: return fast_ad_t<16>(ctx, src, stop);
+    default: return fast_ad_t<32>(ctx, src, stop);
+    }
+}
+template <int P>
+cudaError_t fast_rows_t(coopcg_gpu_ctx* ctx, double* dst, const double* b, const double* D, const double* R,
+                        const double* Qfull, int mode, const int* stop) {
+    fast_rows_kernel<P><<<ctx->f_rgrid, 256, 0, ctx->stream>>>(ctx->qpart, ctx->f_kchunks, ctx->n_loc, ctx->row0, dst,
+                                                               b, D, R, Qfull, ctx->p, mode, ctx->gpart, stop);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+cudaError_t fast_rows(coopcg_gpu_ctx* ctx, double* dst, const double* b, const double* D, const double* R,
+                      const double* Qfull, int mode, const int* stop) {
+    switch (ctx->P) {
+    case 8: return fast_rows_t<8>(ctx, dst, b, D, R, Qfull, mode, stop);
+    case 16: return fast_rows_t<16>(ctx, dst, b, D, R, Qfull, mode, stop);
+    default: return fast_rows_t<32>(ctx, dst, b, D, R, Qfull, mode, stop);
+    }
+}
+template <int P>
+cudaError_t fast_update_t(coopcg_gpu_ctx* ctx, const double* D, double* Dn, int mode, const int* stop) {
+    fast_update_kernel<P><<<ctx->f_ugrid, 256, 0, ctx->stream>>>(ctx->X, ctx->R, ctx->Q, D, Dn, ctx->small, ctx->n,
+                                                                 ctx->p, mode, ctx->npart, ctx->partials, stop);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+cudaError_t fast_update(coopcg_gpu_ctx* ctx, const double* D, double* Dn, int mode, const int* stop) {
+    switch (ctx->P) {
+    case 8: return fast_update_t<8>(ctx, D, Dn, mode, stop);
+    case 16: return fast_update_t<16>(ctx, D, Dn, mode, stop);
+    default: return fast_update_t<32>(ctx, D, Dn, mode, stop);
+    }
+}
+cudaError_t fast_solve(coopcg_gpu_ctx* ctx, int mode) {
+    const size_t smem = (size_t)(4 * ctx->P * ctx->P + 1024) * sizeof(double);
+    fast_solve_kernel<<<1, 1024, smem, ctx->stream>>>(ctx->gpart, ctx->f_rgrid, ctx->small, ctx->ctl, mode);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+
 AdConfig pick_ad_config(int n_loc, int P) {
     AdConfig c;
     // Measured sweep (tools/probe/ad_probe.cu, profiles/): T=32, S=4 rings;
@@ -263,6 +335,9 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaFree(ctx->S);
     cudaFree(ctx->V);
     cudaFree(ctx->b);
+    cudaFree(ctx->qpart);
+    cudaFree(ctx->gpart);
+    cudaFree(ctx->npart);
     cudaFree(ctx->small);
     cudaFree(ctx->partials);
     cudaFree(ctx->init_norms);
@@ -325,7 +400,7 @@ double host_normal(uint64_t key, uint64_t t) {
 // =============================================================================
 extern "C" {
 
-const char* coopcg_gpu_version(void) { return "coopcg_gpu 1 sm_100a exact"; }
+const char* coopcg_gpu_version(void) { return "coopcg_gpu 1 sm_100a exact+fast"; }
 
 int coopcg_gpu_last_error(const coopcg_gpu_ctx* ctx, char* buf, size_t len) {
     if (!buf || len == 0) return COOPCG_E_INVALID;
@@ -349,16 +424,50 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     auto* ctx = new coopcg_gpu_ctx();
     ctx->n = n;
     ctx->p = p;
-    ctx->P = pad_cols(p);
+    ctx->P = (arith == COOPCG_ARITH_FAST) ? std::max(8, pad_cols(p)) : pad_cols(p);
     ctx->device = device;
     ctx->arith = arith;
     ctx->row0 = row_begin;
     ctx->row1 = row_end;
     ctx->n_loc = row_end - row_begin;
     ctx->ad = pick_ad_config(ctx->n_loc, ctx->P);
-    ctx->brs = (ctx->ad.BR == 32) ? 5 : 6;
-    ctx->npanels = (ctx->n_loc + ctx->ad.BR - 1) / ctx->ad.BR;
-    ctx->ap_elems = (size_t)ctx->npanels * n * ctx->ad.BR;
+    if (arith == COOPCG_ARITH_FAST) {
+        const int ntiles = (n + kFastT - 1) / kFastT;
+        ctx->npanels = (ctx->n_loc + kFastBR - 1) / kFastBR;
+        ctx->lay = ALay{1, 6, ntiles};
+        ctx->ap_elems = (size_t)ctx->npanels * ntiles * kFastBR * kFastT;
+        // Work units = (panel, k-chunk) on persistent CTAs (2 per SM).  Pick the
+        // k-split with the best wave efficiency units/slots / ceil(units/slots)
+        // (one wave for small n; e.g. n=65536: 1024 panels x 2 = 6.92 waves).
+        const int slots = 2 * 148;
+        int best_k = 1;
+        double best_eff = -1.0;
+        for (int kc = 1; kc <= std::min(16, ntiles); ++kc) {
+            const double w = (double)ctx->npanels * kc / slots;
+            const double eff = w / std::ceil(w);
+            if (eff > best_eff + 1e-3) {
+                best_eff = eff;
+                best_k = kc;
+            }
+        }
+        const int tpc = (ntiles + best_k - 1) / best_k;
+        const int kch = (ntiles + tpc - 1) / tpc;
+        ctx->f_kchunks = kch;
+        ctx->f_tpc = tpc;
+        ctx->f_units = ctx->npanels * kch;
+        ctx->f_grid = std::min(ctx->f_units, slots);
+        // Row / update passes are light; fewer CTAs keep the single-CTA
+        // partial reductions short (~P^2 x grid doubles).
+        const int TR = (256 / ctx->P) * 2;  // (smaller) rows per tile of fast_rows / fast_update
+        const int rg = (ctx->P <= 8) ? 128 : (ctx->P == 16 ? 192 : 296);
+        ctx->f_rgrid = std::min(rg, (ctx->n_loc + TR - 1) / TR);
+        ctx->f_ugrid = std::min(rg, (n + TR - 1) / TR);
+    } else {
+        ctx->brs = (ctx->ad.BR == 32) ? 5 : 6;
+        ctx->npanels = (ctx->n_loc + ctx->ad.BR - 1) / ctx->ad.BR;
+        ctx->lay = ALay{0, ctx->brs, 0};
+        ctx->ap_elems = (size_t)ctx->npanels * n * ctx->ad.BR;
+    }
     auto bail = [&](int code) {
         g_create_error = ctx->msg;
         destroy_impl(ctx);
@@ -387,6 +496,13 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         CKC(cudaMemsetAsync(*bp, 0, sizeof(double) * blk, ctx->stream));
     }
     CKC(cudaMalloc(&ctx->b, sizeof(double) * n));
+    if (arith == COOPCG_ARITH_FAST) {
+        CKC(cudaMalloc(&ctx->qpart, sizeof(double) * (size_t)ctx->f_kchunks * ctx->n_loc * ctx->P));
+        CKC(cudaMalloc(&ctx->gpart, sizeof(double) * (size_t)ctx->f_rgrid * 4 * ctx->P * ctx->P));
+        CKC(cudaMalloc(&ctx->npart, sizeof(double) * (size_t)ctx->f_ugrid * ctx->P));
+        CKC(cudaFuncSetAttribute(fast_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)((4 * 32 * 32 + 1024) * sizeof(double))));
+    }
     const SmallLayout L{ctx->P};
     CKC(cudaMalloc(&ctx->small, sizeof(double) * L.total()));
     CKC(cudaMemsetAsync(ctx->small, 0, sizeof(double) * L.total(), ctx->stream));
@@ -437,7 +553,7 @@ int coopcg_gpu_set_A(coopcg_gpu_ctx* ctx, const double* A_rows) {
         CK(cudaMemcpyAsync(ctx->stage, A_rows + (size_t)r0 * n, sizeof(double) * (size_t)rows * n,
                            cudaMemcpyHostToDevice, ctx->stream));
         dim3 grid((n + 31) / 32, (rows + 31) / 32);
-        transpose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->stage, rows, n, ctx->At, ctx->brs, r0);
+        transpose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->stage, rows, n, ctx->At, ctx->lay, r0);
         CKL();
     }
     CK(cudaStreamSynchronize(ctx->stream));
@@ -454,7 +570,7 @@ int coopcg_gpu_get_A(coopcg_gpu_ctx* ctx, double* A_rows) {
     for (int r0 = 0; r0 < ctx->n_loc; r0 += chunk) {
         const int rows = std::min(chunk, ctx->n_loc - r0);
         dim3 grid((n + 31) / 32, (rows + 31) / 32);
-        untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->brs, r0, rows, n, ctx->stage);
+        untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->lay, r0, rows, n, ctx->stage);
         CKL();
         CK(cudaMemcpyAsync(A_rows + (size_t)r0 * n, ctx->stage, sizeof(double) * (size_t)rows * n,
                            cudaMemcpyDeviceToHost, ctx->stream));
@@ -497,10 +613,10 @@ int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double
     const int n = ctx->n;
     if (kind == COOPCG_MATRIX_DIAGDOM) {
         const uint64_t key = stream_key(seed, 101, (uint64_t)n);
-        gen_dd_offdiag_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->brs, n, ctx->n_loc, ctx->row0, key,
+        gen_dd_offdiag_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, ctx->n_loc, ctx->row0, key,
                                                                  ctx->ap_elems);
         CKL();
-        gen_dd_diag_kernel<<<(ctx->n_loc + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->brs, n, ctx->n_loc,
+        gen_dd_diag_kernel<<<(ctx->n_loc + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->lay, n, ctx->n_loc,
                                                                              ctx->row0);
         CKL();
     } else if (kind == COOPCG_MATRIX_HOUSEHOLDER) {
@@ -515,13 +631,13 @@ int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double
         CK(cudaMalloc(&dt, sizeof(double) * 2));
         CK(cudaMemcpyAsync(dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, ctx->stream));
         CK(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-        hh_init_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->brs, n, dl, ctx->ap_elems);
+        hh_init_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, dl, ctx->ap_elems);
         CKL();
         for (int r = m - 1; r >= 0; --r) {
             const double* v = dV + (size_t)r * n;
-            hh_w_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->brs, n, v, dw);
+            hh_w_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->lay, n, v, dw);
             hh_scalars_kernel<<<1, 32, 0, ctx->stream>>>(n, v, dw, dt);
-            hh_update_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->brs, n, v, dw, dt, ctx->ap_elems);
+            hh_update_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, v, dw, dt, ctx->ap_elems);
             CKL();
         }
         CK(cudaStreamSynchronize(ctx->stream));
@@ -580,20 +696,30 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     const SmallLayout L{P};
 
     ctx->launches = 0;
+    const bool fast = ctx->arith == COOPCG_ARITH_FAST;
     CK(cudaEventRecord(ctx->ev_run0, st));
     // ---- setup: stage_setup + setup_coordinator (solvers.hpp:263-264) ----
-    CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, nullptr));
-    CK(cudaMemcpyAsync(ctx->Dblk[0], ctx->R, sizeof(double) * (size_t)n * P, cudaMemcpyDeviceToDevice, st));
-    CK(chains_launch(ctx, kPhSetup, ctx->R, nullptr, nullptr, 1, nullptr));
-    setup_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->init_norms);
+    const int rows_per_tile = 256 / P;
+    const int dgrid = fast ? ctx->f_ugrid : std::min(ctx->nparts, (n + rows_per_tile - 1) / rows_per_tile);
+    if (!fast) {
+        CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, nullptr));
+        CK(cudaMemcpyAsync(ctx->Dblk[0], ctx->R, sizeof(double) * (size_t)n * P, cudaMemcpyDeviceToDevice, st));
+        CK(chains_launch(ctx, kPhSetup, ctx->R, nullptr, nullptr, 1, nullptr));
+        setup_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->init_norms);
+    } else {
+        CK(fast_ad(ctx, ctx->X, nullptr));
+        CK(fast_rows(ctx, ctx->R, ctx->b, nullptr, nullptr, nullptr, 1, nullptr));
+        CK(cudaMemcpyAsync(ctx->Dblk[0], ctx->R, sizeof(double) * (size_t)n * P, cudaMemcpyDeviceToDevice, st));
+        fast_norms_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->ctl,
+                                            ctx->init_norms, 1, ctx->small);
+    }
     CKL();
     ++ctx->launches;
-    const int rows_per_tile = 256 / P;
-    const int dgrid = std::min(ctx->nparts, (n + rows_per_tile - 1) / rows_per_tile);
     direction_kernel<<<dgrid, 256, 0, st>>>(nullptr, ctx->Dblk[0], nullptr, nullptr, n, p, P, ctx->partials, stop);
     CKL();
     ++ctx->launches;
-    rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[0], ctx->V, n, ctx->ctl, 1);
+    rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[0], ctx->V, n, ctx->ctl, 1,
+                                                   fast ? ctx->small : nullptr);
     CKL();
     ++ctx->launches;
     CK(cudaEventRecord(ctx->ev_loop0, st));
@@ -643,30 +769,56 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
         for (int u = 0; u < U; ++u, ++k_host) {
             double* D = ctx->Dblk[k_host & 1];
             double* Dn = ctx->Dblk[(k_host + 1) & 1];
-            CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2], st));
-            CK(ad_launch(ctx, D, ctx->Q, nullptr, stop));
-            CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1], st));
-            CK(chains_launch(ctx, kPhGram, D, ctx->Q, ctx->R, 3, stop));
-            solve_alpha_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl);
-            CKL();
-    ++ctx->launches;
             const bool recompute = every > 0 && (k_host + 1) % every == 0;  // solvers.hpp:33-35
-            update_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->R, ctx->X, ctx->Q, D, ctx->small, n, p,
-                                                                        P, recompute ? 1 : 0, stop);
+            CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2], st));
+            if (!fast) {
+                CK(ad_launch(ctx, D, ctx->Q, nullptr, stop));
+                CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1], st));
+                CK(chains_launch(ctx, kPhGram, D, ctx->Q, ctx->R, 3, stop));
+                solve_alpha_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl);
+                CKL();
+                ++ctx->launches;
+                update_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->R, ctx->X, ctx->Q, D, ctx->small, n,
+                                                                            p, P, recompute ? 1 : 0, stop);
+                CKL();
+                ++ctx->launches;
+                if (recompute) CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, stop));
+                CK(chains_launch(ctx, kPhBeta, ctx->R, ctx->Q, nullptr, 2, stop));
+                solve_beta_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres,
+                                                    ctx->tr_wall, ctx->tr_capacity);
+                CKL();
+                ++ctx->launches;
+                direction_kernel<<<dgrid, 256, 0, st>>>(ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop);
+                CKL();
+                ++ctx->launches;
+            } else {
+                CK(fast_ad(ctx, D, stop));
+                CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1], st));
+                CK(fast_rows(ctx, ctx->Q, nullptr, D, ctx->R, nullptr, 0, stop));
+                if (!recompute) {
+                    CK(fast_solve(ctx, 0));
+                    CK(fast_update(ctx, D, Dn, 0, stop));
+                    fast_record_kernel<<<1, 256, 0, st>>>(ctx->npart, ctx->f_ugrid, P, 0, 1, ctx->small, ctx->ctl,
+                                                          ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
+                                                          ctx->tr_capacity);
+                } else {
+                    CK(fast_solve(ctx, 1));
+                    CK(fast_update(ctx, D, Dn, 1, stop));
+                    CK(fast_ad(ctx, ctx->X, stop));
+                    CK(fast_rows(ctx, ctx->R, ctx->b, nullptr, nullptr, ctx->Q, 1, stop));
+                    CK(fast_solve(ctx, 2));
+                    CK(fast_update(ctx, D, Dn, 2, stop));
+                    fast_record_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1,
+                                                          ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres,
+                                                          ctx->tr_wall, ctx->tr_capacity);
+                }
+                CKL();
+                ++ctx->launches;
+            }
+            rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, Dn, ctx->V, n, ctx->ctl, 0,
+                                                           fast ? ctx->small : nullptr);
             CKL();
-    ++ctx->launches;
-            if (recompute) CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, stop));
-            CK(chains_launch(ctx, kPhBeta, ctx->R, ctx->Q, nullptr, 2, stop));
-            solve_beta_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
-                                                ctx->tr_capacity);
-            CKL();
-    ++ctx->launches;
-            direction_kernel<<<dgrid, 256, 0, st>>>(ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop);
-            CKL();
-    ++ctx->launches;
-            rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, Dn, ctx->V, n, ctx->ctl, 0);
-            CKL();
-    ++ctx->launches;
+            ++ctx->launches;
         }
         CK(cudaMemcpyAsync(&ctx->ctl_host[slot], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(ctx->ev_chunk[slot], st));
@@ -679,9 +831,16 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     CK(cudaEventRecord(ctx->ev_loop1, st));
 
     // ---- finalize_trace (solvers.hpp:188-210) ----
-    CK(ad_launch(ctx, ctx->X, ctx->S, ctx->b, nullptr));
-    CK(chains_launch(ctx, kPhFinal, ctx->S, nullptr, nullptr, 1, nullptr));
-    final_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->final_norms);
+    if (!fast) {
+        CK(ad_launch(ctx, ctx->X, ctx->S, ctx->b, nullptr));
+        CK(chains_launch(ctx, kPhFinal, ctx->S, nullptr, nullptr, 1, nullptr));
+        final_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->final_norms);
+    } else {
+        CK(fast_ad(ctx, ctx->X, nullptr));
+        CK(fast_rows(ctx, ctx->S, ctx->b, nullptr, nullptr, nullptr, 1, nullptr));
+        fast_norms_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->ctl,
+                                            ctx->final_norms, 0, ctx->small);
+    }
     CKL();
     ++ctx->launches;
     CK(cudaEventRecord(ctx->ev_run1, st));
@@ -767,7 +926,12 @@ int coopcg_gpu_matvec_block(coopcg_gpu_ctx* ctx, const double* D, double* out) {
     CK(cudaMemcpyAsync(ctx->stage, D, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, st));
     colmajor_to_rowmajor_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->stage, ctx->Dblk[0], n, p, P);
     CKL();
-    CK(ad_launch(ctx, ctx->Dblk[0], ctx->Q, nullptr, nullptr));
+    if (ctx->arith == COOPCG_ARITH_FAST) {
+        CK(fast_ad(ctx, ctx->Dblk[0], nullptr));
+        CK(fast_rows(ctx, ctx->Q, nullptr, nullptr, nullptr, nullptr, 1, nullptr));
+    } else {
+        CK(ad_launch(ctx, ctx->Dblk[0], ctx->Q, nullptr, nullptr));
+    }
     rowmajor_to_colmajor_kernel<<<grid_for((size_t)ctx->n_loc * p, 256), 256, 0, st>>>(
         ctx->Q + (size_t)ctx->row0 * P, ctx->stage, ctx->n_loc, p, P);
     CKL();
@@ -796,7 +960,7 @@ int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D, double to
     const int dgrid = std::min(ctx->nparts, (n + rows_per_tile - 1) / rows_per_tile);
     direction_kernel<<<dgrid, 256, 0, st>>>(nullptr, ctx->Dblk[1], nullptr, nullptr, n, p, P, ctx->partials, nullptr);
     CKL();
-    rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[1], ctx->V, n, ctx->ctl, 2);
+    rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[1], ctx->V, n, ctx->ctl, 2, nullptr);
     CKL();
     CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

@@ -645,7 +645,7 @@ constexpr int kRankTile = 64;
 // mode 2: rank only (kernel-level entry point).
 __global__ void __launch_bounds__(1024)
     rank_end_kernel(const double* __restrict__ partials, int nparts, const double* __restrict__ Dn,
-                    double* __restrict__ V, int n, Ctl* ctl, int mode) {
+                    double* __restrict__ V, int n, Ctl* ctl, int mode, double* __restrict__ small_out) {
     if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int p = ctl->p, P = ctl->P;
@@ -655,34 +655,24 @@ __global__ void __launch_bounds__(1024)
     __shared__ int xcol[kMaxP], ycol[kMaxP];
     const int tid = threadIdx.x;
     const int npairs = p * (p + 1) / 2;
-    // 1. fixed-order reduction of the partial Grams: `lanes_per_pair` threads
-    // sum strided subsets of the CTA partials, combined in a fixed order.
+    // 1. fixed-order reduction of the partial Grams (pairs i <= j).
     {
-        __shared__ double red[1024];
-        const int lpp = max(1, min(32, static_cast<int>(blockDim.x) / max(npairs, 1)));
-        const int q = tid / lpp, sub = tid % lpp;
-        double s = 0.0;
-        if (q < npairs)
-            for (int b = sub; b < nparts; b += lpp) s += partials[static_cast<size_t>(b) * npairs + q];
-        red[tid] = s;
-        __syncthreads();
+        __shared__ double red[1024], pv[kMaxP * (kMaxP + 1) / 2];
+        cta_reduce_fixed(partials, nparts, npairs, 0, 1, npairs, pv, red);
         for (int qq = tid; qq < npairs; qq += blockDim.x) {
-            double tot = 0.0;
-            if (lpp * npairs <= static_cast<int>(blockDim.x)) {
-                for (int j = 0; j < lpp; ++j) tot += red[qq * lpp + j];
-            } else {
-                for (int b = 0; b < nparts; ++b) tot += partials[static_cast<size_t>(b) * npairs + qq];
-            }
             int t = qq, i = 0;
             while (t >= p - i) {
                 t -= p - i;
                 ++i;
             }
-            rs.g[i][i + t] = tot;
-            rs.g[i + t][i] = tot;
+            rs.g[i][i + t] = pv[qq];
+            rs.g[i + t][i] = pv[qq];
         }
         __syncthreads();
     }
+    // The next iteration's |D_i|^2 (fast mode's SPD-guard input; the exact
+    // path recomputes it with an exact chain).
+    if (small_out != nullptr && tid < p) small_out[SmallLayout{P}.nsq_d() + tid] = rs.g[tid][tid];
     // 2. certificate on warp 0
     if (tid < 32) {
         const int lane = tid;
@@ -934,7 +924,7 @@ __global__ void rowmajor_to_colmajor_kernel(const double* __restrict__ src, doub
 }
 // rows [c0, c0+rows) of a row-major n-wide matrix (staging) -> panels.
 __global__ void transpose_rows_kernel(const double* __restrict__ stage, int rows, int n, double* __restrict__ Ap,
-                                      int brs, int c0) {
+                                      ALay L, int c0) {
     __shared__ double tile[32][33];
     const int bx = blockIdx.x * 32;  // k
     const int by = blockIdx.y * 32;  // local row
@@ -945,17 +935,17 @@ __global__ void transpose_rows_kernel(const double* __restrict__ stage, int rows
     __syncthreads();
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
         const int k = bx + yy, i = by + threadIdx.x;
-        if (k < n && i < rows) Ap[ap_idx(n, brs, k, c0 + i)] = tile[threadIdx.x][yy];
+        if (k < n && i < rows) Ap[a_idx(L, n, k, c0 + i)] = tile[threadIdx.x][yy];
     }
 }
-__global__ void untranspose_rows_kernel(const double* __restrict__ Ap, int brs, int c0, int rows, int n,
+__global__ void untranspose_rows_kernel(const double* __restrict__ Ap, ALay L, int c0, int rows, int n,
                                         double* __restrict__ stage) {
     __shared__ double tile[32][33];
     const int bx = blockIdx.x * 32;  // k
     const int by = blockIdx.y * 32;  // local row
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
         const int k = bx + yy, i = by + threadIdx.x;
-        tile[yy][threadIdx.x] = (k < n && i < rows) ? Ap[ap_idx(n, brs, k, c0 + i)] : 0.0;
+        tile[yy][threadIdx.x] = (k < n && i < rows) ? Ap[a_idx(L, n, k, c0 + i)] : 0.0;
     }
     __syncthreads();
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {

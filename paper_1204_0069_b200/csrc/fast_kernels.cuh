@@ -1,0 +1,573 @@
+// fast_kernels.cuh -- roofline ("fast") arithmetic mode of the cCG iteration.
+//
+// Same iteration as the reference (coopcg/block_cg.hpp:132-277) but with the
+// floating-point work reordered for the hardware: FP64 tensor-core MMAs
+// (mma.sync m8n8k4 .f64, SASS DMMA) for Q = A.D, the p x p Gram products
+// fused into one reduction pass with fixed-order (deterministic, run-to-run
+// reproducible) two-stage sums, Cholesky instead of LU for the step solves,
+// beta's right-hand side formed algebraically as
+//     R_new^T Q = R^T Q + alpha (Q^T Q)            (block_cg.hpp:262-264)
+// and ONE fused pass for X += D alpha^T, R += Q alpha^T, D' = R + D beta^T
+// (block_cg.hpp:222-244, :270-273).  Parity is "within tolerance" (X to 1e-8
+// relative, pre-floor residual history), not bit-exact: DESIGN.md §2.
+#pragma once
+#include "common.cuh"
+
+namespace coopcg_gpu {
+
+constexpr int kFastBR = 64;   // rows per A panel (2 consumer warps x 32 rows)
+constexpr int kFastT = 36;    // k per A tile; 36*8 B row stride keeps DMMA A-fragment loads conflict-free
+constexpr int kFastS = 4;     // ring stages
+
+// Fast A layout ("tiles"): panel q (kFastBR rows), k-tile t: a contiguous
+// [r][kk] block of kFastBR x kFastT doubles at ((q*ntiles + t)*BR + r)*T + kk.
+__host__ __device__ __forceinline__ size_t at_fast_idx(int ntiles, int k, int il) {
+    const int q = il / kFastBR, r = il % kFastBR, t = k / kFastT, kk = k % kFastT;
+    return ((static_cast<size_t>(q) * ntiles + t) * kFastBR + r) * kFastT + kk;
+}
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+// ---------------------------------------------------------------------------
+// (1) Qpart[c] = A_panel(:, kchunk c) . D(kchunk c, :) for work units
+// (panel, kchunk); persistent CTAs; warp 0 = bulk-copy producer, warps 1..2
+// consume with m8n8k4 DMMA (warp w: 32 rows = 4 M-tiles x P/8 N-tiles).
+template <int P>
+__global__ void __launch_bounds__(96)
+    ad_fast_kernel(const double* __restrict__ Af, int n, int n_loc, int ntiles, const double* __restrict__ D,
+                   double* __restrict__ Qpart, int kchunks, int tiles_per_chunk, int nunits,
+                   const int* __restrict__ stop) {
+    static_assert(P % 8 == 0, "fast contexts pad p to a multiple of 8");
+    constexpr int NT = P / 8;  // N tiles of 8 columns
+    constexpr int BR = kFastBR, T = kFastT, S = kFastS;
+    constexpr int DP = P;      // D tile row stride in smem
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* As = reinterpret_cast<double*>(smem_raw);  // S x BR x T
+    double* Ds = As + S * BR * T;                       // S x T x DP
+    uint64_t* full = reinterpret_cast<uint64_t*>(Ds + S * T * DP);
+    uint64_t* empty = full + S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 2);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            int it = 0;
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                const int q = u / kchunks, c = u % kchunks;
+                const int t0 = c * tiles_per_chunk, t1 = min(ntiles, t0 + tiles_per_chunk);
+                for (int t = t0; t < t1; ++t, ++it) {
+                    if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
+                    const int rows = min(T, n - t * T);
+                    double* ds = Ds + s * T * DP;
+                    // the ragged last k-tile: zero the D rows past n (the A tile is
+                    // zero padded in global memory)
+                    for (int e = rows * DP; e < T * DP; ++e) ds[e] = 0.0;
+                    const uint32_t abytes = BR * T * 8u;
+                    const uint32_t dbytes = static_cast<uint32_t>(rows) * P * 8u;
+                    mbar_arrive_expect_tx(&full[s], abytes + dbytes);
+                    bulk_g2s(As + s * BR * T, Af + (static_cast<size_t>(q) * ntiles + t) * BR * T, abytes, &full[s]);
+                    bulk_g2s(ds, D + static_cast<size_t>(t) * T * P, dbytes, &full[s]);
+                    if (++s == S) {
+                        s = 0;
+                        ph ^= 1u;
+                    }
+                }
+            }
+        }
+        return;
+    }
+    const int cw = warp - 1;  // consumer warp: rows [32 cw, 32 cw + 32)
+    const int g = lane >> 2, tg = lane & 3;
+    int s = 0;
+    uint32_t phase = 0;
+    for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+        const int q = u / kchunks, c = u % kchunks;
+        const int t0 = c * tiles_per_chunk, t1 = min(ntiles, t0 + tiles_per_chunk);
+        double acc[4][NT][2];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+        for (int t = t0; t < t1; ++t) {
+            mbar_wait(&full[s], phase);
+            const double* as = As + s * BR * T + (32 * cw + g) * T + tg;
+            const double* ds = Ds + s * T * DP + tg * DP + g;
+#pragma unroll
+            for (int ks = 0; ks < T / 4; ++ks) {
+                double a[4], b[NT];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt) a[mt] = as[8 * mt * T + 4 * ks];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) b[nt] = ds[4 * ks * DP + 8 * nt];
+#pragma unroll
+                for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            if (++s == S) {
+                s = 0;
+                phase ^= 1u;
+            }
+        }
+        double* qp = Qpart + static_cast<size_t>(c) * n_loc * P;
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt) {
+            const int il = q * BR + 32 * cw + 8 * mt + g;
+            if (il < n_loc) {
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    const int col = 8 * nt + 2 * tg;
+                    if (col < P) qp[static_cast<size_t>(il) * P + col] = acc[mt][nt][0];
+                    if (col + 1 < P) qp[static_cast<size_t>(il) * P + col + 1] = acc[mt][nt][1];
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// (2) Row pass after the MMA: dst = sum_c Qpart[c] (- b), written to the
+// global rows row0.. of `dst`, plus per-CTA partial Grams over the rows:
+//   mode 0 (iteration):  G0 = D^T Q, G1 = R^T D, G2 = R^T Q, G3 = Q^T Q
+//   mode 1 (residual):   G0 = dst^T Q (if Q != null), diag(dst^T dst) -> G1[j][j]
+// Rows are processed in tiles of 256/P (thread per element).
+template <int P>
+__global__ void __launch_bounds__(256)
+    fast_rows_kernel(const double* __restrict__ Qpart, int kchunks, int n_loc, int row0, double* __restrict__ dst,
+                     const double* __restrict__ b, const double* __restrict__ D, const double* __restrict__ R,
+                     const double* __restrict__ Qfull, int p, int mode, double* __restrict__ partials,
+                     const int* __restrict__ stop) {
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
+    constexpr int RP = 4;                 // rows per thread per tile (loads in flight together)
+    constexpr int TR = (256 / P) * RP;    // rows per tile
+    constexpr int NOUT = 4 * P * P;
+    constexpr int PER = (NOUT + 255) / 256;
+    __shared__ double tq[TR][P], td[TR][P], trr[TR][P];
+    const int tid = threadIdx.x;
+    const int lr0 = tid / P, j = tid % P;
+    double acc[PER];
+#pragma unroll
+    for (int q = 0; q < PER; ++q) acc[q] = 0.0;
+    const int ntile = (n_loc + TR - 1) / TR;
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        double v[RP], dv[RP], rv[RP];
+#pragma unroll
+        for (int u = 0; u < RP; ++u) {
+            const int il = t * TR + lr0 + u * (256 / P);
+            v[u] = 0.0;
+            dv[u] = 0.0;
+            rv[u] = 0.0;
+            if (il < n_loc) {
+                const int row = row0 + il;
+                for (int c = 0; c < kchunks; ++c) v[u] += Qpart[(static_cast<size_t>(c) * n_loc + il) * P + j];
+                if (mode == 0) {
+                    dv[u] = D[static_cast<size_t>(row) * P + j];
+                    rv[u] = R[static_cast<size_t>(row) * P + j];
+                } else if (Qfull != nullptr) {
+                    dv[u] = Qfull[static_cast<size_t>(row) * P + j];
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < RP; ++u) {
+            const int lr = lr0 + u * (256 / P);
+            const int il = t * TR + lr;
+            if (il < n_loc) {
+                const int row = row0 + il;
+                if (b != nullptr) v[u] = (j < p) ? v[u] - b[row] : 0.0;
+                dst[static_cast<size_t>(row) * P + j] = v[u];
+            }
+            tq[lr][j] = v[u];
+            td[lr][j] = dv[u];
+            trr[lr][j] = rv[u];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int o = tid + q * 256;
+            if (o < NOUT) {
+                const int gsel = o / (P * P), a = (o / P) % P, c2 = o % P;
+                double s = acc[q];
+                if (mode == 0) {
+                    if (gsel == 0)
+                        for (int r = 0; r < TR; ++r) s = fma(td[r][a], tq[r][c2], s);
+                    else if (gsel == 1)
+                        for (int r = 0; r < TR; ++r) s = fma(trr[r][a], td[r][c2], s);
+                    else if (gsel == 2)
+                        for (int r = 0; r < TR; ++r) s = fma(trr[r][a], tq[r][c2], s);
+                    else
+                        for (int r = 0; r < TR; ++r) s = fma(tq[r][a], tq[r][c2], s);
+                } else {
+                    if (gsel == 0 && Qfull != nullptr)
+                        for (int r = 0; r < TR; ++r) s = fma(tq[r][a], td[r][c2], s);
+                    else if (gsel == 1 && a == c2)
+                        for (int r = 0; r < TR; ++r) s = fma(tq[r][a], tq[r][a], s);
+                }
+                acc[q] = s;
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < PER; ++q) {
+        const int o = tid + q * 256;
+        if (o < NOUT) partials[static_cast<size_t>(blockIdx.x) * NOUT + o] = acc[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// (3) Step matrices on one CTA: reduce the Gram partials, then warp 0 runs
+// the SPD guard (block_cg.hpp:196-202), Cholesky of M = sym(D^T Q) with the
+// reference's pivot floor max|M| * 1e-14 (block_cg.hpp:180-190), and solves
+//   alpha_i: M alpha_i^T = -(R^T D)_i            (block_cg.hpp:203-217)
+//   beta_i:  M beta_i^T  = -(R^T Q + alpha Q^T Q)_i   (algebraic R_new^T Q)
+// mode 0: alpha + beta; mode 1: alpha only (recompute iteration, beta later);
+// mode 2: beta only from G0 = R_new^T Q of a residual pass (uses ctl->lu).
+struct FastSolveScratch {
+    double l[kMaxP][kMaxP + 1];
+    double y[kMaxP][kMaxP + 1];
+};
+
+__device__ void chol_solve_row(const double (*l)[kMaxP + 1], int p, const double* rhs, double* y, double* x) {
+    // L L^T x = rhs
+    for (int i = 0; i < p; ++i) {
+        double s = rhs[i];
+        for (int j = 0; j < i; ++j) s = fma(-l[i][j], y[j], s);
+        y[i] = s / l[i][i];
+    }
+    for (int i = p - 1; i >= 0; --i) {
+        double s = y[i];
+        for (int j = i + 1; j < p; ++j) s = fma(-l[j][i], x[j], s);
+        x[i] = s / l[i][i];
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+    fast_solve_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ small, Ctl* ctl,
+                      int mode) {
+    if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
+    __shared__ FastSolveScratch sc;
+    extern __shared__ __align__(16) double dyn[];  // flat[4 P P] then red[blockDim]
+    const int p = ctl->p, P = ctl->P;
+    const SmallLayout L{P};
+    const int tid = threadIdx.x;
+    const int nout = (mode == 2) ? P * P : 4 * P * P;
+    double* flat = dyn;
+    double* red = dyn + 4 * P * P;
+    cta_reduce_fixed(partials, nparts, 4 * P * P, 0, 1, nout, flat, red);
+    __syncthreads();
+    // G[gsel][a][c] = flat[(gsel * P + a) * P + c]
+    auto G = [&](int gsel, int a, int c) { return flat[(gsel * P + a) * P + c]; };
+    if (tid >= 32) return;
+    const int lane = tid;
+    double* yrow = sc.y[lane];
+    double x[kMaxP];
+    if (mode != 2) {
+        // M = (raw + raw^T)/2, floor = max|M| * 1e-14
+        double maxabs = 0.0;
+        if (lane < p)
+            for (int j = 0; j < p; ++j) {
+                const double v = 0.5 * (G(0, lane, j) + G(0, j, lane));
+                sc.l[lane][j] = v;
+                maxabs = fmax(maxabs, fabs(v));
+            }
+        for (int off = 16; off > 0; off >>= 1) maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, off));
+        __syncwarp();
+        const double floor = maxabs * 1e-14;
+        bool bad = false;
+        if (lane < p) bad = !(sc.l[lane][lane] > 0.0) && (small[L.nsq_d() + lane] > 0.0);
+        if (__any_sync(0xffffffffu, bad)) {
+            if (lane == 0) {
+                ctl->err = 2;
+                ctl->err_iter = ctl->k;
+                ctl->stop = 1;
+            }
+            return;
+        }
+        // Cholesky (lower, lane owns row)
+        bool ok = true;
+        for (int k = 0; k < p; ++k) {
+            if (lane == k) {
+                double s = sc.l[k][k];
+                for (int m = 0; m < k; ++m) s = fma(-sc.l[k][m], sc.l[k][m], s);
+                sc.l[k][k] = (s > floor) ? sqrt(s) : -1.0;
+            }
+            __syncwarp();
+            if (!(sc.l[k][k] > 0.0)) {
+                ok = false;
+                break;
+            }
+            if (lane > k && lane < p) {
+                double s = sc.l[lane][k];
+                for (int m = 0; m < k; ++m) s = fma(-sc.l[lane][m], sc.l[k][m], s);
+                sc.l[lane][k] = s / sc.l[k][k];
+            }
+            __syncwarp();
+        }
+        if (!ok) {
+            if (lane == 0) {
+                ctl->status = 1;  // rank collapse (pivot vanished)
+                ctl->stop = 1;
+            }
+            return;
+        }
+        for (int idx = lane; idx < p * p; idx += 32) ctl->lu[idx] = sc.l[idx / p][idx % p];
+        if (lane < p) {
+            double rhs[kMaxP];
+            for (int j = 0; j < p; ++j) rhs[j] = -G(1, lane, j);
+            chol_solve_row(sc.l, p, rhs, yrow, x);
+            for (int j = 0; j < P; ++j) small[L.alpha() + lane * P + j] = (j < p) ? x[j] : 0.0;
+            if (mode == 0) {
+                // rhs_beta(i, j) = -(R^T Q + alpha Q^T Q)(i, j)
+                for (int j = 0; j < p; ++j) {
+                    double s = G(2, lane, j);
+                    for (int m = 0; m < p; ++m) s = fma(x[m], G(3, m, j), s);
+                    rhs[j] = -s;
+                }
+                double xb[kMaxP];
+                chol_solve_row(sc.l, p, rhs, yrow, xb);
+                for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? xb[j] : 0.0;
+            }
+        }
+    } else {
+        for (int idx = lane; idx < p * p; idx += 32) sc.l[idx / p][idx % p] = ctl->lu[idx];
+        __syncwarp();
+        if (lane < p) {
+            double rhs[kMaxP];
+            for (int j = 0; j < p; ++j) rhs[j] = -G(0, lane, j);
+            chol_solve_row(sc.l, p, rhs, yrow, x);
+            for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? x[j] : 0.0;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// (4) The fused update pass (one read of X, R, D, Q; one write of X, R, D'):
+//   mode 0: X += D alpha^T; R += Q alpha^T; D' = R + D beta^T
+//   mode 1: X += D alpha^T only (recompute iteration)
+//   mode 2: D' = R + D beta^T only (after the recompute)
+// plus per-CTA partials of |R_j|^2 (P values; modes 0) and the pairs of
+// D'^T D' (rank certificate, the exact path's direction_kernel format).
+template <int P>
+__global__ void __launch_bounds__(256)
+    fast_update_kernel(double* __restrict__ X, double* __restrict__ R, const double* __restrict__ Q,
+                       const double* __restrict__ D, double* __restrict__ Dn, const double* __restrict__ small, int n,
+                       int p, int mode, double* __restrict__ norm_part, double* __restrict__ pair_part,
+                       const int* __restrict__ stop) {
+    if (*reinterpret_cast<volatile const int*>(stop)) return;
+    constexpr int RP = (P >= 32) ? 2 : 4;
+    constexpr int TR = (256 / P) * RP;
+    const SmallLayout L{P};
+    __shared__ double al[P][P + 1], be[P][P + 1];
+    __shared__ double tr_[TR][P], tdn[TR][P], td_[TR][P], tq_[TR][P];
+    const int tid = threadIdx.x;
+    for (int idx = tid; idx < p * p; idx += 256) {
+        al[idx / p][idx % p] = small[L.alpha() + (idx / p) * P + idx % p];
+        be[idx / p][idx % p] = small[L.beta() + (idx / p) * P + idx % p];
+    }
+    const int npairs = p * (p + 1) / 2;
+    int pi[3], pj[3];
+    double part[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+        int t = tid + q * 256;
+        pi[q] = pj[q] = -1;
+        if (t < npairs) {
+            int i = 0;
+            while (t >= p - i) {
+                t -= p - i;
+                ++i;
+            }
+            pi[q] = i;
+            pj[q] = i + t;
+        }
+    }
+    double nrm = 0.0;
+    const int lr0 = tid / P, i = tid % P;
+    __syncthreads();
+    const int ntile = (n + TR - 1) / TR;
+    for (int t = blockIdx.x; t < ntile; t += gridDim.x) {
+        // stage the D (and Q) rows of the tile: loads for RP rows in flight together
+        double dv[RP], qv[RP], xv[RP], rv[RP];
+#pragma unroll
+        for (int u = 0; u < RP; ++u) {
+            const int row = t * TR + lr0 + u * (256 / P);
+            const size_t e = static_cast<size_t>(row) * P + i;
+            const bool ok = row < n;
+            dv[u] = ok ? D[e] : 0.0;
+            qv[u] = (ok && mode == 0) ? Q[e] : 0.0;
+            xv[u] = (ok && mode <= 1) ? X[e] : 0.0;
+            rv[u] = (ok && mode != 1) ? R[e] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < RP; ++u) {
+            td_[lr0 + u * (256 / P)][i] = dv[u];
+            tq_[lr0 + u * (256 / P)][i] = qv[u];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < RP; ++u) {
+            const int lr = lr0 + u * (256 / P);
+            const int row = t * TR + lr;
+            const size_t e = static_cast<size_t>(row) * P + i;
+            double rnew = 0.0;
+            if (row < n && i < p) {
+                if (mode <= 1) {
+                    double x = xv[u];
+                    for (int j = 0; j < p; ++j) x = fma(al[i][j], td_[lr][j], x);
+                    X[e] = x;
+                }
+                if (mode == 0) {
+                    double r = rv[u];
+                    for (int j = 0; j < p; ++j) r = fma(al[i][j], tq_[lr][j], r);
+                    R[e] = r;
+                    rnew = r;
+                    nrm = fma(r, r, nrm);
+                } else {
+                    rnew = rv[u];
+                }
+            }
+            tr_[lr][i] = rnew;
+        }
+        __syncthreads();
+        if (mode != 1) {
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                const int lr = lr0 + u * (256 / P);
+                const int row = t * TR + lr;
+                double dn = 0.0;
+                if (row < n && i < p) {
+                    dn = tr_[lr][i];
+                    for (int j = 0; j < p; ++j) dn = fma(be[i][j], td_[lr][j], dn);
+                }
+                if (row < n) Dn[static_cast<size_t>(row) * P + i] = dn;
+                tdn[lr][i] = dn;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (pi[q] >= 0) {
+                    double s = part[q];
+                    for (int r = 0; r < TR; ++r) s = fma(tdn[r][pi[q]], tdn[r][pj[q]], s);
+                    part[q] = s;
+                }
+        }
+        __syncthreads();
+    }
+    // column norms: threads with the same i (tid % P) hold partial sums; reduce
+    // them in a fixed order through shared memory.
+    __shared__ double nred[256];
+    nred[tid] = nrm;
+    __syncthreads();
+    if (tid < P) {
+        double s = 0.0;
+        for (int r = 0; r < 256 / P; ++r) s += nred[r * P + tid];
+        if (mode == 0) norm_part[static_cast<size_t>(blockIdx.x) * P + tid] = s;
+    }
+    if (mode != 1) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+            if (pi[q] >= 0) pair_part[static_cast<size_t>(blockIdx.x) * npairs + tid + q * 256] = part[q];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// (5) Norms from partials -> record + convergence (the fast twin of the tail of
+// solve_beta_kernel; solvers.hpp:125-154).  `diag_stride` selects the layout:
+// norm partials are P values per CTA (stride P), residual-pass partials keep
+// the squared norms on the diagonal of G1 (offset P*P, stride P+1).
+__global__ void __launch_bounds__(256)
+    fast_record_kernel(const double* __restrict__ part, int nparts, int part_stride, int part_off, int diag_stride,
+                       double* __restrict__ small, Ctl* ctl, double* __restrict__ tr_norms,
+                       double* __restrict__ tr_minres, unsigned long long* __restrict__ tr_wall, int capacity) {
+    if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
+    __shared__ double norms[kMaxP], sums[kMaxP], red[256];
+    const int p = ctl->p, P = ctl->P;
+    const SmallLayout L{P};
+    const int tid = threadIdx.x;
+    cta_reduce_fixed(part, nparts, part_stride, part_off, diag_stride, p, sums, red);
+    if (tid < p) {
+        const double s = sums[tid];
+        small[L.nsq_r() + tid] = s;
+        norms[tid] = sqrt(s);
+        small[L.norm() + tid] = norms[tid];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        const unsigned long long now = globaltimer_ns();
+        const int k = ctl->k;
+        double m = norms[0];
+        int slot = -1;
+        for (int j = 0; j < p; ++j) {
+            m = (norms[j] < m) ? norms[j] : m;
+            if (slot < 0 && norms[j] <= ctl->tol) slot = j;
+        }
+        if (k < capacity) {
+            for (int j = 0; j < p; ++j) tr_norms[static_cast<size_t>(k) * p + j] = norms[j];
+            tr_minres[k] = m;
+            tr_wall[k] = now - ctl->t_last;
+        }
+        ctl->t_last = now;
+        ctl->iterations = k + 1;
+        if (slot >= 0) {
+            ctl->status = 0;
+            ctl->converged_agent = slot;
+            ctl->stop = 1;
+        }
+    }
+}
+
+// Initial / final norms from residual-pass partials (diag of G1).
+__global__ void fast_norms_kernel(const double* __restrict__ part, int nparts, int part_stride, int part_off,
+                                  int diag_stride, Ctl* ctl, double* __restrict__ out, int setup,
+                                  double* __restrict__ small) {
+    __shared__ double nv[kMaxP], sums[kMaxP], red[256];
+    const int p = ctl->p;
+    const SmallLayout L{ctl->P};
+    const int tid = threadIdx.x;
+    cta_reduce_fixed(part, nparts, part_stride, part_off, diag_stride, p, sums, red);
+    if (tid < p) {
+        const double s = sums[tid];
+        nv[tid] = sqrt(s);
+        out[tid] = nv[tid];
+        if (setup) {
+            small[L.nsq_r() + tid] = s;
+            small[L.norm() + tid] = nv[tid];
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double m = nv[0];
+        int slot = -1;
+        for (int j = 0; j < p; ++j) {
+            m = (nv[j] < m) ? nv[j] : m;
+            if (slot < 0 && nv[j] <= ctl->tol) slot = j;
+        }
+        out[p] = m;
+        if (setup) {
+            if (slot >= 0) {
+                ctl->status = 0;
+                ctl->converged_agent = slot;
+                ctl->stop = 1;
+            }
+            ctl->t_last = globaltimer_ns();
+        }
+    }
+}
+
+} // namespace coopcg_gpu

@@ -30,19 +30,17 @@ __device__ __forceinline__ double uniform_pm1_dev(uint64_t key, uint64_t c) {
 
 // Off-diagonal entries of the diagonally dominant matrix: A_ij = A_ji =
 // (B_lo,hi + B_hi,lo) / 2 with B_ij ~ U[-1,1] at counter i*n + j + 1.
-__global__ void gen_dd_offdiag_kernel(double* __restrict__ Ap, int brs, int n, int n_loc, int row0, uint64_t key,
+// Iterates over storage order (coalesced writes for either layout).
+__global__ void gen_dd_offdiag_kernel(double* __restrict__ Ap, ALay L, int n, int n_loc, int row0, uint64_t key,
                                       size_t total) {
-    const int BR = 1 << brs;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t panel = e / (static_cast<size_t>(n) << brs);
-        const size_t rem = e - panel * (static_cast<size_t>(n) << brs);
-        const uint64_t k = rem >> brs;
-        const int il = static_cast<int>(panel * BR + (rem & (BR - 1)));
+        int k, il;
+        a_decode(L, n, e, k, il);
         double v = 0.0;
-        const uint64_t i = static_cast<uint64_t>(row0 + il);
-        if (il < n_loc && k != i) {
-            const uint64_t lo = k < i ? k : i, hi = k < i ? i : k;
+        const uint64_t i = static_cast<uint64_t>(row0 + il), kk = static_cast<uint64_t>(k);
+        if (il < n_loc && k < n && kk != i) {
+            const uint64_t lo = kk < i ? kk : i, hi = kk < i ? i : kk;
             const uint64_t un = static_cast<uint64_t>(n);
             const double u1 = uniform_pm1_dev(key, lo * un + hi + 1);
             const double u2 = uniform_pm1_dev(key, hi * un + lo + 1);
@@ -52,20 +50,18 @@ __global__ void gen_dd_offdiag_kernel(double* __restrict__ Ap, int brs, int n, i
     }
 }
 
-// Diagonal: A_ii = (sum_{j != i, ascending} |A_ij|) + 1.  One chain per row,
-// reading the row's panel column (coalesced across consecutive rows).
-__global__ void gen_dd_diag_kernel(double* __restrict__ Ap, int brs, int n, int n_loc, int row0) {
+// Diagonal: A_ii = (sum_{j != i, ascending} |A_ij|) + 1.  One chain per row.
+__global__ void gen_dd_diag_kernel(double* __restrict__ Ap, ALay L, int n, int n_loc, int row0) {
     const int il = blockIdx.x * blockDim.x + threadIdx.x;
     if (il >= n_loc) return;
     const int i = row0 + il;
     double acc = 0.0;
-    const double* col = Ap + ap_idx(n, brs, 0, il);
-#pragma unroll 8
+#pragma unroll 4
     for (int j = 0; j < n; ++j) {
-        const double a = fabs(col[static_cast<size_t>(j) << brs]);
+        const double a = fabs(Ap[a_idx(L, n, j, il)]);
         if (j != i) acc = __dadd_rn(acc, a);
     }
-    Ap[ap_idx(n, brs, i, il)] = __dadd_rn(acc, 1.0);
+    Ap[a_idx(L, n, i, il)] = __dadd_rn(acc, 1.0);
 }
 
 // Householder construction (single-GPU contexts hold the full matrix):
@@ -73,26 +69,22 @@ __global__ void gen_dd_diag_kernel(double* __restrict__ Ap, int brs, int n, int 
 //   s = v.v, w = M v, c = v.w, t1 = 2/s, t2 = (4 c)/(s s),
 //   M_ij <- (M_ij - t1 (v_i w_j + w_i v_j)) + t2 (v_i v_j)
 // (every sum sequential ascending, one rounding per op).
-__global__ void hh_init_kernel(double* __restrict__ Ap, int brs, int n, const double* __restrict__ lambda,
+__global__ void hh_init_kernel(double* __restrict__ Ap, ALay L, int n, const double* __restrict__ lambda,
                                size_t total) {
-    const int BR = 1 << brs;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t panel = e / (static_cast<size_t>(n) << brs);
-        const size_t rem = e - panel * (static_cast<size_t>(n) << brs);
-        const size_t k = rem >> brs;
-        const size_t i = panel * BR + (rem & (BR - 1));
-        Ap[e] = (i == k && i < static_cast<size_t>(n)) ? lambda[i] : 0.0;
+        int k, i;
+        a_decode(L, n, e, k, i);
+        Ap[e] = (i == k && i < n) ? lambda[i] : 0.0;
     }
 }
-__global__ void hh_w_kernel(const double* __restrict__ Ap, int brs, int n, const double* __restrict__ v,
+__global__ void hh_w_kernel(const double* __restrict__ Ap, ALay L, int n, const double* __restrict__ v,
                             double* __restrict__ w) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     double acc = 0.0;
-    const double* col = Ap + ap_idx(n, brs, 0, i);
-#pragma unroll 8
-    for (int k = 0; k < n; ++k) acc = mac_exact(acc, col[static_cast<size_t>(k) << brs], v[k]);
+#pragma unroll 4
+    for (int k = 0; k < n; ++k) acc = mac_exact(acc, Ap[a_idx(L, n, k, i)], v[k]);
     w[i] = acc;
 }
 __global__ void hh_scalars_kernel(int n, const double* __restrict__ v, const double* __restrict__ w,
@@ -104,17 +96,14 @@ __global__ void hh_scalars_kernel(int n, const double* __restrict__ v, const dou
     t12[0] = __ddiv_rn(2.0, s);
     t12[1] = __ddiv_rn(__dmul_rn(4.0, c), __dmul_rn(s, s));
 }
-__global__ void hh_update_kernel(double* __restrict__ Ap, int brs, int n, const double* __restrict__ v,
+__global__ void hh_update_kernel(double* __restrict__ Ap, ALay L, int n, const double* __restrict__ v,
                                  const double* __restrict__ w, const double* __restrict__ t12, size_t total) {
     const double t1 = t12[0], t2 = t12[1];
-    const int BR = 1 << brs;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const size_t panel = e / (static_cast<size_t>(n) << brs);
-        const size_t rem = e - panel * (static_cast<size_t>(n) << brs);
-        const int k = static_cast<int>(rem >> brs);
-        const int i = static_cast<int>(panel * BR + (rem & (BR - 1)));
-        if (i >= n) continue;
+        int k, i;
+        a_decode(L, n, e, k, i);
+        if (i >= n || k >= n) continue;
         // element (i, k); the expression is symmetric in (i, k) bit for bit.
         const double q = __dadd_rn(__dmul_rn(v[i], w[k]), __dmul_rn(w[i], v[k]));
         const double m1 = __dsub_rn(Ap[e], __dmul_rn(t1, q));

@@ -1,0 +1,123 @@
+"""Fast (roofline) mode parity: DMMA A.D, fused Grams, Cholesky steps, fused
+update.  Not bit-exact by design; checked against the oracle
+with the tolerances of SURVEY.md §8d / BASELINE.json's north star:
+  * final X within 1e-8 relative (per-agent 2-norm),
+  * residual-norm history within 1e-8 relative before the round-off floor
+    (minres / ||b|| > 1e-11) on well-conditioned problems,
+  * iteration count to tolerance within +-2 (diagonally dominant, cfg-0 family).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def m():
+    import paper_1204_0069_b200 as mod
+    with mod.GpuContext(16, 2, arith="fast") as _:
+        pass
+    return mod
+
+
+def rel_x(a, b):
+    return float(np.max(np.linalg.norm(a - b, axis=0) / np.maximum(np.linalg.norm(b, axis=0), 1e-300)))
+
+
+@pytest.mark.parametrize("n,p", [(1000, 3), (700, 8), (513, 16), (300, 32)])
+def test_fast_matvec_block(m, po, n, p):
+    rng = np.random.default_rng(n + p)
+    A = po.gen_diagdom(n, 4)
+    D = rng.uniform(-1, 1, (n, p))
+    with m.GpuContext(n, p, arith="fast") as ctx:
+        ctx.set_A(A)
+        Q = ctx.matvec_block(D)
+    ref = A @ D
+    scale = np.abs(A) @ np.abs(D)
+    assert np.max(np.abs(Q - ref) / scale) < 1e-14
+
+
+@pytest.mark.parametrize("n,p", [(1000, 3), (2000, 8), (1500, 16)])
+def test_fast_diagdom_to_tolerance(m, po, n, p):
+    A = po.gen_diagdom(n, n + 1)
+    b = po.gen_rhs(n, "uniform", n + 1)
+    X0 = po.gen_starts(n, p, n + 1)
+    tol = 1e-10 * po.seq_norm(b)
+    ot = po.oracle_ccg(A, b, X0, tol=tol)
+    gt = m.ccg_solve(A, b, X0, m.SolveOptions(tol=tol), m.GpuOptions(arith="fast"))
+    assert str(gt.status) == ot.status == "converged"
+    assert abs(gt.iteration_count() - ot.iterations) <= 2
+    assert rel_x(gt.final_x, ot.final_x) < 1e-8
+    k = min(gt.iteration_count(), ot.iterations)
+    nb = po.seq_norm(b)
+    pre = ot.minres[:k] / nb > 1e-11
+    rel = np.abs(gt.residual_norms[:k] - ot.residual_norms[:k]) / ot.residual_norms[:k]
+    assert np.all(rel[pre] < 1e-8)
+
+
+def test_fast_fixed_iterations_tail(m, po):
+    """cfg-2 family: 120 fixed iterations deep into the post-convergence tail
+    (two residual recomputations)."""
+    n, p = 1024, 8
+    A = po.gen_diagdom(n, 3)
+    b = po.gen_rhs(n, "uniform", 3)
+    X0 = po.gen_starts(n, p, 3)
+    ot = po.oracle_ccg(A, b, X0, max_iters=120)
+    gt = m.ccg_solve(A, b, X0, m.SolveOptions(max_iters=120), m.GpuOptions(arith="fast"))
+    assert str(gt.status) == ot.status == "max-iterations"
+    assert gt.iteration_count() == 120
+    assert rel_x(gt.final_x, ot.final_x) < 1e-8
+    # true final residuals both at the round-off floor
+    nb = po.seq_norm(b)
+    assert np.all(gt.final_residual_norms / nb < 1e-11)
+
+
+def test_fast_householder(m, po):
+    n, p = 512, 4
+    A = po.gen_householder(n, 8, 1e4, 21)
+    b = po.gen_rhs(n, "normal", 21)
+    X0 = po.gen_starts(n, p, 21)
+    tol = 1e-10 * po.seq_norm(b)
+    ot = po.oracle_ccg(A, b, X0, tol=tol)
+    gt = m.ccg_solve(A, b, X0, m.SolveOptions(tol=tol), m.GpuOptions(arith="fast"))
+    assert str(gt.status) == "converged"
+    # kappa = 1e4: finite-precision CG is chaotic past ~k=30;
+    # the iteration count is reported, X must still agree to 1e-8.
+    assert abs(gt.iteration_count() - ot.iterations) <= max(4, ot.iterations // 20)
+    assert rel_x(gt.final_x, ot.final_x) < 1e-8
+
+
+def test_fast_generated_config0(m, po):
+    cfg = m.CONFIGS[0]
+    with m.GpuContext(cfg.n, cfg.p, arith="fast") as ctx:
+        b, X0, opts = m.make_problem_on_device(ctx, cfg)
+        gt = ctx.solve(b, X0, opts)
+        A = ctx.get_A()
+    assert np.array_equal(A, po.gen_diagdom(cfg.n, cfg.seed))  # fast layout round trip
+    ot = po.oracle_ccg(A, b, X0, tol=opts.tol)
+    assert abs(gt.iteration_count() - ot.iterations) <= 2
+    assert rel_x(gt.final_x, ot.final_x) < 1e-8
+
+
+def test_fast_degenerate_and_spd(m, po):
+    n = 200
+    A = po.gen_diagdom(n, 2)
+    b = po.gen_rhs(n, "uniform", 2)
+    t = m.ccg_solve(A, b, np.zeros((n, 3)), m.SolveOptions(tol=1e-10), m.GpuOptions(arith="fast"))
+    assert str(t.status) == "rank-collapse" and t.iteration_count() == 0
+    with pytest.raises(m.SpdViolationError):
+        m.ccg_solve(-np.eye(30), np.linspace(-1, 1, 30),
+                    np.stack([np.zeros(30), np.linspace(0.5, -0.25, 30)], 1),
+                    m.SolveOptions(tol=1e-12), m.GpuOptions(arith="fast"))
+
+
+def test_fast_deterministic(m, po):
+    n, p = 900, 16
+    with m.GpuContext(n, p, arith="fast") as ctx:
+        ctx.gen_A("diagdom", 5)
+        b = m.gen_rhs(n, "uniform", 5)
+        X0 = m.gen_starts(n, p, 5)
+        t1 = ctx.solve(b, X0, m.SolveOptions(max_iters=60))
+        t2 = ctx.solve(b, X0, m.SolveOptions(max_iters=60))
+    assert np.array_equal(t1.final_x, t2.final_x)
+    assert np.array_equal(t1.residual_norms, t2.residual_norms)
