@@ -167,32 +167,25 @@ def _profile_traffic(cfg_name: str):
     return None
 
 
-def run_ours(args, cfg):
+def _measure(m, torch, cfg, args, arith, dev):
+    """K timed solves (inputs resident) + K e2e solves through the drop-in call."""
+    import ctypes as C
     import numpy as np
-    import torch
-    import paper_1204_0069_b200 as m
+    from paper_1204_0069_b200 import _capi
     from paper_1204_0069_b200.configs import make_problem_on_device
 
-    ws, rank, local = _dist()
-    if ws > 1:
-        from paper_1204_0069_b200 import sharded
-        return sharded.bench_main(args, cfg, BASELINE_METRIC)
-    dev = args.device
-    torch.cuda.set_device(dev)
-    ctx = m.GpuContext(cfg.n, cfg.p, device=dev, arith=args.arith)
+    ctx = m.GpuContext(cfg.n, cfg.p, device=dev, arith=arith)
     b, X0, opts = make_problem_on_device(ctx, cfg)
     ctx.upload(b, X0)
     stream = torch.cuda.ExternalStream(ctx.stream_handle(), device=dev)
-
     for _ in range(args.warmup):
         ctx.run(opts, want_x=False)
     torch.cuda.synchronize()
-
-    # ---- timed region: K solves with inputs resident in HBM ----
     iters_total = 0
     mv_ms = 0.0
     mv_n = 0
     launches = 0
+    exact_rank_checks = 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
@@ -201,6 +194,7 @@ def run_ours(args, cfg):
         for _ in range(args.steps):
             t = ctx.run(opts, want_x=False)
             iters_total += t.iteration_count()
+            exact_rank_checks += t.exact_rank_checks
             tm = ctx.timing()
             mv_ms += tm["matvec_ms_total"]
             mv_n += tm["matvec_launches"]
@@ -208,15 +202,12 @@ def run_ours(args, cfg):
         e1.record(stream)
         torch.cuda.synchronize()
     elapsed_ms = e0.elapsed_time(e1)
-    value = iters_total / (elapsed_ms * 1e-3)
 
-    # ---- e2e: the drop-in call with pinned host buffers ----
+    # e2e: the drop-in call (coopcg_gpu_solve) with pinned host buffers
     n, p = cfg.n, cfg.p
     bh = torch.from_numpy(b).pin_memory()
     X0c = torch.from_numpy(np.ascontiguousarray(X0.T)).pin_memory()
     fx = torch.empty((p, n), dtype=torch.float64).pin_memory()
-    import ctypes as C
-    from paper_1204_0069_b200 import _capi
     L = _capi.lib()
     cap = max(opts.max_iters if opts.max_iters >= 0 else 2 * n, 1)
     norms = torch.empty((cap, p), dtype=torch.float64).pin_memory()
@@ -225,18 +216,20 @@ def run_ours(args, cfg):
     tr.residual_norms = C.cast(norms.data_ptr(), C.POINTER(C.c_double))
     tr.final_x = C.cast(fx.data_ptr(), C.POINTER(C.c_double))
     co = opts.to_c()
-    e2e_iters = 0
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
+
+    def e2e_once():
         rc = L.coopcg_gpu_solve(ctx._h, C.c_void_p(bh.data_ptr()), C.c_void_p(X0c.data_ptr()),
                                 C.byref(co), C.byref(tr))
         if rc != 0:
             raise RuntimeError(f"coopcg_gpu_solve failed: {rc}")
-        e2e_iters += tr.iterations
+        return tr.iterations
+
+    e2e_once()  # warm (pinned registration etc.)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_iters = sum(e2e_once() for _ in range(args.steps))
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    e2e_value = e2e_iters / e2e_s
     h2d = (n + n * p) * 8
     d2h = (n * p + tr.iterations * p) * 8
 
@@ -245,37 +238,72 @@ def run_ours(args, cfg):
     ad_bytes = 8.0 * cfg.n * cfg.n
     ad_flops = 2.0 * cfg.n * cfg.n * cfg.p
     achieved = ad_bytes / (ad_ms * 1e-3) / 1e9
-    traffic = _profile_traffic(cfg.name)
-    line = {
-        "metric": BASELINE_METRIC, "value": value, "unit": "iterations/s", "n_gpus": 1,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded SplitMix64 generators, DESIGN.md §3; A generated on device)",
-        "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "matrix": cfg.matrix,
-                   "iterations_per_step": iters_total // max(args.steps, 1), "arith": args.arith,
-                   "step": "one full solve (setup + iterations + true-residual finalize)",
-                   "l2": f"A = {ad_bytes / 1e9:.2f} GB streamed per iteration (> 126 MB L2)",
-                   "parallelism": "single GPU"},
+    ctx.close()
+    return {
+        "value": iters_total / (elapsed_ms * 1e-3),
+        "ms_per_step": elapsed_ms / args.steps,
+        "iterations_per_step": iters_total // max(args.steps, 1),
+        "exact_rank_checks": exact_rank_checks,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "ad_exact_kernel (Q = A.D)" if args.arith == "exact" else "ad_fast_kernel",
-                     "ad_ms_per_launch": ad_ms, "ad_launches_timed": mv_n,
-                     "peak_source": peak_src,
+                     "frac": achieved / hbm_peak, "traffic": _profile_traffic(f"{cfg.name}_{arith}"),
+                     "kernel": "ad_exact_kernel (Q = A.D)" if arith == "exact" else "ad_fast_kernel (Q = A.D, DMMA)",
+                     "ad_ms_per_launch": ad_ms, "ad_launches_timed": mv_n, "peak_source": peak_src,
                      "fp64": {"achieved_tflops": ad_flops / (ad_ms * 1e-3) / 1e12, "peak_tflops": fp64_peak,
                               "peak_source": "measured DFMA/DMMA probe (tools/probe/fp64_probe.cu)"},
                      "roofline_ms": max(ad_bytes / (hbm_peak * 1e9), ad_flops / (fp64_peak * 1e12)) * 1e3},
-        "e2e": {"value": e2e_value, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
+        "e2e": {"value": e2e_iters / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
-        "gpu_launches": launches,
-        "clocks": clk.summary(),
     }
+
+
+def run_ours(args, cfg):
+    import torch
+    import paper_1204_0069_b200 as m
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        from paper_1204_0069_b200 import sharded
+        return sharded.bench_main(args, cfg, BASELINE_METRIC)
+    dev = args.device
+    torch.cuda.set_device(dev)
+    main_arith = args.arith
+    res = _measure(m, torch, cfg, args, main_arith, dev)
+    line = {
+        "metric": BASELINE_METRIC, "value": res["value"], "unit": "iterations/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["ms_per_step"],
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded SplitMix64 generators, DESIGN.md §3; A generated on device)",
+        "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "matrix": cfg.matrix,
+                   "iterations_per_step": res["iterations_per_step"], "arith": main_arith,
+                   "parity": ("bit-identical to the reference ccg_solve (tests/test_gpu_parity.py)"
+                              if main_arith == "exact" else
+                              "X within 1e-8, pre-floor history within 1e-8 (tests/test_gpu_fast.py)"),
+                   "step": "one full solve (setup + iterations + true-residual finalize)",
+                   "l2": f"A = {8.0 * cfg.n * cfg.n / 1e9:.2f} GB streamed per iteration (> 126 MB L2)",
+                   "parallelism": "single GPU", "exact_rank_fallbacks": res["exact_rank_checks"]},
+        "roofline": res["roofline"],
+        "e2e": res["e2e"],
+        "gpu_launches": res["gpu_launches"],
+        "clocks": res["clocks"],
+    }
+    if not args.no_secondary:
+        other = "fast" if main_arith == "exact" else "exact"
+        r2 = _measure(m, torch, cfg, args, other, dev)
+        line[other] = {"value": r2["value"], "unit": "iterations/s", "ms_per_step": r2["ms_per_step"],
+                       "roofline": r2["roofline"], "e2e": r2["e2e"], "gpu_launches": r2["gpu_launches"],
+                       "clocks": r2["clocks"],
+                       "parity": ("X within 1e-8, pre-floor history within 1e-8, +-2 iterations "
+                                  "(tests/test_gpu_fast.py); not bit-identical by design"
+                                  if other == "fast" else "bit-identical")}
     if not args.no_cpu_baseline:
         walls, kind, cores = cpu_reference_run(cfg, args.cpu_iters)
         secs = sum(walls)
         line["cpu_baseline"] = {"value": len(walls) / secs if secs > 0 else None, "unit": "iterations/s",
                                 "cores": cores, "kind": kind,
-                                "sample": f"{len(walls)} iterations of {cfg.name} (reference per-iteration wall)"}
-    ctx.close()
+                                "sample": f"{len(walls)} iterations of {cfg.name} (parallel_ccg, "
+                                          "reference per-iteration wall times)"}
     print(json.dumps(line))
     return 0
 
@@ -291,6 +319,7 @@ def main():
     ap.add_argument("--device", type=int, default=int(os.environ.get("LOCAL_RANK", "0")))
     ap.add_argument("--cpu-iters", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the other arithmetic mode")
     args = ap.parse_args()
     from paper_1204_0069_b200.configs import CONFIGS
     cfg = CONFIGS[args.config]

@@ -1,0 +1,163 @@
+// gpu_ccg.hpp -- C++ drop-in for the reference's ccg_solve on a B200.
+//
+// Header-only wrapper over the C ABI (coopcg_gpu.h).  It includes the
+// reference's own headers (coopcg/solvers.hpp and what it pulls in) and
+// returns the reference's SolveTrace<double>, so a caller switches with
+//
+//     auto t = coopcg::ccg_solve(A, b, X0, opts);          // CPU reference
+//     auto t = coopcg::gpu_ccg(A, b, X0, opts);            // this library
+//
+// Semantics follow ccg_solve (coopcg/solvers.hpp:325-333): the same shape
+// checks and DimensionError messages (solvers.hpp:300-306), the same statuses
+// (trace.hpp:13-17), SpdViolationError for a nonpositive direction energy
+// (solvers.hpp:111-115), per-iteration records with the reference's mult
+// counting (workplan.hpp:693-715), final_residual_norms by true
+// recomputation (solvers.hpp:188-210).  In the default exact arithmetic mode
+// the trace is bit-identical to ccg_solve's.
+//
+// GpuSolver keeps A resident on the device between solves (SpdMatrix is
+// immutable, dense.hpp:95-96), the common "many right-hand sides" use.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "coopcg/solvers.hpp"
+#include "coopcg_gpu.h"
+
+namespace coopcg {
+
+struct GpuOptions {
+    enum class Arith { exact, fast };
+    int device = 0;
+    Arith arith = Arith::exact;
+};
+
+namespace gpu_detail {
+
+[[noreturn]] inline void raise(int rc, const std::string& msg) {
+    switch (rc) {
+    case COOPCG_E_DIMENSION: throw DimensionError(msg);
+    case COOPCG_E_SPD_VIOLATION: throw SpdViolationError(msg);
+    case COOPCG_E_NUMERICAL_BREAKDOWN: throw NumericalBreakdownError(msg);
+    case COOPCG_E_SINGULAR: throw SingularMatrixError(msg);
+    default: throw Error("coopcg_gpu: " + msg);
+    }
+}
+
+inline std::string last_error(const coopcg_gpu_ctx* ctx) {
+    char buf[512];
+    coopcg_gpu_last_error(ctx, buf, sizeof buf);
+    return buf;
+}
+
+inline TerminalStatus status_of(int s) {
+    switch (s) {
+    case COOPCG_CONVERGED: return TerminalStatus::Converged;
+    case COOPCG_RANK_COLLAPSE: return TerminalStatus::RankCollapse;
+    default: return TerminalStatus::MaxIterations;
+    }
+}
+
+}  // namespace gpu_detail
+
+/// A context bound to one matrix on one GPU; solve() may be called repeatedly.
+class GpuSolver {
+public:
+    GpuSolver(const SpdMatrix<double>& A, int p, const GpuOptions& g = {}) : n_(A.dim()), p_(p) {
+        const int arith = g.arith == GpuOptions::Arith::fast ? COOPCG_ARITH_FAST : COOPCG_ARITH_EXACT;
+        if (p < 1 || p >= n_) throw DimensionError("solver: need 1 <= p < n starting columns");
+        int rc = coopcg_gpu_create(n_, p, g.device, arith, &ctx_);
+        if (rc != COOPCG_OK) gpu_detail::raise(rc, gpu_detail::last_error(nullptr));
+        rc = coopcg_gpu_set_A(ctx_, A.entries().data());
+        if (rc != COOPCG_OK) {
+            const std::string m = gpu_detail::last_error(ctx_);
+            coopcg_gpu_destroy(ctx_);
+            gpu_detail::raise(rc, m);
+        }
+    }
+    GpuSolver(const GpuSolver&) = delete;
+    GpuSolver& operator=(const GpuSolver&) = delete;
+    ~GpuSolver() { coopcg_gpu_destroy(ctx_); }
+
+    SolveTrace<double> solve(const Vec<double>& b, const DenseBlock<double>& X0, const SolveOptions<double>& opts = {}) {
+        // check_block_inputs (solvers.hpp:300-306)
+        if (static_cast<int>(b.size()) != n_ || X0.rows() != n_)
+            throw DimensionError("solver: operand shapes do not match the system matrix");
+        if (X0.cols() < 1 || X0.cols() >= n_) throw DimensionError("solver: need 1 <= p < n starting columns");
+        if (X0.cols() != p_) throw DimensionError("gpu_ccg: agent count differs from the solver's");
+        const int n = n_, p = p_;
+        const int max_iters = opts.max_iters >= 0 ? opts.max_iters : 2 * n;  // solvers.hpp:18-23
+        const int cap = max_iters > 0 ? max_iters : 1;
+        std::vector<double> norms(static_cast<size_t>(cap) * p), minres(cap), init(p), fres(p);
+        std::vector<uint64_t> wall(cap);
+        // DenseBlock is one contiguous column-major buffer (dense.hpp:105-155).
+        std::vector<double> x0(static_cast<size_t>(n) * p), fx(static_cast<size_t>(n) * p);
+        for (int j = 0; j < p; ++j) {
+            auto c = X0.col(j);
+            std::copy(c.begin(), c.end(), x0.begin() + static_cast<size_t>(j) * n);
+        }
+        coopcg_opts o{opts.tol, opts.max_iters, opts.recompute_residual_every, opts.rank_rel_tol};
+        coopcg_trace tr{};
+        tr.capacity = cap;
+        tr.residual_norms = norms.data();
+        tr.minres = minres.data();
+        tr.wall_ns = wall.data();
+        tr.initial_residual_norms = init.data();
+        tr.final_x = fx.data();
+        tr.final_residual_norms = fres.data();
+        const int rc = coopcg_gpu_solve(ctx_, b.data(), x0.data(), &o, &tr);
+        if (rc != COOPCG_OK) gpu_detail::raise(rc, gpu_detail::last_error(ctx_));
+
+        SolveTrace<double> t;
+        const int every = opts.recompute_residual_every >= 0 ? opts.recompute_residual_every : 50;
+        std::vector<int> agents(p);
+        for (int j = 0; j < p; ++j) agents[j] = j;
+        for (int k = 0; k < tr.iterations; ++k) {
+            IterationRecord rec;
+            rec.k = k;
+            rec.active_agents = p;
+            rec.agents = agents;
+            rec.residual_norms.assign(norms.begin() + static_cast<size_t>(k) * p,
+                                      norms.begin() + static_cast<size_t>(k + 1) * p);
+            rec.minres = minres[k];
+            const bool rcmp = detail::recompute_now(k, every);
+            std::uint64_t m = 0;
+            for (int ph = 0; ph < kPhaseCount; ++ph) m += phase_counted_mults(static_cast<Phase>(ph), n, p, rcmp);
+            rec.mults = m;
+            rec.mults_per_worker.assign(p, m);
+            rec.wall_ns = wall[k];
+            t.iterations.push_back(std::move(rec));
+        }
+        t.status = gpu_detail::status_of(tr.status);
+        t.converged_agent = tr.converged_agent;
+        t.final_x = DenseBlock<double>(n, p);
+        for (int j = 0; j < p; ++j)
+            for (int i = 0; i < n; ++i) t.final_x(i, j) = fx[static_cast<size_t>(j) * n + i];
+        t.active_agents = agents;
+        t.initial_residual_norms = init;
+        t.initial_minres = tr.initial_minres;
+        t.final_residual_norms = fres;
+        t.final_minres = tr.final_minres;
+        t.setup_mults = static_cast<std::uint64_t>(n) * static_cast<std::uint64_t>(n);
+        t.loop_wall_ns = tr.loop_wall_ns;
+        t.barriers_per_iteration = 0;
+        return t;
+    }
+
+private:
+    int n_, p_;
+    coopcg_gpu_ctx* ctx_ = nullptr;
+};
+
+/// ccg_solve's signature plus GPU options (solvers.hpp:329-333).
+inline SolveTrace<double> gpu_ccg(const SpdMatrix<double>& A, const Vec<double>& b, const DenseBlock<double>& X0,
+                                  const SolveOptions<double>& opts = {}, const GpuOptions& g = {}) {
+    detail::check_block_inputs(A, b, X0);
+    GpuSolver s(A, X0.cols(), g);
+    return s.solve(b, X0, opts);
+}
+
+}  // namespace coopcg

@@ -160,6 +160,31 @@ int coopcg_gpu_numerical_rank(coopcg_gpu_ctx* ctx, const double* D_colmajor, dou
 int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D_colmajor, double tol,
                                  int force_exact, int* rank);
 
+/* ---- row-sharded (multi-GPU) driving -------------------------------------
+ * A context created with coopcg_gpu_create_shard owns rows [row_begin,
+ * row_end) of A; all n x p blocks are replicated.  The caller runs a solve as
+ *   begin; SETUP_LOCAL; <all-gather R rows>; SETUP_REST;
+ *   for k: ITER_LOCAL(k); <all-gather Q rows>; ITER_MID(k);
+ *          if recompute_at(k): <all-gather R rows>;  ITER_REST(k);
+ *          (poll coopcg_gpu_state now and then; after a stop, phases are no-ops)
+ *   FINAL_LOCAL; <all-gather S rows>; FINAL_REST; end.
+ * A "local" phase writes only this context's rows of the named block;
+ * coopcg_gpu_block returns the device pointer (row-major, leading dimension
+ * `ld` doubles) for the exchange.  All work is ordered on the context stream
+ * (coopcg_gpu_stream).  DESIGN.md §7; paper_1204_0069_b200/sharded.py. */
+enum coopcg_phase {
+    COOPCG_PH_SETUP_LOCAL = 0, COOPCG_PH_SETUP_REST = 1,
+    COOPCG_PH_ITER_LOCAL = 2, COOPCG_PH_ITER_MID = 3, COOPCG_PH_ITER_REST = 4,
+    COOPCG_PH_FINAL_LOCAL = 5, COOPCG_PH_FINAL_REST = 6
+};
+enum coopcg_block { COOPCG_BLOCK_X = 0, COOPCG_BLOCK_R = 1, COOPCG_BLOCK_D = 2, COOPCG_BLOCK_Q = 3, COOPCG_BLOCK_S = 4 };
+int coopcg_gpu_begin(coopcg_gpu_ctx* ctx, const coopcg_opts* opts);
+int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k);
+int coopcg_gpu_recompute_at(const coopcg_gpu_ctx* ctx, int k);
+int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int* ld);
+int coopcg_gpu_state(coopcg_gpu_ctx* ctx, int* stop, int* iterations);
+int coopcg_gpu_end(coopcg_gpu_ctx* ctx, coopcg_trace* trace);
+
 #ifdef __cplusplus
 }
 #endif

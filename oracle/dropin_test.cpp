@@ -1,0 +1,103 @@
+// dropin_test.cpp -- TEST INFRASTRUCTURE.  Compares the C++ drop-in
+// coopcg::gpu_ccg (include/coopcg/gpu_ccg.hpp) with the reference's own
+// coopcg::ccg_solve, field by field, bit for bit (exact mode), through the
+// reference's types.  Built by `make -C oracle dropin` against the reference
+// headers (this container); the binary travels to the GPU box and
+// tests/test_gpu_dropin.py runs it.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "coopcg/gpu_ccg.hpp"
+#include "coopcg/problem.hpp"
+#include "coopcg/solvers.hpp"
+
+using namespace coopcg;
+
+static int failures = 0;
+
+static bool same(double a, double b) { return std::memcmp(&a, &b, sizeof a) == 0; }
+
+static void compare(const char* name, const SolveTrace<double>& r, const SolveTrace<double>& g) {
+    bool ok = r.status == g.status && r.converged_agent == g.converged_agent &&
+              r.iteration_count() == g.iteration_count() && r.final_x == g.final_x &&
+              r.active_agents == g.active_agents && r.setup_mults == g.setup_mults &&
+              same(r.initial_minres, g.initial_minres) && same(r.final_minres, g.final_minres) &&
+              r.initial_residual_norms.size() == g.initial_residual_norms.size() &&
+              r.final_residual_norms.size() == g.final_residual_norms.size();
+    for (size_t i = 0; ok && i < r.initial_residual_norms.size(); ++i)
+        ok = same(r.initial_residual_norms[i], g.initial_residual_norms[i]);
+    for (size_t i = 0; ok && i < r.final_residual_norms.size(); ++i)
+        ok = same(r.final_residual_norms[i], g.final_residual_norms[i]);
+    for (int k = 0; ok && k < r.iteration_count(); ++k) {
+        const auto& a = r.iterations[k];
+        const auto& b = g.iterations[k];
+        ok = a.k == b.k && a.active_agents == b.active_agents && a.agents == b.agents && same(a.minres, b.minres) &&
+             a.mults == b.mults && a.mults_per_worker == b.mults_per_worker &&
+             a.residual_norms.size() == b.residual_norms.size();
+        for (size_t j = 0; ok && j < a.residual_norms.size(); ++j) ok = same(a.residual_norms[j], b.residual_norms[j]);
+    }
+    std::printf("%-34s %-14s it=%4d  %s\n", name, to_string(g.status), g.iteration_count(), ok ? "bit-identical" : "MISMATCH");
+    if (!ok) ++failures;
+}
+
+int main() {
+    struct Case { int n, p; double cond; unsigned long long seed; double tol; int max_iters; int recompute; };
+    const Case cases[] = {
+        {60, 3, 1e2, 1, 1e-8, -1, -1}, {120, 4, 1e3, 7, 1e-9, -1, -1}, {150, 8, 1e4, 3, 1e-8, -1, -1},
+        {200, 1, 1e3, 5, 1e-10, -1, -1}, {96, 4, 1e3, 7, 1e-8, -1, 1}, {96, 4, 1e3, 7, 1e-8, -1, 0},
+        {300, 16, 1e2, 11, 0.0, 40, -1}, {128, 32, 1e1, 12, 1e-12, -1, -1},
+    };
+    for (const auto& c : cases) {
+        ProblemSpec spec;
+        spec.n = c.n;
+        spec.p = c.p;
+        spec.cond = c.cond;
+        spec.seed = c.seed;
+        auto inst = make_problem<double>(spec);
+        SolveOptions<double> o;
+        o.tol = c.tol;
+        o.max_iters = c.max_iters;
+        o.recompute_residual_every = c.recompute;
+        char name[96];
+        std::snprintf(name, sizeof name, "make_problem n=%d p=%d cond=%.0e", c.n, c.p, c.cond);
+        compare(name, ccg_solve(inst.A, inst.b, inst.X0, o), gpu_ccg(inst.A, inst.b, inst.X0, o));
+    }
+    {   // degenerate start: x0 = 0 for every agent -> rank collapse at k = 0
+        ProblemSpec spec;
+        spec.n = 80;
+        spec.p = 3;
+        spec.cond = 10.0;
+        spec.seed = 2;
+        auto inst = make_problem<double>(spec);
+        DenseBlock<double> z(80, 3);
+        SolveOptions<double> o;
+        o.tol = 1e-8;
+        compare("degenerate x0 = 0", ccg_solve(inst.A, inst.b, z, o), gpu_ccg(inst.A, inst.b, z, o));
+        // GpuSolver: A resident, two right-hand sides
+        GpuSolver s(inst.A, 3);
+        compare("GpuSolver reuse #1", ccg_solve(inst.A, inst.b, inst.X0, o), s.solve(inst.b, inst.X0, o));
+        compare("GpuSolver reuse #2", ccg_solve(inst.A, inst.b, inst.X0, o), s.solve(inst.b, inst.X0, o));
+    }
+    {   // error behaviour: indefinite matrix -> SpdViolationError; bad shapes -> DimensionError
+        const int n = 30;
+        std::vector<double> e(static_cast<size_t>(n) * n, 0.0);
+        for (int i = 0; i < n; ++i) e[static_cast<size_t>(i) * n + i] = -1.0;
+        SpdMatrix<double> A(n, e, SpdCheck::skip);
+        Vec<double> b(n, 1.0);
+        DenseBlock<double> X0(n, 2);
+        for (int i = 0; i < n; ++i) X0(i, 1) = 0.01 * i;
+        std::string ref_msg, gpu_msg;
+        try { ccg_solve(A, b, X0, {}); } catch (const SpdViolationError& ex) { ref_msg = ex.what(); }
+        try { gpu_ccg(A, b, X0, {}); } catch (const SpdViolationError& ex) { gpu_msg = ex.what(); }
+        const bool ok = !ref_msg.empty() && ref_msg == gpu_msg;
+        std::printf("%-34s %s (\"%s\")\n", "SpdViolationError", ok ? "same exception" : "MISMATCH", gpu_msg.c_str());
+        if (!ok) ++failures;
+        bool dim = false;
+        try { gpu_ccg(A, Vec<double>(n - 1, 1.0), X0, {}); } catch (const DimensionError&) { dim = true; }
+        std::printf("%-34s %s\n", "DimensionError", dim ? "same exception" : "MISMATCH");
+        if (!dim) ++failures;
+    }
+    std::printf("DROPIN %s (%d failures)\n", failures ? "FAIL" : "OK", failures);
+    return failures ? 1 : 0;
+}

@@ -62,7 +62,16 @@ SIGNATURES = [
     ("coopcg_gpu_matvec_block", _I, [_VP, _VP, _VP]),
     ("coopcg_gpu_numerical_rank", _I, [_VP, _VP, C.c_double, C.POINTER(_I)]),
     ("coopcg_gpu_numerical_rank_ex", _I, [_VP, _VP, C.c_double, _I, C.POINTER(_I)]),
+    ("coopcg_gpu_begin", _I, [_VP, C.POINTER(coopcg_opts)]),
+    ("coopcg_gpu_phase", _I, [_VP, _I, _I]),
+    ("coopcg_gpu_recompute_at", _I, [_VP, _I]),
+    ("coopcg_gpu_block", _I, [_VP, _I, _I, C.POINTER(_VP), C.POINTER(_I)]),
+    ("coopcg_gpu_state", _I, [_VP, C.POINTER(_I), C.POINTER(_I)]),
+    ("coopcg_gpu_end", _I, [_VP, C.POINTER(coopcg_trace)]),
 ]
+
+PH_SETUP_LOCAL, PH_SETUP_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST, PH_FINAL_LOCAL, PH_FINAL_REST = range(7)
+BLOCK_X, BLOCK_R, BLOCK_D, BLOCK_Q, BLOCK_S = range(5)
 
 _lib = None
 

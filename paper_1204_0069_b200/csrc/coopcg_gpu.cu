@@ -95,6 +95,7 @@ struct coopcg_gpu_ctx {
     cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
     coopcg_timing timing{};
     long long launches = 0;  // kernels launched since the last run started
+    int max_iters = 0, every = 50;  // resolved SolveOptions of the current solve
 };
 
 namespace {
@@ -665,63 +666,284 @@ int coopcg_gpu_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0) {
     return COOPCG_OK;
 }
 
-static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* trace) {
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// The solve, split into phases so that a row-sharded (multi-GPU) caller can
+// exchange rows between them.  "local" phases touch only this
+// context's rows [row0, row1) of the output block; everything else works on
+// the full, replicated n x P blocks.  A single-GPU solve runs the phases back
+// to back (run_impl); sharded.py runs them with an all-gather in between.
+#define LAUNCHED()              \
+    do {                        \
+        CKL();                  \
+        ++ctx->launches;        \
+    } while (0)
+
+static bool sharded(const coopcg_gpu_ctx* ctx) { return ctx->n_loc != ctx->n; }
+static int dgrid_of(const coopcg_gpu_ctx* ctx) {
+    if (ctx->arith == COOPCG_ARITH_FAST) return ctx->f_ugrid;
+    const int rows_per_tile = 256 / ctx->P;
+    return std::min(ctx->nparts, (ctx->n + rows_per_tile - 1) / rows_per_tile);
+}
+
+// fast_rows over arbitrary (Qpart, kchunks, rows) -- the local row pass or a
+// full-n Gram pass over a replicated block (Qpart = the block itself).
+template <int P>
+cudaError_t fast_rows_any_t(coopcg_gpu_ctx* ctx, const double* qpart, int kchunks, int nrows, int row0, double* dst,
+                            const double* b, const double* D, const double* R, const double* Qfull, int mode,
+                            const int* stop) {
+    fast_rows_kernel<P><<<ctx->f_rgrid, 256, 0, ctx->stream>>>(qpart, kchunks, nrows, row0, dst, b, D, R, Qfull,
+                                                               ctx->p, mode, ctx->gpart, stop);
+    ++ctx->launches;
+    return cudaGetLastError();
+}
+static cudaError_t fast_rows_any(coopcg_gpu_ctx* ctx, const double* qpart, int kchunks, int nrows, int row0,
+                                 double* dst, const double* b, const double* D, const double* R,
+                                 const double* Qfull, int mode, const int* stop) {
+    switch (ctx->P) {
+    case 8: return fast_rows_any_t<8>(ctx, qpart, kchunks, nrows, row0, dst, b, D, R, Qfull, mode, stop);
+    case 16: return fast_rows_any_t<16>(ctx, qpart, kchunks, nrows, row0, dst, b, D, R, Qfull, mode, stop);
+    default: return fast_rows_any_t<32>(ctx, qpart, kchunks, nrows, row0, dst, b, D, R, Qfull, mode, stop);
+    }
+}
+
+static int begin_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     if (!ctx->a_ready) return fail(ctx, COOPCG_E_STATE, "A not set (coopcg_gpu_set_A / coopcg_gpu_gen_A)");
     if (!ctx->inputs_ready) return fail(ctx, COOPCG_E_STATE, "b / X0 not uploaded");
-    if (ctx->n_loc != ctx->n)
-        return fail(ctx, COOPCG_E_STATE, "sharded contexts are driven by the multi-GPU orchestrator");
-    const int n = ctx->n, p = ctx->p, P = ctx->P;
     coopcg_opts o{0.0, -1, -1, 1e-10};
     if (opts) o = *opts;
-    const int max_iters = o.max_iters >= 0 ? o.max_iters : 2 * n;      // solvers.hpp:18-23
-    const int every = o.recompute_residual_every >= 0 ? o.recompute_residual_every : 50;
-    if (int rc = ensure_trace_capacity(ctx, std::max(max_iters, 1))) return rc;
-    cudaStream_t st = ctx->stream;
-
+    ctx->max_iters = o.max_iters >= 0 ? o.max_iters : 2 * ctx->n;  // solvers.hpp:18-23
+    ctx->every = o.recompute_residual_every >= 0 ? o.recompute_residual_every : 50;
+    if (int rc = ensure_trace_capacity(ctx, std::max(ctx->max_iters, 1))) return rc;
     Ctl h{};
     h.stop = 0;
     h.status = COOPCG_MAX_ITERATIONS;
-    h.err = 0;
     h.k = 0;
-    h.iterations = 0;
     h.converged_agent = -1;
     h.tol = o.tol;
     h.rank_rel_tol = o.rank_rel_tol;
-    h.max_iters = max_iters;
-    h.p = p;
-    h.P = P;
+    h.max_iters = ctx->max_iters;
+    h.p = ctx->p;
+    h.P = ctx->P;
     std::memcpy(&ctx->ctl_host[0], &h, sizeof(Ctl));
-    CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_host[0], sizeof(Ctl), cudaMemcpyHostToDevice, st));
-    int* stop = &ctx->ctl->stop;
-    const SmallLayout L{P};
-
+    CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_host[0], sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
     ctx->launches = 0;
-    const bool fast = ctx->arith == COOPCG_ARITH_FAST;
-    CK(cudaEventRecord(ctx->ev_run0, st));
-    // ---- setup: stage_setup + setup_coordinator (solvers.hpp:263-264) ----
-    const int rows_per_tile = 256 / P;
-    const int dgrid = fast ? ctx->f_ugrid : std::min(ctx->nparts, (n + rows_per_tile - 1) / rows_per_tile);
-    if (!fast) {
+    return COOPCG_OK;
+}
+
+// R_loc = A_loc X - b (stage_setup, block_cg.hpp:132-138)
+static int setup_local(coopcg_gpu_ctx* ctx) {
+    if (ctx->arith != COOPCG_ARITH_FAST) {
         CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, nullptr));
-        CK(cudaMemcpyAsync(ctx->Dblk[0], ctx->R, sizeof(double) * (size_t)n * P, cudaMemcpyDeviceToDevice, st));
-        CK(chains_launch(ctx, kPhSetup, ctx->R, nullptr, nullptr, 1, nullptr));
-        setup_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->init_norms);
     } else {
         CK(fast_ad(ctx, ctx->X, nullptr));
         CK(fast_rows(ctx, ctx->R, ctx->b, nullptr, nullptr, nullptr, 1, nullptr));
-        CK(cudaMemcpyAsync(ctx->Dblk[0], ctx->R, sizeof(double) * (size_t)n * P, cudaMemcpyDeviceToDevice, st));
-        fast_norms_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->ctl,
-                                            ctx->init_norms, 1, ctx->small);
     }
-    CKL();
-    ++ctx->launches;
+    return COOPCG_OK;
+}
+
+// D = R, norms, tolerance and rank checks (block_cg.hpp:139-144, solvers.hpp:55-100)
+static int setup_rest(coopcg_gpu_ctx* ctx) {
+    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    cudaStream_t st = ctx->stream;
+    int* stop = &ctx->ctl->stop;
+    const bool fast = ctx->arith == COOPCG_ARITH_FAST;
+    CK(cudaMemcpyAsync(ctx->Dblk[0], ctx->R, sizeof(double) * (size_t)n * P, cudaMemcpyDeviceToDevice, st));
+    if (!fast) {
+        CK(chains_launch(ctx, kPhSetup, ctx->R, nullptr, nullptr, 1, nullptr));
+        setup_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->init_norms);
+    } else {
+        if (sharded(ctx))  // full-n residual norms over the replicated R
+            CK(fast_rows_any(ctx, ctx->R, 1, n, 0, ctx->R, nullptr, nullptr, nullptr, nullptr, 1, nullptr));
+        fast_norms_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->ctl,
+                                             ctx->init_norms, 1, ctx->small);
+    }
+    LAUNCHED();
+    const int dgrid = dgrid_of(ctx);
     direction_kernel<<<dgrid, 256, 0, st>>>(nullptr, ctx->Dblk[0], nullptr, nullptr, n, p, P, ctx->partials, stop);
-    CKL();
-    ++ctx->launches;
+    LAUNCHED();
     rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[0], ctx->V, n, ctx->ctl, 1,
                                                    fast ? ctx->small : nullptr);
-    CKL();
-    ++ctx->launches;
+    LAUNCHED();
+    return COOPCG_OK;
+}
+
+// Q_loc = A_loc D_k  (stage_matvec, block_cg.hpp:146-151), bracketed by events.
+static int iter_local(coopcg_gpu_ctx* ctx, int k, cudaEvent_t ev0, cudaEvent_t ev1) {
+    int* stop = &ctx->ctl->stop;
+    double* D = ctx->Dblk[k & 1];
+    if (ev0) CK(cudaEventRecord(ev0, ctx->stream));
+    if (ctx->arith != COOPCG_ARITH_FAST) {
+        CK(ad_launch(ctx, D, ctx->Q, nullptr, stop));
+        if (ev1) CK(cudaEventRecord(ev1, ctx->stream));
+    } else {
+        CK(fast_ad(ctx, D, stop));
+        if (ev1) CK(cudaEventRecord(ev1, ctx->stream));
+        // single GPU: fuse the four Gram partials into the local row pass
+        CK(fast_rows(ctx, ctx->Q, nullptr, D, ctx->R, nullptr, sharded(ctx) ? 1 : 0, stop));
+    }
+    return COOPCG_OK;
+}
+
+static bool recompute_at(const coopcg_gpu_ctx* ctx, int k) {
+    return ctx->every > 0 && (k + 1) % ctx->every == 0;  // solvers.hpp:33-35
+}
+
+// After Q is complete: Grams, alpha, update; in recompute iterations ends with
+// R_loc = A_loc X - b (the caller exchanges R before iter_rest).
+static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
+    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    cudaStream_t st = ctx->stream;
+    int* stop = &ctx->ctl->stop;
+    double* D = ctx->Dblk[k & 1];
+    double* Dn = ctx->Dblk[(k + 1) & 1];
+    const bool rec = recompute_at(ctx, k);
+    if (ctx->arith != COOPCG_ARITH_FAST) {
+        CK(chains_launch(ctx, kPhGram, D, ctx->Q, ctx->R, 3, stop));
+        solve_alpha_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl);
+        LAUNCHED();
+        update_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->R, ctx->X, ctx->Q, D, ctx->small, n, p, P,
+                                                                    rec ? 1 : 0, stop);
+        LAUNCHED();
+        if (rec) CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, stop));
+    } else {
+        if (sharded(ctx))  // the four Gram partials over the full replicated blocks
+            CK(fast_rows_any(ctx, ctx->Q, 1, n, 0, ctx->Q, nullptr, D, ctx->R, nullptr, 0, stop));
+        if (!rec) {
+            CK(fast_solve(ctx, 0));
+            CK(fast_update(ctx, D, Dn, 0, stop));
+            fast_record_kernel<<<1, 256, 0, st>>>(ctx->npart, ctx->f_ugrid, P, 0, 1, ctx->small, ctx->ctl,
+                                                  ctx->tr_norms, ctx->tr_minres, ctx->tr_wall, ctx->tr_capacity);
+            LAUNCHED();
+        } else {
+            CK(fast_solve(ctx, 1));
+            CK(fast_update(ctx, D, Dn, 1, stop));
+            CK(fast_ad(ctx, ctx->X, stop));
+            // local rows of R = A X - b (with R^T Q / |R|^2 partials when unsharded)
+            CK(fast_rows(ctx, ctx->R, ctx->b, nullptr, nullptr, sharded(ctx) ? nullptr : ctx->Q, 1, stop));
+        }
+    }
+    return COOPCG_OK;
+}
+
+// The rest of the iteration: beta, D', norms/record, rank check, k++.
+static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
+    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    cudaStream_t st = ctx->stream;
+    int* stop = &ctx->ctl->stop;
+    double* D = ctx->Dblk[k & 1];
+    double* Dn = ctx->Dblk[(k + 1) & 1];
+    const bool rec = recompute_at(ctx, k);
+    const bool fast = ctx->arith == COOPCG_ARITH_FAST;
+    if (!fast) {
+        CK(chains_launch(ctx, kPhBeta, ctx->R, ctx->Q, nullptr, 2, stop));
+        solve_beta_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
+                                            ctx->tr_capacity);
+        LAUNCHED();
+        direction_kernel<<<dgrid_of(ctx), 256, 0, st>>>(ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop);
+        LAUNCHED();
+    } else if (rec) {
+        if (sharded(ctx))  // R^T Q and |R|^2 over the full replicated, recomputed R
+            CK(fast_rows_any(ctx, ctx->R, 1, n, 0, ctx->R, nullptr, nullptr, nullptr, ctx->Q, 1, stop));
+        CK(fast_solve(ctx, 2));
+        CK(fast_update(ctx, D, Dn, 2, stop));
+        fast_record_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->small,
+                                              ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
+                                              ctx->tr_capacity);
+        LAUNCHED();
+    }
+    rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid_of(ctx), Dn, ctx->V, n, ctx->ctl, 0,
+                                                   fast ? ctx->small : nullptr);
+    LAUNCHED();
+    return COOPCG_OK;
+}
+
+// S_loc = A_loc X - b (finalize_trace, solvers.hpp:196-205)
+static int final_local(coopcg_gpu_ctx* ctx) {
+    if (ctx->arith != COOPCG_ARITH_FAST) {
+        CK(ad_launch(ctx, ctx->X, ctx->S, ctx->b, nullptr));
+    } else {
+        CK(fast_ad(ctx, ctx->X, nullptr));
+        CK(fast_rows(ctx, ctx->S, ctx->b, nullptr, nullptr, nullptr, 1, nullptr));
+    }
+    return COOPCG_OK;
+}
+
+static int final_rest(coopcg_gpu_ctx* ctx) {
+    const int n = ctx->n, P = ctx->P;
+    cudaStream_t st = ctx->stream;
+    if (ctx->arith != COOPCG_ARITH_FAST) {
+        CK(chains_launch(ctx, kPhFinal, ctx->S, nullptr, nullptr, 1, nullptr));
+        final_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->final_norms);
+    } else {
+        if (sharded(ctx))
+            CK(fast_rows_any(ctx, ctx->S, 1, n, 0, ctx->S, nullptr, nullptr, nullptr, nullptr, 1, nullptr));
+        fast_norms_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->ctl,
+                                             ctx->final_norms, 0, ctx->small);
+    }
+    LAUNCHED();
+    return COOPCG_OK;
+}
+
+// Copy the trace out (after the stream is synchronised).
+static int end_impl(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
+    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    cudaStream_t st = ctx->stream;
+    CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const Ctl& fin = ctx->ctl_host[0];
+    if (trace) {
+        const int iters = fin.iterations;
+        trace->status = fin.status;
+        trace->converged_agent = fin.converged_agent;
+        trace->iterations = iters;
+        trace->exact_rank_checks = fin.exact_rank_checks;
+        const int cap = std::min(iters, trace->capacity);
+        std::vector<unsigned long long> wall(std::max(iters, 1));
+        if (iters > 0)
+            CK(cudaMemcpy(wall.data(), ctx->tr_wall, sizeof(unsigned long long) * iters, cudaMemcpyDeviceToHost));
+        uint64_t total = 0;
+        for (int k = 0; k < iters; ++k) total += wall[k];
+        trace->loop_wall_ns = total;
+        if (cap > 0) {
+            if (trace->residual_norms)
+                CK(cudaMemcpy(trace->residual_norms, ctx->tr_norms, sizeof(double) * (size_t)cap * p,
+                              cudaMemcpyDeviceToHost));
+            if (trace->minres)
+                CK(cudaMemcpy(trace->minres, ctx->tr_minres, sizeof(double) * cap, cudaMemcpyDeviceToHost));
+            if (trace->wall_ns) std::memcpy(trace->wall_ns, wall.data(), sizeof(uint64_t) * cap);
+        }
+        std::vector<double> tmp(P + 1);
+        CK(cudaMemcpy(tmp.data(), ctx->init_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
+        if (trace->initial_residual_norms) std::memcpy(trace->initial_residual_norms, tmp.data(), sizeof(double) * p);
+        trace->initial_minres = tmp[p];
+        CK(cudaMemcpy(tmp.data(), ctx->final_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
+        if (trace->final_residual_norms) std::memcpy(trace->final_residual_norms, tmp.data(), sizeof(double) * p);
+        trace->final_minres = tmp[p];
+        if (trace->final_x) {
+            rowmajor_to_colmajor_kernel<<<grid_for((size_t)n * p, 256), 256, 0, st>>>(ctx->X, ctx->stage, n, p, P);
+            CKL();
+            CK(cudaMemcpyAsync(trace->final_x, ctx->stage, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost,
+                               st));
+            CK(cudaStreamSynchronize(st));
+        }
+    }
+    if (fin.err == COOPCG_E_SPD_VIOLATION)
+        return fail(ctx, COOPCG_E_SPD_VIOLATION, "nonpositive direction energy d^T A d at iteration %d",
+                    fin.err_iter);  // solvers.hpp:111-115
+    return COOPCG_OK;
+}
+
+static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* trace) {
+    if (sharded(ctx))
+        return fail(ctx, COOPCG_E_STATE, "row-sharded contexts are driven phase by phase (coopcg_gpu_phase)");
+    if (int rc = begin_impl(ctx, opts)) return rc;
+    cudaStream_t st = ctx->stream;
+    const int max_iters = ctx->max_iters;
+    CK(cudaEventRecord(ctx->ev_run0, st));
+    if (int rc = setup_local(ctx)) return rc;
+    if (int rc = setup_rest(ctx)) return rc;
     CK(cudaEventRecord(ctx->ev_loop0, st));
 
     // ---- main loop, enqueued in chunks; device-side stop makes extras no-ops ----
@@ -767,58 +989,11 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
         chunk_iters[slot] = U;
         chunk_k0[slot] = k_host;
         for (int u = 0; u < U; ++u, ++k_host) {
-            double* D = ctx->Dblk[k_host & 1];
-            double* Dn = ctx->Dblk[(k_host + 1) & 1];
-            const bool recompute = every > 0 && (k_host + 1) % every == 0;  // solvers.hpp:33-35
-            CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2], st));
-            if (!fast) {
-                CK(ad_launch(ctx, D, ctx->Q, nullptr, stop));
-                CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1], st));
-                CK(chains_launch(ctx, kPhGram, D, ctx->Q, ctx->R, 3, stop));
-                solve_alpha_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl);
-                CKL();
-                ++ctx->launches;
-                update_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->R, ctx->X, ctx->Q, D, ctx->small, n,
-                                                                            p, P, recompute ? 1 : 0, stop);
-                CKL();
-                ++ctx->launches;
-                if (recompute) CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, stop));
-                CK(chains_launch(ctx, kPhBeta, ctx->R, ctx->Q, nullptr, 2, stop));
-                solve_beta_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres,
-                                                    ctx->tr_wall, ctx->tr_capacity);
-                CKL();
-                ++ctx->launches;
-                direction_kernel<<<dgrid, 256, 0, st>>>(ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop);
-                CKL();
-                ++ctx->launches;
-            } else {
-                CK(fast_ad(ctx, D, stop));
-                CK(cudaEventRecord(ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1], st));
-                CK(fast_rows(ctx, ctx->Q, nullptr, D, ctx->R, nullptr, 0, stop));
-                if (!recompute) {
-                    CK(fast_solve(ctx, 0));
-                    CK(fast_update(ctx, D, Dn, 0, stop));
-                    fast_record_kernel<<<1, 256, 0, st>>>(ctx->npart, ctx->f_ugrid, P, 0, 1, ctx->small, ctx->ctl,
-                                                          ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
-                                                          ctx->tr_capacity);
-                } else {
-                    CK(fast_solve(ctx, 1));
-                    CK(fast_update(ctx, D, Dn, 1, stop));
-                    CK(fast_ad(ctx, ctx->X, stop));
-                    CK(fast_rows(ctx, ctx->R, ctx->b, nullptr, nullptr, ctx->Q, 1, stop));
-                    CK(fast_solve(ctx, 2));
-                    CK(fast_update(ctx, D, Dn, 2, stop));
-                    fast_record_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1,
-                                                          ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres,
-                                                          ctx->tr_wall, ctx->tr_capacity);
-                }
-                CKL();
-                ++ctx->launches;
-            }
-            rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, Dn, ctx->V, n, ctx->ctl, 0,
-                                                           fast ? ctx->small : nullptr);
-            CKL();
-            ++ctx->launches;
+            if (int rc = iter_local(ctx, k_host, ctx->mv_ev[(slot * kChunkMax + u) * 2],
+                                    ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1]))
+                return rc;
+            if (int rc = iter_mid(ctx, k_host)) return rc;
+            if (int rc = iter_rest(ctx, k_host)) return rc;
         }
         CK(cudaMemcpyAsync(&ctx->ctl_host[slot], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(ctx->ev_chunk[slot], st));
@@ -829,25 +1004,10 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     for (int q = 0; q < npending; ++q)
         if (int rc = read_chunk(pending[q])) return rc;
     CK(cudaEventRecord(ctx->ev_loop1, st));
-
-    // ---- finalize_trace (solvers.hpp:188-210) ----
-    if (!fast) {
-        CK(ad_launch(ctx, ctx->X, ctx->S, ctx->b, nullptr));
-        CK(chains_launch(ctx, kPhFinal, ctx->S, nullptr, nullptr, 1, nullptr));
-        final_norms_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->final_norms);
-    } else {
-        CK(fast_ad(ctx, ctx->X, nullptr));
-        CK(fast_rows(ctx, ctx->S, ctx->b, nullptr, nullptr, nullptr, 1, nullptr));
-        fast_norms_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->ctl,
-                                            ctx->final_norms, 0, ctx->small);
-    }
-    CKL();
-    ++ctx->launches;
+    if (int rc = final_local(ctx)) return rc;
+    if (int rc = final_rest(ctx)) return rc;
     CK(cudaEventRecord(ctx->ev_run1, st));
-    CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    const Ctl& fin = ctx->ctl_host[0];
-
     float run_ms = 0.f, loop_ms = 0.f;
     CK(cudaEventElapsedTime(&run_ms, ctx->ev_run0, ctx->ev_run1));
     CK(cudaEventElapsedTime(&loop_ms, ctx->ev_loop0, ctx->ev_loop1));
@@ -856,51 +1016,71 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     ctx->timing.matvec_ms_total = mv_total;
     ctx->timing.matvec_launches = mv_count;
     ctx->timing.kernel_launches = ctx->launches;
-
-    if (trace) {
-        const int iters = fin.iterations;
-        trace->status = fin.status;
-        trace->converged_agent = fin.converged_agent;
-        trace->iterations = iters;
-        trace->exact_rank_checks = fin.exact_rank_checks;
-        const int cap = std::min(iters, trace->capacity);
-        std::vector<unsigned long long> wall(std::max(iters, 1));
-        if (iters > 0) CK(cudaMemcpy(wall.data(), ctx->tr_wall, sizeof(unsigned long long) * iters, cudaMemcpyDeviceToHost));
-        uint64_t total = 0;
-        for (int k = 0; k < iters; ++k) total += wall[k];
-        trace->loop_wall_ns = total;
-        if (cap > 0) {
-            if (trace->residual_norms)
-                CK(cudaMemcpy(trace->residual_norms, ctx->tr_norms, sizeof(double) * (size_t)cap * p,
-                              cudaMemcpyDeviceToHost));
-            if (trace->minres) CK(cudaMemcpy(trace->minres, ctx->tr_minres, sizeof(double) * cap, cudaMemcpyDeviceToHost));
-            if (trace->wall_ns) std::memcpy(trace->wall_ns, wall.data(), sizeof(uint64_t) * cap);
-        }
-        std::vector<double> tmp(P + 1);
-        CK(cudaMemcpy(tmp.data(), ctx->init_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
-        if (trace->initial_residual_norms) std::memcpy(trace->initial_residual_norms, tmp.data(), sizeof(double) * p);
-        trace->initial_minres = tmp[p];
-        CK(cudaMemcpy(tmp.data(), ctx->final_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
-        if (trace->final_residual_norms) std::memcpy(trace->final_residual_norms, tmp.data(), sizeof(double) * p);
-        trace->final_minres = tmp[p];
-        if (trace->final_x) {
-            rowmajor_to_colmajor_kernel<<<grid_for((size_t)n * p, 256), 256, 0, st>>>(ctx->X, ctx->stage, n, p, P);
-            CKL();
-    ++ctx->launches;
-            CK(cudaMemcpyAsync(trace->final_x, ctx->stage, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-        }
-    }
-    if (fin.err == COOPCG_E_SPD_VIOLATION)
-        return fail(ctx, COOPCG_E_SPD_VIOLATION, "nonpositive direction energy d^T A d at iteration %d",
-                    fin.err_iter);  // solvers.hpp:111-115
-    return COOPCG_OK;
+    return end_impl(ctx, trace);
 }
+
+extern "C" {
 
 int coopcg_gpu_run(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* trace) {
     if (!ctx) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     return run_impl(ctx, opts, trace);
+}
+
+int coopcg_gpu_begin(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
+    if (!ctx) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    return begin_impl(ctx, opts);
+}
+
+int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k) {
+    if (!ctx) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    switch (phase) {
+    case COOPCG_PH_SETUP_LOCAL: return setup_local(ctx);
+    case COOPCG_PH_SETUP_REST: return setup_rest(ctx);
+    case COOPCG_PH_ITER_LOCAL: return iter_local(ctx, k, nullptr, nullptr);
+    case COOPCG_PH_ITER_MID: return iter_mid(ctx, k);
+    case COOPCG_PH_ITER_REST: return iter_rest(ctx, k);
+    case COOPCG_PH_FINAL_LOCAL: return final_local(ctx);
+    case COOPCG_PH_FINAL_REST: return final_rest(ctx);
+    default: return fail(ctx, COOPCG_E_INVALID, "unknown phase %d", phase);
+    }
+}
+
+int coopcg_gpu_recompute_at(const coopcg_gpu_ctx* ctx, int k) { return ctx ? (recompute_at(ctx, k) ? 1 : 0) : 0; }
+
+int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int* ld) {
+    if (!ctx || !dev_ptr) return COOPCG_E_INVALID;
+    double* b = nullptr;
+    switch (which) {
+    case COOPCG_BLOCK_X: b = ctx->X; break;
+    case COOPCG_BLOCK_R: b = ctx->R; break;
+    case COOPCG_BLOCK_D: b = ctx->Dblk[k & 1]; break;
+    case COOPCG_BLOCK_Q: b = ctx->Q; break;
+    case COOPCG_BLOCK_S: b = ctx->S; break;
+    default: return fail(ctx, COOPCG_E_INVALID, "unknown block %d", which);
+    }
+    *dev_ptr = b;
+    if (ld) *ld = ctx->P;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_state(coopcg_gpu_ctx* ctx, int* stop, int* iterations) {
+    if (!ctx) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpyAsync(&ctx->ctl_host[1], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (stop) *stop = ctx->ctl_host[1].stop;
+    if (iterations) *iterations = ctx->ctl_host[1].iterations;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_end(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
+    if (!ctx) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    ctx->timing.kernel_launches = ctx->launches;
+    return end_impl(ctx, trace);
 }
 
 int coopcg_gpu_solve(coopcg_gpu_ctx* ctx, const double* b, const double* X0, const coopcg_opts* opts,

@@ -1,0 +1,122 @@
+"""The row-sharded phase API of the CUDA library (include/coopcg_gpu.h) with
+two shard contexts on one GPU, exchanged in-process in lockstep (host-driven
+copies between phases; no kernel ever waits on another).  Exact mode must be
+bit-identical to the single-context solve and to the oracle; fast mode within
+the fast-mode tolerances."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+from paper_1204_0069_b200.sharded import (BLOCK_Q, BLOCK_R, BLOCK_S, PH_FINAL_LOCAL, PH_FINAL_REST, PH_ITER_LOCAL,
+                                          PH_ITER_MID, PH_ITER_REST, PH_SETUP_LOCAL, PH_SETUP_REST,
+                                          GpuShardEngine)
+
+
+def exchange(engines, which, k):
+    torch.cuda.synchronize()
+    blocks = [e.block(which, k) for e in engines]
+    for i, e in enumerate(engines):
+        for j, o in enumerate(engines):
+            if i != j:
+                blocks[j][e.row0:e.row1].copy_(blocks[i][e.row0:e.row1])
+    torch.cuda.synchronize()
+
+
+def lockstep_solve(engines, opts):
+    for e in engines:
+        e.begin(opts)
+    for e in engines:
+        e.phase(PH_SETUP_LOCAL, 0)
+    exchange(engines, BLOCK_R, 0)
+    for e in engines:
+        e.phase(PH_SETUP_REST, 0)
+    stop = engines[0].state()[0]
+    k = 0
+    while not stop and k < engines[0].max_iters:
+        for e in engines:
+            e.phase(PH_ITER_LOCAL, k)
+        exchange(engines, BLOCK_Q, k)
+        for e in engines:
+            e.phase(PH_ITER_MID, k)
+        if engines[0].recompute_at(k):
+            exchange(engines, BLOCK_R, k)
+        for e in engines:
+            e.phase(PH_ITER_REST, k)
+        k += 1
+        stops = [e.state()[0] for e in engines]
+        assert len(set(stops)) == 1  # replicated state => identical decisions
+        stop = stops[0]
+    for e in engines:
+        e.phase(PH_FINAL_LOCAL, 0)
+    exchange(engines, BLOCK_S, 0)
+    for e in engines:
+        e.phase(PH_FINAL_REST, 0)
+    return [e.end() for e in engines]
+
+
+@pytest.mark.parametrize("n,p,world,max_iters", [(600, 4, 2, -1), (517, 8, 3, 60), (256, 16, 2, 55)])
+def test_sharded_exact_bitwise(po, n, p, world, max_iters):
+    import paper_1204_0069_b200 as m
+    A = po.gen_diagdom(n, n) if p != 4 else po.gen_householder(n, 8, 1e3, n)
+    b = po.gen_rhs(n, "uniform", n)
+    X0 = po.gen_starts(n, p, n)
+    opts = m.SolveOptions(tol=(1e-10 * po.seq_norm(b) if max_iters < 0 else 0.0), max_iters=max_iters)
+    engines = [GpuShardEngine(n, p, r, world, 0, "exact") for r in range(world)]
+    for e in engines:
+        e.ctx.set_A(A[e.row0:e.row1])
+        e.ctx.upload(b, X0)
+    traces = lockstep_solve(engines, opts)
+    ref = po.oracle_ccg(A, b, X0, tol=opts.tol, max_iters=max_iters)
+    for t in traces:
+        assert str(t.status) == ref.status and t.iteration_count() == ref.iterations
+        assert np.array_equal(t.residual_norms, ref.residual_norms)
+        assert np.array_equal(t.final_x, ref.final_x)
+        assert np.array_equal(t.final_residual_norms, ref.final_residual_norms)
+    for e in engines:
+        e.close()
+
+
+def test_sharded_generated_diagdom_matches_single(po):
+    """Shards generate their own rows of A on the device (gen_A on a shard)."""
+    import paper_1204_0069_b200 as m
+    n, p, world = 700, 8, 2
+    engines = [GpuShardEngine(n, p, r, world, 0, "exact") for r in range(world)]
+    b = m.gen_rhs(n, "uniform", 3)
+    X0 = m.gen_starts(n, p, 3)
+    for e in engines:
+        e.ctx.gen_A("diagdom", 3)
+        assert np.array_equal(e.ctx.get_A(), po.gen_diagdom(n, 3)[e.row0:e.row1])
+        e.ctx.upload(b, X0)
+    opts = m.SolveOptions(max_iters=40)
+    traces = lockstep_solve(engines, opts)
+    with m.GpuContext(n, p) as ctx:
+        ctx.gen_A("diagdom", 3)
+        single = ctx.solve(b, X0, opts)
+    assert np.array_equal(traces[0].final_x, single.final_x)
+    assert np.array_equal(traces[1].residual_norms, single.residual_norms)
+    for e in engines:
+        e.close()
+
+
+def test_sharded_fast_within_tolerance(po):
+    import paper_1204_0069_b200 as m
+    n, p, world = 900, 8, 2
+    A = po.gen_diagdom(n, 11)
+    b = po.gen_rhs(n, "uniform", 11)
+    X0 = po.gen_starts(n, p, 11)
+    opts = m.SolveOptions(tol=1e-10 * po.seq_norm(b))
+    engines = [GpuShardEngine(n, p, r, world, 0, "fast") for r in range(world)]
+    for e in engines:
+        e.ctx.set_A(A[e.row0:e.row1])
+        e.ctx.upload(b, X0)
+    traces = lockstep_solve(engines, opts)
+    ref = po.oracle_ccg(A, b, X0, tol=opts.tol)
+    for t in traces:
+        assert str(t.status) == "converged" and abs(t.iteration_count() - ref.iterations) <= 2
+        rel = np.linalg.norm(t.final_x - ref.final_x, axis=0) / np.linalg.norm(ref.final_x, axis=0)
+        assert rel.max() < 1e-8
+    assert np.array_equal(traces[0].final_x, traces[1].final_x)  # ranks agree bit for bit
+    for e in engines:
+        e.close()
