@@ -19,6 +19,7 @@
 // immutable, dense.hpp:95-96), the common "many right-hand sides" use.
 #pragma once
 
+#include <cmath>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -82,7 +83,9 @@ public:
     GpuSolver& operator=(const GpuSolver&) = delete;
     ~GpuSolver() { coopcg_gpu_destroy(ctx_); }
 
-    SolveTrace<double> solve(const Vec<double>& b, const DenseBlock<double>& X0, const SolveOptions<double>& opts = {}) {
+    /// algo 0: ccg_solve semantics; 1: mccg_solve (restriction on rank drop).
+    SolveTrace<double> solve(const Vec<double>& b, const DenseBlock<double>& X0, const SolveOptions<double>& opts = {},
+                             int algo = 0) {
         // check_block_inputs (solvers.hpp:300-306)
         if (static_cast<int>(b.size()) != n_ || X0.rows() != n_)
             throw DimensionError("solver: operand shapes do not match the system matrix");
@@ -99,8 +102,10 @@ public:
             auto c = X0.col(j);
             std::copy(c.begin(), c.end(), x0.begin() + static_cast<size_t>(j) * n);
         }
-        coopcg_opts o{opts.tol, opts.max_iters, opts.recompute_residual_every, opts.rank_rel_tol};
+        coopcg_opts o{opts.tol, opts.max_iters, opts.recompute_residual_every, opts.rank_rel_tol, algo};
+        std::vector<int> act(p);
         coopcg_trace tr{};
+        tr.active_agents = act.data();
         tr.capacity = cap;
         tr.residual_norms = norms.data();
         tr.minres = minres.data();
@@ -113,33 +118,38 @@ public:
 
         SolveTrace<double> t;
         const int every = opts.recompute_residual_every >= 0 ? opts.recompute_residual_every : 50;
-        std::vector<int> agents(p);
-        for (int j = 0; j < p; ++j) agents[j] = j;
         for (int k = 0; k < tr.iterations; ++k) {
+            // rows hold norms per ORIGINAL agent id, NaN for agents mccg dropped
             IterationRecord rec;
             rec.k = k;
-            rec.active_agents = p;
-            rec.agents = agents;
-            rec.residual_norms.assign(norms.begin() + static_cast<size_t>(k) * p,
-                                      norms.begin() + static_cast<size_t>(k + 1) * p);
+            for (int j = 0; j < p; ++j) {
+                const double v = norms[static_cast<size_t>(k) * p + j];
+                if (!std::isnan(v)) {
+                    rec.agents.push_back(j);
+                    rec.residual_norms.push_back(v);
+                }
+            }
+            rec.active_agents = static_cast<int>(rec.agents.size());
             rec.minres = minres[k];
             const bool rcmp = detail::recompute_now(k, every);
             std::uint64_t m = 0;
-            for (int ph = 0; ph < kPhaseCount; ++ph) m += phase_counted_mults(static_cast<Phase>(ph), n, p, rcmp);
+            for (int ph = 0; ph < kPhaseCount; ++ph)
+                m += phase_counted_mults(static_cast<Phase>(ph), n, rec.active_agents, rcmp);
             rec.mults = m;
-            rec.mults_per_worker.assign(p, m);
+            rec.mults_per_worker.assign(rec.active_agents, m);
             rec.wall_ns = wall[k];
             t.iterations.push_back(std::move(rec));
         }
         t.status = gpu_detail::status_of(tr.status);
         t.converged_agent = tr.converged_agent;
-        t.final_x = DenseBlock<double>(n, p);
-        for (int j = 0; j < p; ++j)
-            for (int i = 0; i < n; ++i) t.final_x(i, j) = fx[static_cast<size_t>(j) * n + i];
-        t.active_agents = agents;
+        const int na = tr.n_active;
+        t.active_agents.assign(act.begin(), act.begin() + na);
+        t.final_x = DenseBlock<double>(n, na);
+        for (int s = 0; s < na; ++s)
+            for (int i = 0; i < n; ++i) t.final_x(i, s) = fx[static_cast<size_t>(t.active_agents[s]) * n + i];
         t.initial_residual_norms = init;
         t.initial_minres = tr.initial_minres;
-        t.final_residual_norms = fres;
+        for (int s = 0; s < na; ++s) t.final_residual_norms.push_back(fres[t.active_agents[s]]);
         t.final_minres = tr.final_minres;
         t.setup_mults = static_cast<std::uint64_t>(n) * static_cast<std::uint64_t>(n);
         t.loop_wall_ns = tr.loop_wall_ns;
@@ -151,6 +161,14 @@ private:
     int n_, p_;
     coopcg_gpu_ctx* ctx_ = nullptr;
 };
+
+/// mccg_solve's signature plus GPU options (solvers.hpp:338-342).
+inline SolveTrace<double> gpu_mccg(const SpdMatrix<double>& A, const Vec<double>& b, const DenseBlock<double>& X0,
+                                   const SolveOptions<double>& opts = {}, const GpuOptions& g = {}) {
+    detail::check_block_inputs(A, b, X0);
+    GpuSolver s(A, X0.cols(), g);
+    return s.solve(b, X0, opts, 1);
+}
 
 /// ccg_solve's signature plus GPU options (solvers.hpp:329-333).
 inline SolveTrace<double> gpu_ccg(const SpdMatrix<double>& A, const Vec<double>& b, const DenseBlock<double>& X0,

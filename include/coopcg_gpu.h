@@ -70,6 +70,7 @@ typedef struct {
     int max_iters;                /* -1 => 2n (solvers.hpp:18-23) */
     int recompute_residual_every; /* -1 => 50; 0 disables (solvers.hpp:25-35) */
     double rank_rel_tol;          /* numerical_rank tolerance, reference default 1e-10 */
+    int algo;                     /* 0 = ccg_solve (solvers.hpp:329-333), 1 = mccg_solve (:338-342) */
 } coopcg_opts;
 
 /* SolveTrace<double> (trace.hpp:46-71), caller-allocated arrays.
@@ -90,7 +91,13 @@ typedef struct {
     double final_minres;
     uint64_t loop_wall_ns;          /* sum of wall_ns (solvers.hpp:145) */
     int exact_rank_checks;          /* diagnostics: certificate fell back to exact MGS */
+    int* active_agents;             /* [p] surviving agent ids (SolveTrace::active_agents), may be NULL */
+    int n_active;                   /* number of surviving agents (p unless mccg restricted) */
 } coopcg_trace;
+/* mccg: per-iteration norms are stored per ORIGINAL agent id (row k of
+ * residual_norms has NaN for agents no longer active, IterationRecord::agents
+ * = the non-NaN ids); final_x / final_residual_norms hold NaN for dropped
+ * agents. */
 
 /* Per-kernel timing of the last run, from CUDA events on the context stream. */
 typedef struct {

@@ -206,12 +206,24 @@ static void residual_of(const double* A, const double* b, int n, const double* x
     for (int i = 0; i < n; ++i) r[i] -= b[i];
 }
 
+/* BlockCgWorkspace::restrict_to (block_cg.hpp:84-96): keep the listed slots
+ * (ascending) of the n x p column-major blocks. */
+static void keep_columns(double* blk, int n, const int* keep, int pk) {
+    for (int c = 0; c < pk; ++c)
+        if (keep[c] != c) memmove(blk + (size_t)c * n, blk + (size_t)keep[c] * n, sizeof(double) * n);
+}
+
+static int cmp_int(const void* a, const void* b) { return *(const int*)a - *(const int*)b; }
+
 /*
- * The serial ccg_solve driver: run_serial_block (solvers.hpp:308-321) with
- * drive() (solvers.hpp:259-283), allow_restriction = false.
+ * The serial block driver: run_serial_block (solvers.hpp:308-321) with
+ * drive() (solvers.hpp:259-283).  allow_restriction = 0 is ccg_solve
+ * (solvers.hpp:329-333), 1 is mccg_solve (solvers.hpp:338-342).  Per-iteration
+ * norms are written per ORIGINAL agent id (NaN for agents no longer active);
+ * final_x / final_residual_norms likewise (NaN columns for dropped agents).
  */
-int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* X0,
-                  const orc_opts* opts, orc_trace* tr) {
+int orc_block_solve(int n, int p, const double* A, const double* b, const double* X0,
+                    const orc_opts* opts, int allow_restriction, orc_trace* tr) {
     tr->status = ORC_STATUS_MAX_ITERATIONS;
     tr->converged_agent = -1;
     tr->iterations = 0;
@@ -240,6 +252,9 @@ int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* 
     int perm[COOPCG_ORACLE_MAX_P];
     double nsq[COOPCG_ORACLE_MAX_P], norm[COOPCG_ORACLE_MAX_P];
     int rc = ORC_OK;
+    int ids[COOPCG_ORACLE_MAX_P];
+    const int p0 = p;
+    for (int j = 0; j < p; ++j) ids[j] = j;
     memcpy(X, X0, sizeof(double) * np);
 
     /* stage_setup (block_cg.hpp:132-144): R = A X - b, D = R, norms. */
@@ -254,14 +269,33 @@ int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* 
     if (tr->initial_residual_norms) memcpy(tr->initial_residual_norms, norm, sizeof(double) * p);
     tr->initial_minres = min_norm(norm, p);
     {
-        const int rank0 = orc_numerical_rank(D, n, p, opts->rank_rel_tol, NULL);
+        int cols[COOPCG_ORACLE_MAX_P];
+        const int rank0 = orc_numerical_rank(D, n, p, opts->rank_rel_tol, cols);
+        if (allow_restriction && rank0 > 0 && rank0 < p) {  /* solvers.hpp:67-76 */
+            qsort(cols, rank0, sizeof(int), cmp_int);
+            keep_columns(X, n, cols, rank0);
+            keep_columns(R, n, cols, rank0);
+            keep_columns(D, n, cols, rank0);
+            int nid[COOPCG_ORACLE_MAX_P];
+            for (int c = 0; c < rank0; ++c) nid[c] = ids[cols[c]];
+            memcpy(ids, nid, sizeof(int) * rank0);
+            p = rank0;
+            for (int j = 0; j < p; ++j) {
+                nsq[j] = orc_dot(R + (size_t)j * n, R + (size_t)j * n, n);
+                norm[j] = sqrt(nsq[j]);
+            }
+        }
         const int slot = first_converged(norm, p, opts->tol);
         if (slot >= 0) {
             tr->status = ORC_STATUS_CONVERGED;
-            tr->converged_agent = slot;
+            tr->converged_agent = ids[slot];
             stop = 1;
-        } else if (rank0 < p) {
+        } else if (!allow_restriction && rank0 < p) {
             tr->status = ORC_STATUS_RANK_COLLAPSE;
+            stop = 1;
+        } else if (allow_restriction && rank0 == 0) {      /* solvers.hpp:86-91 */
+            snprintf(tr->error_msg, sizeof tr->error_msg, "every starting direction is numerically zero");
+            rc = ORC_E_NUMERICAL_BREAKDOWN;
             stop = 1;
         }
         if (!stop && max_iters == 0) {
@@ -341,7 +375,10 @@ int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* 
             break;
         }
         if (k < tr->capacity) {
-            if (tr->residual_norms) memcpy(tr->residual_norms + (size_t)k * p, norm, sizeof(double) * p);
+            if (tr->residual_norms) {
+                for (int j = 0; j < p0; ++j) tr->residual_norms[(size_t)k * p0 + j] = NAN;
+                for (int j = 0; j < p; ++j) tr->residual_norms[(size_t)k * p0 + ids[j]] = norm[j];
+            }
             if (tr->minres) tr->minres[k] = min_norm(norm, p);
             if (tr->wall_ns) tr->wall_ns[k] = wall;
         }
@@ -350,12 +387,34 @@ int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* 
         const int slot = first_converged(norm, p, opts->tol);
         if (slot >= 0) {
             tr->status = ORC_STATUS_CONVERGED;
-            tr->converged_agent = slot;
+            tr->converged_agent = ids[slot];
             break;
         }
-        if (orc_numerical_rank(Dn, n, p, opts->rank_rel_tol, NULL) < p) {
-            tr->status = ORC_STATUS_RANK_COLLAPSE;
-            break;
+        {
+            const int rr = orc_numerical_rank(Dn, n, p, opts->rank_rel_tol, NULL);
+            if (rr < p) {                                   /* solvers.hpp:156-175 */
+                if (!allow_restriction) {
+                    tr->status = ORC_STATUS_RANK_COLLAPSE;
+                    break;
+                }
+                int cols[COOPCG_ORACLE_MAX_P];
+                const int nsel = orc_numerical_rank(R, n, p, opts->rank_rel_tol, cols);
+                const int pnext = rr < nsel ? rr : nsel;
+                if (pnext == 0) {
+                    snprintf(tr->error_msg, sizeof tr->error_msg,
+                             "all agents degenerate at iteration %d with residual above tolerance", k);
+                    rc = ORC_E_NUMERICAL_BREAKDOWN;
+                    break;
+                }
+                qsort(cols, pnext, sizeof(int), cmp_int);
+                keep_columns(X, n, cols, pnext);
+                keep_columns(R, n, cols, pnext);
+                keep_columns(Dn, n, cols, pnext);
+                int nid[COOPCG_ORACLE_MAX_P];
+                for (int c = 0; c < pnext; ++c) nid[c] = ids[cols[c]];
+                memcpy(ids, nid, sizeof(int) * pnext);
+                p = pnext;
+            }
         }
         if (k + 1 >= max_iters) {
             tr->status = ORC_STATUS_MAX_ITERATIONS;
@@ -368,14 +427,24 @@ int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* 
         t_iter = now_ns();
     }
     /* finalize_trace (solvers.hpp:188-210): true residuals of the final X. */
-    if (tr->final_x) memcpy(tr->final_x, X, sizeof(double) * np);
+    if (tr->final_x) {
+        for (size_t e = 0; e < (size_t)n * p0; ++e) tr->final_x[e] = NAN;
+        for (int j = 0; j < p; ++j) memcpy(tr->final_x + (size_t)ids[j] * n, X + (size_t)j * n, sizeof(double) * n);
+    }
+    if (tr->active_agents) {
+        for (int j = 0; j < p; ++j) tr->active_agents[j] = ids[j];
+    }
+    tr->n_active = p;
     {
         double fr[COOPCG_ORACLE_MAX_P];
         for (int j = 0; j < p; ++j) {
             residual_of(A, b, n, X + (size_t)j * n, AD); /* AD reused as scratch */
             fr[j] = sqrt(orc_dot(AD, AD, n));
         }
-        if (tr->final_residual_norms) memcpy(tr->final_residual_norms, fr, sizeof(double) * p);
+        if (tr->final_residual_norms) {
+            for (int j = 0; j < p0; ++j) tr->final_residual_norms[j] = NAN;
+            for (int j = 0; j < p; ++j) tr->final_residual_norms[ids[j]] = fr[j];
+        }
         double m = fr[0];
         for (int j = 0; j < p; ++j) m = (fr[j] < m) ? fr[j] : m; /* std::min_element */
         tr->final_minres = m;
@@ -386,4 +455,14 @@ int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* 
     free(Dn);
     free(AD);
     return rc;
+}
+
+int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* X0,
+                  const orc_opts* opts, orc_trace* tr) {
+    return orc_block_solve(n, p, A, b, X0, opts, 0, tr);
+}
+
+int orc_mccg_solve(int n, int p, const double* A, const double* b, const double* X0,
+                   const orc_opts* opts, orc_trace* tr) {
+    return orc_block_solve(n, p, A, b, X0, opts, 1, tr);
 }

@@ -37,6 +37,8 @@ typedef struct {
     double final_minres;
     uint64_t loop_wall_ns;
     char error_msg[256];
+    int* active_agents;            /* [p], may be NULL: surviving agent ids */
+    int n_active;
 } orc_trace;
 
 double orc_dot(const double* a, const double* b, long n);
@@ -49,6 +51,10 @@ int orc_solve_small(const double* M, int p, const double* B, int q, double* X);
 int orc_numerical_rank(const double* D, int n, int p, double tol, int* columns);
 int orc_ccg_solve(int n, int p, const double* A, const double* b, const double* X0,
                   const orc_opts* opts, orc_trace* tr);
+int orc_mccg_solve(int n, int p, const double* A, const double* b, const double* X0,
+                   const orc_opts* opts, orc_trace* tr);
+int orc_block_solve(int n, int p, const double* A, const double* b, const double* X0,
+                    const orc_opts* opts, int allow_restriction, orc_trace* tr);
 
 /* BASELINE generators, restated independently of the product (gen_oracle.c). */
 void orc_gen_diagdom(int n, uint64_t seed, double* A);

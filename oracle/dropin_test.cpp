@@ -79,6 +79,26 @@ int main() {
         compare("GpuSolver reuse #1", ccg_solve(inst.A, inst.b, inst.X0, o), s.solve(inst.b, inst.X0, o));
         compare("GpuSolver reuse #2", ccg_solve(inst.A, inst.b, inst.X0, o), s.solve(inst.b, inst.X0, o));
     }
+    {   // mccg_solve: restrictions (tests/test_solvers.cpp:369-433 scenarios)
+        struct M { int n, p; double cond; unsigned long long seed; double tol; bool dup; };
+        const M ms[] = {{40, 3, 1e3, 37, 1e-6, false}, {30, 3, 1e2, 59, 1e-8, true}, {50, 8, 1e3, 5, 1e-9, false},
+                        {40, 3, 1e2, 67, 1e-8, false}};
+        for (const auto& c : ms) {
+            ProblemSpec spec;
+            spec.n = c.n;
+            spec.p = c.p;
+            spec.cond = c.cond;
+            spec.seed = c.seed;
+            auto inst = make_problem<double>(spec);
+            if (c.dup)
+                for (int i = 0; i < c.n; ++i) inst.X0(i, 2) = inst.X0(i, 1);
+            SolveOptions<double> o;
+            o.tol = c.tol;
+            char name[96];
+            std::snprintf(name, sizeof name, "mccg n=%d p=%d seed=%llu%s", c.n, c.p, c.seed, c.dup ? " dup" : "");
+            compare(name, mccg_solve(inst.A, inst.b, inst.X0, o), gpu_mccg(inst.A, inst.b, inst.X0, o));
+        }
+    }
     {   // error behaviour: indefinite matrix -> SpdViolationError; bad shapes -> DimensionError
         const int n = 30;
         std::vector<double> e(static_cast<size_t>(n) * n, 0.0);

@@ -39,7 +39,8 @@ class OrcTrace(C.Structure):
                 ("initial_residual_norms", C.POINTER(C.c_double)), ("initial_minres", C.c_double),
                 ("final_x", C.POINTER(C.c_double)),
                 ("final_residual_norms", C.POINTER(C.c_double)), ("final_minres", C.c_double),
-                ("loop_wall_ns", C.c_uint64), ("error_msg", C.c_char * 256)]
+                ("loop_wall_ns", C.c_uint64), ("error_msg", C.c_char * 256),
+                ("active_agents", C.POINTER(C.c_int)), ("n_active", C.c_int)]
 
 
 @dataclass
@@ -75,6 +76,7 @@ def oracle_lib() -> C.CDLL:
         lib = C.CDLL(ORACLE_SO)
         lib.orc_ccg_solve.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.POINTER(OrcOpts), C.POINTER(OrcTrace)]
+        lib.orc_mccg_solve.argtypes = lib.orc_ccg_solve.argtypes
         lib.orc_dot.restype = C.c_double
         lib.orc_dot.argtypes = [C.c_void_p, C.c_void_p, C.c_long]
         lib.orc_gen_diagdom.argtypes = [C.c_int, C.c_uint64, C.c_void_p]
@@ -121,7 +123,9 @@ def _run(fn, n, p, capacity, *args) -> Trace:
     init = np.zeros(p)
     fx = np.zeros((p, n))  # column-major n x p == row-major p x n
     fr = np.zeros(p)
+    act = np.zeros(p, dtype=np.int32)
     tr = OrcTrace()
+    tr.active_agents = act.ctypes.data_as(C.POINTER(C.c_int))
     tr.capacity = capacity
     tr.residual_norms = _dp(norms)
     tr.minres = _dp(minres)
@@ -136,7 +140,8 @@ def _run(fn, n, p, capacity, *args) -> Trace:
                  residual_norms=norms[:it].copy(), minres=minres[:it].copy(), wall_ns=wall[:it].copy(),
                  initial_residual_norms=init, initial_minres=tr.initial_minres,
                  final_x=fx.T.copy(), final_residual_norms=fr, final_minres=tr.final_minres,
-                 loop_wall_ns=int(tr.loop_wall_ns))
+                 loop_wall_ns=int(tr.loop_wall_ns),
+                 extra={"active_agents": act[:tr.n_active].tolist()})
 
 
 def _opts(tol, max_iters, recompute, rank_tol):
@@ -157,13 +162,13 @@ def _prep(A, b, X0):
     return A, b, X0c, n, p
 
 
-def oracle_ccg(A, b, X0, tol=0.0, max_iters=-1, recompute=-1, rank_tol=1e-10) -> Trace:
-    """The C restatement of ccg_solve.  X0 is an (n, p) array."""
+def oracle_ccg(A, b, X0, tol=0.0, max_iters=-1, recompute=-1, rank_tol=1e-10, algo="ccg") -> Trace:
+    """The C restatement of ccg_solve (algo="mccg": mccg_solve).  X0 is an (n, p) array."""
     A, b, X0c, n, p = _prep(A, b, X0)
     cap = max_iters if max_iters >= 0 else 2 * n
     o = _opts(tol, max_iters, recompute, rank_tol)
-    return _run(oracle_lib().orc_ccg_solve, n, p, cap, n, p, A.ctypes.data, b.ctypes.data,
-                X0c.ctypes.data, C.byref(o))
+    fn = oracle_lib().orc_ccg_solve if algo == "ccg" else oracle_lib().orc_mccg_solve
+    return _run(fn, n, p, cap, n, p, A.ctypes.data, b.ctypes.data, X0c.ctypes.data, C.byref(o))
 
 
 def ref_solve(A, b, X0, tol=0.0, max_iters=-1, recompute=-1, rank_tol=1e-10, algo="ccg") -> Trace:

@@ -82,13 +82,19 @@ void fill_trace(const SolveTrace<double>& t, int n, orc_trace* tr) {
         std::copy(t.initial_residual_norms.begin(), t.initial_residual_norms.end(), tr->initial_residual_norms);
     tr->initial_minres = t.initial_minres;
     if (tr->final_x) {
-        // final_x is n x (surviving agents), column-major; scatter by agent id.
+        // final_x is n x (surviving agents), column-major; scatter by agent id
+        // (NaN columns for agents a restriction dropped).
+        for (size_t e = 0; e < static_cast<size_t>(n) * p0; ++e) tr->final_x[e] = __builtin_nan("");
         for (int s = 0; s < t.final_x.cols(); ++s) {
             auto c = t.final_x.col(s);
             std::copy(c.begin(), c.end(), tr->final_x + (size_t)t.active_agents[(size_t)s] * n);
         }
     }
+    if (tr->active_agents)
+        for (size_t s = 0; s < t.active_agents.size(); ++s) tr->active_agents[s] = t.active_agents[s];
+    tr->n_active = static_cast<int>(t.active_agents.size());
     if (tr->final_residual_norms) {
+        for (int j = 0; j < p0; ++j) tr->final_residual_norms[j] = __builtin_nan("");
         for (size_t s = 0; s < t.final_residual_norms.size(); ++s)
             tr->final_residual_norms[t.active_agents[s]] = t.final_residual_norms[s];
     }

@@ -17,7 +17,7 @@ LIB_PATH = _build.LIB
 
 class coopcg_opts(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iters", C.c_int),
-                ("recompute_residual_every", C.c_int), ("rank_rel_tol", C.c_double)]
+                ("recompute_residual_every", C.c_int), ("rank_rel_tol", C.c_double), ("algo", C.c_int)]
 
 
 class coopcg_trace(C.Structure):
@@ -30,7 +30,8 @@ class coopcg_trace(C.Structure):
                 ("final_residual_norms", C.POINTER(C.c_double)),
                 ("status", C.c_int), ("converged_agent", C.c_int), ("iterations", C.c_int),
                 ("initial_minres", C.c_double), ("final_minres", C.c_double),
-                ("loop_wall_ns", C.c_uint64), ("exact_rank_checks", C.c_int)]
+                ("loop_wall_ns", C.c_uint64), ("exact_rank_checks", C.c_int),
+                ("active_agents", C.POINTER(C.c_int)), ("n_active", C.c_int)]
 
 
 class coopcg_timing(C.Structure):

@@ -48,9 +48,13 @@ struct Ctl {
     double tol;
     double rank_rel_tol;
     int max_iters;
-    int p;
+    int p;                // active agents
     int P;
-    int pad_;
+    int algo;             // 0 ccg, 1 mccg (restriction allowed)
+    int p0;               // agents at the start (trace row width)
+    int restrict_pending; // mccg: rank drop seen; device paused for the host to restrict
+    int rank_cols[kMaxP]; // pivot columns of the last exact MGS (dense_ops.hpp:254-256)
+    int ids[kMaxP];       // original agent id of each active slot (block_cg.hpp:48)
 };
 
 // One sequential dot-product chain (kernels.hpp:20-26):

@@ -65,6 +65,7 @@ struct coopcg_gpu_ctx {
 
     double* At = nullptr;
     double* X = nullptr;
+    double* X0 = nullptr;  // uploaded starting block; copied into X at every solve start
     double* R = nullptr;
     double* Dblk[2] = {nullptr, nullptr};
     double* Q = nullptr;
@@ -96,6 +97,11 @@ struct coopcg_gpu_ctx {
     coopcg_timing timing{};
     long long launches = 0;  // kernels launched since the last run started
     int max_iters = 0, every = 50;  // resolved SolveOptions of the current solve
+    int p_orig = 0;                 // agents at creation (mccg restricts ctx->p during a solve)
+    int algo = 0;                   // 0 ccg, 1 mccg for the current solve
+    int host_err = 0;               // error raised by the host-side mccg logic
+    std::string host_err_msg;
+    std::vector<int> ids;           // original id of each active slot
 };
 
 namespace {
@@ -329,6 +335,7 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     cudaFree(ctx->At);
     cudaFree(ctx->X);
+    cudaFree(ctx->X0);
     cudaFree(ctx->R);
     cudaFree(ctx->Dblk[0]);
     cudaFree(ctx->Dblk[1]);
@@ -425,6 +432,7 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     auto* ctx = new coopcg_gpu_ctx();
     ctx->n = n;
     ctx->p = p;
+    ctx->p_orig = p;
     ctx->P = (arith == COOPCG_ARITH_FAST) ? std::max(8, pad_cols(p)) : pad_cols(p);
     ctx->device = device;
     ctx->arith = arith;
@@ -491,7 +499,7 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CKC(cudaMalloc(&ctx->At, sizeof(double) * ctx->ap_elems));
     CKC(cudaMemsetAsync(ctx->At, 0, sizeof(double) * ctx->ap_elems, ctx->stream));
-    double** blocks[] = {&ctx->X, &ctx->R, &ctx->Dblk[0], &ctx->Dblk[1], &ctx->Q, &ctx->S, &ctx->V};
+    double** blocks[] = {&ctx->X, &ctx->X0, &ctx->R, &ctx->Dblk[0], &ctx->Dblk[1], &ctx->Q, &ctx->S, &ctx->V};
     for (double** bp : blocks) {
         CKC(cudaMalloc(bp, sizeof(double) * blk));
         CKC(cudaMemsetAsync(*bp, 0, sizeof(double) * blk, ctx->stream));
@@ -657,10 +665,10 @@ int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double
 int coopcg_gpu_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0) {
     if (!ctx || !b || !X0) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
-    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    const int n = ctx->n, p = ctx->p_orig, P = ctx->P;
     CK(cudaMemcpyAsync(ctx->b, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->stage, X0, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, ctx->stream));
-    colmajor_to_rowmajor_kernel<<<grid_for((size_t)n * P, 256), 256, 0, ctx->stream>>>(ctx->stage, ctx->X, n, p, P);
+    colmajor_to_rowmajor_kernel<<<grid_for((size_t)n * P, 256), 256, 0, ctx->stream>>>(ctx->stage, ctx->X0, n, p, P);
     CKL();
     ctx->inputs_ready = true;
     return COOPCG_OK;
@@ -681,6 +689,151 @@ int coopcg_gpu_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0) {
     } while (0)
 
 static bool sharded(const coopcg_gpu_ctx* ctx) { return ctx->n_loc != ctx->n; }
+
+// Active agent count + chain descriptors for it (mccg shrinks p mid-solve).
+static int set_active_p(coopcg_gpu_ctx* ctx, int p) {
+    ctx->p = p;
+    std::vector<ChainDesc> descs;
+    build_descs(p, ctx->P, descs, ctx->desc_off, ctx->desc_cnt);
+    CK(cudaMemcpyAsync(ctx->descs, descs.data(), sizeof(ChainDesc) * descs.size(), cudaMemcpyHostToDevice,
+                       ctx->stream));
+    return COOPCG_OK;
+}
+
+// BlockCgWorkspace::restrict_to (block_cg.hpp:84-96): keep the listed slots
+// (ascending) of X, R and the given direction block; update ids / p on host
+// and device.  The stream is synchronised by the caller.
+static int restrict_to(coopcg_gpu_ctx* ctx, const std::vector<int>& keep, double* dir) {
+    KeepList kl{};
+    for (size_t c = 0; c < keep.size(); ++c) kl.keep[c] = keep[c];
+    const int pk = (int)keep.size();
+    const int n = ctx->n;
+    double* blks[3] = {ctx->X, ctx->R, dir};
+    for (double* b : blks) {
+        compact_columns_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(b, n, ctx->P, kl, pk);
+        CKL();
+    }
+    std::vector<int> nid(pk);
+    for (int c = 0; c < pk; ++c) nid[c] = ctx->ids[keep[c]];
+    ctx->ids = nid;
+    if (int rc = set_active_p(ctx, pk)) return rc;
+    Ctl& h = ctx->ctl_host[0];
+    CK(cudaMemcpyAsync(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    h.p = pk;
+    for (int c = 0; c < pk; ++c) h.ids[c] = nid[c];
+    CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+    return COOPCG_OK;
+}
+
+// numerical_rank(block) by the exact MGS on the device; returns rank, columns.
+static int exact_rank_of(coopcg_gpu_ctx* ctx, double* blk, int& rank, std::vector<int>& cols) {
+    Ctl& h = ctx->ctl_host[0];
+    CK(cudaMemcpyAsync(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const int saved_stop = h.stop;
+    h.force_exact = 1;
+    h.stop = 0;
+    CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+    rank_end_kernel<<<1, 1024, rank_smem(ctx->P), ctx->stream>>>(ctx->partials, 1, blk, ctx->V, ctx->n, ctx->ctl, 2,
+                                                                 nullptr);
+    CKL();
+    CK(cudaMemcpyAsync(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    rank = h.rank_result;
+    cols.assign(h.rank_cols, h.rank_cols + rank);
+    h.force_exact = 0;
+    h.stop = saved_stop;
+    CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+    return COOPCG_OK;
+}
+
+// mccg setup_coordinator (solvers.hpp:63-98), after the device set
+// restrict_pending with rank0 (and its columns when rank0 < p).
+static int mccg_setup(coopcg_gpu_ctx* ctx) {
+    Ctl& h = ctx->ctl_host[0];
+    CK(cudaMemcpyAsync(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const int p = ctx->p;
+    const int rank0 = h.rank_result;
+    std::vector<double> init(p + 1);
+    CK(cudaMemcpy(init.data(), ctx->init_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
+    std::vector<int> keep(p);
+    for (int j = 0; j < p; ++j) keep[j] = j;
+    if (rank0 > 0 && rank0 < p) {
+        keep.assign(h.rank_cols, h.rank_cols + rank0);
+        std::sort(keep.begin(), keep.end());
+        if (int rc = restrict_to(ctx, keep, ctx->Dblk[0])) return rc;
+    }
+    CK(cudaMemcpyAsync(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    h.restrict_pending = 0;
+    int slot = -1;
+    for (int j = 0; j < (int)keep.size(); ++j)
+        if (init[keep[j]] <= h.tol) {
+            slot = j;
+            break;
+        }
+    if (slot >= 0) {
+        h.status = COOPCG_CONVERGED;
+        h.converged_agent = ctx->ids[slot];
+        h.stop = 1;
+    } else if (rank0 == 0) {
+        ctx->host_err = COOPCG_E_NUMERICAL_BREAKDOWN;
+        ctx->host_err_msg = "every starting direction is numerically zero";  // solvers.hpp:86-91
+        h.stop = 1;
+    }
+    if (!h.stop && h.max_iters == 0) {
+        h.status = COOPCG_MAX_ITERATIONS;
+        h.stop = 1;
+    }
+    CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return COOPCG_OK;
+}
+
+// mccg end_of_iteration restriction (solvers.hpp:156-185) for iteration kr,
+// whose D' block is Dblk[(kr+1)&1].  Returns the next k (or -1 when stopped).
+static int mccg_restrict(coopcg_gpu_ctx* ctx, int kr, int* next_k) {
+    Ctl& h = ctx->ctl_host[0];
+    CK(cudaMemcpyAsync(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    const int rr = h.rank_result;
+    int nsel = 0;
+    std::vector<int> cols;
+    if (int rc = exact_rank_of(ctx, ctx->R, nsel, cols)) return rc;
+    const int pnext = std::min(rr, nsel);
+    *next_k = -1;
+    if (pnext == 0) {
+        char buf[160];
+        std::snprintf(buf, sizeof buf, "all agents degenerate at iteration %d with residual above tolerance", kr);
+        ctx->host_err = COOPCG_E_NUMERICAL_BREAKDOWN;
+        ctx->host_err_msg = buf;
+        CK(cudaMemcpyAsync(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        h.restrict_pending = 0;
+        h.stop = 1;
+        CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+        return COOPCG_OK;
+    }
+    std::vector<int> keep(cols.begin(), cols.begin() + pnext);
+    std::sort(keep.begin(), keep.end());
+    if (int rc = restrict_to(ctx, keep, ctx->Dblk[(kr + 1) & 1])) return rc;
+    CK(cudaMemcpyAsync(&h, ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    h.restrict_pending = 0;
+    if (kr + 1 >= h.max_iters) {
+        h.status = COOPCG_MAX_ITERATIONS;
+        h.stop = 1;
+    } else {
+        h.k = kr + 1;
+        h.stop = 0;
+        *next_k = kr + 1;
+    }
+    CK(cudaMemcpyAsync(ctx->ctl, &h, sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return COOPCG_OK;
+}
 static int dgrid_of(const coopcg_gpu_ctx* ctx) {
     if (ctx->arith == COOPCG_ARITH_FAST) return ctx->f_ugrid;
     const int rows_per_tile = 256 / ctx->P;
@@ -716,6 +869,15 @@ static int begin_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     ctx->max_iters = o.max_iters >= 0 ? o.max_iters : 2 * ctx->n;  // solvers.hpp:18-23
     ctx->every = o.recompute_residual_every >= 0 ? o.recompute_residual_every : 50;
     if (int rc = ensure_trace_capacity(ctx, std::max(ctx->max_iters, 1))) return rc;
+    ctx->algo = o.algo == 1 ? 1 : 0;
+    if (ctx->algo == 1 && sharded(ctx))
+        return fail(ctx, COOPCG_E_INVALID, "mccg_solve is single-GPU in this version");
+    ctx->host_err = 0;
+    ctx->host_err_msg.clear();
+    if (ctx->p != ctx->p_orig)
+        if (int rc = set_active_p(ctx, ctx->p_orig)) return rc;
+    ctx->ids.resize(ctx->p_orig);
+    for (int j = 0; j < ctx->p_orig; ++j) ctx->ids[j] = j;
     Ctl h{};
     h.stop = 0;
     h.status = COOPCG_MAX_ITERATIONS;
@@ -726,8 +888,14 @@ static int begin_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     h.max_iters = ctx->max_iters;
     h.p = ctx->p;
     h.P = ctx->P;
+    h.algo = ctx->algo;
+    h.p0 = ctx->p_orig;
+    for (int j = 0; j < ctx->p_orig; ++j) h.ids[j] = j;
     std::memcpy(&ctx->ctl_host[0], &h, sizeof(Ctl));
     CK(cudaMemcpyAsync(ctx->ctl, &ctx->ctl_host[0], sizeof(Ctl), cudaMemcpyHostToDevice, ctx->stream));
+    // every solve starts from the uploaded X0 (the previous solve overwrote X)
+    CK(cudaMemcpyAsync(ctx->X, ctx->X0, sizeof(double) * (size_t)ctx->n * ctx->P, cudaMemcpyDeviceToDevice,
+                       ctx->stream));
     ctx->launches = 0;
     return COOPCG_OK;
 }
@@ -907,28 +1075,50 @@ static int end_impl(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
         for (int k = 0; k < iters; ++k) total += wall[k];
         trace->loop_wall_ns = total;
         if (cap > 0) {
-            if (trace->residual_norms)
-                CK(cudaMemcpy(trace->residual_norms, ctx->tr_norms, sizeof(double) * (size_t)cap * p,
+            if (trace->residual_norms)  // rows of p_orig, NaN for inactive agents
+                CK(cudaMemcpy(trace->residual_norms, ctx->tr_norms, sizeof(double) * (size_t)cap * ctx->p_orig,
                               cudaMemcpyDeviceToHost));
             if (trace->minres)
                 CK(cudaMemcpy(trace->minres, ctx->tr_minres, sizeof(double) * cap, cudaMemcpyDeviceToHost));
             if (trace->wall_ns) std::memcpy(trace->wall_ns, wall.data(), sizeof(uint64_t) * cap);
         }
         std::vector<double> tmp(P + 1);
-        CK(cudaMemcpy(tmp.data(), ctx->init_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
-        if (trace->initial_residual_norms) std::memcpy(trace->initial_residual_norms, tmp.data(), sizeof(double) * p);
-        trace->initial_minres = tmp[p];
+        const int pi = ctx->p_orig;  // initial norms were recorded before any restriction
+        CK(cudaMemcpy(tmp.data(), ctx->init_norms, sizeof(double) * (pi + 1), cudaMemcpyDeviceToHost));
+        if (trace->initial_residual_norms) std::memcpy(trace->initial_residual_norms, tmp.data(), sizeof(double) * pi);
+        trace->initial_minres = tmp[pi];
         CK(cudaMemcpy(tmp.data(), ctx->final_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
         if (trace->final_residual_norms) std::memcpy(trace->final_residual_norms, tmp.data(), sizeof(double) * p);
         trace->final_minres = tmp[p];
+        const int p0 = ctx->p_orig;
+        const bool scatter = p != p0;
+        if (scatter) {  // mccg: per original agent id, NaN for dropped agents
+            std::vector<double> fr(p0, std::nan(""));
+            for (int j = 0; j < p; ++j) fr[ctx->ids[j]] = tmp[j];
+            if (trace->final_residual_norms) std::memcpy(trace->final_residual_norms, fr.data(), sizeof(double) * p0);
+        }
+        if (trace->active_agents)
+            for (int j = 0; j < p; ++j) trace->active_agents[j] = ctx->ids[j];
+        trace->n_active = p;
         if (trace->final_x) {
             rowmajor_to_colmajor_kernel<<<grid_for((size_t)n * p, 256), 256, 0, st>>>(ctx->X, ctx->stage, n, p, P);
             CKL();
-            CK(cudaMemcpyAsync(trace->final_x, ctx->stage, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost,
-                               st));
-            CK(cudaStreamSynchronize(st));
+            if (!scatter) {
+                CK(cudaMemcpyAsync(trace->final_x, ctx->stage, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost,
+                                   st));
+                CK(cudaStreamSynchronize(st));
+            } else {
+                std::vector<double> xs((size_t)n * p);
+                CK(cudaMemcpyAsync(xs.data(), ctx->stage, sizeof(double) * xs.size(), cudaMemcpyDeviceToHost, st));
+                CK(cudaStreamSynchronize(st));
+                for (size_t e = 0; e < (size_t)n * p0; ++e) trace->final_x[e] = std::nan("");
+                for (int j = 0; j < p; ++j)
+                    std::memcpy(trace->final_x + (size_t)ctx->ids[j] * n, xs.data() + (size_t)j * n,
+                                sizeof(double) * n);
+            }
         }
     }
+    if (ctx->host_err) return fail(ctx, ctx->host_err, "%s", ctx->host_err_msg.c_str());
     if (fin.err == COOPCG_E_SPD_VIOLATION)
         return fail(ctx, COOPCG_E_SPD_VIOLATION, "nonpositive direction energy d^T A d at iteration %d",
                     fin.err_iter);  // solvers.hpp:111-115
@@ -944,6 +1134,8 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     CK(cudaEventRecord(ctx->ev_run0, st));
     if (int rc = setup_local(ctx)) return rc;
     if (int rc = setup_rest(ctx)) return rc;
+    if (ctx->algo == 1)
+        if (int rc = mccg_setup(ctx)) return rc;
     CK(cudaEventRecord(ctx->ev_loop0, st));
 
     // ---- main loop, enqueued in chunks; device-side stop makes extras no-ops ----
@@ -977,7 +1169,8 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
         return COOPCG_OK;
     };
     int chunk = 4;
-    while (!stopped && k_host < max_iters) {
+    for (;;) {
+      while (!stopped && k_host < max_iters) {
         if (npending == 2) {
             if (int rc = read_chunk(pending[0])) return rc;
             pending[0] = pending[1];
@@ -1000,9 +1193,22 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
         pending[npending++] = chunk_id;
         ++chunk_id;
         chunk = std::min(kChunkMax, chunk * 2);
+      }
+      for (int q = 0; q < npending; ++q)
+          if (int rc = read_chunk(pending[q])) return rc;
+      npending = 0;
+      // mccg: the device paused on a rank drop (restrict_pending); restrict and resume.
+      if (ctx->algo != 1) break;
+      CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (!ctx->ctl_host[0].restrict_pending) break;
+      int next_k = -1;
+      if (int rc = mccg_restrict(ctx, ctx->ctl_host[0].k, &next_k)) return rc;
+      if (next_k < 0) break;
+      k_host = next_k;
+      stopped = false;
+      chunk = 4;
     }
-    for (int q = 0; q < npending; ++q)
-        if (int rc = read_chunk(pending[q])) return rc;
     CK(cudaEventRecord(ctx->ev_loop1, st));
     if (int rc = final_local(ctx)) return rc;
     if (int rc = final_rest(ctx)) return rc;
@@ -1101,6 +1307,8 @@ int coopcg_gpu_matvec_block(coopcg_gpu_ctx* ctx, const double* D, double* out) {
     if (!ctx || !D || !out) return COOPCG_E_INVALID;
     if (!ctx->a_ready) return fail(ctx, COOPCG_E_STATE, "A not set");
     CK(cudaSetDevice(ctx->device));
+    if (ctx->p != ctx->p_orig)
+        if (int rc = set_active_p(ctx, ctx->p_orig)) return rc;
     const int n = ctx->n, p = ctx->p, P = ctx->P;
     cudaStream_t st = ctx->stream;
     CK(cudaMemcpyAsync(ctx->stage, D, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, st));
@@ -1123,6 +1331,8 @@ int coopcg_gpu_matvec_block(coopcg_gpu_ctx* ctx, const double* D, double* out) {
 int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D, double tol, int force_exact, int* rank) {
     if (!ctx || !D || !rank) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
+    if (ctx->p != ctx->p_orig)
+        if (int rc = set_active_p(ctx, ctx->p_orig)) return rc;
     const int n = ctx->n, p = ctx->p, P = ctx->P;
     cudaStream_t st = ctx->stream;
     Ctl h{};

@@ -449,7 +449,9 @@ __global__ void __launch_bounds__(32)
             if (slot < 0 && norms[j] <= ctl->tol) slot = j;
         }
         if (k < capacity) {
-            for (int j = 0; j < p; ++j) tr_norms[static_cast<size_t>(k) * p + j] = norms[j];
+            const int p0 = ctl->p0;
+            for (int j = 0; j < p0; ++j) tr_norms[static_cast<size_t>(k) * p0 + j] = __longlong_as_double(0x7ff8000000000000ll);
+            for (int j = 0; j < p; ++j) tr_norms[static_cast<size_t>(k) * p0 + ctl->ids[j]] = norms[j];
             tr_minres[k] = m;
             tr_wall[k] = now - ctl->t_last;
         }
@@ -457,7 +459,7 @@ __global__ void __launch_bounds__(32)
         ctl->iterations = k + 1;
         if (slot >= 0) {
             ctl->status = 0;  // Converged
-            ctl->converged_agent = slot;
+            ctl->converged_agent = ctl->ids[slot];
             ctl->stop = 1;
         }
     }
@@ -789,6 +791,7 @@ __global__ void __launch_bounds__(1024)
                 rs.brk = !(best_sq > __dmul_rn(tol_sq, max_pivot_sq));
                 if (!rs.brk) {
                     rs.used[best] = 1;
+                    ctl->rank_cols[rs.rank] = best;
                     rs.rank += 1;
                 }
                 rs.best = best;
@@ -833,7 +836,12 @@ __global__ void __launch_bounds__(1024)
     if (tid == 0) {
         ctl->rank_result = rank;
         if (mode == 0) {
-            if (rank < p) {
+            if (rank < p && ctl->algo == 1) {
+                // mccg (solvers.hpp:162-175): pause; the host selects the
+                // surviving columns from numerical_rank(R), compacts and resumes.
+                ctl->restrict_pending = 1;
+                ctl->stop = 1;
+            } else if (rank < p) {
                 ctl->status = 1;  // RankCollapse (solvers.hpp:157-161)
                 ctl->stop = 1;
             } else if (ctl->k + 1 >= ctl->max_iters) {
@@ -843,7 +851,11 @@ __global__ void __launch_bounds__(1024)
                 ctl->k += 1;
             }
         } else if (mode == 1) {
-            if (rank < p) {
+            if (ctl->algo == 1) {
+                // mccg: the host applies setup_coordinator's restriction and
+                // tolerance logic (solvers.hpp:63-98) after reading rank/columns.
+                ctl->restrict_pending = 1;
+            } else if (rank < p) {
                 ctl->status = 1;  // setup_coordinator, solvers.hpp:83-85
                 ctl->stop = 1;
             } else if (ctl->max_iters == 0) {
@@ -876,13 +888,27 @@ __global__ void setup_norms_kernel(double* __restrict__ small, Ctl* ctl, double*
             if (slot < 0 && nv[j] <= ctl->tol) slot = j;
         }
         init_norms[p] = m;
-        if (slot >= 0) {
+        if (slot >= 0 && ctl->algo == 0) {
             ctl->status = 0;
             ctl->converged_agent = slot;
             ctl->stop = 1;
         }
         ctl->t_last = globaltimer_ns();
     }
+}
+
+// mccg column compaction (BlockCgWorkspace::restrict_to, block_cg.hpp:84-96):
+// new[:, c] = old[:, keep[c]] for c < pk, zero beyond.  One thread per row.
+struct KeepList {
+    int keep[kMaxP];
+};
+__global__ void compact_columns_kernel(double* __restrict__ blk, int n, int P, KeepList kl, int pk) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= n) return;
+    double v[kMaxP];
+    double* r = blk + static_cast<size_t>(row) * P;
+    for (int c = 0; c < pk; ++c) v[c] = r[kl.keep[c]];
+    for (int c = 0; c < P; ++c) r[c] = (c < pk) ? v[c] : 0.0;
 }
 
 // finalize_trace (solvers.hpp:188-210): final_residual_norms = ||A x_j - b||.

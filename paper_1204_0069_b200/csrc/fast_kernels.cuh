@@ -518,7 +518,9 @@ __global__ void __launch_bounds__(256)
             if (slot < 0 && norms[j] <= ctl->tol) slot = j;
         }
         if (k < capacity) {
-            for (int j = 0; j < p; ++j) tr_norms[static_cast<size_t>(k) * p + j] = norms[j];
+            const int p0 = ctl->p0;
+            for (int j = 0; j < p0; ++j) tr_norms[static_cast<size_t>(k) * p0 + j] = __longlong_as_double(0x7ff8000000000000ll);
+            for (int j = 0; j < p; ++j) tr_norms[static_cast<size_t>(k) * p0 + ctl->ids[j]] = norms[j];
             tr_minres[k] = m;
             tr_wall[k] = now - ctl->t_last;
         }
@@ -526,7 +528,7 @@ __global__ void __launch_bounds__(256)
         ctl->iterations = k + 1;
         if (slot >= 0) {
             ctl->status = 0;
-            ctl->converged_agent = slot;
+            ctl->converged_agent = ctl->ids[slot];
             ctl->stop = 1;
         }
     }
@@ -560,7 +562,7 @@ __global__ void fast_norms_kernel(const double* __restrict__ part, int nparts, i
         }
         out[p] = m;
         if (setup) {
-            if (slot >= 0) {
+            if (slot >= 0 && ctl->algo == 0) {
                 ctl->status = 0;
                 ctl->converged_agent = slot;
                 ctl->stop = 1;

@@ -174,7 +174,9 @@ class GpuShardEngine:
         init = np.zeros(p)
         fres = np.zeros(p)
         fx = np.zeros((p, n)) if want_x else None
+        act = np.zeros(p, dtype=np.int32)
         tr = _capi.coopcg_trace()
+        tr.active_agents = act.ctypes.data_as(C.POINTER(C.c_int))
         tr.capacity = cap
         tr.residual_norms = _dp(norms)
         tr.minres = _dp(minres)
@@ -183,7 +185,7 @@ class GpuShardEngine:
         tr.final_residual_norms = _dp(fres)
         tr.final_x = _dp(fx) if want_x else C.POINTER(C.c_double)()
         _check(self.ctx._h, _capi.lib().coopcg_gpu_end(self.ctx._h, C.byref(tr)))
-        return self.ctx._make_trace(tr, norms, minres, wall, init, fres, fx, self.opts)
+        return self.ctx._make_trace(tr, norms, minres, wall, init, fres, fx, self.opts, act)
 
     def close(self):
         self.ctx.close()

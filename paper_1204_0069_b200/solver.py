@@ -67,6 +67,7 @@ class SolveOptions:
     max_iters: int = -1
     recompute_residual_every: int = -1
     rank_rel_tol: float = 1e-10
+    algo: str = "ccg"  # "ccg" (ccg_solve) | "mccg" (mccg_solve, solvers.hpp:338-342)
 
     def to_c(self) -> _capi.coopcg_opts:
         o = _capi.coopcg_opts()
@@ -74,6 +75,7 @@ class SolveOptions:
         o.max_iters = int(self.max_iters)
         o.recompute_residual_every = int(self.recompute_residual_every)
         o.rank_rel_tol = float(self.rank_rel_tol)
+        o.algo = 1 if self.algo == "mccg" else 0
         return o
 
 
@@ -108,6 +110,7 @@ class SolveTrace:
     final_minres: float
     setup_mults: int
     loop_wall_ns: int
+    final_residual_norms_by_id: np.ndarray = field(default=None)
     barriers_per_iteration: int = 0
     residual_norms: np.ndarray = field(default=None)  # (iterations, p)
     minres: np.ndarray = field(default=None)
@@ -224,7 +227,9 @@ class GpuContext:
         init = np.zeros(p)
         fres = np.zeros(p)
         fx = np.zeros((p, n)) if want_x else None
+        act = np.zeros(p, dtype=np.int32)
         tr = _capi.coopcg_trace()
+        tr.active_agents = act.ctypes.data_as(C.POINTER(C.c_int))
         tr.capacity = cap
         tr.residual_norms = _dp(norms)
         tr.minres = _dp(minres)
@@ -236,25 +241,29 @@ class GpuContext:
         rc = _capi.lib().coopcg_gpu_run(self._h, C.byref(co), C.byref(tr))
         _check(self._h, rc)
         _capi.lib().coopcg_gpu_timing(self._h, C.byref(self._timing))
-        return self._make_trace(tr, norms, minres, wall, init, fres, fx, opts)
+        return self._make_trace(tr, norms, minres, wall, init, fres, fx, opts, act)
 
-    def _make_trace(self, tr, norms, minres, wall, init, fres, fx, opts) -> SolveTrace:
+    def _make_trace(self, tr, norms, minres, wall, init, fres, fx, opts, act=None) -> SolveTrace:
         n, p = self.n, self.p
         it = tr.iterations
         every = opts.recompute_residual_every if opts.recompute_residual_every >= 0 else 50
         recs = []
         for k in range(it):
             rc = every > 0 and (k + 1) % every == 0
-            m = iteration_mults(n, p, rc)
-            recs.append(IterationRecord(k=k, active_agents=p, agents=list(range(p)),
-                                        residual_norms=norms[k].copy(), minres=float(minres[k]),
-                                        mults=m, mults_per_worker=[m] * p, wall_ns=int(wall[k])))
+            agents = [j for j in range(p) if not np.isnan(norms[k, j])]
+            pk = len(agents)
+            m = iteration_mults(n, pk, rc)
+            recs.append(IterationRecord(k=k, active_agents=pk, agents=agents,
+                                        residual_norms=norms[k, agents].copy(), minres=float(minres[k]),
+                                        mults=m, mults_per_worker=[m] * pk, wall_ns=int(wall[k])))
+        active = [int(a) for a in act[:tr.n_active]] if act is not None else list(range(p))
         return SolveTrace(iterations=recs, status=TerminalStatus(tr.status),
                           converged_agent=tr.converged_agent,
-                          final_x=(fx.T.copy() if fx is not None else None),
-                          active_agents=list(range(p)), initial_residual_norms=init,
-                          initial_minres=tr.initial_minres, final_residual_norms=fres,
+                          final_x=(fx.T[:, active].copy() if fx is not None else None),
+                          active_agents=active, initial_residual_norms=init,
+                          initial_minres=tr.initial_minres, final_residual_norms=fres[active].copy(),
                           final_minres=tr.final_minres, setup_mults=n * n,
+                          final_residual_norms_by_id=fres.copy(),
                           loop_wall_ns=int(tr.loop_wall_ns), residual_norms=norms[:it].copy(),
                           minres=minres[:it].copy(), wall_ns=wall[:it].copy(),
                           exact_rank_checks=tr.exact_rank_checks)
