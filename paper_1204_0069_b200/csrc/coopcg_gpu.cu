@@ -36,6 +36,10 @@ constexpr int kAdS = 4;
 constexpr int kChunkMax = 16;
 constexpr int kMaxParts = 296;  // 2 x 148 SMs
 
+int grid_for(size_t elems, int block) {
+    size_t g = (elems + block - 1) / block;
+    return (int)std::min<size_t>(g, 148ull * 16);
+}
 int pad_cols(int p) {
     int P = 4;
     while (P < p) P *= 2;
@@ -59,6 +63,7 @@ struct coopcg_gpu_ctx {
     double* qpart = nullptr;     // kchunks x n_loc x P
     double* gpart = nullptr;     // rgrid x 4 P^2 (row-pass Gram partials)
     double* npart = nullptr;     // ugrid x P (norm partials)
+    double* dtiles = nullptr;    // the A.D operand re-laid out as [col][kk] k-tiles
     bool a_ready = false, inputs_ready = false;
     cudaStream_t stream = nullptr;
     std::string msg;
@@ -181,9 +186,15 @@ template <int P>
 size_t fast_ad_smem() {
     return (size_t)kFastS * (kFastBR * kFastT + kFastT * P) * sizeof(double) + 2 * kFastS * sizeof(uint64_t);
 }
+// column groups per CTA: P=8 -> 1 (2 DMMA warps), P=16/32 -> 2 (4 DMMA warps)
+template <int P>
+constexpr int fast_wn() { return P >= 16 ? 2 : 1; }
+
 template <int P>
 cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
-    auto kern = ad_fast_kernel<P>;
+    constexpr int WN = fast_wn<P>();
+    constexpr bool TR = P >= 16;
+    auto kern = ad_fast_kernel<P, WN, TR>;
     static bool attr_done[64] = {};
     const int dev = ctx->device & 63;
     if (!attr_done[dev]) {
@@ -191,9 +202,17 @@ cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
         if (e != cudaSuccess) return e;
         attr_done[dev] = true;
     }
-    kern<<<ctx->f_grid, 96, fast_ad_smem<P>(), ctx->stream>>>(ctx->At, ctx->n, ctx->n_loc, ctx->lay.ntiles, src,
-                                                              ctx->qpart, ctx->f_kchunks, ctx->f_tpc, ctx->f_units,
-                                                              stop);
+    const double* operand = src;
+    if (TR) {  // operand -> [col][kk] k-tiles (conflict-free B fragments at P >= 16)
+        const size_t tot = (size_t)ctx->lay.ntiles * P * kFastT;
+        operand_tiles_kernel<P><<<grid_for(tot, 256), 256, 0, ctx->stream>>>(src, ctx->n, ctx->lay.ntiles,
+                                                                             ctx->dtiles, stop);
+        ++ctx->launches;
+        operand = ctx->dtiles;
+    }
+    kern<<<ctx->f_grid, 32 + 64 * WN, fast_ad_smem<P>(), ctx->stream>>>(
+        ctx->At, ctx->n, ctx->n_loc, ctx->lay.ntiles, operand, ctx->qpart, ctx->f_kchunks, ctx->f_tpc,
+        ctx->f_units, stop);
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -274,12 +293,12 @@ cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, co
     return cudaGetLastError();
 }
 
-// ~96 KB rings: P=4: 3 x 256 rows; P=8: 4 x 128; P=16: 4 x 64; P=32: 4 x 32.
+// ~96 KB rings (tools/probe/chain_kernel_probe.cu): P=4: 3 x 256 rows; P=8: 2 x 256; P=16: 4 x 64; P=32: 4 x 32.
 cudaError_t chains_launch(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
                           int nsrc, const int* stop) {
     switch (ctx->P) {
     case 4: return chains_launch_t<4, 256, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
-    case 8: return chains_launch_t<8, 128, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 8: return chains_launch_t<8, 256, 2>(ctx, phase, s0, s1, s2, nsrc, stop);
     case 16: return chains_launch_t<16, 64, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
     default: return chains_launch_t<32, 32, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
     }
@@ -324,10 +343,6 @@ void build_descs(int p, int P, std::vector<ChainDesc>& all, int off[4], int cnt[
 
 size_t rank_smem(int P) { return 2ull * kRankTile * P * sizeof(double) + 2 * sizeof(uint64_t); }
 
-int grid_for(size_t elems, int block) {
-    size_t g = (elems + block - 1) / block;
-    return (int)std::min<size_t>(g, 148ull * 16);
-}
 
 int destroy_impl(coopcg_gpu_ctx* ctx) {
     if (!ctx) return COOPCG_OK;
@@ -346,6 +361,7 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaFree(ctx->qpart);
     cudaFree(ctx->gpart);
     cudaFree(ctx->npart);
+    cudaFree(ctx->dtiles);
     cudaFree(ctx->small);
     cudaFree(ctx->partials);
     cudaFree(ctx->init_norms);
@@ -509,6 +525,7 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         CKC(cudaMalloc(&ctx->qpart, sizeof(double) * (size_t)ctx->f_kchunks * ctx->n_loc * ctx->P));
         CKC(cudaMalloc(&ctx->gpart, sizeof(double) * (size_t)ctx->f_rgrid * 4 * ctx->P * ctx->P));
         CKC(cudaMalloc(&ctx->npart, sizeof(double) * (size_t)ctx->f_ugrid * ctx->P));
+        CKC(cudaMalloc(&ctx->dtiles, sizeof(double) * (size_t)ctx->lay.ntiles * ctx->P * kFastT));
         CKC(cudaFuncSetAttribute(fast_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)((4 * 32 * 32 + 1024) * sizeof(double))));
     }

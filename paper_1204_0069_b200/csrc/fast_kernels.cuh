@@ -33,29 +33,55 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 }
 
 // ---------------------------------------------------------------------------
-// (1) Qpart[c] = A_panel(:, kchunk c) . D(kchunk c, :) for work units
-// (panel, kchunk); persistent CTAs; warp 0 = bulk-copy producer, warps 1..2
-// consume with m8n8k4 DMMA (warp w: 32 rows = 4 M-tiles x P/8 N-tiles).
+// (0) Operand re-layout for the MMA: a row-major n x P block (D or X) into
+// k-tiles of [col][kk] (P x kFastT doubles per tile, zero past n), so the
+// DMMA B-fragment loads (8 columns x 4 consecutive k per warp) hit distinct
+// banks like the A fragments (288-byte stride) instead of 4-way conflicts.
 template <int P>
-__global__ void __launch_bounds__(96)
-    ad_fast_kernel(const double* __restrict__ Af, int n, int n_loc, int ntiles, const double* __restrict__ D,
+__global__ void __launch_bounds__(256)
+    operand_tiles_kernel(const double* __restrict__ src, int n, int ntiles, double* __restrict__ dst,
+                         const int* __restrict__ stop) {
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
+    const size_t total = static_cast<size_t>(ntiles) * P * kFastT;
+    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int kk = static_cast<int>(e % kFastT);
+        const size_t rest = e / kFastT;
+        const int col = static_cast<int>(rest % P);
+        const int t = static_cast<int>(rest / P);
+        const int k = t * kFastT + kk;
+        dst[e] = (k < n) ? src[static_cast<size_t>(k) * P + col] : 0.0;
+    }
+}
+
+// (1) Qpart[c] = A_panel(:, kchunk c) . D(kchunk c, :) for work units
+// (panel, kchunk); persistent CTAs; warp 0 = bulk-copy producer, 2*WN warps
+// consume with m8n8k4 DMMA: warp w covers 32 rows (4 M-tiles) x P/WN
+// columns.  Both operands arrive as contiguous tiles (A: [r][kk], the
+// operand: [col][kk]), one bulk copy each per stage.
+// TR (transposed operand) = true: Dt holds [col][kk] k-tiles (P >= 16);
+// false: Dt is the row-major n x P block itself (P = 8: its 64-byte rows
+// already give conflict-free B fragments), tail rows zero-filled in smem.
+template <int P, int WN, bool TR>
+__global__ void __launch_bounds__(32 + 64 * WN)
+    ad_fast_kernel(const double* __restrict__ Af, int n, int n_loc, int ntiles, const double* __restrict__ Dt,
                    double* __restrict__ Qpart, int kchunks, int tiles_per_chunk, int nunits,
                    const int* __restrict__ stop) {
-    static_assert(P % 8 == 0, "fast contexts pad p to a multiple of 8");
-    constexpr int NT = P / 8;  // N tiles of 8 columns
+    static_assert(P % (8 * WN) == 0, "fast contexts pad p to a multiple of 8 per column group");
+    constexpr int NT = P / 8 / WN;  // N tiles of 8 columns per warp
+    constexpr int NCW = 2 * WN;     // consumer warps
     constexpr int BR = kFastBR, T = kFastT, S = kFastS;
-    constexpr int DP = P;      // D tile row stride in smem
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);  // S x BR x T
-    double* Ds = As + S * BR * T;                       // S x T x DP
-    uint64_t* full = reinterpret_cast<uint64_t*>(Ds + S * T * DP);
+    double* Ds = As + S * BR * T;                       // S x P x T
+    uint64_t* full = reinterpret_cast<uint64_t*>(Ds + S * P * T);
     uint64_t* empty = full + S;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 2);
+            mbar_init(&empty[s], NCW);
         }
         fence_mbar_init();
     }
@@ -70,16 +96,17 @@ __global__ void __launch_bounds__(96)
                 const int t0 = c * tiles_per_chunk, t1 = min(ntiles, t0 + tiles_per_chunk);
                 for (int t = t0; t < t1; ++t, ++it) {
                     if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
-                    const int rows = min(T, n - t * T);
-                    double* ds = Ds + s * T * DP;
-                    // the ragged last k-tile: zero the D rows past n (the A tile is
-                    // zero padded in global memory)
-                    for (int e = rows * DP; e < T * DP; ++e) ds[e] = 0.0;
                     const uint32_t abytes = BR * T * 8u;
-                    const uint32_t dbytes = static_cast<uint32_t>(rows) * P * 8u;
+                    uint32_t dbytes = P * T * 8u;
+                    if (!TR) {  // row-major operand: copy the valid rows, zero the tail
+                        const int rows = min(T, n - t * T);
+                        double* ds = Ds + s * P * T;
+                        for (int e = rows * P; e < T * P; ++e) ds[e] = 0.0;
+                        dbytes = static_cast<uint32_t>(rows) * P * 8u;
+                    }
                     mbar_arrive_expect_tx(&full[s], abytes + dbytes);
                     bulk_g2s(As + s * BR * T, Af + (static_cast<size_t>(q) * ntiles + t) * BR * T, abytes, &full[s]);
-                    bulk_g2s(ds, D + static_cast<size_t>(t) * T * P, dbytes, &full[s]);
+                    bulk_g2s(Ds + s * P * T, Dt + static_cast<size_t>(t) * P * T, dbytes, &full[s]);
                     if (++s == S) {
                         s = 0;
                         ph ^= 1u;
@@ -89,7 +116,9 @@ __global__ void __launch_bounds__(96)
         }
         return;
     }
-    const int cw = warp - 1;  // consumer warp: rows [32 cw, 32 cw + 32)
+    const int cw = warp - 1;
+    const int rb = cw / WN;          // row block: rows [32 rb, 32 rb + 32)
+    const int cg = cw % WN;          // column group: N tiles [cg*NT, cg*NT + NT)
     const int g = lane >> 2, tg = lane & 3;
     int s = 0;
     uint32_t phase = 0;
@@ -103,19 +132,21 @@ __global__ void __launch_bounds__(96)
             for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
         for (int t = t0; t < t1; ++t) {
             mbar_wait(&full[s], phase);
-            const double* as = As + s * BR * T + (32 * cw + g) * T + tg;
-            const double* ds = Ds + s * T * DP + tg * DP + g;
+            const double* as = As + s * BR * T + (32 * rb + g) * T + tg;
+            // B fragment (k = tg, n = g): [col][kk] tiles read like A; row-major [kk][col] otherwise
+            const double* ds = TR ? Ds + s * P * T + (8 * NT * cg + g) * T + tg
+                                  : Ds + s * P * T + tg * P + 8 * NT * cg + g;
 #pragma unroll
             for (int ks = 0; ks < T / 4; ++ks) {
-                double a[4], b[NT];
+                double a[4], bb[NT];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt) a[mt] = as[8 * mt * T + 4 * ks];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) b[nt] = ds[4 * ks * DP + 8 * nt];
+                for (int nt = 0; nt < NT; ++nt) bb[nt] = TR ? ds[8 * nt * T + 4 * ks] : ds[4 * ks * P + 8 * nt];
 #pragma unroll
                 for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], b[nt]);
+                    for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], bb[nt]);
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -127,13 +158,13 @@ __global__ void __launch_bounds__(96)
         double* qp = Qpart + static_cast<size_t>(c) * n_loc * P;
 #pragma unroll
         for (int mt = 0; mt < 4; ++mt) {
-            const int il = q * BR + 32 * cw + 8 * mt + g;
+            const int il = q * BR + 32 * rb + 8 * mt + g;
             if (il < n_loc) {
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
-                    const int col = 8 * nt + 2 * tg;
-                    if (col < P) qp[static_cast<size_t>(il) * P + col] = acc[mt][nt][0];
-                    if (col + 1 < P) qp[static_cast<size_t>(il) * P + col + 1] = acc[mt][nt][1];
+                    const int col = 8 * (NT * cg + nt) + 2 * tg;
+                    qp[static_cast<size_t>(il) * P + col] = acc[mt][nt][0];
+                    qp[static_cast<size_t>(il) * P + col + 1] = acc[mt][nt][1];
                 }
             }
         }
