@@ -70,7 +70,10 @@ typedef struct {
     int max_iters;                /* -1 => 2n (solvers.hpp:18-23) */
     int recompute_residual_every; /* -1 => 50; 0 disables (solvers.hpp:25-35) */
     double rank_rel_tol;          /* numerical_rank tolerance, reference default 1e-10 */
-    int algo;                     /* 0 = ccg_solve (solvers.hpp:329-333), 1 = mccg_solve (:338-342) */
+    int algo;                     /* 0 = ccg_solve (solvers.hpp:329-333), 1 = mccg_solve (:338-342),
+                                     2 = steepest_descent_solve (p = 1, exact; :532-646).
+                                     cg_solve (:388-530) is algo 0 with p = 1 and
+                                     recompute_residual_every defaulting to 1. */
 } coopcg_opts;
 
 /* SolveTrace<double> (trace.hpp:46-71), caller-allocated arrays.

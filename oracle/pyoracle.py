@@ -106,6 +106,7 @@ def ref_lib() -> C.CDLL:
                                         C.POINTER(OrcOpts), C.POINTER(OrcTrace)]
         lib.ref_cg_solve.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                      C.POINTER(OrcOpts), C.POINTER(OrcTrace)]
+        lib.ref_sd_solve.argtypes = lib.ref_cg_solve.argtypes
         lib.ref_make_problem.argtypes = [C.c_int, C.c_int, C.c_double, C.c_ulonglong,
                                          C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_matvec_block.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
@@ -181,15 +182,16 @@ def ref_solve(A, b, X0, tol=0.0, max_iters=-1, recompute=-1, rank_tol=1e-10, alg
                 X0c.ctypes.data, C.byref(o))
 
 
-def ref_cg(A, b, x0, tol=0.0, max_iters=-1, recompute=-1) -> Trace:
+def ref_cg(A, b, x0, tol=0.0, max_iters=-1, recompute=-1, algo="cg") -> Trace:
+    """The reference's cg_solve (algo="sd": steepest_descent_solve)."""
     A = np.ascontiguousarray(A, dtype=np.float64)
     b = np.ascontiguousarray(b, dtype=np.float64)
     x0 = np.ascontiguousarray(x0, dtype=np.float64)
     n = len(b)
     cap = max_iters if max_iters >= 0 else 2 * n
     o = _opts(tol, max_iters, recompute, 1e-10)
-    return _run(ref_lib().ref_cg_solve, n, 1, cap, n, A.ctypes.data, b.ctypes.data,
-                x0.ctypes.data, C.byref(o))
+    fn = ref_lib().ref_cg_solve if algo == "cg" else ref_lib().ref_sd_solve
+    return _run(fn, n, 1, cap, n, A.ctypes.data, b.ctypes.data, x0.ctypes.data, C.byref(o))
 
 
 def ref_make_problem(n, p, cond, seed):

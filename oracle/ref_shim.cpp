@@ -148,6 +148,21 @@ int ref_cg_solve(int n, const double* A, const double* b, const double* x0, cons
     });
 }
 
+int ref_sd_solve(int n, const double* A, const double* b, const double* x0, const orc_opts* o,
+                 orc_trace* tr) {
+    tr->error_msg[0] = '\0';
+    return guarded(tr, [&] {
+        auto Am = make_A(n, A);
+        std::vector<double> bv(b, b + n), xv(x0, x0 + n);
+        SolveOptions<double> opts;
+        opts.tol = o->tol;
+        opts.max_iters = o->max_iters;
+        opts.recompute_residual_every = o->recompute_residual_every;
+        auto t = steepest_descent_solve(Am, bv, xv, opts);
+        fill_trace(t, n, tr);
+    });
+}
+
 /// The reference's own problem family (random_spd + rhs/starts, float mode).
 int ref_make_problem(int n, int p, double cond, unsigned long long seed, double* A, double* b,
                      double* X0) {

@@ -19,6 +19,8 @@ from .solver import (  # noqa: F401
     SpdViolationError,
     TerminalStatus,
     ccg_solve,
+    cg_solve,
+    steepest_descent_solve,
     gen_householder_factors,
     gen_rhs,
     gen_starts,

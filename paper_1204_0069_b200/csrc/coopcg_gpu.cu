@@ -886,9 +886,11 @@ static int begin_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     ctx->max_iters = o.max_iters >= 0 ? o.max_iters : 2 * ctx->n;  // solvers.hpp:18-23
     ctx->every = o.recompute_residual_every >= 0 ? o.recompute_residual_every : 50;
     if (int rc = ensure_trace_capacity(ctx, std::max(ctx->max_iters, 1))) return rc;
-    ctx->algo = o.algo == 1 ? 1 : 0;
+    ctx->algo = (o.algo == 1 || o.algo == 2) ? o.algo : 0;
     if (ctx->algo == 1 && sharded(ctx))
         return fail(ctx, COOPCG_E_INVALID, "mccg_solve is single-GPU in this version");
+    if (ctx->algo == 2 && (ctx->p != 1 || ctx->arith != COOPCG_ARITH_EXACT))
+        return fail(ctx, COOPCG_E_INVALID, "steepest descent needs p = 1 and the exact mode");
     ctx->host_err = 0;
     ctx->host_err_msg.clear();
     if (ctx->p != ctx->p_orig)
@@ -1026,7 +1028,8 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
         solve_beta_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
                                             ctx->tr_capacity);
         LAUNCHED();
-        direction_kernel<<<dgrid_of(ctx), 256, 0, st>>>(ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop);
+        direction_kernel<<<dgrid_of(ctx), 256, 0, st>>>(ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop,
+                                                        ctx->algo == 2 ? 1 : 0);
         LAUNCHED();
     } else if (rec) {
         if (sharded(ctx))  // R^T Q and |R|^2 over the full replicated, recomputed R

@@ -405,7 +405,10 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
     }
     if (!warp_lu_factor(w, perm, p, floor)) {
         if (lane == 0) {
-            ctl->status = 1;  // RankCollapse (solvers.hpp:117-123)
+            // RankCollapse (solvers.hpp:117-123); steepest descent reports a
+            // vanished gradient energy with r = 0 as Converged (solvers.hpp:588-594)
+            ctl->status = (ctl->algo == 2) ? 0 : 1;
+            if (ctl->algo == 2) ctl->converged_agent = 0;
             ctl->stop = 1;
         }
         return;
@@ -434,7 +437,11 @@ __global__ void __launch_bounds__(32)
     if (lane < p) perm[lane] = ctl->perm[lane];
     __syncwarp();
     if (lane < p) {
-        warp_lu_solve_row(w, perm, p, P, small + L.rhs_b() + lane * P, small + L.beta() + lane * P);
+        if (ctl->algo == 2) {  // steepest descent: D' = R (no conjugation)
+            for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = 0.0;
+        } else {
+            warp_lu_solve_row(w, perm, p, P, small + L.rhs_b() + lane * P, small + L.beta() + lane * P);
+        }
         norms[lane] = __dsqrt_rn(small[L.nsq_r() + lane]);
         small[L.norm() + lane] = norms[lane];
     }
@@ -510,7 +517,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     direction_kernel(const double* __restrict__ R, const double* __restrict__ D, double* __restrict__ Dn,
                      const double* __restrict__ small, int n, int p, int P, double* __restrict__ partials,
-                     const int* __restrict__ stop) {
+                     const int* __restrict__ stop, int sd_copy = 0) {
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     __shared__ double coef[kMaxP * (kMaxP + 1)];
     __shared__ double tile[256];
@@ -552,9 +559,11 @@ __global__ void __launch_bounds__(256)
             if (i < p) {
                 if (with_beta) {
                     double acc = R[e];
-                    const double* a = coef + i * (kMaxP + 1);
-                    const size_t rowoff = e - i;
-                    for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], D[rowoff + j]);
+                    if (!sd_copy) {
+                        const double* a = coef + i * (kMaxP + 1);
+                        const size_t rowoff = e - i;
+                        for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], D[rowoff + j]);
+                    }
                     v = acc;
                     Dn[e] = v;
                 } else {
@@ -836,7 +845,13 @@ __global__ void __launch_bounds__(1024)
     if (tid == 0) {
         ctl->rank_result = rank;
         if (mode == 0) {
-            if (rank < p && ctl->algo == 1) {
+            if (rank < p && ctl->algo == 2) {
+                // steepest descent has no rank check: r = 0 ends with Converged
+                // at the next gradient-energy test (solvers.hpp:588-594)
+                ctl->status = 0;
+                ctl->converged_agent = 0;
+                ctl->stop = 1;
+            } else if (rank < p && ctl->algo == 1) {
                 // mccg (solvers.hpp:162-175): pause; the host selects the
                 // surviving columns from numerical_rank(R), compacts and resumes.
                 ctl->restrict_pending = 1;
@@ -855,6 +870,10 @@ __global__ void __launch_bounds__(1024)
                 // mccg: the host applies setup_coordinator's restriction and
                 // tolerance logic (solvers.hpp:63-98) after reading rank/columns.
                 ctl->restrict_pending = 1;
+            } else if (rank < p && ctl->algo == 2) {
+                ctl->status = 0;  // steepest descent: zero gradient -> Converged (solvers.hpp:588-594)
+                ctl->converged_agent = 0;
+                ctl->stop = 1;
             } else if (rank < p) {
                 ctl->status = 1;  // setup_coordinator, solvers.hpp:83-85
                 ctl->stop = 1;

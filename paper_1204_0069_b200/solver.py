@@ -67,7 +67,7 @@ class SolveOptions:
     max_iters: int = -1
     recompute_residual_every: int = -1
     rank_rel_tol: float = 1e-10
-    algo: str = "ccg"  # "ccg" (ccg_solve) | "mccg" (mccg_solve, solvers.hpp:338-342)
+    algo: str = "ccg"  # "ccg" (ccg_solve) | "mccg" (mccg_solve, solvers.hpp:338-342) | "sd" (internal)
 
     def to_c(self) -> _capi.coopcg_opts:
         o = _capi.coopcg_opts()
@@ -75,7 +75,7 @@ class SolveOptions:
         o.max_iters = int(self.max_iters)
         o.recompute_residual_every = int(self.recompute_residual_every)
         o.rank_rel_tol = float(self.rank_rel_tol)
-        o.algo = 1 if self.algo == "mccg" else 0
+        o.algo = {"ccg": 0, "mccg": 1, "sd": 2}[self.algo]
         return o
 
 
@@ -321,6 +321,47 @@ def ccg_solve(A: np.ndarray, b: np.ndarray, X0: np.ndarray, opts: Optional[Solve
     with GpuContext(n, p, gpu.device, gpu.arith) as ctx:
         ctx.set_A(A)
         return ctx.solve(b, X0, opts)
+
+
+def _single_vector_solve(A, b, x0, opts, gpu, algo):
+    import dataclasses
+    gpu = gpu or GpuOptions()
+    opts = opts or SolveOptions()
+    A = np.asarray(A, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    x0 = np.asarray(x0, dtype=np.float64)
+    n = A.shape[0]
+    if A.shape != (n, n) or b.shape != (n,) or x0.shape != (n,):
+        raise DimensionError(f"{'cg_solve' if algo == 'ccg' else 'steepest_descent_solve'}: "
+                             "operand shapes do not match")
+    every = opts.recompute_residual_every if opts.recompute_residual_every >= 0 else 1
+    o = dataclasses.replace(opts, recompute_residual_every=every, algo=algo)
+    with GpuContext(n, 1, gpu.device, gpu.arith if algo == "ccg" else "exact") as ctx:
+        ctx.set_A(A)
+        t = ctx.solve(b, x0[:, None], o)
+    # the scalar solvers' own counting (solvers.hpp:438-486, :571-603)
+    for rec in t.iterations:
+        rc = every > 0 and (rec.k + 1) % every == 0
+        if algo == "ccg":
+            m = (2 * n * n + 5 * n + 2) if rc else (n * n + 6 * n + 2)
+        else:
+            m = (2 * n * n + 3 * n + 1) if rc else (n * n + 4 * n + 1)
+        rec.mults = m
+        rec.mults_per_worker = [m]
+    return t
+
+
+def cg_solve(A, b, x0, opts: Optional[SolveOptions] = None, gpu: Optional[GpuOptions] = None) -> SolveTrace:
+    """Classical CG (solvers.hpp:388-530) on the block kernels: the p = 1 block
+    solver with the same residual policy (default: recompute every step)
+    reproduces cg_solve bit for bit (tests/test_solvers.cpp:176-201)."""
+    return _single_vector_solve(A, b, x0, opts, gpu, "ccg")
+
+
+def steepest_descent_solve(A, b, x0, opts: Optional[SolveOptions] = None,
+                           gpu: Optional[GpuOptions] = None) -> SolveTrace:
+    """Steepest descent (solvers.hpp:532-646): p = 1 with beta = 0 (exact mode)."""
+    return _single_vector_solve(A, b, x0, opts, gpu, "sd")
 
 
 # ---- host generators for b, X0 (DESIGN.md §3) -------------------------------

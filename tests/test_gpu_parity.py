@@ -43,6 +43,15 @@ def assert_same(gt, ot):
 def test_golden_bitwise(m, name):
     A, z = load_golden(name)
     algo = str(z["algo"]) if "algo" in z else "ccg"
+    if algo in ("cg", "sd"):
+        fn = m.cg_solve if algo == "cg" else m.steepest_descent_solve
+        t = fn(A, z["b"], z["X0"][:, 0], m.SolveOptions(tol=float(z["tol"]), max_iters=int(z["max_iters"]),
+                                                          recompute_residual_every=int(z["recompute"])))
+        assert str(t.status) == str(z["status"]) and t.iteration_count() == int(z["iterations"])
+        assert np.array_equal(t.residual_norms, z["residual_norms"])
+        assert np.array_equal(t.final_x, z["final_x"])
+        assert np.array_equal(t.final_residual_norms, z["final_residual_norms"])
+        return
     opts = m.SolveOptions(tol=float(z["tol"]), max_iters=int(z["max_iters"]),
                           recompute_residual_every=int(z["recompute"]), algo=algo)
     if int(z["rc"]) == 2:
