@@ -146,9 +146,15 @@ size_t ad_smem() {
     return static_cast<size_t>(kAdS) * kAdT * (BR + P) * sizeof(double) + 2 * kAdS * sizeof(uint64_t);
 }
 
+// rows per thread: 2 at P >= 16 (one LDS.128 of A feeds 2 x CPT chains;
+// tools/probe/ad_probe.cu: -11% / -12% time at P = 16 / 32), 1 otherwise.
+template <int P>
+constexpr int ad_rpt() { return P >= 16 ? 2 : 1; }
+
 template <int P, int CPT, int BR>
 cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
-    auto kern = ad_exact_kernel<P, CPT, BR, kAdT, kAdS>;
+    constexpr int RPT = ad_rpt<P>();
+    auto kern = ad_exact_kernel<P, CPT, BR, kAdT, kAdS, RPT>;
     const size_t smem = ad_smem<P, CPT, BR>();
     static bool attr_done[64] = {};
     const int dev = ctx->device & 63;
@@ -158,7 +164,7 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
         attr_done[dev] = true;
     }
     dim3 grid((ctx->n_loc + BR - 1) / BR);
-    dim3 block(32 + BR * (P / CPT));
+    dim3 block(32 + (BR / RPT) * (P / CPT));
     kern<<<grid, block, smem, ctx->stream>>>(ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop);
     ++ctx->launches;
     return cudaGetLastError();
@@ -176,8 +182,8 @@ cudaError_t ad_launch(coopcg_gpu_ctx* ctx, const double* src, double* dst, const
     switch (ctx->P) {
     case 4: return ad_launch_br<4, 2>(ctx, src, dst, b, stop);
     case 8: return ad_launch_br<8, 4>(ctx, src, dst, b, stop);
-    case 16: return ad_launch_br<16, 8>(ctx, src, dst, b, stop);
-    default: return ad_launch_br<32, 8>(ctx, src, dst, b, stop);
+    case 16: return ad_launch_br<16, 4>(ctx, src, dst, b, stop);
+    default: return ad_launch_br<32, 4>(ctx, src, dst, b, stop);
     }
 }
 
@@ -264,9 +270,9 @@ AdConfig pick_ad_config(int n_loc, int P) {
     AdConfig c;
     // Measured sweep (tools/probe/ad_probe.cu, profiles/): T=32, S=4 rings;
     // P=4: 2 cols/thread (7.1 TB/s at n=16384), P=8: 4 (5.0 TB/s),
-    // P=16/32: 8 (FP64-issue bound in exact mode, ~12 of 18 T instr/s).
+    // P=16/32: 4 cols x 2 rows (FP64-issue bound in exact mode, ~13 of 18 T instr/s).
     c.BR = (n_loc >= 148 * 64) ? 64 : 32;
-    c.CPT = (P == 4) ? 2 : (P == 8 ? 4 : 8);
+    c.CPT = (P == 4) ? 2 : 4;  // with 2 rows per thread at P >= 16
     return c;
 }
 

@@ -31,12 +31,14 @@ namespace coopcg_gpu {
 // Epilogue (sub_b != 0): Y = acc - b (block_cg.hpp:132-138 / :236-241
 // `r[row] -= b[row]`), used for R0 = A X0 - b, the periodic residual
 // recomputation and the final true residual (solvers.hpp:188-210).
-template <int P, int CPT, int BR, int T, int S>
-__global__ void __launch_bounds__(32 + BR*(P / CPT))
+template <int P, int CPT, int BR, int T, int S, int RPT = 1>
+__global__ void __launch_bounds__(32 + (BR / RPT) * (P / CPT))
     ad_exact_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
                     const double* __restrict__ b, int p, const int* __restrict__ stop) {
-    constexpr int kConsumerWarps = BR * (P / CPT) / 32;
+    constexpr int RT = BR / RPT;  // row-threads per column group
+    constexpr int kConsumerWarps = RT * (P / CPT) / 32;
+    static_assert(RPT == 1 || RPT == 2, "1 or 2 rows per thread");
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);
@@ -83,66 +85,77 @@ __global__ void __launch_bounds__(32 + BR*(P / CPT))
     }
 
     const int tid = threadIdx.x - 32;
-    const int r = tid % BR;
-    const int g = tid / BR;
-    double acc[CPT];
+    const int r = tid % RT;   // this thread's rows: RPT * r .. RPT * r + RPT - 1
+    const int g = tid / RT;
+    double acc[RPT][CPT];
 #pragma unroll
-    for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
+    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[q][c] = 0.0;
 
     int s = 0;
     uint32_t phase = 0;
     for (int t = 0; t < ntiles; ++t) {
         mbar_wait(&full[s], phase);
-        const double* a_t = As + s * T * BR + r;
+        const double* a_t = As + s * T * BR + RPT * r;
         const double* d_t = Ds + s * T * P + g * CPT;
         const int rows = min(T, n - t * T);
         if (rows == T) {
             // Register software pipeline: the products of a batch of U k-steps
             // are formed, the next batch's shared-memory loads are issued, and
             // only then the dependent DADD chains run (k ascending per column).
-            constexpr int U = (CPT >= 8) ? 2 : 4;
+            constexpr int U = (CPT * RPT >= 8) ? 2 : 4;
             static_assert(T % U == 0, "T must be a multiple of U");
-            double av[U];
+            double av[U][RPT];
             double2 dv[U][CPT / 2];
+            auto load = [&](int kk, int u) {
+                if (RPT == 2) {
+                    const double2 a2 = *reinterpret_cast<const double2*>(a_t + kk * BR);
+                    av[u][0] = a2.x;
+                    av[u][RPT - 1] = a2.y;
+                } else {
+                    av[u][0] = a_t[kk * BR];
+                }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                av[u] = a_t[u * BR];
+                for (int c = 0; c < CPT / 2; ++c) dv[u][c] = reinterpret_cast<const double2*>(d_t + kk * P)[c];
+            };
 #pragma unroll
-                for (int c = 0; c < CPT / 2; ++c) dv[u][c] = reinterpret_cast<const double2*>(d_t + u * P)[c];
-            }
+            for (int u = 0; u < U; ++u) load(u, u);
 #pragma unroll
             for (int kb = 0; kb < T; kb += U) {
-                double prod[U][CPT];
+                double prod[U][RPT][CPT];
 #pragma unroll
                 for (int u = 0; u < U; ++u)
 #pragma unroll
-                    for (int c = 0; c < CPT / 2; ++c) {
-                        prod[u][2 * c] = __dmul_rn(av[u], dv[u][c].x);
-                        prod[u][2 * c + 1] = __dmul_rn(av[u], dv[u][c].y);
-                    }
+                    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+                        for (int c = 0; c < CPT / 2; ++c) {
+                            prod[u][q][2 * c] = __dmul_rn(av[u][q], dv[u][c].x);
+                            prod[u][q][2 * c + 1] = __dmul_rn(av[u][q], dv[u][c].y);
+                        }
                 if (kb + U < T) {
 #pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        av[u] = a_t[(kb + U + u) * BR];
-#pragma unroll
-                        for (int c = 0; c < CPT / 2; ++c)
-                            dv[u][c] = reinterpret_cast<const double2*>(d_t + (kb + U + u) * P)[c];
-                    }
+                    for (int u = 0; u < U; ++u) load(kb + U + u, u);
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u)
 #pragma unroll
-                    for (int c = 0; c < CPT; ++c) acc[c] = __dadd_rn(acc[c], prod[u][c]);
+                    for (int q = 0; q < RPT; ++q)
+#pragma unroll
+                        for (int c = 0; c < CPT; ++c) acc[q][c] = __dadd_rn(acc[q][c], prod[u][q][c]);
             }
         } else {
             for (int kk = 0; kk < rows; ++kk) {
-                const double a = a_t[kk * BR];
                 const double2* d2 = reinterpret_cast<const double2*>(d_t + kk * P);
 #pragma unroll
-                for (int c = 0; c < CPT / 2; ++c) {
-                    const double2 dv = d2[c];
-                    acc[2 * c] = mac_exact(acc[2 * c], a, dv.x);
-                    acc[2 * c + 1] = mac_exact(acc[2 * c + 1], a, dv.y);
+                for (int q = 0; q < RPT; ++q) {
+                    const double a = a_t[kk * BR + q];
+#pragma unroll
+                    for (int c = 0; c < CPT / 2; ++c) {
+                        const double2 dv = d2[c];
+                        acc[q][2 * c] = mac_exact(acc[q][2 * c], a, dv.x);
+                        acc[q][2 * c + 1] = mac_exact(acc[q][2 * c + 1], a, dv.y);
+                    }
                 }
             }
         }
@@ -154,17 +167,20 @@ __global__ void __launch_bounds__(32 + BR*(P / CPT))
         }
     }
 
-    const int il = i0 + r;
-    if (il < n_loc) {
-        const int row = row0 + il;
-        double* y = Y + static_cast<size_t>(row) * P + g * CPT;
-        const double bb = (b != nullptr) ? b[row] : 0.0;
 #pragma unroll
-        for (int c = 0; c < CPT; ++c) {
-            const int col = g * CPT + c;
-            double v = 0.0;
-            if (col < p) v = (b != nullptr) ? __dsub_rn(acc[c], bb) : acc[c];
-            y[c] = v;
+    for (int q = 0; q < RPT; ++q) {
+        const int il = i0 + RPT * r + q;
+        if (il < n_loc) {
+            const int row = row0 + il;
+            double* y = Y + static_cast<size_t>(row) * P + g * CPT;
+            const double bb = (b != nullptr) ? b[row] : 0.0;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                const int col = g * CPT + c;
+                double v = 0.0;
+                if (col < p) v = (b != nullptr) ? __dsub_rn(acc[q][c], bb) : acc[q][c];
+                y[c] = v;
+            }
         }
     }
 }

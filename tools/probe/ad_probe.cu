@@ -6,13 +6,13 @@
 
 using namespace coopcg_gpu;
 
-template <int P, int CPT, int BR, int T, int S>
+template <int P, int CPT, int BR, int T, int S, int RPT = 1>
 void run(const double* Ap, int n, const double* D, double* Y, int p) {
-    auto k = ad_exact_kernel<P, CPT, BR, T, S>;
+    auto k = ad_exact_kernel<P, CPT, BR, T, S, RPT>;
     size_t smem = (size_t)S * T * (BR + P) * 8 + 2 * S * 8;
     if (smem > 227 * 1024) return;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((n + BR - 1) / BR), block(32 + BR * (P / CPT));
+    dim3 grid((n + BR - 1) / BR), block(32 + (BR / RPT) * (P / CPT));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -26,8 +26,8 @@ void run(const double* Ap, int n, const double* D, double* Y, int p) {
     cudaEventElapsedTime(&ms, e0, e1);
     ms /= reps;
     cudaError_t e = cudaGetLastError();
-    std::printf("n=%6d P=%2d CPT=%d BR=%3d T=%3d S=%d smem=%6zu : %8.3f ms  %7.1f GB/s  %5.2f TF/s %s\n", n, P, CPT, BR,
-                T, S, smem, ms, 8.0 * n * n / (ms * 1e-3) / 1e9, 2.0 * n * n * p / (ms * 1e-3) / 1e12,
+    std::printf("n=%6d P=%2d CPT=%d RPT=%d BR=%3d T=%3d S=%d smem=%6zu : %8.3f ms  %7.1f GB/s  %5.2f TF/s %s\n", n, P,
+                CPT, RPT, BR, T, S, smem, ms, 8.0 * n * n / (ms * 1e-3) / 1e9, 2.0 * n * n * p / (ms * 1e-3) / 1e12,
                 e == cudaSuccess ? "" : cudaGetErrorString(e));
 }
 
@@ -39,27 +39,22 @@ int main(int argc, char** argv) {
     cudaMalloc(&Y, (size_t)n * 32 * 8);
     cudaMemset(Ap, 0, (size_t)n * n * 8);
     cudaMemset(D, 0, (size_t)n * 32 * 8);
-    // P = 8 (cfg 2)
-    run<8, 8, 64, 32, 4>(Ap, n, D, Y, 8);
     run<8, 4, 64, 32, 4>(Ap, n, D, Y, 8);
-    run<8, 2, 64, 32, 4>(Ap, n, D, Y, 8);
-    run<8, 4, 32, 32, 4>(Ap, n, D, Y, 8);
-    run<8, 8, 32, 32, 4>(Ap, n, D, Y, 8);
-    run<8, 4, 128, 32, 4>(Ap, n, D, Y, 8);
-    run<8, 2, 128, 32, 4>(Ap, n, D, Y, 8);
-    run<8, 4, 64, 64, 4>(Ap, n, D, Y, 8);
-    run<8, 4, 64, 16, 6>(Ap, n, D, Y, 8);
-    run<8, 4, 64, 32, 8>(Ap, n, D, Y, 8);
-    run<8, 2, 64, 32, 6>(Ap, n, D, Y, 8);
-    run<8, 2, 32, 64, 4>(Ap, n, D, Y, 8);
-    // P = 4 / 16 / 32 at the same n (per-byte behaviour)
+    run<8, 2, 64, 32, 4, 2>(Ap, n, D, Y, 8);
+    run<8, 4, 64, 32, 4, 2>(Ap, n, D, Y, 8);
+    run<8, 4, 128, 32, 4, 2>(Ap, n, D, Y, 8);
+    run<8, 8, 64, 32, 4, 2>(Ap, n, D, Y, 8);
+    run<8, 2, 32, 32, 4, 2>(Ap, n, D, Y, 8);
     run<4, 2, 64, 32, 4>(Ap, n, D, Y, 4);
-    run<4, 4, 64, 32, 4>(Ap, n, D, Y, 4);
+    run<4, 2, 64, 32, 4, 2>(Ap, n, D, Y, 4);
+    run<4, 4, 64, 32, 4, 2>(Ap, n, D, Y, 4);
     run<16, 8, 64, 32, 4>(Ap, n, D, Y, 16);
-    run<16, 4, 64, 32, 4>(Ap, n, D, Y, 16);
-    run<16, 8, 128, 32, 4>(Ap, n, D, Y, 16);
+    run<16, 8, 64, 32, 4, 2>(Ap, n, D, Y, 16);
+    run<16, 4, 64, 32, 4, 2>(Ap, n, D, Y, 16);
+    run<16, 8, 128, 32, 3, 2>(Ap, n, D, Y, 16);
     run<32, 8, 64, 32, 4>(Ap, n, D, Y, 32);
-    run<32, 8, 128, 32, 3>(Ap, n, D, Y, 32);
-    run<32, 4, 64, 32, 4>(Ap, n, D, Y, 32);
+    run<32, 8, 64, 32, 4, 2>(Ap, n, D, Y, 32);
+    run<32, 8, 128, 32, 3, 2>(Ap, n, D, Y, 32);
+    run<32, 4, 64, 32, 4, 2>(Ap, n, D, Y, 32);
     return 0;
 }
