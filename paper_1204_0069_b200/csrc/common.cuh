@@ -141,6 +141,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// One arrive per warp from lane 0, predicated instead of branched: a
+// `if (lane == 0)` branch makes ptxas treat the code after it as divergent,
+// which (for the chain kernel) costs the uniform loop and its schedule.
+__device__ __forceinline__ void mbar_arrive_lane0(uint64_t* bar, int lane) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "setp.eq.s32 P1, %1, 0;\n"
+        "@P1 mbarrier.arrive.shared::cta.b64 _, [%0];\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(lane)
+        : "memory");
+}
 // Global -> shared bulk copy completing on an mbarrier (bytes % 16 == 0,
 // both addresses 16-byte aligned).
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {

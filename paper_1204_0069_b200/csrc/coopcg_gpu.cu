@@ -283,7 +283,7 @@ template <int P, int T, int S>
 cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
                             int nsrc, const int* stop) {
     auto kern = chain_kernel<P, T, S>;
-    const size_t smem_max = (size_t)S * 3 * T * P * sizeof(double) + 2 * S * sizeof(uint64_t);
+    const size_t smem_max = chain_smem_bytes(P, T, S, 3);
     static bool attr_done[64] = {};
     const int dev = ctx->device & 63;
     if (!attr_done[dev]) {
@@ -292,21 +292,23 @@ cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, co
         attr_done[dev] = true;
     }
     const int cnt = ctx->desc_cnt[phase];
-    const size_t smem = (size_t)S * nsrc * T * P * sizeof(double) + 2 * S * sizeof(uint64_t);
-    kern<<<(cnt + 63) / 64, 96, smem, ctx->stream>>>(s0, s1, s2, nsrc, ctx->n, ctx->descs + ctx->desc_off[phase],
+    const size_t smem = chain_smem_bytes(P, T, S, nsrc);
+    kern<<<(cnt + 63) / 64, kChainThreads, smem, ctx->stream>>>(s0, s1, s2, nsrc, ctx->n, ctx->descs + ctx->desc_off[phase],
                                                      cnt, ctx->small, stop);
     ++ctx->launches;
     return cudaGetLastError();
 }
 
-// ~96 KB rings (tools/probe/chain_kernel_probe.cu): P=4: 3 x 256 rows; P=8: 2 x 256; P=16: 4 x 64; P=32: 4 x 32.
+// Rings (tools/probe/chain_kernel_probe.cu, n = 16384): P=4/8: 3 x 256 rows
+// (99 us per phase vs 113-144 us for shallower or shorter rings); P=16:
+// 4 x 128 (the 3 x 256 ring does not fit); P=32: 4 x 64.
 cudaError_t chains_launch(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
                           int nsrc, const int* stop) {
     switch (ctx->P) {
     case 4: return chains_launch_t<4, 256, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
-    case 8: return chains_launch_t<8, 256, 2>(ctx, phase, s0, s1, s2, nsrc, stop);
-    case 16: return chains_launch_t<16, 64, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
-    default: return chains_launch_t<32, 32, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 8: return chains_launch_t<8, 256, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 16: return chains_launch_t<16, 128, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
+    default: return chains_launch_t<32, 64, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
     }
 }
 

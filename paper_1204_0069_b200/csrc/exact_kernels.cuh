@@ -188,23 +188,41 @@ __global__ void __launch_bounds__(32 + (BR / RPT) * (P / CPT))
 // ---------------------------------------------------------------------------
 // (2) Sequential dot-product chains: Gram rows, step right-hand sides and
 // norms (block_cg.hpp:153-160, :214-216, :262-264, :275-276; kernels.hpp:20-26).
-// Each chain is one thread walking k = 0..n-1 in order (a DADD latency chain,
-// ~9 cycles per step).  Tiles of T rows of up to three n x P row-major source
-// blocks stream through an S-stage shared-memory ring (bulk async copies) so
-// S-1 tiles are in flight while the chains consume one.  64 chains per CTA
-// keeps the per-step shared-memory traffic under the DADD latency.
+// Each chain is one thread walking k = 0..n-1 in order, acc = acc + x_k*y_k
+// with both roundings kept: a dependent-DADD chain (8.5 cycles per DADD
+// measured, tools/probe/clock_probe.cu).  Written naively, ptxas schedules
+// DMUL(k) right before DADD(k) with the LDS of its operands just ahead, and
+// each step pays the load, DMUL and DADD latencies (~16 cycles).  Here the
+// chain is software-pipelined over batches of U rows: step b adds batch b's
+// products (formed one step earlier), forms batch b+1's products and loads
+// batch b+2's operands, alternating two operand register sets so that the
+// loads never wait on the DMULs reading the other set.  One loop iteration
+// covers a whole tile (straight-line steps, a single basic block for ptxas);
+// tile t+1 is waited for at the top and tile t released at the bottom.
+// Static issue cost ~10 cycles per step (tools/probe/chain_kernel_probe.cu).
 //
-// Warp-specialised: warp 0 is the producer (one lane issues the bulk copies,
-// waiting on per-stage "empty" barriers); warps 1..W consume, one chain per
-// thread, and release each stage with one arrive per warp.
+// Tiles of T rows of up to three n x P row-major source blocks stream through
+// an S-stage shared-memory ring: warp 0 is the producer (one lane issues the
+// bulk copies, waiting on per-stage "empty" barriers); warps 1..2 run one
+// chain per thread (64 chains per CTA) and release a stage with one
+// (predicated) arrive per warp.
+constexpr int kChainWarps = 2;
+constexpr int kChainU = 16;  // rows per pipelined batch
+constexpr int kChainThreads = 32 * (1 + kChainWarps);
+
+__host__ __device__ constexpr size_t chain_smem_bytes(int P, int T, int S, int nsrc) {
+    return static_cast<size_t>(S) * nsrc * T * P * sizeof(double) + 2 * S * sizeof(uint64_t);
+}
+
 template <int P, int T, int S>
-__global__ void __launch_bounds__(96)
+__global__ void __launch_bounds__(kChainThreads)
     chain_kernel(const double* __restrict__ s0, const double* __restrict__ s1,
                  const double* __restrict__ s2, int nsrc, int n,
                  const ChainDesc* __restrict__ descs, int nchains, double* __restrict__ out,
                  const int* __restrict__ stop) {
-    static_assert(T % 16 == 0, "tile rows must be a multiple of the batch");
-    constexpr int kConsumerWarps = 2;
+    constexpr int U = kChainU;
+    static_assert(T % (2 * U) == 0, "tile rows must be an even number of batches");
+    constexpr int NBT = T / U;  // batches per tile
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* buf = reinterpret_cast<double*>(smem_raw);
@@ -217,7 +235,7 @@ __global__ void __launch_bounds__(96)
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
+            mbar_init(&empty[s], kChainWarps);
         }
         fence_mbar_init();
     }
@@ -243,57 +261,82 @@ __global__ void __launch_bounds__(96)
         }
         return;
     }
-    const int c = blockIdx.x * (kConsumerWarps * 32) + (tid - 32);
-    const bool active = c < nchains;
+    const int c = blockIdx.x * (kChainWarps * 32) + (tid - 32);
     ChainDesc d{0, 0, 0, 0, 0, 0, 0};
-    if (active) d = descs[c];
-    double acc = 0.0;
+    if (c < nchains) d = descs[c];
     const int xoff = d.sx * T * P + d.a;
     const int yoff = d.sy * T * P + d.b;
-    int s = 0;
-    uint32_t phase = 0;
-    for (int t = 0; t < ntiles; ++t) {
-        mbar_wait(&full[s], phase);
-        const double* base = buf + static_cast<size_t>(s) * nsrc * T * P;
-        const double* xs = base + xoff;
-        const double* ys = base + yoff;
-        if (t * T + T <= n) {
-            // Batches of 16 products; the next batch's loads are in flight
-            // while this batch's 16 dependent DADDs retire (k ascending).
-            constexpr int U = 16;
-            double xv[U], yv[U];
+    const int nb = (n + U - 1) / U;  // batches; all full except possibly the last
+    auto tile_wait = [&](int t) {
+        if (t < ntiles) mbar_wait(&full[t % S], static_cast<uint32_t>((t / S) & 1));
+    };
+    // operands of batch j (may lie past the last tile: stale ring data that
+    // is multiplied but never added)
+    auto batch_base = [&](int j) -> const double* {
+        return buf + static_cast<size_t>((j / NBT) % S) * nsrc * T * P + (j % NBT) * U * P;
+    };
+    double acc = 0.0;
+    // pr: products of the batch being added; operands of batch j live in the
+    // even (xe/ye) or odd (xo/yo) register set by the parity of j, so a step
+    // reads one set and loads into the other (no WAR hazard to serialise the
+    // loads behind the DMULs)
+    double pr[U], xe[U], ye[U], xo[U], yo[U];
+    // add batch b, form batch b+1 (from xr/yr), load batch b+2 (into xw/yw)
+    auto step = [&](int b, const double (&xr)[U], const double (&yr)[U], double (&xw)[U], double (&yw)[U]) {
+        const double* b2 = batch_base(b + 2);
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                xv[u] = xs[u * P];
-                yv[u] = ys[u * P];
-            }
-#pragma unroll
-            for (int kb = 0; kb < T; kb += U) {
-                double prod[U];
-#pragma unroll
-                for (int u = 0; u < U; ++u) prod[u] = __dmul_rn(xv[u], yv[u]);
-                if (kb + U < T) {
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        xv[u] = xs[(kb + U + u) * P];
-                        yv[u] = ys[(kb + U + u) * P];
-                    }
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, prod[u]);
-            }
-        } else {
-            const int rows = n - t * T;
-            for (int kk = 0; kk < rows; ++kk) acc = mac_exact(acc, xs[kk * P], ys[kk * P]);
+        for (int u = 0; u < U; ++u) {
+            acc = __dadd_rn(acc, pr[u]);
+            pr[u] = __dmul_rn(xr[u], yr[u]);
+            xw[u] = b2[xoff + u * P];
+            yw[u] = b2[yoff + u * P];
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (++s == S) {
-            s = 0;
-            phase ^= 1u;
+    };
+    tile_wait(0);
+    {
+        const double* b0 = batch_base(0);
+        const double* b1 = batch_base(1);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            pr[u] = __dmul_rn(b0[xoff + u * P], b0[yoff + u * P]);
+            xo[u] = b1[xoff + u * P];
+            yo[u] = b1[yoff + u * P];
         }
     }
-    if (active) out[d.out] = d.neg ? -acc : acc;
+    // One iteration per tile: tile t+1 is waited for first (the steps load up
+    // to two batches ahead), the NBT steps run straight-line (one basic block
+    // for ptxas to schedule), and tile t is released once its last batch has
+    // been multiplied.
+#pragma unroll 1
+    for (int t = 0; t < ntiles; ++t) {
+        tile_wait(t + 1);
+        const int b0 = t * NBT;
+        if ((t + 1) * T <= n) {
+#pragma unroll
+            for (int q = 0; q < NBT; q += 2) {
+                step(b0 + q, xo, yo, xe, ye);
+                step(b0 + q + 1, xe, ye, xo, yo);
+            }
+        } else {
+            // partial last tile: the batches that hold rows, the last one masked
+            for (int q = 0; q < NBT && b0 + q < nb; ++q) {
+                const int b = b0 + q;
+                if (b == nb - 1) {
+                    const int rem = n - b * U;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (u < rem) acc = __dadd_rn(acc, pr[u]);
+                } else if (q & 1) {
+                    step(b, xe, ye, xo, yo);
+                } else {
+                    step(b, xo, yo, xe, ye);
+                }
+            }
+        }
+        __syncwarp();
+        mbar_arrive_lane0(&empty[t % S], lane);
+    }
+    if (c < nchains) out[d.out] = d.neg ? -acc : acc;
 }
 
 // ---------------------------------------------------------------------------

@@ -10,14 +10,14 @@ using namespace coopcg_gpu;
 template <int P, int T, int S>
 float run(const double* s0, const double* s1, const double* s2, int n, const ChainDesc* d, int nch, double* out) {
     auto k = chain_kernel<P, T, S>;
-    size_t smem = (size_t)S * 3 * T * P * 8 + 2 * S * 8;
+    size_t smem = chain_smem_bytes(P, T, S, 3);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    k<<<(nch + 63) / 64, 96, smem>>>(s0, s1, s2, 3, n, d, nch, out, nullptr);
+    k<<<(nch + 63) / 64, kChainThreads, smem>>>(s0, s1, s2, 3, n, d, nch, out, nullptr);
     cudaEventRecord(e0);
-    for (int r = 0; r < 10; ++r) k<<<(nch + 63) / 64, 96, smem>>>(s0, s1, s2, 3, n, d, nch, out, nullptr);
+    for (int r = 0; r < 10; ++r) k<<<(nch + 63) / 64, kChainThreads, smem>>>(s0, s1, s2, 3, n, d, nch, out, nullptr);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -27,33 +27,41 @@ float run(const double* s0, const double* s1, const double* s2, int n, const Cha
     return ms / 10;
 }
 
-int main() {
-    const int n = 16384, P = 8, p = 8;
+template <int P>
+void sweep(int n) {
+    const int p = P;
     double *s0, *s1, *s2, *out;
-    cudaMalloc(&s0, n * P * 8);
-    cudaMalloc(&s1, n * P * 8);
-    cudaMalloc(&s2, n * P * 8);
-    cudaMalloc(&out, 4096 * 8);
-    cudaMemset(s0, 0, n * P * 8);
-    cudaMemset(s1, 0, n * P * 8);
-    cudaMemset(s2, 0, n * P * 8);
+    cudaMalloc(&s0, (size_t)n * P * 8);
+    cudaMalloc(&s1, (size_t)n * P * 8);
+    cudaMalloc(&s2, (size_t)n * P * 8);
+    cudaMalloc(&out, 8192 * 8);
+    cudaMemset(s0, 0, (size_t)n * P * 8);
+    cudaMemset(s1, 0, (size_t)n * P * 8);
+    cudaMemset(s2, 0, (size_t)n * P * 8);
     std::vector<ChainDesc> h;
     for (int i = 0; i < p; ++i)
         for (int j = 0; j < p; ++j) h.push_back(ChainDesc{0, (uint8_t)i, 1, (uint8_t)j, (uint16_t)(i * P + j), 0, 0});
     for (int i = 0; i < p; ++i)
-        for (int j = 0; j < p; ++j) h.push_back(ChainDesc{2, (uint8_t)i, 0, (uint8_t)j, (uint16_t)(64 + i * P + j), 1, 0});
-    for (int i = 0; i < p; ++i) h.push_back(ChainDesc{0, (uint8_t)i, 0, (uint8_t)i, (uint16_t)(128 + i), 0, 0});
+        for (int j = 0; j < p; ++j) h.push_back(ChainDesc{2, (uint8_t)i, 0, (uint8_t)j, (uint16_t)(P * P + i * P + j), 1, 0});
+    for (int i = 0; i < p; ++i) h.push_back(ChainDesc{0, (uint8_t)i, 0, (uint8_t)i, (uint16_t)(2 * P * P + i), 0, 0});
     ChainDesc* d;
     cudaMalloc(&d, h.size() * sizeof(ChainDesc));
     cudaMemcpy(d, h.data(), h.size() * sizeof(ChainDesc), cudaMemcpyHostToDevice);
     const int nch = (int)h.size();
+#define R(T, S)                                                                                             \
+    if (chain_smem_bytes(P, T, S, 3) <= 227 * 1024)                                                       \
+        std::printf("P=%2d n=%d T=%3d S=%2d smem=%6zu : %8.1f us\n", P, n, T, S, chain_smem_bytes(P, T, S, 3), \
+                    1e3 * run<P, T, S>(s0, s1, s2, n, d, nch, out));
+    R(256, 2) R(256, 3) R(128, 4) R(128, 6) R(64, 8) R(64, 12)
+#undef R
+    cudaFree(s0); cudaFree(s1); cudaFree(s2); cudaFree(out); cudaFree(d);
+}
+
+int main() {
     for (int w = 0; w < 2; ++w) {
-        std::printf("T=64  S=6 : %8.1f us\n", 1e3 * run<8, 64, 6>(s0, s1, s2, n, d, nch, out));
-        std::printf("T=64  S=3 : %8.1f us\n", 1e3 * run<8, 64, 3>(s0, s1, s2, n, d, nch, out));
-        std::printf("T=128 S=4 : %8.1f us\n", 1e3 * run<8, 128, 4>(s0, s1, s2, n, d, nch, out));
-        std::printf("T=32  S=8 : %8.1f us\n", 1e3 * run<8, 32, 8>(s0, s1, s2, n, d, nch, out));
-        std::printf("T=256 S=2 : %8.1f us\n", 1e3 * run<8, 256, 2>(s0, s1, s2, n, d, nch, out));
+        sweep<8>(16384);
+        if (w == 1) { sweep<4>(16384); sweep<16>(16384); sweep<32>(16384); }
     }
-    std::printf("(chain of %d steps: %.1f us at 12 cycles/step, 1.9 GHz)\n", n, n * 12 / 1.9e3);
+    std::printf("(chain of 16384 steps: %.1f us at 9.4 cycles/step, 1.965 GHz)\n", 16384 * 9.4 / 1.965e3);
     return 0;
 }

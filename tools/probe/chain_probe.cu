@@ -88,6 +88,74 @@ __global__ void v2_prod_then_chain(double* out, long long* cyc, int reps) {
     if (threadIdx.x == 0) cyc[0] = t1 - t0;
 }
 
+// products precomputed in shared memory, [k][chain] layout; DADD-only chain
+template <int U>
+__global__ void v4_prod_smem(double* out, long long* cyc, int reps) {
+    __shared__ double prod[T][64];
+    for (int i = threadIdx.x; i < T * 64; i += blockDim.x) prod[i / 64][i % 64] = 1.0 + i * 1e-3;
+    __syncthreads();
+    const double* ps = &prod[0][threadIdx.x];
+    double acc = 0.0;
+    long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+        double v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = ps[u * 64];
+#pragma unroll 1
+        for (int kb = 0; kb < T; kb += U) {
+            const int kn = (kb + U < T) ? kb + U : 0;
+            double nv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) nv[u] = ps[(kn + u) * 64];
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, v[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = nv[u];
+        }
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = acc;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+// in-thread products, software-pipelined: iteration b adds batch b's products
+// (computed in iteration b-1, loop-carried) while forming batch b+1's products
+// and loading batch b+2's operands.
+template <int U>
+__global__ void v5_pipelined(double* out, long long* cyc, int reps) {
+    __shared__ double tile[2][T * P];
+    for (int i = threadIdx.x; i < T * P; i += blockDim.x) { tile[0][i] = 1.0 + i * 1e-3; tile[1][i] = 0.5 - i * 1e-4; }
+    __syncthreads();
+    const double* xs = tile[0] + (threadIdx.x & 7);
+    const double* ys = tile[1] + (threadIdx.x >> 3);
+    double acc = 0.0;
+    constexpr int NB = T / U;
+    const int nb = reps * NB;
+    double pr[U], xv[U], yv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) pr[u] = __dmul_rn(xs[u * P], ys[u * P]);
+#pragma unroll
+    for (int u = 0; u < U; ++u) { xv[u] = xs[((U + u) % T) * P]; yv[u] = ys[((U + u) % T) * P]; }
+    long long t0 = clock64();
+#pragma unroll 1
+    for (int b = 0; b < nb; ++b) {
+        const int k2 = ((b + 2) % NB) * U;
+        double npr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            acc = __dadd_rn(acc, pr[u]);
+            npr[u] = __dmul_rn(xv[u], yv[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) { xv[u] = xs[(k2 + u) * P]; yv[u] = ys[(k2 + u) * P]; }
+#pragma unroll
+        for (int u = 0; u < U; ++u) pr[u] = npr[u];
+    }
+    long long t1 = clock64();
+    out[threadIdx.x] = acc;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
 // pure register chain (lower bound)
 __global__ void v3_regs(double* out, long long* cyc, int reps) {
     double acc = 0.0, x = 1.0 + threadIdx.x * 1e-3, y = 0.5;
@@ -119,6 +187,12 @@ int main() {
         v1_batched<16><<<1, 64>>>(out, cyc, reps); report("v1 batched U=16");
         v2_prod_then_chain<4><<<1, 64>>>(out, cyc, reps); report("v2 products then chain");
         v3_regs<<<1, 64>>>(out, cyc, reps); report("v3 register-only chain");
+        v5_pipelined<8><<<1, 64>>>(out, cyc, reps); report("v5 pipelined U=8");
+        v5_pipelined<16><<<1, 64>>>(out, cyc, reps); report("v5 pipelined U=16");
+        v5_pipelined<32><<<1, 64>>>(out, cyc, reps); report("v5 pipelined U=32");
+        v4_prod_smem<8><<<1, 64>>>(out, cyc, reps); report("v4 smem products U=8");
+        v4_prod_smem<16><<<1, 64>>>(out, cyc, reps); report("v4 smem products U=16");
+        v4_prod_smem<32><<<1, 64>>>(out, cyc, reps); report("v4 smem products U=32");
     }
     return 0;
 }
