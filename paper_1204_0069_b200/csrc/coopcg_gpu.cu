@@ -99,6 +99,13 @@ struct coopcg_gpu_ctx {
     std::vector<cudaEvent_t> mv_ev;  // [2 * 2 * kChunkMax]
     cudaEvent_t ev_run0 = nullptr, ev_run1 = nullptr, ev_loop0 = nullptr, ev_loop1 = nullptr;
     cudaEvent_t ev_chunk[2] = {nullptr, nullptr};
+    // rank_end off the critical path (run_impl only): it runs on `side`,
+    // concurrently with the next iteration's A.D, and is joined before the
+    // first kernel that reads what it writes (ctl->k / stop / nsq_d).
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    bool rank_async = false;   // set by run_impl for its loop
+    bool join_pending = false;
     coopcg_timing timing{};
     long long launches = 0;  // kernels launched since the last run started
     int max_iters = 0, every = 50;  // resolved SolveOptions of the current solve
@@ -154,7 +161,7 @@ constexpr int ad_rpt() { return P >= 16 ? 2 : 1; }
 template <int P, int CPT, int BR>
 cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
     constexpr int RPT = ad_rpt<P>();
-    auto kern = ad_exact_kernel<P, CPT, BR, kAdT, kAdS, RPT>;
+    auto kern = (RPT == 1) ? ad_exact_kernel<P, CPT, BR, kAdT, kAdS> : ad_exact_rpt_kernel<P, CPT, BR, kAdT, kAdS, 2>;
     const size_t smem = ad_smem<P, CPT, BR>();
     static bool attr_done[64] = {};
     const int dev = ctx->device & 63;
@@ -382,9 +389,14 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaFree(ctx->stage);
     if (ctx->ctl_host) cudaFreeHost(ctx->ctl_host);
     for (auto e : ctx->mv_ev) cudaEventDestroy(e);
-    cudaEvent_t evs[] = {ctx->ev_run0, ctx->ev_run1, ctx->ev_loop0, ctx->ev_loop1, ctx->ev_chunk[0], ctx->ev_chunk[1]};
+    cudaEvent_t evs[] = {ctx->ev_run0,      ctx->ev_run1,      ctx->ev_loop0, ctx->ev_loop1,
+                         ctx->ev_chunk[0], ctx->ev_chunk[1], ctx->ev_fork,  ctx->ev_join};
     for (auto e : evs)
         if (e) cudaEventDestroy(e);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
     return COOPCG_OK;
@@ -561,6 +573,9 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     CKC(cudaEventCreate(&ctx->ev_loop1));
     CKC(cudaEventCreateWithFlags(&ctx->ev_chunk[0], cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_chunk[1], cudaEventDisableTiming));
+    CKC(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     // dynamic shared-memory opt-ins
     CKC(cudaFuncSetAttribute(rank_end_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)rank_smem(32)));
@@ -965,6 +980,14 @@ static int setup_rest(coopcg_gpu_ctx* ctx) {
 }
 
 // Q_loc = A_loc D_k  (stage_matvec, block_cg.hpp:146-151), bracketed by events.
+// Make the main stream wait for an outstanding side-stream rank_end.
+static int join_rank(coopcg_gpu_ctx* ctx) {
+    if (!ctx->join_pending) return COOPCG_OK;
+    CK(cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0));
+    ctx->join_pending = false;
+    return COOPCG_OK;
+}
+
 static int iter_local(coopcg_gpu_ctx* ctx, int k, cudaEvent_t ev0, cudaEvent_t ev1) {
     int* stop = &ctx->ctl->stop;
     double* D = ctx->Dblk[k & 1];
@@ -972,9 +995,11 @@ static int iter_local(coopcg_gpu_ctx* ctx, int k, cudaEvent_t ev0, cudaEvent_t e
     if (ctx->arith != COOPCG_ARITH_FAST) {
         CK(ad_launch(ctx, D, ctx->Q, nullptr, stop));
         if (ev1) CK(cudaEventRecord(ev1, ctx->stream));
+        if (int rc = join_rank(ctx)) return rc;
     } else {
         CK(fast_ad(ctx, D, stop));
         if (ev1) CK(cudaEventRecord(ev1, ctx->stream));
+        if (int rc = join_rank(ctx)) return rc;
         // single GPU: fuse the four Gram partials into the local row pass
         CK(fast_rows(ctx, ctx->Q, nullptr, D, ctx->R, nullptr, sharded(ctx) ? 1 : 0, stop));
     }
@@ -1049,9 +1074,24 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
                                               ctx->tr_capacity);
         LAUNCHED();
     }
-    rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid_of(ctx), Dn, ctx->V, n, ctx->ctl, 0,
+    // The rank certificate of D' gates only what comes after the next A.D
+    // (which reads D' and nothing rank_end writes): in run_impl it runs on
+    // the side stream, concurrently with that A.D.  A stop it raises turns
+    // the rest of the iteration into no-ops as before; the A.D it overlapped
+    // only wrote the scratch Q.
+    cudaStream_t rs = st;
+    if (ctx->rank_async) {
+        CK(cudaEventRecord(ctx->ev_fork, st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
+        rs = ctx->side;
+    }
+    rank_end_kernel<<<1, 1024, rank_smem(P), rs>>>(ctx->partials, dgrid_of(ctx), Dn, ctx->V, n, ctx->ctl, 0,
                                                    fast ? ctx->small : nullptr);
     LAUNCHED();
+    if (ctx->rank_async) {
+        CK(cudaEventRecord(ctx->ev_join, ctx->side));
+        ctx->join_pending = true;
+    }
     return COOPCG_OK;
 }
 
@@ -1165,6 +1205,11 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     if (ctx->algo == 1)
         if (int rc = mccg_setup(ctx)) return rc;
     CK(cudaEventRecord(ctx->ev_loop0, st));
+    ctx->rank_async = true;
+    struct AsyncOff {
+        coopcg_gpu_ctx* c;
+        ~AsyncOff() { c->rank_async = false; }
+    } async_off{ctx};
 
     // ---- main loop, enqueued in chunks; device-side stop makes extras no-ops ----
     // One host read after setup (the setup coordinator may already stop).
@@ -1216,6 +1261,7 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
             if (int rc = iter_mid(ctx, k_host)) return rc;
             if (int rc = iter_rest(ctx, k_host)) return rc;
         }
+        if (int rc = join_rank(ctx)) return rc;
         CK(cudaMemcpyAsync(&ctx->ctl_host[slot], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(ctx->ev_chunk[slot], st));
         pending[npending++] = chunk_id;
@@ -1237,6 +1283,8 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
       stopped = false;
       chunk = 4;
     }
+    if (int rc = join_rank(ctx)) return rc;
+    ctx->rank_async = false;
     CK(cudaEventRecord(ctx->ev_loop1, st));
     if (int rc = final_local(ctx)) return rc;
     if (int rc = final_rest(ctx)) return rc;

@@ -8,7 +8,7 @@ using namespace coopcg_gpu;
 
 template <int P, int CPT, int BR, int T, int S, int RPT = 1>
 void run(const double* Ap, int n, const double* D, double* Y, int p) {
-    auto k = ad_exact_kernel<P, CPT, BR, T, S, RPT>;
+    auto k = (RPT == 1) ? ad_exact_kernel<P, CPT, BR, T, S> : ad_exact_rpt_kernel<P, CPT, BR, T, S, 2>;
     size_t smem = (size_t)S * T * (BR + P) * 8 + 2 * S * 8;
     if (smem > 227 * 1024) return;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

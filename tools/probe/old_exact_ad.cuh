@@ -6,10 +6,11 @@
 // add -- the reference forbids FMA contraction, CMakeLists.txt:25).  Only
 // the assignment of independent chains to threads differs.  Every multiply /
 // add below is an explicit __dmul_rn / __dadd_rn so ptxas cannot contract.
-#pragma once
-#include "common.cuh"
 
-namespace coopcg_gpu {
+#include "common.cuh"
+namespace coopcg_old { using namespace coopcg_gpu; }
+
+namespace coopcg_old {
 
 // ---------------------------------------------------------------------------
 // (1) Q = A . D, the hot kernel.
@@ -169,199 +170,26 @@ __global__ void __launch_bounds__(32 + BR*(P / CPT))
     }
 }
 
-// Two rows per thread (RPT = 2, used at p >= 16): one 16-byte load of A
-// serves both rows' chains.  Same arithmetic as ad_exact_kernel, kept as a
-// separate kernel because the RPT = 1 case compiles ~5% slower inside this
-// template (tools/probe/ad_cmp_probe.cu).
-template <int P, int CPT, int BR, int T, int S, int RPT = 2>
-__global__ void __launch_bounds__(32 + (BR / RPT) * (P / CPT))
-    ad_exact_rpt_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
-                    const double* __restrict__ D, double* __restrict__ Y,
-                    const double* __restrict__ b, int p, const int* __restrict__ stop) {
-    constexpr int RT = BR / RPT;  // row-threads per column group
-    constexpr int kConsumerWarps = RT * (P / CPT) / 32;
-    static_assert(RPT == 1 || RPT == 2, "1 or 2 rows per thread");
-    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    double* As = reinterpret_cast<double*>(smem_raw);
-    double* Ds = As + S * T * BR;
-    uint64_t* full = reinterpret_cast<uint64_t*>(Ds + S * T * P);
-    uint64_t* empty = full + S;
-
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int i0 = blockIdx.x * BR;
-    const int ntiles = (n + T - 1) / T;
-    const double* panel = Ap + static_cast<size_t>(blockIdx.x) * n * BR;
-
-    if (threadIdx.x == 0) {
-#pragma unroll
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-        }
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    if (warp == 0) {
-        // Producer: one lane streams the A panel tiles and the D tiles.
-        if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
-            for (int t = 0; t < ntiles; ++t) {
-                if (t >= S) mbar_wait(&empty[s], ph ^ 1u);
-                const int k0 = t * T;
-                const int rows = min(T, n - k0);
-                mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
-                bulk_g2s(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
-                         static_cast<uint32_t>(rows) * BR * 8u, &full[s]);
-                bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
-                         &full[s]);
-                if (++s == S) {
-                    s = 0;
-                    ph ^= 1u;
-                }
-            }
-        }
-        return;
-    }
-
-    const int tid = threadIdx.x - 32;
-    const int r = tid % RT;   // this thread's rows: RPT * r .. RPT * r + RPT - 1
-    const int g = tid / RT;
-    double acc[RPT][CPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q)
-#pragma unroll
-        for (int c = 0; c < CPT; ++c) acc[q][c] = 0.0;
-
-    int s = 0;
-    uint32_t phase = 0;
-    for (int t = 0; t < ntiles; ++t) {
-        mbar_wait(&full[s], phase);
-        const double* a_t = As + s * T * BR + RPT * r;
-        const double* d_t = Ds + s * T * P + g * CPT;
-        const int rows = min(T, n - t * T);
-        if (rows == T) {
-            constexpr int U = (CPT * RPT >= 8) ? 2 : 4;
-            static_assert(T % U == 0, "T must be a multiple of U");
-            double av[U][RPT];
-            double2 dv[U][CPT / 2];
-            auto load = [&](int kk, int u) {
-                if (RPT == 2) {
-                    const double2 a2 = *reinterpret_cast<const double2*>(a_t + kk * BR);
-                    av[u][0] = a2.x;
-                    av[u][RPT - 1] = a2.y;
-                } else {
-                    av[u][0] = a_t[kk * BR];
-                }
-#pragma unroll
-                for (int c = 0; c < CPT / 2; ++c) dv[u][c] = reinterpret_cast<const double2*>(d_t + kk * P)[c];
-            };
-#pragma unroll
-            for (int u = 0; u < U; ++u) load(u, u);
-#pragma unroll
-            for (int kb = 0; kb < T; kb += U) {
-                double prod[U][RPT][CPT];
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
-                    for (int q = 0; q < RPT; ++q)
-#pragma unroll
-                        for (int c = 0; c < CPT / 2; ++c) {
-                            prod[u][q][2 * c] = __dmul_rn(av[u][q], dv[u][c].x);
-                            prod[u][q][2 * c + 1] = __dmul_rn(av[u][q], dv[u][c].y);
-                        }
-                if (kb + U < T) {
-#pragma unroll
-                    for (int u = 0; u < U; ++u) load(kb + U + u, u);
-                }
-#pragma unroll
-                for (int u = 0; u < U; ++u)
-#pragma unroll
-                    for (int q = 0; q < RPT; ++q)
-#pragma unroll
-                        for (int c = 0; c < CPT; ++c) acc[q][c] = __dadd_rn(acc[q][c], prod[u][q][c]);
-            }
-        } else {
-            for (int kk = 0; kk < rows; ++kk) {
-                const double2* d2 = reinterpret_cast<const double2*>(d_t + kk * P);
-#pragma unroll
-                for (int q = 0; q < RPT; ++q) {
-                    const double a = a_t[kk * BR + q];
-#pragma unroll
-                    for (int c = 0; c < CPT / 2; ++c) {
-                        const double2 dv = d2[c];
-                        acc[q][2 * c] = mac_exact(acc[q][2 * c], a, dv.x);
-                        acc[q][2 * c + 1] = mac_exact(acc[q][2 * c + 1], a, dv.y);
-                    }
-                }
-            }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
-        if (++s == S) {
-            s = 0;
-            phase ^= 1u;
-        }
-    }
-
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        const int il = i0 + RPT * r + q;
-        if (il < n_loc) {
-            const int row = row0 + il;
-            double* y = Y + static_cast<size_t>(row) * P + g * CPT;
-            const double bb = (b != nullptr) ? b[row] : 0.0;
-#pragma unroll
-            for (int c = 0; c < CPT; ++c) {
-                const int col = g * CPT + c;
-                double v = 0.0;
-                if (col < p) v = (b != nullptr) ? __dsub_rn(acc[q][c], bb) : acc[q][c];
-                y[c] = v;
-            }
-        }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // (2) Sequential dot-product chains: Gram rows, step right-hand sides and
 // norms (block_cg.hpp:153-160, :214-216, :262-264, :275-276; kernels.hpp:20-26).
-// Each chain is one thread walking k = 0..n-1 in order, acc = acc + x_k*y_k
-// with both roundings kept: a dependent-DADD chain (8.5 cycles per DADD
-// measured, tools/probe/clock_probe.cu).  Written naively, ptxas schedules
-// DMUL(k) right before DADD(k) with the LDS of its operands just ahead, and
-// each step pays the load, DMUL and DADD latencies (~16 cycles).  Here the
-// chain is software-pipelined over batches of U rows: step b adds batch b's
-// products (formed one step earlier), forms batch b+1's products and loads
-// batch b+2's operands, alternating two operand register sets so that the
-// loads never wait on the DMULs reading the other set.  One loop iteration
-// covers a whole tile (straight-line steps, a single basic block for ptxas);
-// tile t+1 is waited for at the top and tile t released at the bottom.
-// Static issue cost ~10 cycles per step (tools/probe/chain_kernel_probe.cu).
+// Each chain is one thread walking k = 0..n-1 in order (a DADD latency chain,
+// ~9 cycles per step).  Tiles of T rows of up to three n x P row-major source
+// blocks stream through an S-stage shared-memory ring (bulk async copies) so
+// S-1 tiles are in flight while the chains consume one.  64 chains per CTA
+// keeps the per-step shared-memory traffic under the DADD latency.
 //
-// Tiles of T rows of up to three n x P row-major source blocks stream through
-// an S-stage shared-memory ring: warp 0 is the producer (one lane issues the
-// bulk copies, waiting on per-stage "empty" barriers); warps 1..2 run one
-// chain per thread (64 chains per CTA) and release a stage with one
-// (predicated) arrive per warp.
-constexpr int kChainWarps = 2;
-constexpr int kChainU = 16;  // rows per pipelined batch
-constexpr int kChainThreads = 32 * (1 + kChainWarps);
-
-__host__ __device__ constexpr size_t chain_smem_bytes(int P, int T, int S, int nsrc) {
-    return static_cast<size_t>(S) * nsrc * T * P * sizeof(double) + 2 * S * sizeof(uint64_t);
-}
-
+// Warp-specialised: warp 0 is the producer (one lane issues the bulk copies,
+// waiting on per-stage "empty" barriers); warps 1..W consume, one chain per
+// thread, and release each stage with one arrive per warp.
 template <int P, int T, int S>
-__global__ void __launch_bounds__(kChainThreads)
+__global__ void __launch_bounds__(96)
     chain_kernel(const double* __restrict__ s0, const double* __restrict__ s1,
                  const double* __restrict__ s2, int nsrc, int n,
                  const ChainDesc* __restrict__ descs, int nchains, double* __restrict__ out,
                  const int* __restrict__ stop) {
-    constexpr int U = kChainU;
-    static_assert(T % (2 * U) == 0, "tile rows must be an even number of batches");
-    constexpr int NBT = T / U;  // batches per tile
+    static_assert(T % 16 == 0, "tile rows must be a multiple of the batch");
+    constexpr int kConsumerWarps = 2;
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* buf = reinterpret_cast<double*>(smem_raw);
@@ -374,7 +202,7 @@ __global__ void __launch_bounds__(kChainThreads)
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kChainWarps);
+            mbar_init(&empty[s], kConsumerWarps);
         }
         fence_mbar_init();
     }
@@ -400,82 +228,57 @@ __global__ void __launch_bounds__(kChainThreads)
         }
         return;
     }
-    const int c = blockIdx.x * (kChainWarps * 32) + (tid - 32);
+    const int c = blockIdx.x * (kConsumerWarps * 32) + (tid - 32);
+    const bool active = c < nchains;
     ChainDesc d{0, 0, 0, 0, 0, 0, 0};
-    if (c < nchains) d = descs[c];
+    if (active) d = descs[c];
+    double acc = 0.0;
     const int xoff = d.sx * T * P + d.a;
     const int yoff = d.sy * T * P + d.b;
-    const int nb = (n + U - 1) / U;  // batches; all full except possibly the last
-    auto tile_wait = [&](int t) {
-        if (t < ntiles) mbar_wait(&full[t % S], static_cast<uint32_t>((t / S) & 1));
-    };
-    // operands of batch j (may lie past the last tile: stale ring data that
-    // is multiplied but never added)
-    auto batch_base = [&](int j) -> const double* {
-        return buf + static_cast<size_t>((j / NBT) % S) * nsrc * T * P + (j % NBT) * U * P;
-    };
-    double acc = 0.0;
-    // pr: products of the batch being added; operands of batch j live in the
-    // even (xe/ye) or odd (xo/yo) register set by the parity of j, so a step
-    // reads one set and loads into the other (no WAR hazard to serialise the
-    // loads behind the DMULs)
-    double pr[U], xe[U], ye[U], xo[U], yo[U];
-    // add batch b, form batch b+1 (from xr/yr), load batch b+2 (into xw/yw)
-    auto step = [&](int b, const double (&xr)[U], const double (&yr)[U], double (&xw)[U], double (&yw)[U]) {
-        const double* b2 = batch_base(b + 2);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            acc = __dadd_rn(acc, pr[u]);
-            pr[u] = __dmul_rn(xr[u], yr[u]);
-            xw[u] = b2[xoff + u * P];
-            yw[u] = b2[yoff + u * P];
-        }
-    };
-    tile_wait(0);
-    {
-        const double* b0 = batch_base(0);
-        const double* b1 = batch_base(1);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            pr[u] = __dmul_rn(b0[xoff + u * P], b0[yoff + u * P]);
-            xo[u] = b1[xoff + u * P];
-            yo[u] = b1[yoff + u * P];
-        }
-    }
-    // One iteration per tile: tile t+1 is waited for first (the steps load up
-    // to two batches ahead), the NBT steps run straight-line (one basic block
-    // for ptxas to schedule), and tile t is released once its last batch has
-    // been multiplied.
-#pragma unroll 1
+    int s = 0;
+    uint32_t phase = 0;
     for (int t = 0; t < ntiles; ++t) {
-        tile_wait(t + 1);
-        const int b0 = t * NBT;
-        if ((t + 1) * T <= n) {
+        mbar_wait(&full[s], phase);
+        const double* base = buf + static_cast<size_t>(s) * nsrc * T * P;
+        const double* xs = base + xoff;
+        const double* ys = base + yoff;
+        if (t * T + T <= n) {
+            // Batches of 16 products; the next batch's loads are in flight
+            // while this batch's 16 dependent DADDs retire (k ascending).
+            constexpr int U = 16;
+            double xv[U], yv[U];
 #pragma unroll
-            for (int q = 0; q < NBT; q += 2) {
-                step(b0 + q, xo, yo, xe, ye);
-                step(b0 + q + 1, xe, ye, xo, yo);
+            for (int u = 0; u < U; ++u) {
+                xv[u] = xs[u * P];
+                yv[u] = ys[u * P];
+            }
+#pragma unroll
+            for (int kb = 0; kb < T; kb += U) {
+                double prod[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) prod[u] = __dmul_rn(xv[u], yv[u]);
+                if (kb + U < T) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        xv[u] = xs[(kb + U + u) * P];
+                        yv[u] = ys[(kb + U + u) * P];
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, prod[u]);
             }
         } else {
-            // partial last tile: the batches that hold rows, the last one masked
-            for (int q = 0; q < NBT && b0 + q < nb; ++q) {
-                const int b = b0 + q;
-                if (b == nb - 1) {
-                    const int rem = n - b * U;
-#pragma unroll
-                    for (int u = 0; u < U; ++u)
-                        if (u < rem) acc = __dadd_rn(acc, pr[u]);
-                } else if (q & 1) {
-                    step(b, xe, ye, xo, yo);
-                } else {
-                    step(b, xo, yo, xe, ye);
-                }
-            }
+            const int rows = n - t * T;
+            for (int kk = 0; kk < rows; ++kk) acc = mac_exact(acc, xs[kk * P], ys[kk * P]);
         }
         __syncwarp();
-        mbar_arrive_lane0(&empty[t % S], lane);
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) {
+            s = 0;
+            phase ^= 1u;
+        }
     }
-    if (c < nchains) out[d.out] = d.neg ? -acc : acc;
+    if (active) out[d.out] = d.neg ? -acc : acc;
 }
 
 // ---------------------------------------------------------------------------
@@ -603,10 +406,7 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
     }
     if (!warp_lu_factor(w, perm, p, floor)) {
         if (lane == 0) {
-            // RankCollapse (solvers.hpp:117-123); steepest descent reports a
-            // vanished gradient energy with r = 0 as Converged (solvers.hpp:588-594)
-            ctl->status = (ctl->algo == 2) ? 0 : 1;
-            if (ctl->algo == 2) ctl->converged_agent = 0;
+            ctl->status = 1;  // RankCollapse (solvers.hpp:117-123)
             ctl->stop = 1;
         }
         return;
@@ -635,11 +435,7 @@ __global__ void __launch_bounds__(32)
     if (lane < p) perm[lane] = ctl->perm[lane];
     __syncwarp();
     if (lane < p) {
-        if (ctl->algo == 2) {  // steepest descent: D' = R (no conjugation)
-            for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = 0.0;
-        } else {
-            warp_lu_solve_row(w, perm, p, P, small + L.rhs_b() + lane * P, small + L.beta() + lane * P);
-        }
+        warp_lu_solve_row(w, perm, p, P, small + L.rhs_b() + lane * P, small + L.beta() + lane * P);
         norms[lane] = __dsqrt_rn(small[L.nsq_r() + lane]);
         small[L.norm() + lane] = norms[lane];
     }
@@ -715,7 +511,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     direction_kernel(const double* __restrict__ R, const double* __restrict__ D, double* __restrict__ Dn,
                      const double* __restrict__ small, int n, int p, int P, double* __restrict__ partials,
-                     const int* __restrict__ stop, int sd_copy = 0) {
+                     const int* __restrict__ stop) {
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     __shared__ double coef[kMaxP * (kMaxP + 1)];
     __shared__ double tile[256];
@@ -757,11 +553,9 @@ __global__ void __launch_bounds__(256)
             if (i < p) {
                 if (with_beta) {
                     double acc = R[e];
-                    if (!sd_copy) {
-                        const double* a = coef + i * (kMaxP + 1);
-                        const size_t rowoff = e - i;
-                        for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], D[rowoff + j]);
-                    }
+                    const double* a = coef + i * (kMaxP + 1);
+                    const size_t rowoff = e - i;
+                    for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], D[rowoff + j]);
                     v = acc;
                     Dn[e] = v;
                 } else {
@@ -1043,13 +837,7 @@ __global__ void __launch_bounds__(1024)
     if (tid == 0) {
         ctl->rank_result = rank;
         if (mode == 0) {
-            if (rank < p && ctl->algo == 2) {
-                // steepest descent has no rank check: r = 0 ends with Converged
-                // at the next gradient-energy test (solvers.hpp:588-594)
-                ctl->status = 0;
-                ctl->converged_agent = 0;
-                ctl->stop = 1;
-            } else if (rank < p && ctl->algo == 1) {
+            if (rank < p && ctl->algo == 1) {
                 // mccg (solvers.hpp:162-175): pause; the host selects the
                 // surviving columns from numerical_rank(R), compacts and resumes.
                 ctl->restrict_pending = 1;
@@ -1068,10 +856,6 @@ __global__ void __launch_bounds__(1024)
                 // mccg: the host applies setup_coordinator's restriction and
                 // tolerance logic (solvers.hpp:63-98) after reading rank/columns.
                 ctl->restrict_pending = 1;
-            } else if (rank < p && ctl->algo == 2) {
-                ctl->status = 0;  // steepest descent: zero gradient -> Converged (solvers.hpp:588-594)
-                ctl->converged_agent = 0;
-                ctl->stop = 1;
             } else if (rank < p) {
                 ctl->status = 1;  // setup_coordinator, solvers.hpp:83-85
                 ctl->stop = 1;
