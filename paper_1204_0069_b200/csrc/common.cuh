@@ -106,6 +106,13 @@ __host__ __device__ __forceinline__ void a_decode(const ALay& L, int n, size_t e
     }
 }
 
+// Programmatic dependent launch (coopcg_gpu.cu pdl_launch): a kernel
+// launched with programmatic stream serialization may be scheduled while the
+// previous kernel in the stream drains; griddepcontrol.wait blocks until that
+// kernel has completed and its memory is visible.  Every kernel of the
+// iteration loop calls it before reading anything (a no-op otherwise).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -20,6 +20,8 @@
 #include <cstring>
 #include <string>
 #include <vector>
+#include <cstdlib>
+#include <utility>
 
 #include "../../include/coopcg_gpu.h"
 #include "common.cuh"
@@ -147,6 +149,31 @@ int fail(coopcg_gpu_ctx* c, int code, const char* fmt, ...) {
                         __FILE__, __LINE__);                                                    \
     } while (0)
 
+// ---- programmatic dependent launch ------------------------------------------
+// Iteration-loop kernels are launched with programmatic stream serialization:
+// the launch and CTA scheduling of kernel k+1 overlap the tail of kernel k,
+// and kernel k+1's first statement (pdl_wait, griddepcontrol.wait) holds it
+// until kernel k has completed.  COOPCG_NO_PDL=1 disables (A/B timing).
+static bool pdl_enabled() {
+    static const bool on = std::getenv("COOPCG_NO_PDL") == nullptr;
+    return on;
+}
+template <typename... KArgs, typename... Args>
+cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 // ---- A.D launcher: template dispatch on (P, CPT, BR) -------------------------
 template <int P, int CPT, int BR>
 size_t ad_smem() {
@@ -171,8 +198,8 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
         attr_done[dev] = true;
     }
     dim3 grid((ctx->n_loc + BR - 1) / BR);
-    dim3 block(32 + (BR / RPT) * (P / CPT));
-    kern<<<grid, block, smem, ctx->stream>>>(ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop);
+    dim3 block(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT));
+    pdl_launch(kern, dim3(grid), dim3(block), smem, ctx->stream, ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop);
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -218,12 +245,12 @@ cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
     const double* operand = src;
     if (TR) {  // operand -> [col][kk] k-tiles (conflict-free B fragments at P >= 16)
         const size_t tot = (size_t)ctx->lay.ntiles * P * kFastT;
-        operand_tiles_kernel<P><<<grid_for(tot, 256), 256, 0, ctx->stream>>>(src, ctx->n, ctx->lay.ntiles,
+        pdl_launch(operand_tiles_kernel<P>, dim3(grid_for(tot, 256)), dim3(256), 0, ctx->stream, src, ctx->n, ctx->lay.ntiles,
                                                                              ctx->dtiles, stop);
         ++ctx->launches;
         operand = ctx->dtiles;
     }
-    kern<<<ctx->f_grid, 32 + 64 * WN, fast_ad_smem<P>(), ctx->stream>>>(
+    pdl_launch(kern, dim3(ctx->f_grid), dim3(32 + 64 * WN), fast_ad_smem<P>(), ctx->stream, 
         ctx->At, ctx->n, ctx->n_loc, ctx->lay.ntiles, operand, ctx->qpart, ctx->f_kchunks, ctx->f_tpc,
         ctx->f_units, stop);
     ++ctx->launches;
@@ -239,7 +266,7 @@ cudaError_t fast_ad(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
 template <int P>
 cudaError_t fast_rows_t(coopcg_gpu_ctx* ctx, double* dst, const double* b, const double* D, const double* R,
                         const double* Qfull, int mode, const int* stop) {
-    fast_rows_kernel<P><<<ctx->f_rgrid, 256, 0, ctx->stream>>>(ctx->qpart, ctx->f_kchunks, ctx->n_loc, ctx->row0, dst,
+    pdl_launch(fast_rows_kernel<P>, dim3(ctx->f_rgrid), dim3(256), 0, ctx->stream, ctx->qpart, ctx->f_kchunks, ctx->n_loc, ctx->row0, dst,
                                                                b, D, R, Qfull, ctx->p, mode, ctx->gpart, stop);
     ++ctx->launches;
     return cudaGetLastError();
@@ -254,7 +281,7 @@ cudaError_t fast_rows(coopcg_gpu_ctx* ctx, double* dst, const double* b, const d
 }
 template <int P>
 cudaError_t fast_update_t(coopcg_gpu_ctx* ctx, const double* D, double* Dn, int mode, const int* stop) {
-    fast_update_kernel<P><<<ctx->f_ugrid, 256, 0, ctx->stream>>>(ctx->X, ctx->R, ctx->Q, D, Dn, ctx->small, ctx->n,
+    pdl_launch(fast_update_kernel<P>, dim3(ctx->f_ugrid), dim3(256), 0, ctx->stream, ctx->X, ctx->R, ctx->Q, D, Dn, ctx->small, ctx->n,
                                                                  ctx->p, mode, ctx->npart, ctx->partials, stop);
     ++ctx->launches;
     return cudaGetLastError();
@@ -268,7 +295,7 @@ cudaError_t fast_update(coopcg_gpu_ctx* ctx, const double* D, double* Dn, int mo
 }
 cudaError_t fast_solve(coopcg_gpu_ctx* ctx, int mode) {
     const size_t smem = (size_t)(4 * ctx->P * ctx->P + 1024) * sizeof(double);
-    fast_solve_kernel<<<1, 1024, smem, ctx->stream>>>(ctx->gpart, ctx->f_rgrid, ctx->small, ctx->ctl, mode);
+    pdl_launch(fast_solve_kernel, dim3(1), dim3(1024), smem, ctx->stream, ctx->gpart, ctx->f_rgrid, ctx->small, ctx->ctl, mode);
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -300,7 +327,7 @@ cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, co
     }
     const int cnt = ctx->desc_cnt[phase];
     const size_t smem = chain_smem_bytes(P, T, S, nsrc);
-    kern<<<(cnt + 63) / 64, kChainThreads, smem, ctx->stream>>>(s0, s1, s2, nsrc, ctx->n, ctx->descs + ctx->desc_off[phase],
+    pdl_launch(kern, dim3((cnt + 63) / 64), dim3(kChainThreads), smem, ctx->stream, s0, s1, s2, nsrc, ctx->n, ctx->descs + ctx->desc_off[phase],
                                                      cnt, ctx->small, stop);
     ++ctx->launches;
     return cudaGetLastError();
@@ -886,7 +913,7 @@ template <int P>
 cudaError_t fast_rows_any_t(coopcg_gpu_ctx* ctx, const double* qpart, int kchunks, int nrows, int row0, double* dst,
                             const double* b, const double* D, const double* R, const double* Qfull, int mode,
                             const int* stop) {
-    fast_rows_kernel<P><<<ctx->f_rgrid, 256, 0, ctx->stream>>>(qpart, kchunks, nrows, row0, dst, b, D, R, Qfull,
+    pdl_launch(fast_rows_kernel<P>, dim3(ctx->f_rgrid), dim3(256), 0, ctx->stream, qpart, kchunks, nrows, row0, dst, b, D, R, Qfull,
                                                                ctx->p, mode, ctx->gpart, stop);
     ++ctx->launches;
     return cudaGetLastError();
@@ -1021,9 +1048,9 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
     const bool rec = recompute_at(ctx, k);
     if (ctx->arith != COOPCG_ARITH_FAST) {
         CK(chains_launch(ctx, kPhGram, D, ctx->Q, ctx->R, 3, stop));
-        solve_alpha_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl);
+        pdl_launch(solve_alpha_kernel, dim3(1), dim3(32), 0, st, ctx->small, ctx->ctl);
         LAUNCHED();
-        update_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->R, ctx->X, ctx->Q, D, ctx->small, n, p, P,
+        pdl_launch(update_kernel, dim3(grid_for((size_t)n * P, 256)), dim3(256), 0, st, ctx->R, ctx->X, ctx->Q, D, ctx->small, n, p, P,
                                                                     rec ? 1 : 0, stop);
         LAUNCHED();
         if (rec) CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, stop));
@@ -1033,7 +1060,7 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
         if (!rec) {
             CK(fast_solve(ctx, 0));
             CK(fast_update(ctx, D, Dn, 0, stop));
-            fast_record_kernel<<<1, 256, 0, st>>>(ctx->npart, ctx->f_ugrid, P, 0, 1, ctx->small, ctx->ctl,
+            pdl_launch(fast_record_kernel, dim3(1), dim3(256), 0, st, ctx->npart, ctx->f_ugrid, P, 0, 1, ctx->small, ctx->ctl,
                                                   ctx->tr_norms, ctx->tr_minres, ctx->tr_wall, ctx->tr_capacity);
             LAUNCHED();
         } else {
@@ -1058,10 +1085,10 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
     const bool fast = ctx->arith == COOPCG_ARITH_FAST;
     if (!fast) {
         CK(chains_launch(ctx, kPhBeta, ctx->R, ctx->Q, nullptr, 2, stop));
-        solve_beta_kernel<<<1, 32, 0, st>>>(ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
+        pdl_launch(solve_beta_kernel, dim3(1), dim3(32), 0, st, ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
                                             ctx->tr_capacity);
         LAUNCHED();
-        direction_kernel<<<dgrid_of(ctx), 256, 0, st>>>(ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop,
+        pdl_launch(direction_kernel, dim3(dgrid_of(ctx)), dim3(256), 0, st, ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop,
                                                         ctx->algo == 2 ? 1 : 0);
         LAUNCHED();
     } else if (rec) {
@@ -1069,7 +1096,7 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
             CK(fast_rows_any(ctx, ctx->R, 1, n, 0, ctx->R, nullptr, nullptr, nullptr, ctx->Q, 1, stop));
         CK(fast_solve(ctx, 2));
         CK(fast_update(ctx, D, Dn, 2, stop));
-        fast_record_kernel<<<1, 256, 0, st>>>(ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->small,
+        pdl_launch(fast_record_kernel, dim3(1), dim3(256), 0, st, ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->small,
                                               ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
                                               ctx->tr_capacity);
         LAUNCHED();
@@ -1085,7 +1112,7 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
         rs = ctx->side;
     }
-    rank_end_kernel<<<1, 1024, rank_smem(P), rs>>>(ctx->partials, dgrid_of(ctx), Dn, ctx->V, n, ctx->ctl, 0,
+    pdl_launch(rank_end_kernel, dim3(1), dim3(1024), rank_smem(P), rs, ctx->partials, dgrid_of(ctx), Dn, ctx->V, n, ctx->ctl, 0,
                                                    fast ? ctx->small : nullptr);
     LAUNCHED();
     if (ctx->rank_async) {

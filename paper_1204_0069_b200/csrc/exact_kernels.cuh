@@ -31,12 +31,18 @@ namespace coopcg_gpu {
 // Epilogue (sub_b != 0): Y = acc - b (block_cg.hpp:132-138 / :236-241
 // `r[row] -= b[row]`), used for R0 = A X0 - b, the periodic residual
 // recomputation and the final true residual (solvers.hpp:188-210).
+// Consumer threads: BR rows x P/CPT column groups, rounded up to whole warps
+// (BR need not be a power of two: the panel height is chosen to balance rows
+// over the SMs, coopcg_gpu.cu pick_ad_config); surplus threads idle.
+__host__ __device__ constexpr int ad_consumer_warps(int rows, int groups) { return (rows * groups + 31) / 32; }
+
 template <int P, int CPT, int BR, int T, int S>
-__global__ void __launch_bounds__(32 + BR*(P / CPT))
+__global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
     ad_exact_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
                     const double* __restrict__ b, int p, const int* __restrict__ stop) {
-    constexpr int kConsumerWarps = BR * (P / CPT) / 32;
+    pdl_wait();
+    constexpr int kConsumerWarps = ad_consumer_warps(BR, P / CPT);
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);
@@ -84,7 +90,8 @@ __global__ void __launch_bounds__(32 + BR*(P / CPT))
 
     const int tid = threadIdx.x - 32;
     const int r = tid % BR;
-    const int g = tid / BR;
+    const int g = tid / BR;  // == P / CPT for the surplus threads (no output)
+    const int gl = min(g, P / CPT - 1);
     double acc[CPT];
 #pragma unroll
     for (int c = 0; c < CPT; ++c) acc[c] = 0.0;
@@ -94,7 +101,7 @@ __global__ void __launch_bounds__(32 + BR*(P / CPT))
     for (int t = 0; t < ntiles; ++t) {
         mbar_wait(&full[s], phase);
         const double* a_t = As + s * T * BR + r;
-        const double* d_t = Ds + s * T * P + g * CPT;
+        const double* d_t = Ds + s * T * P + gl * CPT;
         const int rows = min(T, n - t * T);
         if (rows == T) {
             // Register software pipeline: the products of a batch of U k-steps
@@ -155,7 +162,7 @@ __global__ void __launch_bounds__(32 + BR*(P / CPT))
     }
 
     const int il = i0 + r;
-    if (il < n_loc) {
+    if (il < n_loc && g < P / CPT) {
         const int row = row0 + il;
         double* y = Y + static_cast<size_t>(row) * P + g * CPT;
         const double bb = (b != nullptr) ? b[row] : 0.0;
@@ -174,12 +181,13 @@ __global__ void __launch_bounds__(32 + BR*(P / CPT))
 // separate kernel because the RPT = 1 case compiles ~5% slower inside this
 // template (tools/probe/ad_cmp_probe.cu).
 template <int P, int CPT, int BR, int T, int S, int RPT = 2>
-__global__ void __launch_bounds__(32 + (BR / RPT) * (P / CPT))
+__global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT))
     ad_exact_rpt_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
                     const double* __restrict__ b, int p, const int* __restrict__ stop) {
+    pdl_wait();
     constexpr int RT = BR / RPT;  // row-threads per column group
-    constexpr int kConsumerWarps = RT * (P / CPT) / 32;
+    constexpr int kConsumerWarps = ad_consumer_warps(RT, P / CPT);
     static_assert(RPT == 1 || RPT == 2, "1 or 2 rows per thread");
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -228,7 +236,8 @@ __global__ void __launch_bounds__(32 + (BR / RPT) * (P / CPT))
 
     const int tid = threadIdx.x - 32;
     const int r = tid % RT;   // this thread's rows: RPT * r .. RPT * r + RPT - 1
-    const int g = tid / RT;
+    const int g = tid / RT;  // == P / CPT for the surplus threads (no output)
+    const int gl = min(g, P / CPT - 1);
     double acc[RPT][CPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q)
@@ -240,7 +249,7 @@ __global__ void __launch_bounds__(32 + (BR / RPT) * (P / CPT))
     for (int t = 0; t < ntiles; ++t) {
         mbar_wait(&full[s], phase);
         const double* a_t = As + s * T * BR + RPT * r;
-        const double* d_t = Ds + s * T * P + g * CPT;
+        const double* d_t = Ds + s * T * P + gl * CPT;
         const int rows = min(T, n - t * T);
         if (rows == T) {
             constexpr int U = (CPT * RPT >= 8) ? 2 : 4;
@@ -309,7 +318,7 @@ __global__ void __launch_bounds__(32 + (BR / RPT) * (P / CPT))
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int il = i0 + RPT * r + q;
-        if (il < n_loc) {
+        if (il < n_loc && g < P / CPT) {
             const int row = row0 + il;
             double* y = Y + static_cast<size_t>(row) * P + g * CPT;
             const double bb = (b != nullptr) ? b[row] : 0.0;
@@ -359,6 +368,7 @@ __global__ void __launch_bounds__(kChainThreads)
                  const double* __restrict__ s2, int nsrc, int n,
                  const ChainDesc* __restrict__ descs, int nchains, double* __restrict__ out,
                  const int* __restrict__ stop) {
+    pdl_wait();
     constexpr int U = kChainU;
     static_assert(T % (2 * U) == 0, "tile rows must be an even number of batches");
     constexpr int NBT = T / U;  // batches per tile
@@ -567,6 +577,7 @@ __device__ void warp_lu_solve_row(WarpLU& w, const int* perm, int p, int P, cons
 
 // stage_gram_finalize + stage_alpha (block_cg.hpp:165-218), one warp.
 __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ small, Ctl* ctl) {
+    pdl_wait();
     if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
     __shared__ WarpLU w;
     __shared__ int perm[kMaxP];
@@ -624,6 +635,7 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
 __global__ void __launch_bounds__(32)
     solve_beta_kernel(double* __restrict__ small, Ctl* ctl, double* __restrict__ tr_norms,
                       double* __restrict__ tr_minres, unsigned long long* __restrict__ tr_wall, int capacity) {
+    pdl_wait();
     if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
     __shared__ WarpLU w;
     __shared__ int perm[kMaxP];
@@ -684,6 +696,7 @@ __global__ void __launch_bounds__(256)
     update_kernel(double* __restrict__ R, double* __restrict__ X, const double* __restrict__ Q,
                   const double* __restrict__ D, const double* __restrict__ small, int n, int p, int P,
                   int mode, const int* __restrict__ stop) {
+    pdl_wait();
     if (*reinterpret_cast<volatile const int*>(stop)) return;
     __shared__ double coef[kMaxP * (kMaxP + 1)];
     const SmallLayout L{P};
@@ -716,6 +729,7 @@ __global__ void __launch_bounds__(256)
     direction_kernel(const double* __restrict__ R, const double* __restrict__ D, double* __restrict__ Dn,
                      const double* __restrict__ small, int n, int p, int P, double* __restrict__ partials,
                      const int* __restrict__ stop, int sd_copy = 0) {
+    pdl_wait();
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     __shared__ double coef[kMaxP * (kMaxP + 1)];
     __shared__ double tile[256];
@@ -855,6 +869,7 @@ constexpr int kRankTile = 64;
 __global__ void __launch_bounds__(1024)
     rank_end_kernel(const double* __restrict__ partials, int nparts, const double* __restrict__ Dn,
                     double* __restrict__ V, int n, Ctl* ctl, int mode, double* __restrict__ small_out) {
+    pdl_wait();
     if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int p = ctl->p, P = ctl->P;

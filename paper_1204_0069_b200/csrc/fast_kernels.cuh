@@ -41,6 +41,7 @@ template <int P>
 __global__ void __launch_bounds__(256)
     operand_tiles_kernel(const double* __restrict__ src, int n, int ntiles, double* __restrict__ dst,
                          const int* __restrict__ stop) {
+    pdl_wait();
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     const size_t total = static_cast<size_t>(ntiles) * P * kFastT;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(32 + 64 * WN)
     ad_fast_kernel(const double* __restrict__ Af, int n, int n_loc, int ntiles, const double* __restrict__ Dt,
                    double* __restrict__ Qpart, int kchunks, int tiles_per_chunk, int nunits,
                    const int* __restrict__ stop) {
+    pdl_wait();
     static_assert(P % (8 * WN) == 0, "fast contexts pad p to a multiple of 8 per column group");
     constexpr int NT = P / 8 / WN;  // N tiles of 8 columns per warp
     constexpr int NCW = 2 * WN;     // consumer warps
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(256)
                      const double* __restrict__ b, const double* __restrict__ D, const double* __restrict__ R,
                      const double* __restrict__ Qfull, int p, int mode, double* __restrict__ partials,
                      const int* __restrict__ stop) {
+    pdl_wait();
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     constexpr int RP = 4;                 // rows per thread per tile (loads in flight together)
     constexpr int TR = (256 / P) * RP;    // rows per tile
@@ -291,6 +294,7 @@ __device__ void chol_solve_row(const double (*l)[kMaxP + 1], int p, const double
 __global__ void __launch_bounds__(1024)
     fast_solve_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ small, Ctl* ctl,
                       int mode) {
+    pdl_wait();
     if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
     __shared__ FastSolveScratch sc;
     extern __shared__ __align__(16) double dyn[];  // flat[4 P P] then red[blockDim]
@@ -400,6 +404,7 @@ __global__ void __launch_bounds__(256)
                        const double* __restrict__ D, double* __restrict__ Dn, const double* __restrict__ small, int n,
                        int p, int mode, double* __restrict__ norm_part, double* __restrict__ pair_part,
                        const int* __restrict__ stop) {
+    pdl_wait();
     if (*reinterpret_cast<volatile const int*>(stop)) return;
     constexpr int RP = (P >= 32) ? 2 : 4;
     constexpr int TR = (256 / P) * RP;
@@ -526,6 +531,7 @@ __global__ void __launch_bounds__(256)
     fast_record_kernel(const double* __restrict__ part, int nparts, int part_stride, int part_off, int diag_stride,
                        double* __restrict__ small, Ctl* ctl, double* __restrict__ tr_norms,
                        double* __restrict__ tr_minres, unsigned long long* __restrict__ tr_wall, int capacity) {
+    pdl_wait();
     if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
     __shared__ double norms[kMaxP], sums[kMaxP], red[256];
     const int p = ctl->p, P = ctl->P;

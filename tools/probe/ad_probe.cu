@@ -12,7 +12,7 @@ void run(const double* Ap, int n, const double* D, double* Y, int p) {
     size_t smem = (size_t)S * T * (BR + P) * 8 + 2 * S * 8;
     if (smem > 227 * 1024) return;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    dim3 grid((n + BR - 1) / BR), block(32 + (BR / RPT) * (P / CPT));
+    dim3 grid((n + BR - 1) / BR), block(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -39,22 +39,16 @@ int main(int argc, char** argv) {
     cudaMalloc(&Y, (size_t)n * 32 * 8);
     cudaMemset(Ap, 0, (size_t)n * n * 8);
     cudaMemset(D, 0, (size_t)n * 32 * 8);
-    run<8, 4, 64, 32, 4>(Ap, n, D, Y, 8);
-    run<8, 2, 64, 32, 4, 2>(Ap, n, D, Y, 8);
-    run<8, 4, 64, 32, 4, 2>(Ap, n, D, Y, 8);
-    run<8, 4, 128, 32, 4, 2>(Ap, n, D, Y, 8);
-    run<8, 8, 64, 32, 4, 2>(Ap, n, D, Y, 8);
-    run<8, 2, 32, 32, 4, 2>(Ap, n, D, Y, 8);
-    run<4, 2, 64, 32, 4>(Ap, n, D, Y, 4);
-    run<4, 2, 64, 32, 4, 2>(Ap, n, D, Y, 4);
-    run<4, 4, 64, 32, 4, 2>(Ap, n, D, Y, 4);
-    run<16, 8, 64, 32, 4>(Ap, n, D, Y, 16);
-    run<16, 8, 64, 32, 4, 2>(Ap, n, D, Y, 16);
+    run<8, 4, 64, 32, 4, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 56, 32, 4, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 56, 32, 3, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 56, 64, 2, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 48, 32, 4, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 40, 32, 4, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 112, 32, 3, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 64, 64, 2, 1>(Ap, n, D, Y, 8);
     run<16, 4, 64, 32, 4, 2>(Ap, n, D, Y, 16);
-    run<16, 8, 128, 32, 3, 2>(Ap, n, D, Y, 16);
-    run<32, 8, 64, 32, 4>(Ap, n, D, Y, 32);
-    run<32, 8, 64, 32, 4, 2>(Ap, n, D, Y, 32);
-    run<32, 8, 128, 32, 3, 2>(Ap, n, D, Y, 32);
-    run<32, 4, 64, 32, 4, 2>(Ap, n, D, Y, 32);
+    run<16, 4, 56, 32, 4, 2>(Ap, n, D, Y, 16);
+    run<4, 2, 32, 32, 4, 1>(Ap, n, D, Y, 4);
     return 0;
 }
