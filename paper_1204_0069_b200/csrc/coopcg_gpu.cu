@@ -310,6 +310,35 @@ AdConfig pick_ad_config(int n_loc, int P) {
     return c;
 }
 
+// ---- the p x p solves (one warp, templated on P) ---------------------------
+template <int P>
+cudaError_t solve_alpha_launch_t(coopcg_gpu_ctx* ctx) {
+    return pdl_launch(solve_alpha_kernel<P>, dim3(1), dim3(32), 0, ctx->stream, ctx->small, ctx->ctl);
+}
+template <int P>
+cudaError_t solve_beta_launch_t(coopcg_gpu_ctx* ctx) {
+    return pdl_launch(solve_beta_kernel<P>, dim3(1), dim3(32), 0, ctx->stream, ctx->small, ctx->ctl, ctx->tr_norms,
+                      ctx->tr_minres, ctx->tr_wall, ctx->tr_capacity);
+}
+cudaError_t solve_alpha_launch(coopcg_gpu_ctx* ctx) {
+    ++ctx->launches;
+    switch (ctx->P) {
+    case 4: return solve_alpha_launch_t<4>(ctx);
+    case 8: return solve_alpha_launch_t<8>(ctx);
+    case 16: return solve_alpha_launch_t<16>(ctx);
+    default: return solve_alpha_launch_t<32>(ctx);
+    }
+}
+cudaError_t solve_beta_launch(coopcg_gpu_ctx* ctx) {
+    ++ctx->launches;
+    switch (ctx->P) {
+    case 4: return solve_beta_launch_t<4>(ctx);
+    case 8: return solve_beta_launch_t<8>(ctx);
+    case 16: return solve_beta_launch_t<16>(ctx);
+    default: return solve_beta_launch_t<32>(ctx);
+    }
+}
+
 // ---- chain launcher ---------------------------------------------------------
 enum ChainPhase { kPhSetup = 0, kPhGram = 1, kPhBeta = 2, kPhFinal = 3 };
 
@@ -1048,8 +1077,7 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
     const bool rec = recompute_at(ctx, k);
     if (ctx->arith != COOPCG_ARITH_FAST) {
         CK(chains_launch(ctx, kPhGram, D, ctx->Q, ctx->R, 3, stop));
-        pdl_launch(solve_alpha_kernel, dim3(1), dim3(32), 0, st, ctx->small, ctx->ctl);
-        LAUNCHED();
+        CK(solve_alpha_launch(ctx));
         pdl_launch(update_kernel, dim3(grid_for((size_t)n * P, 256)), dim3(256), 0, st, ctx->R, ctx->X, ctx->Q, D, ctx->small, n, p, P,
                                                                     rec ? 1 : 0, stop);
         LAUNCHED();
@@ -1085,9 +1113,7 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
     const bool fast = ctx->arith == COOPCG_ARITH_FAST;
     if (!fast) {
         CK(chains_launch(ctx, kPhBeta, ctx->R, ctx->Q, nullptr, 2, stop));
-        pdl_launch(solve_beta_kernel, dim3(1), dim3(32), 0, st, ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
-                                            ctx->tr_capacity);
-        LAUNCHED();
+        CK(solve_beta_launch(ctx));
         pdl_launch(direction_kernel, dim3(dgrid_of(ctx)), dim3(256), 0, st, ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop,
                                                         ctx->algo == 2 ? 1 : 0);
         LAUNCHED();

@@ -496,114 +496,150 @@ __global__ void __launch_bounds__(kChainThreads)
 // floor = max|M| * 1e-14 (block_cg.hpp:180-190).  Lane i owns row i during
 // elimination; every element sees the reference's update sequence.
 // lu_solve_vec (kernels.hpp:97-115): lane i solves agent i's row.
-struct WarpLU {
-    double m[kMaxP][kMaxP + 1];
-    double y[kMaxP][kMaxP + 1];
-    double x[kMaxP][kMaxP + 1];
-};
-
 // Pivot search with the reference's sequential semantics
 // (`if (cand > best)` scanning i = k+1.. from best = |a_kk|): the first index
 // holding the maximum non-NaN value; a NaN at the diagonal always fails.
+// Only lanes < P hold rows, so log2(P) xor-rounds reduce the maximum; the
+// lowest lane holding it comes from a ballot (ties -> lowest index).
+template <int P>
 __device__ __forceinline__ int warp_pivot(double cand, int lane, int k, int p, bool* ok, double floor) {
-    double v = (lane >= k && lane < p && !isnan(cand)) ? cand : -1.0;
-    int idx = (lane >= k && lane < p) ? lane : 1 << 30;
-    for (int off = 16; off > 0; off >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, v, off);
-        const int oi = __shfl_xor_sync(0xffffffffu, idx, off);
-        if (ov > v || (ov == v && oi < idx)) {
-            v = ov;
-            idx = oi;
-        }
+    const bool elig = lane >= k && lane < p;
+    const double v = (elig && !isnan(cand)) ? cand : -1.0;
+    double vmax = v;
+#pragma unroll
+    for (int off = P / 2; off > 0; off >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, vmax, off);
+        vmax = (ov > vmax) ? ov : vmax;
     }
+    vmax = __shfl_sync(0xffffffffu, vmax, 0);
+    int idx = __ffs(__ballot_sync(0xffffffffu, elig && v == vmax)) - 1;
     const double diag = __shfl_sync(0xffffffffu, cand, k);
-    double best = isnan(diag) ? diag : v;
+    const double best = isnan(diag) ? diag : vmax;
     if (isnan(diag)) idx = k;
     *ok = (best > floor);
     return idx;
 }
 
-__device__ bool warp_lu_factor(WarpLU& w, int* perm, int p, double floor) {
-    const int lane = threadIdx.x & 31;
-    if (lane < p) perm[lane] = lane;
-    __syncwarp();
-    for (int k = 0; k < p; ++k) {
-        const double cand = (lane < p) ? fabs(w.m[lane][k]) : 0.0;
+// LU factorisation with lane i < p holding row i of M in registers (P is the
+// compile-time bound, p <= P the active size).  Row exchanges and the pivot
+// row broadcast are warp shuffles; each element sees the reference's update
+// sequence a_ij = a_ij - mult * a_kj (kernels.hpp:61-95).  pv is the
+// permutation entry of this lane's position.  Returns false on a pivot at or
+// below the floor (uniform across the warp).
+template <int P>
+__device__ __forceinline__ bool lu_factor_regs(double (&m)[P], int& pv, int lane, int p, double floor) {
+    pv = lane;
+#pragma unroll
+    for (int k = 0; k < P; ++k) {
+        if (k >= p) break;
+        const double cand = (lane < p) ? fabs(m[k]) : 0.0;
         bool ok;
-        const int piv = warp_pivot(cand, lane, k, p, &ok, floor);
+        const int piv = warp_pivot<P>(cand, lane, k, p, &ok, floor);
         if (!ok) return false;
         if (piv != k) {
-            if (lane < p) {
-                const double t = w.m[k][lane];
-                w.m[k][lane] = w.m[piv][lane];
-                w.m[piv][lane] = t;
-            }
-            if (lane == 0) {
-                const int t = perm[k];
-                perm[k] = perm[piv];
-                perm[piv] = t;
-            }
+            const int src = (lane == k) ? piv : ((lane == piv) ? k : lane);
+#pragma unroll
+            for (int j = 0; j < P; ++j) m[j] = __shfl_sync(0xffffffffu, m[j], src);
+            pv = __shfl_sync(0xffffffffu, pv, src);
         }
-        __syncwarp();
+        double rk[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) rk[j] = __shfl_sync(0xffffffffu, m[j], k);
         if (lane > k && lane < p) {
-            const double mult = __ddiv_rn(w.m[lane][k], w.m[k][k]);
-            w.m[lane][k] = mult;
-            for (int j = k + 1; j < p; ++j) w.m[lane][j] = msub_exact(w.m[lane][j], mult, w.m[k][j]);
+            const double mult = __ddiv_rn(m[k], rk[k]);
+            m[k] = mult;
+#pragma unroll
+            for (int j = 0; j < P; ++j)
+                if (j > k && j < p) m[j] = msub_exact(m[j], mult, rk[j]);
         }
-        __syncwarp();
     }
     return true;
 }
 
-// Lane `lane` solves L U x = P rhs for its own right-hand side; writes the
-// p solution entries to xout and zeroes xout[p..P).
-__device__ void warp_lu_solve_row(WarpLU& w, const int* perm, int p, int P, const double* rhs, double* xout) {
-    const int i_ = threadIdx.x & 31;
-    if (i_ >= p) return;
-    double* y = w.y[i_];
-    double* x = w.x[i_];
-    for (int i = 0; i < p; ++i) {
-        double acc = rhs[perm[i]];
-        for (int j = 0; j < i; ++j) acc = msub_exact(acc, w.m[i][j], y[j]);
-        y[i] = acc;
+// lu_solve_vec (kernels.hpp:97-115) for one right-hand side: forward
+// y_i = rhs[perm_i] - sum_{j<i} L_ij y_j, backward
+// x_i = (y_i - sum_{j>i} U_ij x_j) / U_ii, j ascending in both.
+template <int P>
+__device__ __forceinline__ void lu_solve_regs(const double (*lu)[P + 1], const int* perm, int p, const double* rhs,
+                                              double (&x)[P]) {
+    double y[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        y[i] = 0.0;
+        x[i] = 0.0;
     }
-    for (int i = p - 1; i >= 0; --i) {
-        double acc = y[i];
-        for (int j = i + 1; j < p; ++j) acc = msub_exact(acc, w.m[i][j], x[j]);
-        x[i] = __ddiv_rn(acc, w.m[i][i]);
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        if (i < p) {
+            double acc = rhs[perm[i]];
+#pragma unroll
+            for (int j = 0; j < i; ++j) acc = msub_exact(acc, lu[i][j], y[j]);
+            y[i] = acc;
+        }
     }
-    for (int j = 0; j < P; ++j) xout[j] = (j < p) ? x[j] : 0.0;
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+        if (i < p) {
+            double acc = y[i];
+#pragma unroll
+            for (int j = i + 1; j < P; ++j)
+                if (j < p) acc = msub_exact(acc, lu[i][j], x[j]);
+            x[i] = __ddiv_rn(acc, lu[i][i]);
+        }
+    }
 }
 
 // stage_gram_finalize + stage_alpha (block_cg.hpp:165-218), one warp.
+template <int P>
 __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ small, Ctl* ctl) {
     pdl_wait();
-    if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
-    __shared__ WarpLU w;
-    __shared__ int perm[kMaxP];
+    __shared__ double lu[P][P + 1];
+    __shared__ double rh[P][P + 1];
+    __shared__ int perm[P];
     const int lane = threadIdx.x;
-    const int p = ctl->p, P = ctl->P;
     const SmallLayout L{P};
     const double* raw = small + L.raw();
-    // M(i,j) = (raw(i,j) + raw(j,i)) / 2.0
-    double maxabs = 0.0;
-    for (int idx = lane; idx < p * p; idx += 32) {
-        const int i = idx / p, j = idx % p;
-        const double v = __ddiv_rn(__dadd_rn(raw[i * P + j], raw[j * P + i]), 2.0);
-        w.m[i][j] = v;
-        const double a = fabs(v);
-        maxabs = (maxabs < a) ? a : maxabs;
+    // Every input is requested up front (L2-coherent loads; griddepcontrol.wait
+    // made the producers' writes visible), before the control fields resolve.
+    const int stop = __ldcg(&ctl->stop);
+    const int p = __ldcg(&ctl->p);
+    double rr[P], rc[P], nsq = 0.0;
+    if (lane < P) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            rr[j] = __ldcg(raw + lane * P + j);
+            rc[j] = __ldcg(raw + j * P + lane);
+            rh[lane][j] = __ldcg(small + L.rhs_a() + lane * P + j);
+        }
+        nsq = __ldcg(small + L.nsq_d() + lane);
+    }
+    if (stop) return;
+    // M(i,j) = (raw(i,j) + raw(j,i)) / 2.0 (x * 0.5 is the same rounding)
+    double m[P];
+    double maxabs = 0.0, diag = 0.0;
+#pragma unroll
+    for (int j = 0; j < P; ++j) m[j] = 0.0;
+    if (lane < p) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            if (j < p) {
+                m[j] = __dmul_rn(__dadd_rn(rr[j], rc[j]), 0.5);
+                const double a = fabs(m[j]);
+                maxabs = (maxabs < a) ? a : maxabs;
+                if (j == lane) diag = m[j];
+            }
+        }
+    } else {
+        nsq = 0.0;
     }
     // std::max over all entries ignores NaN in this formulation; order-free.
     for (int off = 16; off > 0; off >>= 1) {
         const double o = __shfl_xor_sync(0xffffffffu, maxabs, off);
         maxabs = (maxabs < o) ? o : maxabs;
     }
-    __syncwarp();
     const double floor = __dmul_rn(maxabs, 1e-14);
     // SPD guard (block_cg.hpp:196-202): nonpositive d_i^T A d_i with d_i != 0.
-    bool bad = false;
-    if (lane < p) bad = !(w.m[lane][lane] > 0.0) && (small[L.nsq_d() + lane] > 0.0);
+    const bool bad = (lane < p) && !(diag > 0.0) && (nsq > 0.0);
     if (__any_sync(0xffffffffu, bad)) {
         if (lane == 0) {
             ctl->err = 2;  // COOPCG_E_SPD_VIOLATION
@@ -612,7 +648,8 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
         }
         return;
     }
-    if (!warp_lu_factor(w, perm, p, floor)) {
+    int pv;
+    if (!lu_factor_regs<P>(m, pv, lane, p, floor)) {
         if (lane == 0) {
             // RankCollapse (solvers.hpp:117-123); steepest descent reports a
             // vanished gradient energy with r = 0 as Converged (solvers.hpp:588-594)
@@ -622,54 +659,86 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
         }
         return;
     }
+    if (lane < P) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) lu[lane][j] = m[j];
+        perm[lane] = pv;
+    }
     __syncwarp();
-    if (lane < p) warp_lu_solve_row(w, perm, p, P, small + L.rhs_a() + lane * P, small + L.alpha() + lane * P);
-    // Keep the factorisation for the beta solve (same M, same pivots).
-    for (int idx = lane; idx < p * p; idx += 32) ctl->lu[idx] = w.m[idx / p][idx % p];
-    if (lane < p) ctl->perm[lane] = perm[lane];
+    if (lane < p) {
+        double x[P];
+        lu_solve_regs<P>(lu, perm, p, rh[lane], x);
+#pragma unroll
+        for (int j = 0; j < P; ++j) small[L.alpha() + lane * P + j] = (j < p) ? x[j] : 0.0;
+        // keep the factorisation for the beta solve (same M, same pivots)
+#pragma unroll
+        for (int j = 0; j < P; ++j) ctl->lu[lane * P + j] = m[j];
+        ctl->perm[lane] = pv;
+    }
 }
 
 // stage_beta (block_cg.hpp:248-266) + the norms of stage_direction_and_norms
 // (:275-276) + the record / convergence part of end_of_iteration
 // (solvers.hpp:125-154).  One warp.
+template <int P>
 __global__ void __launch_bounds__(32)
     solve_beta_kernel(double* __restrict__ small, Ctl* ctl, double* __restrict__ tr_norms,
                       double* __restrict__ tr_minres, unsigned long long* __restrict__ tr_wall, int capacity) {
     pdl_wait();
-    if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
-    __shared__ WarpLU w;
-    __shared__ int perm[kMaxP];
-    __shared__ double norms[kMaxP];
+    __shared__ double lu[P][P + 1];
+    __shared__ double rh[P][P + 1];
+    __shared__ int perm[P];
+    __shared__ double norms[P];
     const int lane = threadIdx.x;
-    const int p = ctl->p, P = ctl->P;
     const SmallLayout L{P};
-    for (int idx = lane; idx < p * p; idx += 32) w.m[idx / p][idx % p] = ctl->lu[idx];
-    if (lane < p) perm[lane] = ctl->perm[lane];
+    const int stop = __ldcg(&ctl->stop);
+    const int p = __ldcg(&ctl->p);
+    const int algo = __ldcg(&ctl->algo);
+    double nsq = 0.0;
+    if (lane < P) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            lu[lane][j] = __ldcg(&ctl->lu[lane * P + j]);
+            rh[lane][j] = __ldcg(small + L.rhs_b() + lane * P + j);
+        }
+        perm[lane] = __ldcg(&ctl->perm[lane]);
+        nsq = __ldcg(small + L.nsq_r() + lane);
+    }
+    if (stop) return;
     __syncwarp();
     if (lane < p) {
-        if (ctl->algo == 2) {  // steepest descent: D' = R (no conjugation)
-            for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = 0.0;
+        double x[P];
+        if (algo == 2) {  // steepest descent: D' = R (no conjugation)
+#pragma unroll
+            for (int j = 0; j < P; ++j) x[j] = 0.0;
         } else {
-            warp_lu_solve_row(w, perm, p, P, small + L.rhs_b() + lane * P, small + L.beta() + lane * P);
+            lu_solve_regs<P>(lu, perm, p, rh[lane], x);
         }
-        norms[lane] = __dsqrt_rn(small[L.nsq_r() + lane]);
+#pragma unroll
+        for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? x[j] : 0.0;
+        norms[lane] = __dsqrt_rn(nsq);
         small[L.norm() + lane] = norms[lane];
     }
     __syncwarp();
+    const int k = ctl->k;
+    const int p0 = ctl->p0;
+    if (k < capacity) {
+        // per-original-id record; ids that left the block (mccg) stay NaN
+        for (int j = lane; j < p0; j += 32) tr_norms[static_cast<size_t>(k) * p0 + j] = __longlong_as_double(0x7ff8000000000000ll);
+        __syncwarp();
+        if (lane < p) tr_norms[static_cast<size_t>(k) * p0 + ctl->ids[lane]] = norms[lane];
+    }
     if (lane == 0) {
         const unsigned long long now = globaltimer_ns();
-        const int k = ctl->k;
-        double m = norms[0];
+        double mn = norms[0];
         int slot = -1;
+        const double tol = ctl->tol;
         for (int j = 0; j < p; ++j) {
-            m = (norms[j] < m) ? norms[j] : m;  // std::min (block_cg.hpp:297-303)
-            if (slot < 0 && norms[j] <= ctl->tol) slot = j;
+            mn = (norms[j] < mn) ? norms[j] : mn;  // std::min (block_cg.hpp:297-303)
+            if (slot < 0 && norms[j] <= tol) slot = j;
         }
         if (k < capacity) {
-            const int p0 = ctl->p0;
-            for (int j = 0; j < p0; ++j) tr_norms[static_cast<size_t>(k) * p0 + j] = __longlong_as_double(0x7ff8000000000000ll);
-            for (int j = 0; j < p; ++j) tr_norms[static_cast<size_t>(k) * p0 + ctl->ids[j]] = norms[j];
-            tr_minres[k] = m;
+            tr_minres[k] = mn;
             tr_wall[k] = now - ctl->t_last;
         }
         ctl->t_last = now;

@@ -40,15 +40,18 @@ int main(int argc, char** argv) {
     cudaMemset(Ap, 0, (size_t)n * n * 8);
     cudaMemset(D, 0, (size_t)n * 32 * 8);
     run<8, 4, 64, 32, 4, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 56, 32, 4, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 56, 32, 3, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 56, 64, 2, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 48, 32, 4, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 40, 32, 4, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 112, 32, 3, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 64, 32, 4, 1>(Ap, n, D, Y, 8);
     run<8, 4, 64, 64, 2, 1>(Ap, n, D, Y, 8);
-    run<16, 4, 64, 32, 4, 2>(Ap, n, D, Y, 16);
-    run<16, 4, 56, 32, 4, 2>(Ap, n, D, Y, 16);
+    run<8, 4, 64, 64, 2, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 64, 32, 3, 1>(Ap, n, D, Y, 8);
+    run<8, 4, 32, 32, 4, 1>(Ap, n, D, Y, 8);
+    run<8, 8, 64, 32, 3, 1>(Ap, n, D, Y, 8);
+    run<8, 8, 128, 32, 2, 1>(Ap, n, D, Y, 8);
     run<4, 2, 32, 32, 4, 1>(Ap, n, D, Y, 4);
+    run<4, 2, 32, 32, 4, 1>(Ap, n, D, Y, 4);
+    run<4, 2, 64, 32, 4, 1>(Ap, n, D, Y, 4);
+    run<16, 4, 64, 32, 4, 1>(Ap, n, D, Y, 16);
+    run<16, 4, 32, 32, 4, 1>(Ap, n, D, Y, 16);
+    run<32, 4, 32, 32, 4, 1>(Ap, n, D, Y, 32);
     return 0;
 }
