@@ -167,6 +167,27 @@ def _profile_traffic(cfg_name: str):
     return None
 
 
+L2_BYTES = 126 * 2**20  # B200 L2 (nvidia-smi / MEASURED_PEAKS box)
+
+
+def l2_small(cfg):
+    return 8.0 * cfg.n * cfg.n < 2 * L2_BYTES
+
+
+def l2_note(cfg):
+    a = 8.0 * cfg.n * cfg.n
+    if l2_small(cfg):
+        return (f"A = {a / 2**20:.0f} MB < 2x L2: L2 flushed (256 MB write) before every timed step, "
+                f"outside its timing; A is L2-resident across the iterations of a step")
+    return f"inputs larger than L2: A = {a / 1e9:.2f} GB streamed from HBM every iteration (L2 126 MB)"
+
+
+def l2_flush_buffer(torch, cfg, dev):
+    if not l2_small(cfg):
+        return None
+    return torch.empty(256 * 2**20 // 8, dtype=torch.float64, device=f"cuda:{dev}")
+
+
 def _measure(m, torch, cfg, args, arith, dev):
     """K timed solves (inputs resident) + K e2e solves through the drop-in call."""
     import ctypes as C
@@ -186,22 +207,33 @@ def _measure(m, torch, cfg, args, arith, dev):
     mv_n = 0
     launches = 0
     exact_rank_checks = 0
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    # L2 rule: A larger than L2 streams from HBM every iteration; otherwise L2 is
+    # flushed (a 256 MB write on the library stream) before every timed step,
+    # outside its event pair (A then stays L2-resident across the iterations of
+    # the step, as it does for the reference on its host caches).
+    flush = l2_flush_buffer(torch, cfg, dev)
+
+    def flush_l2():
+        if flush is not None:
+            with torch.cuda.stream(stream):
+                flush.fill_(1.0)
+
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
-        e0.record(stream)
-        for _ in range(args.steps):
+        for e0, e1 in evs:
+            flush_l2()
+            e0.record(stream)
             t = ctx.run(opts, want_x=False)
+            e1.record(stream)
             iters_total += t.iteration_count()
             exact_rank_checks += t.exact_rank_checks
             tm = ctx.timing()
             mv_ms += tm["matvec_ms_total"]
             mv_n += tm["matvec_launches"]
             launches += tm["kernel_launches"]
-        e1.record(stream)
         torch.cuda.synchronize()
-    elapsed_ms = e0.elapsed_time(e1)
+    elapsed_ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
 
     # e2e: the drop-in call (coopcg_gpu_solve) with pinned host buffers
     n, p = cfg.n, cfg.p
@@ -226,10 +258,14 @@ def _measure(m, torch, cfg, args, arith, dev):
 
     e2e_once()  # warm (pinned registration etc.)
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    e2e_iters = sum(e2e_once() for _ in range(args.steps))
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
+    e2e_iters = 0
+    e2e_s = 0.0
+    for _ in range(args.steps):
+        flush_l2()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_iters += e2e_once()  # returns after the final X and trace are on the host
+        e2e_s += time.perf_counter() - t0
     h2d = (n + n * p) * 8
     d2h = (n * p + tr.iterations * p) * 8
 
@@ -281,7 +317,7 @@ def run_ours(args, cfg):
                               if main_arith == "exact" else
                               "X within 1e-8, pre-floor history within 1e-8 (tests/test_gpu_fast.py)"),
                    "step": "one full solve (setup + iterations + true-residual finalize)",
-                   "l2": f"A = {8.0 * cfg.n * cfg.n / 1e9:.2f} GB streamed per iteration (> 126 MB L2)",
+                   "l2": l2_note(cfg),
                    "parallelism": "single GPU", "exact_rank_fallbacks": res["exact_rank_checks"]},
         "roofline": res["roofline"],
         "e2e": res["e2e"],

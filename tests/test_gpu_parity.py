@@ -120,10 +120,13 @@ def test_generated_problem_solves_like_oracle(m, po):
     assert str(gt.status) == "converged"
 
 
-@pytest.mark.parametrize("n,p", [(1000, 3), (777, 17), (96, 32), (130, 1)])
+# n >= 148 * 64 selects 64-row panels (and two rows per thread at P >= 16),
+# the A.D configurations of BASELINE configs 2-4 (coopcg_gpu.cu pick_ad_config).
+@pytest.mark.parametrize("n,p", [(1000, 3), (777, 17), (96, 32), (130, 1),
+                                 (9472, 8), (9473, 16), (9500, 24)])
 def test_matvec_block_bitwise(m, po, n, p):
     rng = np.random.default_rng(n + p)
-    A = po.gen_diagdom(n, 5)
+    A = po.gen_diagdom(n, 5) if n < 2000 else rng.uniform(-1, 1, (n, n))
     A[3, :] *= 1.5  # non-symmetric input: the device layout must still follow A's rows
     D = rng.uniform(-1, 1, (n, p))
     ref = np.zeros((p, n))
