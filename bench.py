@@ -270,7 +270,9 @@ def _measure(m, torch, cfg, args, arith, dev):
     d2h = (n * p + tr.iterations * p) * 8
 
     hbm_peak, peak_src, fp64_peak = _peaks()
-    ad_ms = mv_ms / max(mv_n, 1)
+    if mv_n == 0:
+        raise RuntimeError("no A.D launch was timed (COOPCG_MV_EVERY=0?); the roofline needs sampled launches")
+    ad_ms = mv_ms / mv_n
     ad_bytes = 8.0 * cfg.n * cfg.n
     ad_flops = 2.0 * cfg.n * cfg.n * cfg.p
     achieved = ad_bytes / (ad_ms * 1e-3) / 1e9
