@@ -171,6 +171,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// The same copy with an L2 evict-first policy: for A, streamed once per
+// iteration (2.1-137 GB), so it does not push the small n x P blocks and
+// partial sums that the other kernels of the iteration re-read out of L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                     uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], "
+        "%4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+
 // Fixed-order reduction of per-CTA partial vectors inside one CTA:
 //   out[o] = sum_b part[b * stride + off + o * ostride],  o < nout.
 // lpp threads per output each sum a strided subset with 8 independent loads in

@@ -293,11 +293,27 @@ cudaError_t fast_update(coopcg_gpu_ctx* ctx, const double* D, double* Dn, int mo
     default: return fast_update_t<32>(ctx, D, Dn, mode, stop);
     }
 }
+template <int P>
+cudaError_t fast_solve_t(coopcg_gpu_ctx* ctx, int mode) {
+    const size_t smem = (size_t)(4 * P * P + 1024) * sizeof(double);
+    static bool attr_done[64] = {};
+    const int dev = ctx->device & 63;
+    if (!attr_done[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(fast_solve_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr_done[dev] = true;
+    }
+    return pdl_launch(fast_solve_kernel<P>, dim3(1), dim3(1024), smem, ctx->stream, ctx->gpart, ctx->f_rgrid, ctx->small,
+                      ctx->ctl, mode);
+}
 cudaError_t fast_solve(coopcg_gpu_ctx* ctx, int mode) {
-    const size_t smem = (size_t)(4 * ctx->P * ctx->P + 1024) * sizeof(double);
-    pdl_launch(fast_solve_kernel, dim3(1), dim3(1024), smem, ctx->stream, ctx->gpart, ctx->f_rgrid, ctx->small, ctx->ctl, mode);
     ++ctx->launches;
-    return cudaGetLastError();
+    switch (ctx->P) {
+    case 4: return fast_solve_t<4>(ctx, mode);
+    case 8: return fast_solve_t<8>(ctx, mode);
+    case 16: return fast_solve_t<16>(ctx, mode);
+    default: return fast_solve_t<32>(ctx, mode);
+    }
 }
 
 AdConfig pick_ad_config(int n_loc, int P) {
@@ -602,8 +618,6 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         CKC(cudaMalloc(&ctx->gpart, sizeof(double) * (size_t)ctx->f_rgrid * 4 * ctx->P * ctx->P));
         CKC(cudaMalloc(&ctx->npart, sizeof(double) * (size_t)ctx->f_ugrid * ctx->P));
         CKC(cudaMalloc(&ctx->dtiles, sizeof(double) * (size_t)ctx->lay.ntiles * ctx->P * kFastT));
-        CKC(cudaFuncSetAttribute(fast_solve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)((4 * 32 * 32 + 1024) * sizeof(double))));
     }
     const SmallLayout L{ctx->P};
     CKC(cudaMalloc(&ctx->small, sizeof(double) * L.total()));

@@ -68,6 +68,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
     if (warp == 0) {
         // Producer: one lane streams the A panel tiles and the D tiles.
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
             int s = 0;
             uint32_t ph = 0;
             for (int t = 0; t < ntiles; ++t) {
@@ -75,8 +76,8 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
                 const int k0 = t * T;
                 const int rows = min(T, n - k0);
                 mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
-                bulk_g2s(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
-                         static_cast<uint32_t>(rows) * BR * 8u, &full[s]);
+                bulk_g2s_evict_first(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
+                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], pol);
                 bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
                          &full[s]);
                 if (++s == S) {
@@ -214,6 +215,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
     if (warp == 0) {
         // Producer: one lane streams the A panel tiles and the D tiles.
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
             int s = 0;
             uint32_t ph = 0;
             for (int t = 0; t < ntiles; ++t) {
@@ -221,8 +223,8 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
                 const int k0 = t * T;
                 const int rows = min(T, n - k0);
                 mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
-                bulk_g2s(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
-                         static_cast<uint32_t>(rows) * BR * 8u, &full[s]);
+                bulk_g2s_evict_first(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
+                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], pol);
                 bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
                          &full[s]);
                 if (++s == S) {

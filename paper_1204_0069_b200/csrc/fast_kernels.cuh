@@ -90,6 +90,7 @@ __global__ void __launch_bounds__(32 + 64 * WN)
     __syncthreads();
     if (warp == 0) {
         if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -107,7 +108,8 @@ __global__ void __launch_bounds__(32 + 64 * WN)
                         dbytes = static_cast<uint32_t>(rows) * P * 8u;
                     }
                     mbar_arrive_expect_tx(&full[s], abytes + dbytes);
-                    bulk_g2s(As + s * BR * T, Af + (static_cast<size_t>(q) * ntiles + t) * BR * T, abytes, &full[s]);
+                    bulk_g2s_evict_first(As + s * BR * T, Af + (static_cast<size_t>(q) * ntiles + t) * BR * T, abytes, &full[s],
+                                         pol);
                     bulk_g2s(Ds + s * P * T, Dt + static_cast<size_t>(t) * P * T, dbytes, &full[s]);
                     if (++s == S) {
                         s = 0;
@@ -208,7 +210,17 @@ __global__ void __launch_bounds__(256)
             rv[u] = 0.0;
             if (il < n_loc) {
                 const int row = row0 + il;
-                for (int c = 0; c < kchunks; ++c) v[u] += Qpart[(static_cast<size_t>(c) * n_loc + il) * P + j];
+                // k-chunk partial sums, chunks ascending; 8 loads in flight
+                const double* qp = Qpart + static_cast<size_t>(il) * P + j;
+                const size_t cs = static_cast<size_t>(n_loc) * P;
+                for (int c0 = 0; c0 < kchunks; c0 += 8) {
+                    double w[8];
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc) w[cc] = (c0 + cc < kchunks) ? qp[(c0 + cc) * cs] : 0.0;
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc)
+                        if (c0 + cc < kchunks) v[u] += w[cc];
+                }
                 if (mode == 0) {
                     dv[u] = D[static_cast<size_t>(row) * P + j];
                     rv[u] = R[static_cast<size_t>(row) * P + j];
@@ -272,60 +284,82 @@ __global__ void __launch_bounds__(256)
 //   beta_i:  M beta_i^T  = -(R^T Q + alpha Q^T Q)_i   (algebraic R_new^T Q)
 // mode 0: alpha + beta; mode 1: alpha only (recompute iteration, beta later);
 // mode 2: beta only from G0 = R_new^T Q of a residual pass (uses ctl->lu).
-struct FastSolveScratch {
-    double l[kMaxP][kMaxP + 1];
-    double y[kMaxP][kMaxP + 1];
-};
-
-__device__ void chol_solve_row(const double (*l)[kMaxP + 1], int p, const double* rhs, double* y, double* x) {
-    // L L^T x = rhs
-    for (int i = 0; i < p; ++i) {
-        double s = rhs[i];
-        for (int j = 0; j < i; ++j) s = fma(-l[i][j], y[j], s);
-        y[i] = s / l[i][i];
+// L L^T x = rhs for lane-owned right-hand sides, L in shared memory
+// (compile-time P, active p; the operation order of the one-warp version).
+template <int P>
+__device__ __forceinline__ void chol_solve_regs(const double (*l)[P + 1], int p, const double (&rhs)[P],
+                                                double (&x)[P]) {
+    double y[P];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        y[i] = 0.0;
+        x[i] = 0.0;
     }
-    for (int i = p - 1; i >= 0; --i) {
-        double s = y[i];
-        for (int j = i + 1; j < p; ++j) s = fma(-l[j][i], x[j], s);
-        x[i] = s / l[i][i];
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        if (i < p) {
+            double s = rhs[i];
+#pragma unroll
+            for (int j = 0; j < i; ++j) s = fma(-l[i][j], y[j], s);
+            y[i] = s / l[i][i];
+        }
+    }
+#pragma unroll
+    for (int i = P - 1; i >= 0; --i) {
+        if (i < p) {
+            double s = y[i];
+#pragma unroll
+            for (int j = i + 1; j < P; ++j)
+                if (j < p) s = fma(-l[j][i], x[j], s);
+            x[i] = s / l[i][i];
+        }
     }
 }
 
+template <int P>
 __global__ void __launch_bounds__(1024)
     fast_solve_kernel(const double* __restrict__ partials, int nparts, double* __restrict__ small, Ctl* ctl,
                       int mode) {
     pdl_wait();
     if (*reinterpret_cast<volatile int*>(&ctl->stop)) return;
-    __shared__ FastSolveScratch sc;
     extern __shared__ __align__(16) double dyn[];  // flat[4 P P] then red[blockDim]
-    const int p = ctl->p, P = ctl->P;
+    double* flat = dyn;
+    double* red = dyn + 4 * P * P;
+    __shared__ double lsm[P][P + 1];
+    const int p = ctl->p;
     const SmallLayout L{P};
     const int tid = threadIdx.x;
     const int nout = (mode == 2) ? P * P : 4 * P * P;
-    double* flat = dyn;
-    double* red = dyn + 4 * P * P;
+    // inputs of warp 0 requested before the reduction
+    double nsq = 0.0, lu_in[P];
+    if (tid < P) {
+        nsq = small[L.nsq_d() + tid];
+#pragma unroll
+        for (int j = 0; j < P; ++j) lu_in[j] = (mode == 2) ? ctl->lu[tid * P + j] : 0.0;
+    }
     cta_reduce_fixed(partials, nparts, 4 * P * P, 0, 1, nout, flat, red);
     __syncthreads();
     // G[gsel][a][c] = flat[(gsel * P + a) * P + c]
     auto G = [&](int gsel, int a, int c) { return flat[(gsel * P + a) * P + c]; };
     if (tid >= 32) return;
     const int lane = tid;
-    double* yrow = sc.y[lane];
-    double x[kMaxP];
+    double x[P], rhs[P];
     if (mode != 2) {
-        // M = (raw + raw^T)/2, floor = max|M| * 1e-14
-        double maxabs = 0.0;
-        if (lane < p)
-            for (int j = 0; j < p; ++j) {
-                const double v = 0.5 * (G(0, lane, j) + G(0, j, lane));
-                sc.l[lane][j] = v;
-                maxabs = fmax(maxabs, fabs(v));
+        // M = (raw + raw^T)/2, floor = max|M| * 1e-14; lane i holds row i
+        double l[P];
+        double maxabs = 0.0, diag = 0.0;
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            l[j] = 0.0;
+            if (lane < p && j < p) {
+                l[j] = 0.5 * (G(0, lane, j) + G(0, j, lane));
+                maxabs = fmax(maxabs, fabs(l[j]));
+                if (j == lane) diag = l[j];
             }
+        }
         for (int off = 16; off > 0; off >>= 1) maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, off));
-        __syncwarp();
         const double floor = maxabs * 1e-14;
-        bool bad = false;
-        if (lane < p) bad = !(sc.l[lane][lane] > 0.0) && (small[L.nsq_d() + lane] > 0.0);
+        const bool bad = (lane < p) && !(diag > 0.0) && (nsq > 0.0);
         if (__any_sync(0xffffffffu, bad)) {
             if (lane == 0) {
                 ctl->err = 2;
@@ -334,58 +368,77 @@ __global__ void __launch_bounds__(1024)
             }
             return;
         }
-        // Cholesky (lower, lane owns row)
-        bool ok = true;
-        for (int k = 0; k < p; ++k) {
+        // Cholesky (lower, left-looking; lane owns row; row k broadcast by shuffle)
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (k >= p) break;
+            double dk = 0.0;
             if (lane == k) {
-                double s = sc.l[k][k];
-                for (int m = 0; m < k; ++m) s = fma(-sc.l[k][m], sc.l[k][m], s);
-                sc.l[k][k] = (s > floor) ? sqrt(s) : -1.0;
+                double s = l[k];
+#pragma unroll
+                for (int m = 0; m < k; ++m) s = fma(-l[m], l[m], s);
+                dk = (s > floor) ? sqrt(s) : -1.0;
             }
-            __syncwarp();
-            if (!(sc.l[k][k] > 0.0)) {
-                ok = false;
-                break;
+            const double lkk = __shfl_sync(0xffffffffu, dk, k);
+            if (!(lkk > 0.0)) {
+                if (lane == 0) {
+                    ctl->status = 1;  // rank collapse (pivot vanished)
+                    ctl->stop = 1;
+                }
+                return;
             }
+            double rk[P];
+#pragma unroll
+            for (int m = 0; m < k; ++m) rk[m] = __shfl_sync(0xffffffffu, l[m], k);
             if (lane > k && lane < p) {
-                double s = sc.l[lane][k];
-                for (int m = 0; m < k; ++m) s = fma(-sc.l[lane][m], sc.l[k][m], s);
-                sc.l[lane][k] = s / sc.l[k][k];
+                double s = l[k];
+#pragma unroll
+                for (int m = 0; m < k; ++m) s = fma(-l[m], rk[m], s);
+                l[k] = s / lkk;
             }
-            __syncwarp();
+            if (lane == k) l[k] = lkk;
         }
-        if (!ok) {
-            if (lane == 0) {
-                ctl->status = 1;  // rank collapse (pivot vanished)
-                ctl->stop = 1;
+        if (lane < P) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                lsm[lane][j] = l[j];
+                ctl->lu[lane * P + j] = l[j];
             }
-            return;
         }
-        for (int idx = lane; idx < p * p; idx += 32) ctl->lu[idx] = sc.l[idx / p][idx % p];
+        __syncwarp();
         if (lane < p) {
-            double rhs[kMaxP];
-            for (int j = 0; j < p; ++j) rhs[j] = -G(1, lane, j);
-            chol_solve_row(sc.l, p, rhs, yrow, x);
+#pragma unroll
+            for (int j = 0; j < P; ++j) rhs[j] = (j < p) ? -G(1, lane, j) : 0.0;
+            chol_solve_regs<P>(lsm, p, rhs, x);
+#pragma unroll
             for (int j = 0; j < P; ++j) small[L.alpha() + lane * P + j] = (j < p) ? x[j] : 0.0;
             if (mode == 0) {
                 // rhs_beta(i, j) = -(R^T Q + alpha Q^T Q)(i, j)
-                for (int j = 0; j < p; ++j) {
+#pragma unroll
+                for (int j = 0; j < P; ++j) {
                     double s = G(2, lane, j);
-                    for (int m = 0; m < p; ++m) s = fma(x[m], G(3, m, j), s);
-                    rhs[j] = -s;
+#pragma unroll
+                    for (int m = 0; m < P; ++m)
+                        if (m < p) s = fma(x[m], G(3, m, j), s);
+                    rhs[j] = (j < p) ? -s : 0.0;
                 }
-                double xb[kMaxP];
-                chol_solve_row(sc.l, p, rhs, yrow, xb);
+                double xb[P];
+                chol_solve_regs<P>(lsm, p, rhs, xb);
+#pragma unroll
                 for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? xb[j] : 0.0;
             }
         }
     } else {
-        for (int idx = lane; idx < p * p; idx += 32) sc.l[idx / p][idx % p] = ctl->lu[idx];
+        if (lane < P) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) lsm[lane][j] = lu_in[j];
+        }
         __syncwarp();
         if (lane < p) {
-            double rhs[kMaxP];
-            for (int j = 0; j < p; ++j) rhs[j] = -G(0, lane, j);
-            chol_solve_row(sc.l, p, rhs, yrow, x);
+#pragma unroll
+            for (int j = 0; j < P; ++j) rhs[j] = (j < p) ? -G(0, lane, j) : 0.0;
+            chol_solve_regs<P>(lsm, p, rhs, x);
+#pragma unroll
             for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? x[j] : 0.0;
         }
     }
