@@ -243,6 +243,33 @@ class GpuContext:
         _capi.lib().coopcg_gpu_timing(self._h, C.byref(self._timing))
         return self._make_trace(tr, norms, minres, wall, init, fres, fx, opts, act)
 
+    def run_raw(self, opts: Optional[SolveOptions] = None) -> tuple:
+        """One solve through coopcg_gpu_run with reusable trace buffers and no
+        Python trace assembly (the timed steps of bench.py).  Returns
+        (iterations, exact_rank_checks); `run` is the full-trace API."""
+        opts = opts or SolveOptions()
+        cap = max(opts.max_iters if opts.max_iters >= 0 else 2 * self.n, 1)
+        key = (cap, self.p)
+        if getattr(self, "_raw", None) is None or self._raw[0] != key:
+            bufs = [np.zeros((cap, self.p)), np.zeros(cap), np.zeros(cap, dtype=np.uint64), np.zeros(self.p),
+                    np.zeros(self.p), np.zeros(self.p, dtype=np.int32)]
+            tr = _capi.coopcg_trace()
+            tr.capacity = cap
+            tr.residual_norms = _dp(bufs[0])
+            tr.minres = _dp(bufs[1])
+            tr.wall_ns = bufs[2].ctypes.data_as(C.POINTER(C.c_uint64))
+            tr.initial_residual_norms = _dp(bufs[3])
+            tr.final_residual_norms = _dp(bufs[4])
+            tr.active_agents = bufs[5].ctypes.data_as(C.POINTER(C.c_int))
+            tr.final_x = C.POINTER(C.c_double)()
+            self._raw = (key, bufs, tr)
+        tr = self._raw[2]
+        co = opts.to_c()
+        rc = _capi.lib().coopcg_gpu_run(self._h, C.byref(co), C.byref(tr))
+        _check(self._h, rc)
+        _capi.lib().coopcg_gpu_timing(self._h, C.byref(self._timing))
+        return tr.iterations, tr.exact_rank_checks
+
     def _make_trace(self, tr, norms, minres, wall, init, fres, fx, opts, act=None) -> SolveTrace:
         n, p = self.n, self.p
         it = tr.iterations
