@@ -301,9 +301,9 @@ def run_ours(args, cfg):
     import paper_1204_0069_b200 as m
 
     ws, rank, local = _dist()
-    if ws > 1:
+    if ws > 1 or args.sharded_path:
         from paper_1204_0069_b200 import sharded
-        return sharded.bench_main(args, cfg, BASELINE_METRIC)
+        return sharded.bench_main(args, cfg, BASELINE_METRIC, clock_sampler=ClockSampler, peaks=_peaks)
     dev = args.device
     torch.cuda.set_device(dev)
     main_arith = args.arith
@@ -358,6 +358,11 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the other arithmetic mode")
+    ap.add_argument("--sharded-path", action="store_true",
+                    help="(testing) drive the row-sharded orchestrator even with one rank under torchrun")
+    ap.add_argument("--p2p", action="store_true",
+                    help="N > 1: exchange Q through peer memory (CUDA IPC push from the A.D kernel) instead of "
+                         "an NCCL all-gather")
     args = ap.parse_args()
     from paper_1204_0069_b200.configs import CONFIGS
     cfg = CONFIGS[args.config]

@@ -195,6 +195,23 @@ int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int*
 int coopcg_gpu_state(coopcg_gpu_ctx* ctx, int* stop, int* iterations);
 int coopcg_gpu_end(coopcg_gpu_ctx* ctx, coopcg_trace* trace);
 
+/* ---- peer-memory Q exchange (one process per GPU, NVLink / NVSwitch) ------
+ * Replaces the per-iteration all-gather of Q: the kernel that computes this
+ * rank's rows of Q (the A.D epilogue, or the fast row pass) stores them into
+ * every rank's Q through CUDA IPC mappings, so after a stream-ordered barrier
+ * (a tiny NCCL all-reduce, or a host barrier) every rank holds the full Q.
+ * In this mode Q is double-buffered by iteration parity (coopcg_gpu_block
+ * returns the buffer of iteration k), so no rank overwrites rows a slower rank
+ * still reads.  R and S keep their all-gathers (setup, recompute, final).
+ *   coopcg_gpu_ipc_handles: this context's two Q buffers as two 64-byte
+ *     cudaIpcMemHandle_t (written to handles_out[0..127]).
+ *   coopcg_gpu_set_peers: `handles` holds nranks x 128 bytes (rank order);
+ *     the context maps every other rank's buffers (own slot ignored) and
+ *     switches to peer mode.  nranks <= 8. */
+#define COOPCG_IPC_HANDLE_BYTES 64
+int coopcg_gpu_ipc_handles(coopcg_gpu_ctx* ctx, void* handles_out);
+int coopcg_gpu_set_peers(coopcg_gpu_ctx* ctx, int nranks, int self_rank, const void* handles);
+
 #ifdef __cplusplus
 }
 #endif

@@ -25,6 +25,16 @@ struct SmallLayout {
     __host__ __device__ int total() const { return 5 * P * P + 5 * P; }
 };
 
+// Peer-memory row push (row-sharded contexts, one process per GPU): the
+// kernel that produces this rank's rows of Q also stores them into every
+// rank's copy of Q (CUDA IPC mappings over NVLink; dst[self] is the local
+// buffer), so no separate all-gather of Q is needed.  n == 0: local only.
+constexpr int kMaxPeers = 8;
+struct PeerRows {
+    double* dst[kMaxPeers];
+    int n;
+};
+
 // Device control block: the coordinator state of DriverControl
 // (block_cg.hpp:106-125) plus the factorisation shared by the alpha and beta
 // solves (the reference re-factors the same Gram matrix per agent, with

@@ -76,6 +76,13 @@ struct coopcg_gpu_ctx {
     double* R = nullptr;
     double* Dblk[2] = {nullptr, nullptr};
     double* Q = nullptr;
+    // peer-memory Q push (coopcg_gpu_ipc_handles / coopcg_gpu_set_peers): Q is
+    // double-buffered by iteration parity (Qalt) so that a rank already pushing
+    // iteration k+1's rows never overwrites rows a slower rank still reads in k
+    double* Qalt = nullptr;
+    bool p2p = false;
+    PeerRows peers[2] = {};          // [parity]
+    std::vector<void*> ipc_opened;   // mapped peer buffers (closed on destroy)
     double* S = nullptr;
     double* V = nullptr;  // MGS working copy
     double* b = nullptr;
@@ -110,6 +117,7 @@ struct coopcg_gpu_ctx {
     bool join_pending = false;
     coopcg_timing timing{};
     long long launches = 0;  // kernels launched since the last run started
+    int phase_mv = 0;        // phase API: A.D launches timed so far in this solve (<= kChunkMax)
     int max_iters = 0, every = 50;  // resolved SolveOptions of the current solve
     int p_orig = 0;                 // agents at creation (mccg restricts ctx->p during a solve)
     int algo = 0;                   // 0 ccg, 1 mccg for the current solve
@@ -186,7 +194,8 @@ template <int P>
 constexpr int ad_rpt() { return P >= 16 ? 2 : 1; }
 
 template <int P, int CPT, int BR>
-cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
+cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop,
+                        const PeerRows& peers) {
     constexpr int RPT = ad_rpt<P>();
     auto kern = (RPT == 1) ? ad_exact_kernel<P, CPT, BR, kAdT, kAdS> : ad_exact_rpt_kernel<P, CPT, BR, kAdT, kAdS, 2>;
     const size_t smem = ad_smem<P, CPT, BR>();
@@ -199,25 +208,29 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
     }
     dim3 grid((ctx->n_loc + BR - 1) / BR);
     dim3 block(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT));
-    pdl_launch(kern, dim3(grid), dim3(block), smem, ctx->stream, ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop);
+    pdl_launch(kern, dim3(grid), dim3(block), smem, ctx->stream, ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop,
+               peers);
     ++ctx->launches;
     return cudaGetLastError();
 }
 
 template <int P, int CPT>
-cudaError_t ad_launch_br(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
+cudaError_t ad_launch_br(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop,
+                         const PeerRows& peers) {
     switch (ctx->ad.BR) {
-    case 32: return ad_launch_t<P, CPT, 32>(ctx, src, dst, b, stop);
-    default: return ad_launch_t<P, CPT, 64>(ctx, src, dst, b, stop);
+    case 32: return ad_launch_t<P, CPT, 32>(ctx, src, dst, b, stop, peers);
+    default: return ad_launch_t<P, CPT, 64>(ctx, src, dst, b, stop, peers);
     }
 }
 
-cudaError_t ad_launch(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop) {
+// peers: push the rows to every rank's copy of dst (row-sharded Q, peer mode)
+cudaError_t ad_launch(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop,
+                      const PeerRows& peers = PeerRows{}) {
     switch (ctx->P) {
-    case 4: return ad_launch_br<4, 2>(ctx, src, dst, b, stop);
-    case 8: return ad_launch_br<8, 4>(ctx, src, dst, b, stop);
-    case 16: return ad_launch_br<16, 4>(ctx, src, dst, b, stop);
-    default: return ad_launch_br<32, 4>(ctx, src, dst, b, stop);
+    case 4: return ad_launch_br<4, 2>(ctx, src, dst, b, stop, peers);
+    case 8: return ad_launch_br<8, 4>(ctx, src, dst, b, stop, peers);
+    case 16: return ad_launch_br<16, 4>(ctx, src, dst, b, stop, peers);
+    default: return ad_launch_br<32, 4>(ctx, src, dst, b, stop, peers);
     }
 }
 
@@ -265,32 +278,32 @@ cudaError_t fast_ad(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
 }
 template <int P>
 cudaError_t fast_rows_t(coopcg_gpu_ctx* ctx, double* dst, const double* b, const double* D, const double* R,
-                        const double* Qfull, int mode, const int* stop) {
-    pdl_launch(fast_rows_kernel<P>, dim3(ctx->f_rgrid), dim3(256), 0, ctx->stream, ctx->qpart, ctx->f_kchunks, ctx->n_loc, ctx->row0, dst,
-                                                               b, D, R, Qfull, ctx->p, mode, ctx->gpart, stop);
+                        const double* Qfull, int mode, const int* stop, const PeerRows& peers) {
     ++ctx->launches;
-    return cudaGetLastError();
+    return pdl_launch(fast_rows_kernel<P>, dim3(ctx->f_rgrid), dim3(256), 0, ctx->stream, ctx->qpart, ctx->f_kchunks,
+                      ctx->n_loc, ctx->row0, dst, b, D, R, Qfull, ctx->p, mode, ctx->gpart, stop, peers);
 }
 cudaError_t fast_rows(coopcg_gpu_ctx* ctx, double* dst, const double* b, const double* D, const double* R,
-                      const double* Qfull, int mode, const int* stop) {
+                      const double* Qfull, int mode, const int* stop, const PeerRows& peers = PeerRows{}) {
     switch (ctx->P) {
-    case 8: return fast_rows_t<8>(ctx, dst, b, D, R, Qfull, mode, stop);
-    case 16: return fast_rows_t<16>(ctx, dst, b, D, R, Qfull, mode, stop);
-    default: return fast_rows_t<32>(ctx, dst, b, D, R, Qfull, mode, stop);
+    case 8: return fast_rows_t<8>(ctx, dst, b, D, R, Qfull, mode, stop, peers);
+    case 16: return fast_rows_t<16>(ctx, dst, b, D, R, Qfull, mode, stop, peers);
+    default: return fast_rows_t<32>(ctx, dst, b, D, R, Qfull, mode, stop, peers);
     }
 }
 template <int P>
-cudaError_t fast_update_t(coopcg_gpu_ctx* ctx, const double* D, double* Dn, int mode, const int* stop) {
-    pdl_launch(fast_update_kernel<P>, dim3(ctx->f_ugrid), dim3(256), 0, ctx->stream, ctx->X, ctx->R, ctx->Q, D, Dn, ctx->small, ctx->n,
+cudaError_t fast_update_t(coopcg_gpu_ctx* ctx, const double* Q, const double* D, double* Dn, int mode, const int* stop) {
+    pdl_launch(fast_update_kernel<P>, dim3(ctx->f_ugrid), dim3(256), 0, ctx->stream, ctx->X, ctx->R, Q, D, Dn, ctx->small, ctx->n,
                                                                  ctx->p, mode, ctx->npart, ctx->partials, stop);
     ++ctx->launches;
     return cudaGetLastError();
 }
-cudaError_t fast_update(coopcg_gpu_ctx* ctx, const double* D, double* Dn, int mode, const int* stop) {
+cudaError_t fast_update(coopcg_gpu_ctx* ctx, const double* Q, const double* D, double* Dn, int mode,
+                        const int* stop) {
     switch (ctx->P) {
-    case 8: return fast_update_t<8>(ctx, D, Dn, mode, stop);
-    case 16: return fast_update_t<16>(ctx, D, Dn, mode, stop);
-    default: return fast_update_t<32>(ctx, D, Dn, mode, stop);
+    case 8: return fast_update_t<8>(ctx, Q, D, Dn, mode, stop);
+    case 16: return fast_update_t<16>(ctx, Q, D, Dn, mode, stop);
+    default: return fast_update_t<32>(ctx, Q, D, Dn, mode, stop);
     }
 }
 template <int P>
@@ -441,6 +454,8 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaFree(ctx->R);
     cudaFree(ctx->Dblk[0]);
     cudaFree(ctx->Dblk[1]);
+    for (void* ptr : ctx->ipc_opened) cudaIpcCloseMemHandle(ptr);
+    cudaFree(ctx->Qalt);
     cudaFree(ctx->Q);
     cudaFree(ctx->S);
     cudaFree(ctx->V);
@@ -957,7 +972,7 @@ cudaError_t fast_rows_any_t(coopcg_gpu_ctx* ctx, const double* qpart, int kchunk
                             const double* b, const double* D, const double* R, const double* Qfull, int mode,
                             const int* stop) {
     pdl_launch(fast_rows_kernel<P>, dim3(ctx->f_rgrid), dim3(256), 0, ctx->stream, qpart, kchunks, nrows, row0, dst, b, D, R, Qfull,
-                                                               ctx->p, mode, ctx->gpart, stop);
+               ctx->p, mode, ctx->gpart, stop, PeerRows{});
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -1009,6 +1024,7 @@ static int begin_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     CK(cudaMemcpyAsync(ctx->X, ctx->X0, sizeof(double) * (size_t)ctx->n * ctx->P, cudaMemcpyDeviceToDevice,
                        ctx->stream));
     ctx->launches = 0;
+    ctx->phase_mv = 0;
     return COOPCG_OK;
 }
 
@@ -1050,6 +1066,10 @@ static int setup_rest(coopcg_gpu_ctx* ctx) {
 }
 
 // Q_loc = A_loc D_k  (stage_matvec, block_cg.hpp:146-151), bracketed by events.
+// Q of iteration k: double-buffered by parity in peer mode (see Qalt).
+static double* q_of(const coopcg_gpu_ctx* ctx, int k) { return (ctx->p2p && (k & 1)) ? ctx->Qalt : ctx->Q; }
+static PeerRows peers_of(const coopcg_gpu_ctx* ctx, int k) { return ctx->p2p ? ctx->peers[k & 1] : PeerRows{}; }
+
 // Make the main stream wait for an outstanding side-stream rank_end.
 static int join_rank(coopcg_gpu_ctx* ctx) {
     if (!ctx->join_pending) return COOPCG_OK;
@@ -1059,11 +1079,12 @@ static int join_rank(coopcg_gpu_ctx* ctx) {
 }
 
 static int iter_local(coopcg_gpu_ctx* ctx, int k, cudaEvent_t ev0, cudaEvent_t ev1) {
+    double* Qk = q_of(ctx, k);
     int* stop = &ctx->ctl->stop;
     double* D = ctx->Dblk[k & 1];
     if (ev0) CK(cudaEventRecord(ev0, ctx->stream));
     if (ctx->arith != COOPCG_ARITH_FAST) {
-        CK(ad_launch(ctx, D, ctx->Q, nullptr, stop));
+        CK(ad_launch(ctx, D, Qk, nullptr, stop, peers_of(ctx, k)));
         if (ev1) CK(cudaEventRecord(ev1, ctx->stream));
         if (int rc = join_rank(ctx)) return rc;
     } else {
@@ -1071,7 +1092,7 @@ static int iter_local(coopcg_gpu_ctx* ctx, int k, cudaEvent_t ev0, cudaEvent_t e
         if (ev1) CK(cudaEventRecord(ev1, ctx->stream));
         if (int rc = join_rank(ctx)) return rc;
         // single GPU: fuse the four Gram partials into the local row pass
-        CK(fast_rows(ctx, ctx->Q, nullptr, D, ctx->R, nullptr, sharded(ctx) ? 1 : 0, stop));
+        CK(fast_rows(ctx, Qk, nullptr, D, ctx->R, nullptr, sharded(ctx) ? 1 : 0, stop, peers_of(ctx, k)));
     }
     return COOPCG_OK;
 }
@@ -1083,6 +1104,7 @@ static bool recompute_at(const coopcg_gpu_ctx* ctx, int k) {
 // After Q is complete: Grams, alpha, update; in recompute iterations ends with
 // R_loc = A_loc X - b (the caller exchanges R before iter_rest).
 static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
+    double* Qk = q_of(ctx, k);
     const int n = ctx->n, p = ctx->p, P = ctx->P;
     cudaStream_t st = ctx->stream;
     int* stop = &ctx->ctl->stop;
@@ -1090,27 +1112,27 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
     double* Dn = ctx->Dblk[(k + 1) & 1];
     const bool rec = recompute_at(ctx, k);
     if (ctx->arith != COOPCG_ARITH_FAST) {
-        CK(chains_launch(ctx, kPhGram, D, ctx->Q, ctx->R, 3, stop));
+        CK(chains_launch(ctx, kPhGram, D, Qk, ctx->R, 3, stop));
         CK(solve_alpha_launch(ctx));
-        pdl_launch(update_kernel, dim3(grid_for((size_t)n * P, 256)), dim3(256), 0, st, ctx->R, ctx->X, ctx->Q, D, ctx->small, n, p, P,
+        pdl_launch(update_kernel, dim3(grid_for((size_t)n * P, 256)), dim3(256), 0, st, ctx->R, ctx->X, Qk, D, ctx->small, n, p, P,
                                                                     rec ? 1 : 0, stop);
         LAUNCHED();
         if (rec) CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, stop));
     } else {
         if (sharded(ctx))  // the four Gram partials over the full replicated blocks
-            CK(fast_rows_any(ctx, ctx->Q, 1, n, 0, ctx->Q, nullptr, D, ctx->R, nullptr, 0, stop));
+            CK(fast_rows_any(ctx, Qk, 1, n, 0, Qk, nullptr, D, ctx->R, nullptr, 0, stop));
         if (!rec) {
             CK(fast_solve(ctx, 0));
-            CK(fast_update(ctx, D, Dn, 0, stop));
+            CK(fast_update(ctx, Qk, D, Dn, 0, stop));
             pdl_launch(fast_record_kernel, dim3(1), dim3(256), 0, st, ctx->npart, ctx->f_ugrid, P, 0, 1, ctx->small, ctx->ctl,
                                                   ctx->tr_norms, ctx->tr_minres, ctx->tr_wall, ctx->tr_capacity);
             LAUNCHED();
         } else {
             CK(fast_solve(ctx, 1));
-            CK(fast_update(ctx, D, Dn, 1, stop));
+            CK(fast_update(ctx, Qk, D, Dn, 1, stop));
             CK(fast_ad(ctx, ctx->X, stop));
             // local rows of R = A X - b (with R^T Q / |R|^2 partials when unsharded)
-            CK(fast_rows(ctx, ctx->R, ctx->b, nullptr, nullptr, sharded(ctx) ? nullptr : ctx->Q, 1, stop));
+            CK(fast_rows(ctx, ctx->R, ctx->b, nullptr, nullptr, sharded(ctx) ? nullptr : Qk, 1, stop));
         }
     }
     return COOPCG_OK;
@@ -1118,6 +1140,7 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
 
 // The rest of the iteration: beta, D', norms/record, rank check, k++.
 static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
+    double* Qk = q_of(ctx, k);
     const int n = ctx->n, p = ctx->p, P = ctx->P;
     cudaStream_t st = ctx->stream;
     int* stop = &ctx->ctl->stop;
@@ -1126,16 +1149,16 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
     const bool rec = recompute_at(ctx, k);
     const bool fast = ctx->arith == COOPCG_ARITH_FAST;
     if (!fast) {
-        CK(chains_launch(ctx, kPhBeta, ctx->R, ctx->Q, nullptr, 2, stop));
+        CK(chains_launch(ctx, kPhBeta, ctx->R, Qk, nullptr, 2, stop));
         CK(solve_beta_launch(ctx));
         pdl_launch(direction_kernel, dim3(dgrid_of(ctx)), dim3(256), 0, st, ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop,
                                                         ctx->algo == 2 ? 1 : 0);
         LAUNCHED();
     } else if (rec) {
         if (sharded(ctx))  // R^T Q and |R|^2 over the full replicated, recomputed R
-            CK(fast_rows_any(ctx, ctx->R, 1, n, 0, ctx->R, nullptr, nullptr, nullptr, ctx->Q, 1, stop));
+            CK(fast_rows_any(ctx, ctx->R, 1, n, 0, ctx->R, nullptr, nullptr, nullptr, Qk, 1, stop));
         CK(fast_solve(ctx, 2));
-        CK(fast_update(ctx, D, Dn, 2, stop));
+        CK(fast_update(ctx, Qk, D, Dn, 2, stop));
         pdl_launch(fast_record_kernel, dim3(1), dim3(256), 0, st, ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->small,
                                               ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
                                               ctx->tr_capacity);
@@ -1400,7 +1423,15 @@ int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k) {
     switch (phase) {
     case COOPCG_PH_SETUP_LOCAL: return setup_local(ctx);
     case COOPCG_PH_SETUP_REST: return setup_rest(ctx);
-    case COOPCG_PH_ITER_LOCAL: return iter_local(ctx, k, nullptr, nullptr);
+    case COOPCG_PH_ITER_LOCAL: {
+        // A.D launch timing for the phase-driven (sharded) solve: events around
+        // every 8th A.D, the first kChunkMax of them (read by coopcg_gpu_end)
+        const bool rec = k % 8 == 0 && ctx->phase_mv < kChunkMax;
+        cudaEvent_t e0 = rec ? ctx->mv_ev[ctx->phase_mv * 2] : nullptr;
+        cudaEvent_t e1 = rec ? ctx->mv_ev[ctx->phase_mv * 2 + 1] : nullptr;
+        if (rec) ++ctx->phase_mv;
+        return iter_local(ctx, k, e0, e1);
+    }
     case COOPCG_PH_ITER_MID: return iter_mid(ctx, k);
     case COOPCG_PH_ITER_REST: return iter_rest(ctx, k);
     case COOPCG_PH_FINAL_LOCAL: return final_local(ctx);
@@ -1411,6 +1442,53 @@ int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k) {
 
 int coopcg_gpu_recompute_at(const coopcg_gpu_ctx* ctx, int k) { return ctx ? (recompute_at(ctx, k) ? 1 : 0) : 0; }
 
+int coopcg_gpu_ipc_handles(coopcg_gpu_ctx* ctx, void* handles_out) {
+    if (!ctx || !handles_out) return COOPCG_E_INVALID;
+    if (!sharded(ctx)) return fail(ctx, COOPCG_E_STATE, "peer exchange is for row-sharded contexts");
+    CK(cudaSetDevice(ctx->device));
+    if (!ctx->Qalt) {
+        CK(cudaMalloc(&ctx->Qalt, sizeof(double) * (size_t)ctx->n * ctx->P));
+        CK(cudaMemset(ctx->Qalt, 0, sizeof(double) * (size_t)ctx->n * ctx->P));
+    }
+    double* bufs[2] = {ctx->Q, ctx->Qalt};
+    for (int b = 0; b < 2; ++b) {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, bufs[b]));
+        std::memcpy(static_cast<char*>(handles_out) + b * COOPCG_IPC_HANDLE_BYTES, &h, COOPCG_IPC_HANDLE_BYTES);
+    }
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_set_peers(coopcg_gpu_ctx* ctx, int nranks, int self_rank, const void* handles) {
+    if (!ctx || !handles) return COOPCG_E_INVALID;
+    if (nranks < 1 || nranks > kMaxPeers || self_rank < 0 || self_rank >= nranks)
+        return fail(ctx, COOPCG_E_INVALID, "set_peers: nranks %d (max %d), self %d", nranks, kMaxPeers, self_rank);
+    if (!ctx->Qalt) return fail(ctx, COOPCG_E_STATE, "set_peers: call coopcg_gpu_ipc_handles first");
+    CK(cudaSetDevice(ctx->device));
+    static_assert(sizeof(cudaIpcMemHandle_t) == COOPCG_IPC_HANDLE_BYTES, "IPC handle size");
+    double* own[2] = {ctx->Q, ctx->Qalt};
+    PeerRows pr[2] = {};
+    for (int r = 0; r < nranks; ++r)
+        for (int b = 0; b < 2; ++b) {
+            if (r == self_rank) {
+                pr[b].dst[r] = own[b];
+                continue;
+            }
+            cudaIpcMemHandle_t h;
+            std::memcpy(&h, static_cast<const char*>(handles) + (r * 2 + b) * COOPCG_IPC_HANDLE_BYTES,
+                        COOPCG_IPC_HANDLE_BYTES);
+            void* ptr = nullptr;
+            CK(cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+            ctx->ipc_opened.push_back(ptr);
+            pr[b].dst[r] = static_cast<double*>(ptr);
+        }
+    pr[0].n = pr[1].n = nranks;
+    ctx->peers[0] = pr[0];
+    ctx->peers[1] = pr[1];
+    ctx->p2p = true;
+    return COOPCG_OK;
+}
+
 int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int* ld) {
     if (!ctx || !dev_ptr) return COOPCG_E_INVALID;
     double* b = nullptr;
@@ -1418,7 +1496,7 @@ int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int*
     case COOPCG_BLOCK_X: b = ctx->X; break;
     case COOPCG_BLOCK_R: b = ctx->R; break;
     case COOPCG_BLOCK_D: b = ctx->Dblk[k & 1]; break;
-    case COOPCG_BLOCK_Q: b = ctx->Q; break;
+    case COOPCG_BLOCK_Q: b = q_of(ctx, k); break;
     case COOPCG_BLOCK_S: b = ctx->S; break;
     default: return fail(ctx, COOPCG_E_INVALID, "unknown block %d", which);
     }
@@ -1441,7 +1519,21 @@ int coopcg_gpu_end(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
     if (!ctx) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     ctx->timing.kernel_launches = ctx->launches;
-    return end_impl(ctx, trace);
+    const int rc = end_impl(ctx, trace);  // synchronises the stream
+    if (rc != COOPCG_OK) return rc;
+    // the phase API's sampled A.D launches (iteration 8 i; later ones were no-ops)
+    double tot = 0.0;
+    int cnt = 0;
+    for (int i = 0; i < ctx->phase_mv && 8 * i < ctx->ctl_host[0].iterations; ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, ctx->mv_ev[2 * i], ctx->mv_ev[2 * i + 1]) == cudaSuccess) {
+            tot += ms;
+            ++cnt;
+        }
+    }
+    ctx->timing.matvec_ms_total = tot;
+    ctx->timing.matvec_launches = cnt;
+    return COOPCG_OK;
 }
 
 int coopcg_gpu_solve(coopcg_gpu_ctx* ctx, const double* b, const double* X0, const coopcg_opts* opts,

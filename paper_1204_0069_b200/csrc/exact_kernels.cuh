@@ -40,7 +40,7 @@ template <int P, int CPT, int BR, int T, int S>
 __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
     ad_exact_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
-                    const double* __restrict__ b, int p, const int* __restrict__ stop) {
+                    const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers) {
     pdl_wait();
     constexpr int kConsumerWarps = ad_consumer_warps(BR, P / CPT);
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
@@ -165,16 +165,25 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
     const int il = i0 + r;
     if (il < n_loc && g < P / CPT) {
         const int row = row0 + il;
-        double* y = Y + static_cast<size_t>(row) * P + g * CPT;
         const double bb = (b != nullptr) ? b[row] : 0.0;
+        double v[CPT];
 #pragma unroll
         for (int c = 0; c < CPT; ++c) {
             const int col = g * CPT + c;
-            double v = 0.0;
-            if (col < p) v = (b != nullptr) ? __dsub_rn(acc[c], bb) : acc[c];
-            y[c] = v;
+            v[c] = 0.0;
+            if (col < p) v[c] = (b != nullptr) ? __dsub_rn(acc[c], bb) : acc[c];
+        }
+        const size_t o = static_cast<size_t>(row) * P + g * CPT;
+        if (peers.n == 0) {
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) Y[o + c] = v[c];
+        } else {
+            for (int q = 0; q < peers.n; ++q)  // this rank's rows into every rank's copy
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) peers.dst[q][o + c] = v[c];
         }
     }
+    if (peers.n != 0) __threadfence_system();
 }
 
 // Two rows per thread (RPT = 2, used at p >= 16): one 16-byte load of A
@@ -185,7 +194,7 @@ template <int P, int CPT, int BR, int T, int S, int RPT = 2>
 __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT))
     ad_exact_rpt_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
-                    const double* __restrict__ b, int p, const int* __restrict__ stop) {
+                    const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers) {
     pdl_wait();
     constexpr int RT = BR / RPT;  // row-threads per column group
     constexpr int kConsumerWarps = ad_consumer_warps(RT, P / CPT);
@@ -322,17 +331,22 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
         const int il = i0 + RPT * r + q;
         if (il < n_loc && g < P / CPT) {
             const int row = row0 + il;
-            double* y = Y + static_cast<size_t>(row) * P + g * CPT;
             const double bb = (b != nullptr) ? b[row] : 0.0;
+            const size_t o = static_cast<size_t>(row) * P + g * CPT;
 #pragma unroll
             for (int c = 0; c < CPT; ++c) {
                 const int col = g * CPT + c;
                 double v = 0.0;
                 if (col < p) v = (b != nullptr) ? __dsub_rn(acc[q][c], bb) : acc[q][c];
-                y[c] = v;
+                if (peers.n == 0) {
+                    Y[o + c] = v;
+                } else {
+                    for (int pr = 0; pr < peers.n; ++pr) peers.dst[pr][o + c] = v;
+                }
             }
         }
     }
+    if (peers.n != 0) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------

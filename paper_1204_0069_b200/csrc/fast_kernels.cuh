@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256)
     fast_rows_kernel(const double* __restrict__ Qpart, int kchunks, int n_loc, int row0, double* __restrict__ dst,
                      const double* __restrict__ b, const double* __restrict__ D, const double* __restrict__ R,
                      const double* __restrict__ Qfull, int p, int mode, double* __restrict__ partials,
-                     const int* __restrict__ stop) {
+                     const int* __restrict__ stop, PeerRows peers) {
     pdl_wait();
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     constexpr int RP = 4;                 // rows per thread per tile (loads in flight together)
@@ -236,7 +236,12 @@ __global__ void __launch_bounds__(256)
             if (il < n_loc) {
                 const int row = row0 + il;
                 if (b != nullptr) v[u] = (j < p) ? v[u] - b[row] : 0.0;
-                dst[static_cast<size_t>(row) * P + j] = v[u];
+                const size_t o = static_cast<size_t>(row) * P + j;
+                if (peers.n == 0) {
+                    dst[o] = v[u];
+                } else {
+                    for (int q = 0; q < peers.n; ++q) peers.dst[q][o] = v[u];  // every rank's copy
+                }
             }
             tq[lr][j] = v[u];
             td[lr][j] = dv[u];
@@ -274,6 +279,7 @@ __global__ void __launch_bounds__(256)
         const int o = tid + q * 256;
         if (o < NOUT) partials[static_cast<size_t>(blockIdx.x) * NOUT + o] = acc[q];
     }
+    if (peers.n != 0) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------

@@ -20,6 +20,11 @@ CPU engine of tests/test_sharded_gloo.py (gloo):
     engine.state() -> (stop, iterations); engine.end() -> SolveTrace
     engine.collective_stream() -> context manager ordering collectives with
                                   the engine's stream
+
+Peer mode (GpuShardEngine.enable_peers + PeerQExchange): the Q rows are
+pushed into every rank's Q by the kernel that computes them (CUDA IPC
+mappings; one fused compute + exchange step), and the per-iteration Q
+"all-gather" reduces to a stream-ordered barrier.
 """
 from __future__ import annotations
 
@@ -76,6 +81,34 @@ class RowExchange:
         dist.all_gather_into_tensor(out, inp, group=self.group)
         block.copy_(out[: self.n])
 
+    def allgather_q(self, block) -> None:
+        """The per-iteration exchange of Q (an all-gather here)."""
+        self.allgather(block)
+
+
+class PeerQExchange(RowExchange):
+    """Peer mode: Q rows arrive through the peer push of the producing kernel;
+    the Q exchange is only a barrier ordered after it on every rank (a
+    one-element all-reduce on the context stream with NCCL; a stream sync plus
+    a host barrier with gloo).  R and S are still all-gathered."""
+
+    def __init__(self, n: int, P: int, world: int, rank: int, group=None, device: int = 0):
+        super().__init__(n, P, world, rank, group)
+        import torch.distributed as dist
+        self._nccl = dist.get_backend(group) == "nccl"
+        self._flag = self._torch.zeros(1, dtype=self._torch.float64, device=f"cuda:{device}")
+
+    def allgather_q(self, block) -> None:
+        torch = self._torch
+        import torch.distributed as dist
+        if self.world == 1:
+            return
+        if self._nccl:
+            dist.all_reduce(self._flag, group=self.group)  # stream-ordered after this rank's push
+        else:
+            torch.cuda.current_stream().synchronize()
+            dist.barrier(group=self.group)
+
 
 def solve_sharded(engine, exchange: RowExchange, opts: SolveOptions, poll_every: int = 8):
     """Drive one sharded solve (the phase protocol of include/coopcg_gpu.h)."""
@@ -89,7 +122,7 @@ def solve_sharded(engine, exchange: RowExchange, opts: SolveOptions, poll_every:
     while not stop and k < engine.max_iters:
         engine.phase(PH_ITER_LOCAL, k)
         with engine.collective_stream():
-            exchange.allgather(engine.block(BLOCK_Q, k))
+            exchange.allgather_q(engine.block(BLOCK_Q, k))
         engine.phase(PH_ITER_MID, k)
         if engine.recompute_at(k):
             with engine.collective_stream():
@@ -133,6 +166,20 @@ class GpuShardEngine:
         self._views = {}
         self.max_iters = 0
         self.opts = None
+
+    def enable_peers(self, group=None):
+        """Peer-memory Q exchange: share this context's Q buffers (CUDA IPC) with
+        every rank of `group` and map theirs (include/coopcg_gpu.h)."""
+        import torch.distributed as dist
+        own = (C.c_char * 128)()
+        _check(self.ctx._h, _capi.lib().coopcg_gpu_ipc_handles(self.ctx._h, own))
+        world = dist.get_world_size(group)
+        rank = dist.get_rank(group)
+        allh = [None] * world
+        dist.all_gather_object(allh, bytes(own), group=group)
+        buf = (C.c_char * (128 * world)).from_buffer_copy(b"".join(allh))
+        _check(self.ctx._h, _capi.lib().coopcg_gpu_set_peers(self.ctx._h, world, rank, buf))
+        self._views.clear()
 
     def block(self, which: int, k: int):
         ptr = C.c_void_p()
@@ -191,8 +238,13 @@ class GpuShardEngine:
         self.ctx.close()
 
 
-def bench_main(args, cfg, metric: str) -> int:
-    """bench.py under torchrun: row-sharded solve of `cfg` on WORLD_SIZE GPUs."""
+def bench_main(args, cfg, metric: str, clock_sampler=None, peaks=None) -> int:
+    """bench.py under torchrun: row-sharded solve of `cfg` on WORLD_SIZE GPUs.
+
+    value: iterations / max over ranks of the summed CUDA-event time of the
+    timed solves (inputs resident); e2e: b and X0 uploaded from host and the
+    final X + trace downloaded every step, wall clock, max over ranks.
+    --p2p: the peer-memory Q exchange instead of the NCCL all-gather of Q."""
     import torch
     import torch.distributed as dist
     from .configs import host_inputs, solve_options
@@ -207,38 +259,76 @@ def bench_main(args, cfg, metric: str) -> int:
                               "implemented this round (diag-dominant configs shard)"}))
         dist.destroy_process_group()
         return 0
+    p2p = bool(getattr(args, "p2p", False))
     eng = GpuShardEngine(cfg.n, cfg.p, rank, world, local, arith=args.arith)
     eng.ctx.gen_A(cfg.matrix, cfg.seed, cfg.reflectors, cfg.kappa)
     b, X0 = host_inputs(cfg)
     opts = solve_options(cfg, b)
     eng.ctx.upload(b, X0)
-    ex = RowExchange(cfg.n, eng.P, world, rank)
+    if p2p:
+        eng.enable_peers()
+        ex = PeerQExchange(cfg.n, eng.P, world, rank, None, local)
+    else:
+        ex = RowExchange(cfg.n, eng.P, world, rank)
     for _ in range(args.warmup):
         solve_sharded(eng, ex, opts)
     torch.cuda.synchronize()
     dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     iters = 0
-    e0.record(eng._stream)
-    for _ in range(args.steps):
-        t = solve_sharded(eng, ex, opts)
-        iters += t.iteration_count()
-    e1.record(eng._stream)
-    torch.cuda.synchronize()
-    ms = torch.tensor([e0.elapsed_time(e1)], device=f"cuda:{local}")
+    mv_ms, mv_n, launches = 0.0, 0, 0
+    sampler = clock_sampler(local) if (clock_sampler is not None and rank == 0) else contextlib.nullcontext()
+    with sampler:
+        for e0, e1 in evs:
+            e0.record(eng._stream)
+            t = solve_sharded(eng, ex, opts)
+            e1.record(eng._stream)
+            iters += t.iteration_count()
+            tm = eng.ctx.timing()
+            mv_ms += tm["matvec_ms_total"]
+            mv_n += tm["matvec_launches"]
+            launches += tm["kernel_launches"]
+        torch.cuda.synchronize()
+    ms = torch.tensor([sum(e0.elapsed_time(e1) for e0, e1 in evs)], device=f"cuda:{local}")
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    # e2e: host inputs up, final X + trace down, every step
+    dist.barrier()
+    e2e_iters, t0 = 0, time.perf_counter()
+    for _ in range(args.steps):
+        eng.ctx.upload(b, X0)
+        e2e_iters += solve_sharded(eng, ex, opts).iteration_count()
+    torch.cuda.synchronize()
+    e2e_s = torch.tensor([time.perf_counter() - t0], device=f"cuda:{local}")
+    dist.all_reduce(e2e_s, op=dist.ReduceOp.MAX)
     dist.barrier()
     if rank == 0:
         secs = float(ms.item()) * 1e-3
-        print(json.dumps({
+        hbm_peak, peak_src, fp64_peak = peaks() if peaks is not None else (6541.5, "fallback", 36.0)
+        n_loc = eng.row1 - eng.row0
+        ad_ms = mv_ms / max(mv_n, 1)
+        ad_bytes = 8.0 * cfg.n * n_loc
+        achieved = ad_bytes / (ad_ms * 1e-3) / 1e9 if mv_n else None
+        line = {
             "metric": metric, "value": iters / secs, "unit": "iterations/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs * 1e3 / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded SplitMix64 generators, DESIGN.md §3)",
             "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "arith": args.arith,
-                       "parallelism": f"row-block sharded A over {world} GPUs, NCCL all-gather of Q"},
-        }))
+                       "parallelism": (f"row-block sharded A over {world} GPUs, "
+                                       + ("peer-memory push of Q rows (CUDA IPC) + barrier" if p2p
+                                          else "NCCL all-gather of Q")),
+                       "l2": f"inputs larger than L2: A = {8.0 * cfg.n * cfg.n / 1e9:.2f} GB in total"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": (achieved / hbm_peak) if achieved else None, "traffic": None,
+                         "kernel": "A.D on rank 0's rows", "ad_ms_per_launch": ad_ms,
+                         "ad_launches_timed": mv_n, "peak_source": peak_src},
+            "e2e": {"value": e2e_iters / float(e2e_s.item()), "unit": "iterations/s",
+                    "h2d_bytes_per_step": (cfg.n + cfg.n * cfg.p) * 8,
+                    "d2h_bytes_per_step": (cfg.n * cfg.p + iters // max(args.steps, 1) * cfg.p) * 8},
+            "gpu_launches": launches,
+            "clocks": sampler.summary() if hasattr(sampler, "summary") else None,
+        }
+        print(json.dumps(line))
     eng.close()
     dist.destroy_process_group()
     return 0

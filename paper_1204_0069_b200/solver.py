@@ -300,6 +300,8 @@ class GpuContext:
         return self.run(opts)
 
     def timing(self) -> dict:
+        """coopcg_timing of the last solve (run / run_raw / the phase API's end)."""
+        _capi.lib().coopcg_gpu_timing(self._h, C.byref(self._timing))
         t = self._timing
         return {"matvec_launches": t.matvec_launches, "matvec_ms_total": t.matvec_ms_total,
                 "run_ms": t.run_ms, "loop_ms": t.loop_ms, "kernel_launches": t.kernel_launches}
