@@ -33,8 +33,13 @@ using namespace coopcg_gpu;
 
 namespace {
 
-constexpr int kAdT = 32;
-constexpr int kAdS = 4;
+// A.D ring shape (rows of k per stage x stages), tools/probe/ad_probe.cu at the
+// BASELINE sizes: 64 x 2 for P >= 8 (P=8: 0.420 vs 0.427 ms at n=16384; P=16:
+// 8.87 vs 9.34 ms at n=65536; P=32: 66.5 vs 67.9 ms at n=131072), 32 x 4 at P=4.
+template <int P>
+constexpr int ad_T() { return P >= 8 ? 64 : 32; }
+template <int P>
+constexpr int ad_S() { return P >= 8 ? 2 : 4; }
 constexpr int kChunkMax = 16;
 constexpr int kMaxParts = 296;  // 2 x 148 SMs
 
@@ -185,7 +190,7 @@ cudaError_t pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 // ---- A.D launcher: template dispatch on (P, CPT, BR) -------------------------
 template <int P, int CPT, int BR>
 size_t ad_smem() {
-    return static_cast<size_t>(kAdS) * kAdT * (BR + P) * sizeof(double) + 2 * kAdS * sizeof(uint64_t);
+    return static_cast<size_t>(ad_S<P>()) * ad_T<P>() * (BR + P) * sizeof(double) + 2 * ad_S<P>() * sizeof(uint64_t);
 }
 
 // rows per thread: 2 at P >= 16 (one LDS.128 of A feeds 2 x CPT chains;
@@ -197,7 +202,8 @@ template <int P, int CPT, int BR>
 cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop,
                         const PeerRows& peers) {
     constexpr int RPT = ad_rpt<P>();
-    auto kern = (RPT == 1) ? ad_exact_kernel<P, CPT, BR, kAdT, kAdS> : ad_exact_rpt_kernel<P, CPT, BR, kAdT, kAdS, 2>;
+    constexpr int T = ad_T<P>(), S = ad_S<P>();
+    auto kern = (RPT == 1) ? ad_exact_kernel<P, CPT, BR, T, S> : ad_exact_rpt_kernel<P, CPT, BR, T, S, 2>;
     const size_t smem = ad_smem<P, CPT, BR>();
     static bool attr_done[64] = {};
     const int dev = ctx->device & 63;

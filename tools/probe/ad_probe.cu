@@ -16,10 +16,10 @@ void run(const double* Ap, int n, const double* D, double* Y, int p) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    k<<<grid, block, smem>>>(Ap, n, n, 0, D, Y, nullptr, p, nullptr);
+    k<<<grid, block, smem>>>(Ap, n, n, 0, D, Y, nullptr, p, nullptr, PeerRows{});
     cudaEventRecord(e0);
     const int reps = 5;
-    for (int r = 0; r < reps; ++r) k<<<grid, block, smem>>>(Ap, n, n, 0, D, Y, nullptr, p, nullptr);
+    for (int r = 0; r < reps; ++r) k<<<grid, block, smem>>>(Ap, n, n, 0, D, Y, nullptr, p, nullptr, PeerRows{});
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms;
@@ -32,26 +32,29 @@ void run(const double* Ap, int n, const double* D, double* Y, int p) {
 }
 
 int main(int argc, char** argv) {
-    const int n = 16384;
+    // argv[1]: "big" sweeps the P = 16 / 32 configurations at the cfg 3 / 4 sizes
+    const bool big = argc > 1 && argv[1][0] == 'b';
+    const int n = big ? 65536 : 16384;
     double *Ap, *D, *Y;
-    cudaMalloc(&Ap, (size_t)n * n * 8 + (size_t)128 * n * 8);
-    cudaMalloc(&D, (size_t)n * 32 * 8);
-    cudaMalloc(&Y, (size_t)n * 32 * 8);
-    cudaMemset(Ap, 0, (size_t)n * n * 8);
-    cudaMemset(D, 0, (size_t)n * 32 * 8);
+    const size_t nmax = big ? 131072 : 16384;
+    cudaMalloc(&Ap, nmax * nmax * 8 + (size_t)128 * nmax * 8);
+    cudaMalloc(&D, nmax * 32 * 8);
+    cudaMalloc(&Y, nmax * 32 * 8);
+    cudaMemset(Ap, 0, nmax * nmax * 8);
+    cudaMemset(D, 0, nmax * 32 * 8);
+    if (big) {
+        run<16, 4, 64, 32, 4, 2>(Ap, n, D, Y, 16);
+        run<16, 4, 64, 64, 2, 2>(Ap, n, D, Y, 16);
+        run<16, 4, 64, 64, 3, 2>(Ap, n, D, Y, 16);
+        run<16, 4, 64, 128, 2, 2>(Ap, n, D, Y, 16);
+        run<16, 4, 128, 64, 2, 2>(Ap, n, D, Y, 16);
+        const int n4 = 131072;
+        run<32, 4, 64, 32, 4, 2>(Ap, n4, D, Y, 32);
+        run<32, 4, 64, 64, 2, 2>(Ap, n4, D, Y, 32);
+        run<32, 4, 64, 64, 3, 2>(Ap, n4, D, Y, 32);
+        run<32, 4, 128, 64, 2, 2>(Ap, n4, D, Y, 32);
+        return 0;
+    }
     run<8, 4, 64, 32, 4, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 64, 32, 4, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 64, 64, 2, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 64, 64, 2, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 64, 32, 3, 1>(Ap, n, D, Y, 8);
-    run<8, 4, 32, 32, 4, 1>(Ap, n, D, Y, 8);
-    run<8, 8, 64, 32, 3, 1>(Ap, n, D, Y, 8);
-    run<8, 8, 128, 32, 2, 1>(Ap, n, D, Y, 8);
-    run<4, 2, 32, 32, 4, 1>(Ap, n, D, Y, 4);
-    run<4, 2, 32, 32, 4, 1>(Ap, n, D, Y, 4);
-    run<4, 2, 64, 32, 4, 1>(Ap, n, D, Y, 4);
-    run<16, 4, 64, 32, 4, 1>(Ap, n, D, Y, 16);
-    run<16, 4, 32, 32, 4, 1>(Ap, n, D, Y, 16);
-    run<32, 4, 32, 32, 4, 1>(Ap, n, D, Y, 32);
     return 0;
 }
