@@ -397,16 +397,17 @@ cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, co
     return cudaGetLastError();
 }
 
-// Rings (tools/probe/chain_kernel_probe.cu, n = 16384): P=4/8: 3 x 256 rows
-// (99 us per phase vs 113-144 us for shallower or shorter rings); P=16:
-// 4 x 128 (the 3 x 256 ring does not fit); P=32: 4 x 64.
+// Rings (tools/probe/chain_kernel_probe.cu, n = 16384): 3 stages of the
+// longest tile that fits (per-tile overhead dominates shorter tiles):
+// P=4/8: 256 rows (99 us per phase); P=16: 192 (105 vs 115 us at 4 x 128);
+// P=32: 96 (127 vs 144 us at 4 x 64).
 cudaError_t chains_launch(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
                           int nsrc, const int* stop) {
     switch (ctx->P) {
     case 4: return chains_launch_t<4, 256, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
     case 8: return chains_launch_t<8, 256, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
-    case 16: return chains_launch_t<16, 128, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
-    default: return chains_launch_t<32, 64, 4>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 16: return chains_launch_t<16, 192, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
+    default: return chains_launch_t<32, 96, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
     }
 }
 
