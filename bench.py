@@ -289,7 +289,10 @@ def _measure(m, torch, cfg, args, arith, dev):
                      "kernel": "ad_exact_kernel (Q = A.D)" if arith == "exact" else "ad_fast_kernel (Q = A.D, DMMA)",
                      "ad_ms_per_launch": ad_ms, "ad_launches_timed": mv_n, "peak_source": peak_src,
                      "fp64": {"achieved_tflops": ad_flops / (ad_ms * 1e-3) / 1e12, "peak_tflops": fp64_peak,
-                              "peak_source": "measured DFMA/DMMA probe (tools/probe/fp64_probe.cu)"},
+                              "peak_source": "measured DFMA/DMMA probe (tools/probe/fp64_probe.cu)",
+                              # exact mode keeps both roundings: one DMUL + one DADD per multiply-add,
+                              # 18.2 T FP64 instructions/s measured = 18.2 TF/s-equivalent
+                              "exact_issue_ceiling_tflops": 18.2 if arith == "exact" else None},
                      "roofline_ms": max(ad_bytes / (hbm_peak * 1e9), ad_flops / (fp64_peak * 1e12)) * 1e3},
         "e2e": {"value": e2e_iters / e2e_s, "unit": "iterations/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": d2h},
