@@ -1,6 +1,6 @@
 """Peer-memory Q exchange (coopcg_gpu_ipc_handles / coopcg_gpu_set_peers) with
-two ranks (processes) on one GPU.  Each rank's A.D (exact) or row pass (fast)
-stores its rows of Q into both ranks' Q through CUDA IPC mappings; the Q
+two or three ranks (processes) on one GPU.  Each rank's A.D (exact) or row pass
+(fast) stores its rows of Q into every rank's Q through CUDA IPC mappings; the Q
 exchange is then only a barrier (stream sync + gloo barrier: no kernel ever
 waits on another, the two processes time-share the GPU).  R and S (setup,
 recompute, final) travel by a host-staged gloo all-gather.  Exact mode must be
@@ -58,23 +58,23 @@ def _worker(rank, world, port, arith, opts_t, inputs_path, out_path):
     dist.destroy_process_group()
 
 
-def _run(tmp_path, arith, A, b, X0, opts_t):
+def _run(tmp_path, arith, A, b, X0, opts_t, world=2):
     import torch.multiprocessing as mp
     inputs = str(tmp_path / "inputs.npz")
     np.savez(inputs, A=A, b=b, X0=X0)
     out = str(tmp_path / "rank%d.npz")
-    mp.start_processes(_worker, args=(2, _free_port(), arith, opts_t, inputs, out), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(world, _free_port(), arith, opts_t, inputs, out), nprocs=world, join=True,
                        start_method="spawn")
-    return [np.load(out % r) for r in range(2)]
+    return [np.load(out % r) for r in range(world)]
 
 
-def test_peer_q_exchange_exact_bitwise(po, tmp_path):
-    n, p = 301, 4  # uneven rows (151 / 150)
+@pytest.mark.parametrize("n,p,world", [(301, 4, 2), (517, 8, 3)])  # uneven row blocks
+def test_peer_q_exchange_exact_bitwise(po, tmp_path, n, p, world):
     A = po.gen_diagdom(n, 41)
     b = po.gen_rhs(n, "uniform", 41)
     X0 = po.gen_starts(n, p, 41)
     opts_t = (0.0, 30, 7)  # 30 iterations, recompute every 7 (R all-gathers between)
-    res = _run(tmp_path, "exact", A, b, X0, opts_t)
+    res = _run(tmp_path, "exact", A, b, X0, opts_t, world)
     ref = po.oracle_ccg(A, b, X0, tol=0.0, max_iters=30, recompute=7)
     for r in res:
         assert str(r["status"]) == ref.status and int(r["it"]) == ref.iterations
