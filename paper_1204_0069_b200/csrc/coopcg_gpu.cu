@@ -97,6 +97,7 @@ struct coopcg_gpu_ctx {
     double* final_norms = nullptr; // P + 1
     Ctl* ctl = nullptr;
     Ctl* ctl_host = nullptr;  // pinned snapshots [2]
+    double* minres_host = nullptr;  // pinned [2][kChunkMax]: the chunk's recorded minres (enqueue sizing)
     ChainDesc* descs = nullptr;
     int desc_off[4] = {0, 0, 0, 0};
     int desc_cnt[4] = {0, 0, 0, 0};
@@ -203,14 +204,17 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
                         const PeerRows& peers) {
     constexpr int RPT = ad_rpt<P>();
     constexpr int T = ad_T<P>(), S = ad_S<P>();
-    auto kern = (RPT == 1) ? ad_exact_kernel<P, CPT, BR, T, S> : ad_exact_rpt_kernel<P, CPT, BR, T, S, 2>;
+    const bool push = peers.n > 0;
+    auto kern = (RPT == 1) ? (push ? ad_exact_kernel<P, CPT, BR, T, S, true> : ad_exact_kernel<P, CPT, BR, T, S, false>)
+                           : (push ? ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, true>
+                                   : ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, false>);
     const size_t smem = ad_smem<P, CPT, BR>();
-    static bool attr_done[64] = {};
+    static bool attr_done[2][64] = {};
     const int dev = ctx->device & 63;
-    if (!attr_done[dev]) {
+    if (!attr_done[push][dev]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
-        attr_done[dev] = true;
+        attr_done[push][dev] = true;
     }
     dim3 grid((ctx->n_loc + BR - 1) / BR);
     dim3 block(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT));
@@ -286,8 +290,9 @@ template <int P>
 cudaError_t fast_rows_t(coopcg_gpu_ctx* ctx, double* dst, const double* b, const double* D, const double* R,
                         const double* Qfull, int mode, const int* stop, const PeerRows& peers) {
     ++ctx->launches;
-    return pdl_launch(fast_rows_kernel<P>, dim3(ctx->f_rgrid), dim3(256), 0, ctx->stream, ctx->qpart, ctx->f_kchunks,
-                      ctx->n_loc, ctx->row0, dst, b, D, R, Qfull, ctx->p, mode, ctx->gpart, stop, peers);
+    auto kern = peers.n > 0 ? fast_rows_kernel<P, true> : fast_rows_kernel<P, false>;
+    return pdl_launch(kern, dim3(ctx->f_rgrid), dim3(256), 0, ctx->stream, ctx->qpart, ctx->f_kchunks, ctx->n_loc,
+                      ctx->row0, dst, b, D, R, Qfull, ctx->p, mode, ctx->gpart, stop, peers);
 }
 cudaError_t fast_rows(coopcg_gpu_ctx* ctx, double* dst, const double* b, const double* D, const double* R,
                       const double* Qfull, int mode, const int* stop, const PeerRows& peers = PeerRows{}) {
@@ -482,6 +487,7 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaFree(ctx->tr_wall);
     cudaFree(ctx->stage);
     if (ctx->ctl_host) cudaFreeHost(ctx->ctl_host);
+    if (ctx->minres_host) cudaFreeHost(ctx->minres_host);
     for (auto e : ctx->mv_ev) cudaEventDestroy(e);
     cudaEvent_t evs[] = {ctx->ev_run0,      ctx->ev_run1,      ctx->ev_loop0, ctx->ev_loop1,
                          ctx->ev_chunk[0], ctx->ev_chunk[1], ctx->ev_fork,  ctx->ev_join};
@@ -650,6 +656,7 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     CKC(cudaMalloc(&ctx->final_norms, sizeof(double) * (ctx->P + 1)));
     CKC(cudaMalloc(&ctx->ctl, sizeof(Ctl)));
     CKC(cudaHostAlloc(&ctx->ctl_host, 2 * sizeof(Ctl), cudaHostAllocDefault));
+    CKC(cudaHostAlloc(&ctx->minres_host, 2 * kChunkMax * sizeof(double), cudaHostAllocDefault));
     std::vector<ChainDesc> descs;
     build_descs(p, ctx->P, descs, ctx->desc_off, ctx->desc_cnt);
     CKC(cudaMalloc(&ctx->descs, sizeof(ChainDesc) * descs.size()));
@@ -1318,6 +1325,8 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     double mv_total = 0.0;
     int mv_count = 0;
     int chunk_iters[2] = {0, 0};
+    double trend_rate = 1.0, trend_last = 0.0;
+    int trend_k = -1;
     bool chunk_rec[2][kChunkMax] = {};
     // A.D launch timing (coopcg_timing, the bench roofline): CUDA events around
     // every mv_every-th A.D only -- an event between two kernels costs the
@@ -1346,9 +1355,23 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
             }
         }
         if (snap.stop) stopped = true;
+        // residual trend of the chunk (recorded minres), for sizing what to enqueue next
+        const int n_done = std::min(chunk_iters[slot], snap.iterations - chunk_k0[slot]);
+        if (n_done >= 2 && chunk_k0[slot] + n_done <= ctx->tr_capacity) {
+            const double first = ctx->minres_host[slot * kChunkMax];
+            trend_last = ctx->minres_host[slot * kChunkMax + n_done - 1];
+            // geometric-mean decay per iteration over the chunk
+            trend_rate = (first > 0.0 && trend_last > 0.0) ? std::pow(trend_last / first, 1.0 / (n_done - 1)) : 1.0;
+            trend_k = chunk_k0[slot] + n_done - 1;
+        }
         return COOPCG_OK;
     };
-    int chunk = 4;
+    // Enqueue sizing: chunks of 4, 4, 8, 8, 16, 16, ... iterations, two in flight.
+    // With a tolerance, the next chunk is capped by the iterations the recent
+    // geometric decay of minres still needs (no-op launches after the stop are
+    // cheap but not free: they dominated small solves such as config 0).
+    // Sizing never changes results: the device stop flag decides.
+    int chunk = 4, same = 0;
     for (;;) {
       while (!stopped && k_host < max_iters) {
         if (npending == 2) {
@@ -1358,7 +1381,15 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
             if (stopped) break;
         }
         const int slot = chunk_id & 1;
-        const int U = std::min(chunk, max_iters - k_host);
+        int U = std::min(chunk, max_iters - k_host);
+        const double tol = ctx->ctl_host[0].tol;
+        if (tol > 0.0 && trend_k >= 0 && trend_last > tol && trend_rate > 0.0 && trend_rate < 0.9) {
+            // clear geometric convergence: enqueue about what is still needed
+            const double need = std::ceil(std::log(tol / trend_last) / std::log(trend_rate));
+            const int queued = k_host - (trend_k + 1);  // already enqueued beyond the last read
+            const int cap = static_cast<int>(std::max(2.0, need - queued + 1.0));
+            U = std::max(1, std::min(U, cap));
+        }
         chunk_iters[slot] = U;
         chunk_k0[slot] = k_host;
         for (int u = 0; u < U; ++u, ++k_host) {
@@ -1372,10 +1403,16 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
         }
         if (int rc = join_rank(ctx)) return rc;
         CK(cudaMemcpyAsync(&ctx->ctl_host[slot], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        if (chunk_k0[slot] + U <= ctx->tr_capacity)
+            CK(cudaMemcpyAsync(ctx->minres_host + slot * kChunkMax, ctx->tr_minres + chunk_k0[slot],
+                               sizeof(double) * U, cudaMemcpyDeviceToHost, st));
         CK(cudaEventRecord(ctx->ev_chunk[slot], st));
         pending[npending++] = chunk_id;
         ++chunk_id;
-        chunk = std::min(kChunkMax, chunk * 2);
+        if (++same == 2) {
+            chunk = std::min(kChunkMax, chunk * 2);
+            same = 0;
+        }
       }
       for (int q = 0; q < npending; ++q)
           if (int rc = read_chunk(pending[q])) return rc;
@@ -1391,6 +1428,8 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
       k_host = next_k;
       stopped = false;
       chunk = 4;
+      same = 0;
+      trend_k = -1;
     }
     if (int rc = join_rank(ctx)) return rc;
     ctx->rank_async = false;

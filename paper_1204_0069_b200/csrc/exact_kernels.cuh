@@ -36,7 +36,9 @@ namespace coopcg_gpu {
 // over the SMs, coopcg_gpu.cu pick_ad_config); surplus threads idle.
 __host__ __device__ constexpr int ad_consumer_warps(int rows, int groups) { return (rows * groups + 31) / 32; }
 
-template <int P, int CPT, int BR, int T, int S>
+// PUSH (peer mode only): store the rows into every rank's copy of Y through
+// `peers` (a separate instantiation keeps the common path's code unchanged).
+template <int P, int CPT, int BR, int T, int S, bool PUSH = false>
 __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
     ad_exact_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
             if (col < p) v[c] = (b != nullptr) ? __dsub_rn(acc[c], bb) : acc[c];
         }
         const size_t o = static_cast<size_t>(row) * P + g * CPT;
-        if (peers.n == 0) {
+        if (!PUSH) {
 #pragma unroll
             for (int c = 0; c < CPT; ++c) Y[o + c] = v[c];
         } else {
@@ -183,14 +185,14 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
                 for (int c = 0; c < CPT; ++c) peers.dst[q][o + c] = v[c];
         }
     }
-    if (peers.n != 0) __threadfence_system();
+    if (PUSH) __threadfence_system();
 }
 
 // Two rows per thread (RPT = 2, used at p >= 16): one 16-byte load of A
 // serves both rows' chains.  Same arithmetic as ad_exact_kernel, kept as a
 // separate kernel because the RPT = 1 case compiles ~5% slower inside this
 // template (tools/probe/ad_cmp_probe.cu).
-template <int P, int CPT, int BR, int T, int S, int RPT = 2>
+template <int P, int CPT, int BR, int T, int S, int RPT = 2, bool PUSH = false>
 __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT))
     ad_exact_rpt_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
@@ -338,7 +340,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
                 const int col = g * CPT + c;
                 double v = 0.0;
                 if (col < p) v = (b != nullptr) ? __dsub_rn(acc[q][c], bb) : acc[q][c];
-                if (peers.n == 0) {
+                if (!PUSH) {
                     Y[o + c] = v;
                 } else {
                     for (int pr = 0; pr < peers.n; ++pr) peers.dst[pr][o + c] = v;
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
             }
         }
     }
-    if (peers.n != 0) __threadfence_system();
+    if (PUSH) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------

@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(32 + 64 * WN)
 //   mode 0 (iteration):  G0 = D^T Q, G1 = R^T D, G2 = R^T Q, G3 = Q^T Q
 //   mode 1 (residual):   G0 = dst^T Q (if Q != null), diag(dst^T dst) -> G1[j][j]
 // Rows are processed in tiles of 256/P (thread per element).
-template <int P>
+template <int P, bool PUSH = false>
 __global__ void __launch_bounds__(256)
     fast_rows_kernel(const double* __restrict__ Qpart, int kchunks, int n_loc, int row0, double* __restrict__ dst,
                      const double* __restrict__ b, const double* __restrict__ D, const double* __restrict__ R,
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(256)
                 const int row = row0 + il;
                 if (b != nullptr) v[u] = (j < p) ? v[u] - b[row] : 0.0;
                 const size_t o = static_cast<size_t>(row) * P + j;
-                if (peers.n == 0) {
+                if (!PUSH) {
                     dst[o] = v[u];
                 } else {
                     for (int q = 0; q < peers.n; ++q) peers.dst[q][o] = v[u];  // every rank's copy
@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(256)
         const int o = tid + q * 256;
         if (o < NOUT) partials[static_cast<size_t>(blockIdx.x) * NOUT + o] = acc[q];
     }
-    if (peers.n != 0) __threadfence_system();
+    if (PUSH) __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------

@@ -56,5 +56,9 @@ int main(int argc, char** argv) {
         return 0;
     }
     run<8, 4, 64, 32, 4, 1>(Ap, n, D, Y, 8);
+    run<4, 2, 32, 32, 4, 1>(Ap, n, D, Y, 4);
+    run<4, 2, 32, 32, 4, 1>(Ap, 4096, D, Y, 4);
+    run<4, 2, 32, 64, 2, 1>(Ap, 4096, D, Y, 4);
+    run<4, 2, 32, 32, 2, 1>(Ap, 4096, D, Y, 4);
     return 0;
 }
