@@ -404,13 +404,13 @@ cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, co
 
 // Rings (tools/probe/chain_kernel_probe.cu, n = 16384): 3 stages of the
 // longest tile that fits (per-tile overhead dominates shorter tiles):
-// P=4/8: 256 rows (99 us per phase); P=16: 192 (105 vs 115 us at 4 x 128);
-// P=32: 96 (127 vs 144 us at 4 x 64).
+// P=4: 512 rows (93 us per phase vs 99 at 256); P=8: 384 (96.5 vs 98.6);
+// P=16: 192 (105 vs 115 us at 4 x 128); P=32: 96 (127 vs 144 us at 4 x 64).
 cudaError_t chains_launch(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
                           int nsrc, const int* stop) {
     switch (ctx->P) {
-    case 4: return chains_launch_t<4, 256, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
-    case 8: return chains_launch_t<8, 256, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 4: return chains_launch_t<4, 512, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 8: return chains_launch_t<8, 384, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
     case 16: return chains_launch_t<16, 192, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
     default: return chains_launch_t<32, 96, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
     }

@@ -52,7 +52,7 @@ void sweep(int n) {
     if (chain_smem_bytes(P, T, S, 3) <= 227 * 1024)                                                       \
         std::printf("P=%2d n=%d T=%3d S=%2d smem=%6zu : %8.1f us\n", P, n, T, S, chain_smem_bytes(P, T, S, 3), \
                     1e3 * run<P, T, S>(s0, s1, s2, n, d, nch, out));
-    R(256, 3) R(192, 3) R(128, 4) R(96, 3) R(64, 4)
+    R(512, 3) R(384, 3) R(256, 4) R(256, 3) R(192, 3)
 #undef R
     cudaFree(s0); cudaFree(s1); cudaFree(s2); cudaFree(out); cudaFree(d);
 }
