@@ -382,11 +382,12 @@ cudaError_t solve_beta_launch(coopcg_gpu_ctx* ctx) {
 // ---- chain launcher ---------------------------------------------------------
 enum ChainPhase { kPhSetup = 0, kPhGram = 1, kPhBeta = 2, kPhFinal = 3 };
 
-template <int P, int T, int S>
+// NSRC_MAX: the most sources any launch of this instantiation streams
+template <int P, int T, int S, int NSRC_MAX = 3>
 cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
                             int nsrc, const int* stop) {
     auto kern = chain_kernel<P, T, S>;
-    const size_t smem_max = chain_smem_bytes(P, T, S, 3);
+    const size_t smem_max = chain_smem_bytes(P, T, S, NSRC_MAX);
     static bool attr_done[64] = {};
     const int dev = ctx->device & 63;
     if (!attr_done[dev]) {
@@ -404,13 +405,16 @@ cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, co
 
 // Rings (tools/probe/chain_kernel_probe.cu, n = 16384): 3 stages of the
 // longest tile that fits (per-tile overhead dominates shorter tiles):
-// P=4: 512 rows (93 us per phase vs 99 at 256); P=8: 384 (96.5 vs 98.6);
+// P=4: 512 rows (93 us per phase vs 99 at 256); P=8: 384 with three sources
+// (96.5 vs 98.6), 512 with at most two (the beta / setup / final phases);
 // P=16: 192 (105 vs 115 us at 4 x 128); P=32: 96 (127 vs 144 us at 4 x 64).
 cudaError_t chains_launch(coopcg_gpu_ctx* ctx, int phase, const double* s0, const double* s1, const double* s2,
                           int nsrc, const int* stop) {
     switch (ctx->P) {
     case 4: return chains_launch_t<4, 512, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
-    case 8: return chains_launch_t<8, 384, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
+    case 8:
+        return nsrc <= 2 ? chains_launch_t<8, 512, 3, 2>(ctx, phase, s0, s1, s2, nsrc, stop)
+                         : chains_launch_t<8, 384, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
     case 16: return chains_launch_t<16, 192, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
     default: return chains_launch_t<32, 96, 3>(ctx, phase, s0, s1, s2, nsrc, stop);
     }
