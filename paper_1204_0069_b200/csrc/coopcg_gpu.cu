@@ -342,7 +342,7 @@ cudaError_t fast_solve(coopcg_gpu_ctx* ctx, int mode) {
 
 AdConfig pick_ad_config(int n_loc, int P) {
     AdConfig c;
-    // Measured sweep (tools/probe/ad_probe.cu, profiles/): T=32, S=4 rings;
+    // Measured sweep (tools/probe/ad_probe.cu, profiles/; ring shapes: ad_T / ad_S);
     // P=4: 2 cols/thread (7.1 TB/s at n=16384), P=8: 4 (5.0 TB/s),
     // P=16/32: 4 cols x 2 rows (FP64-issue bound in exact mode, ~13 of 18 T instr/s).
     c.BR = (n_loc >= 148 * 64) ? 64 : 32;
