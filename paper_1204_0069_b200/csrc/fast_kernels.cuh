@@ -21,10 +21,7 @@ constexpr int kFastS = 4;     // ring stages
 
 // Fast A layout ("tiles"): panel q (kFastBR rows), k-tile t: a contiguous
 // [r][kk] block of kFastBR x kFastT doubles at ((q*ntiles + t)*BR + r)*T + kk.
-__host__ __device__ __forceinline__ size_t at_fast_idx(int ntiles, int k, int il) {
-    const int q = il / kFastBR, r = il % kFastBR, t = k / kFastT, kk = k % kFastT;
-    return ((static_cast<size_t>(q) * ntiles + t) * kFastBR + r) * kFastT + kk;
-}
+// (index map: a_idx in common.cuh, ALay::fast)
 
 __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
