@@ -3,9 +3,9 @@
 // The driver reproduces the reference's drive() loop (coopcg/solvers.hpp:
 // 259-283) on one CUDA stream: setup (stage_setup + setup_coordinator),
 // then per iteration
-//   ad_exact (Q = A D) -> chains (D^T Q, -R^T D, |D|^2) -> solve_alpha ->
-//   update (R, X | X then R = A X - b) -> chains (-R^T Q, |R|^2) ->
-//   solve_beta (+ record + convergence) -> direction (Dn = R + D beta^T,
+//   ad_exact (Q = A D) -> chains (D^T Q, -R^T D, |D|^2) -> alpha_update
+//   (alpha solve; R, X | X then R = A X - b) -> chains (-R^T Q, |R|^2) ->
+//   beta_direction (beta solve + record + convergence; Dn = R + D beta^T,
 //   Gram partials) -> rank_end (certificate / exact MGS, status, k++)
 // and finalize_trace.  The coordinator decisions live on the device (Ctl):
 // once a stop condition is reached every later kernel is a no-op, so the host
@@ -350,33 +350,78 @@ AdConfig pick_ad_config(int n_loc, int P) {
     return c;
 }
 
-// ---- the p x p solves (one warp, templated on P) ---------------------------
+// ---- the p x p solves fused into their elementwise consumers ----------------
+// Every CTA redoes the solve, so the grid must fit in one wave: one CTA per
+// step of kUpdTiles x 256 elements, at most (resident CTAs per SM) x SMs, and
+// for the direction pass at most nparts (the certificate sums one Gram
+// partial per CTA).
+template <typename K>
+int one_wave(K kern, int cap) {
+    int dev = 0, sms = 148, occ = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, 256, 0);
+    return std::max(1, std::min(cap, std::max(occ, 1) * sms));
+}
+static int blocks_of(int n, int P) { return (n * P + kUpdTiles * 256 - 1) / (kUpdTiles * 256); }
+
 template <int P>
-cudaError_t solve_alpha_launch_t(coopcg_gpu_ctx* ctx) {
-    return pdl_launch(solve_alpha_kernel<P>, dim3(1), dim3(32), 0, ctx->stream, ctx->small, ctx->ctl);
+cudaError_t alpha_update_launch_t(coopcg_gpu_ctx* ctx, const double* Q, const double* D, int mode) {
+    static const int wave = one_wave(alpha_update_kernel<P>, 1 << 30);
+    const int grid = std::min(wave, blocks_of(ctx->n, P));
+    return pdl_launch(alpha_update_kernel<P>, dim3(grid), dim3(256), 0, ctx->stream, ctx->R, ctx->X, Q, D, ctx->small,
+                      ctx->n, ctx->p, mode, ctx->ctl);
 }
 template <int P>
-cudaError_t solve_beta_launch_t(coopcg_gpu_ctx* ctx) {
-    return pdl_launch(solve_beta_kernel<P>, dim3(1), dim3(32), 0, ctx->stream, ctx->small, ctx->ctl, ctx->tr_norms,
-                      ctx->tr_minres, ctx->tr_wall, ctx->tr_capacity);
+int beta_direction_grid_t(const coopcg_gpu_ctx* ctx) {
+    static const int wave = one_wave(beta_direction_kernel<P>, kMaxParts);
+    return std::min({wave, ctx->nparts, blocks_of(ctx->n, P)});
 }
-cudaError_t solve_alpha_launch(coopcg_gpu_ctx* ctx) {
+template <int P>
+cudaError_t beta_direction_launch_t(coopcg_gpu_ctx* ctx, const double* D, double* Dn) {
+    return pdl_launch(beta_direction_kernel<P>, dim3(beta_direction_grid_t<P>(ctx)), dim3(256), 0, ctx->stream, ctx->R,
+                      D, Dn, ctx->small, ctx->n, ctx->p, ctx->partials, ctx->ctl, ctx->tr_norms, ctx->tr_minres,
+                      ctx->tr_wall, ctx->tr_capacity, ctx->algo == 2 ? 1 : 0);
+}
+// alpha solve + X (and R) update, iteration mode 0 (recurrence) / 1 (recompute)
+cudaError_t alpha_update_launch(coopcg_gpu_ctx* ctx, const double* Q, const double* D, int mode) {
     ++ctx->launches;
     switch (ctx->P) {
-    case 4: return solve_alpha_launch_t<4>(ctx);
-    case 8: return solve_alpha_launch_t<8>(ctx);
-    case 16: return solve_alpha_launch_t<16>(ctx);
-    default: return solve_alpha_launch_t<32>(ctx);
+    case 4: return alpha_update_launch_t<4>(ctx, Q, D, mode);
+    case 8: return alpha_update_launch_t<8>(ctx, Q, D, mode);
+    case 16: return alpha_update_launch_t<16>(ctx, Q, D, mode);
+    default: return alpha_update_launch_t<32>(ctx, Q, D, mode);
     }
 }
-cudaError_t solve_beta_launch(coopcg_gpu_ctx* ctx) {
+// beta solve + record + convergence, then Dn = R + D beta^T with Gram partials
+cudaError_t beta_direction_launch(coopcg_gpu_ctx* ctx, const double* D, double* Dn) {
     ++ctx->launches;
     switch (ctx->P) {
-    case 4: return solve_beta_launch_t<4>(ctx);
-    case 8: return solve_beta_launch_t<8>(ctx);
-    case 16: return solve_beta_launch_t<16>(ctx);
-    default: return solve_beta_launch_t<32>(ctx);
+    case 4: return beta_direction_launch_t<4>(ctx, D, Dn);
+    case 8: return beta_direction_launch_t<8>(ctx, D, Dn);
+    case 16: return beta_direction_launch_t<16>(ctx, D, Dn);
+    default: return beta_direction_launch_t<32>(ctx, D, Dn);
     }
+}
+// Exact-mode count of Gram partials (= the direction pass's grid).
+int exact_dgrid(const coopcg_gpu_ctx* ctx) {
+    switch (ctx->P) {
+    case 4: return beta_direction_grid_t<4>(ctx);
+    case 8: return beta_direction_grid_t<8>(ctx);
+    case 16: return beta_direction_grid_t<16>(ctx);
+    default: return beta_direction_grid_t<32>(ctx);
+    }
+}
+// Gram partials of an existing block D (setup D0, the rank entry point).
+cudaError_t gram_partials_launch(coopcg_gpu_ctx* ctx, const double* D, int grid, const int* stop) {
+    const int n = ctx->n, p = ctx->p;
+    switch (ctx->P) {
+    case 4: gram_partials_kernel<4><<<grid, 256, 0, ctx->stream>>>(D, n, p, ctx->partials, stop); break;
+    case 8: gram_partials_kernel<8><<<grid, 256, 0, ctx->stream>>>(D, n, p, ctx->partials, stop); break;
+    case 16: gram_partials_kernel<16><<<grid, 256, 0, ctx->stream>>>(D, n, p, ctx->partials, stop); break;
+    default: gram_partials_kernel<32><<<grid, 256, 0, ctx->stream>>>(D, n, p, ctx->partials, stop); break;
+    }
+    return cudaGetLastError();
 }
 
 // ---- chain launcher ---------------------------------------------------------
@@ -979,8 +1024,7 @@ static int mccg_restrict(coopcg_gpu_ctx* ctx, int kr, int* next_k) {
 }
 static int dgrid_of(const coopcg_gpu_ctx* ctx) {
     if (ctx->arith == COOPCG_ARITH_FAST) return ctx->f_ugrid;
-    const int rows_per_tile = 256 / ctx->P;
-    return std::min(ctx->nparts, (ctx->n + rows_per_tile - 1) / rows_per_tile);
+    return exact_dgrid(ctx);
 }
 
 // fast_rows over arbitrary (Qpart, kchunks, rows) -- the local row pass or a
@@ -1059,7 +1103,7 @@ static int setup_local(coopcg_gpu_ctx* ctx) {
 
 // D = R, norms, tolerance and rank checks (block_cg.hpp:139-144, solvers.hpp:55-100)
 static int setup_rest(coopcg_gpu_ctx* ctx) {
-    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    const int n = ctx->n, P = ctx->P;
     cudaStream_t st = ctx->stream;
     int* stop = &ctx->ctl->stop;
     const bool fast = ctx->arith == COOPCG_ARITH_FAST;
@@ -1075,8 +1119,8 @@ static int setup_rest(coopcg_gpu_ctx* ctx) {
     }
     LAUNCHED();
     const int dgrid = dgrid_of(ctx);
-    direction_kernel<<<dgrid, 256, 0, st>>>(nullptr, ctx->Dblk[0], nullptr, nullptr, n, p, P, ctx->partials, stop);
-    LAUNCHED();
+    CK(gram_partials_launch(ctx, ctx->Dblk[0], dgrid, stop));
+    ++ctx->launches;
     rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[0], ctx->V, n, ctx->ctl, 1,
                                                    fast ? ctx->small : nullptr);
     LAUNCHED();
@@ -1123,7 +1167,7 @@ static bool recompute_at(const coopcg_gpu_ctx* ctx, int k) {
 // R_loc = A_loc X - b (the caller exchanges R before iter_rest).
 static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
     double* Qk = q_of(ctx, k);
-    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    const int n = ctx->n, P = ctx->P;
     cudaStream_t st = ctx->stream;
     int* stop = &ctx->ctl->stop;
     double* D = ctx->Dblk[k & 1];
@@ -1131,10 +1175,7 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
     const bool rec = recompute_at(ctx, k);
     if (ctx->arith != COOPCG_ARITH_FAST) {
         CK(chains_launch(ctx, kPhGram, D, Qk, ctx->R, 3, stop));
-        CK(solve_alpha_launch(ctx));
-        pdl_launch(update_kernel, dim3(grid_for((size_t)n * P, 256)), dim3(256), 0, st, ctx->R, ctx->X, Qk, D, ctx->small, n, p, P,
-                                                                    rec ? 1 : 0, stop);
-        LAUNCHED();
+        CK(alpha_update_launch(ctx, Qk, D, rec ? 1 : 0));
         if (rec) CK(ad_launch(ctx, ctx->X, ctx->R, ctx->b, stop));
     } else {
         if (sharded(ctx))  // the four Gram partials over the full replicated blocks
@@ -1159,7 +1200,7 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
 // The rest of the iteration: beta, D', norms/record, rank check, k++.
 static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
     double* Qk = q_of(ctx, k);
-    const int n = ctx->n, p = ctx->p, P = ctx->P;
+    const int n = ctx->n, P = ctx->P;
     cudaStream_t st = ctx->stream;
     int* stop = &ctx->ctl->stop;
     double* D = ctx->Dblk[k & 1];
@@ -1168,10 +1209,7 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
     const bool fast = ctx->arith == COOPCG_ARITH_FAST;
     if (!fast) {
         CK(chains_launch(ctx, kPhBeta, ctx->R, Qk, nullptr, 2, stop));
-        CK(solve_beta_launch(ctx));
-        pdl_launch(direction_kernel, dim3(dgrid_of(ctx)), dim3(256), 0, st, ctx->R, D, Dn, ctx->small, n, p, P, ctx->partials, stop,
-                                                        ctx->algo == 2 ? 1 : 0);
-        LAUNCHED();
+        CK(beta_direction_launch(ctx, D, Dn));
     } else if (rec) {
         if (sharded(ctx))  // R^T Q and |R|^2 over the full replicated, recomputed R
             CK(fast_rows_any(ctx, ctx->R, 1, n, 0, ctx->R, nullptr, nullptr, nullptr, Qk, 1, stop));
@@ -1643,10 +1681,8 @@ int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D, double to
     CK(cudaMemcpyAsync(ctx->stage, D, sizeof(double) * (size_t)n * p, cudaMemcpyHostToDevice, st));
     colmajor_to_rowmajor_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->stage, ctx->Dblk[1], n, p, P);
     CKL();
-    const int rows_per_tile = 256 / P;
-    const int dgrid = std::min(ctx->nparts, (n + rows_per_tile - 1) / rows_per_tile);
-    direction_kernel<<<dgrid, 256, 0, st>>>(nullptr, ctx->Dblk[1], nullptr, nullptr, n, p, P, ctx->partials, nullptr);
-    CKL();
+    const int dgrid = exact_dgrid(ctx);
+    CK(gram_partials_launch(ctx, ctx->Dblk[1], dgrid, nullptr));
     rank_end_kernel<<<1, 1024, rank_smem(P), st>>>(ctx->partials, dgrid, ctx->Dblk[1], ctx->V, n, ctx->ctl, 2, nullptr);
     CKL();
     CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));

@@ -607,10 +607,19 @@ __device__ __forceinline__ void lu_solve_regs(const double (*lu)[P + 1], const i
     }
 }
 
-// stage_gram_finalize + stage_alpha (block_cg.hpp:165-218), one warp.
+// The two solves run inside the elementwise kernels that consume their
+// coefficients: warp 0 of every CTA recomputes the (tiny, deterministic) p x p
+// solve into shared memory while the other warps stage the CTA's first tile of
+// operands, so a solve costs its latency once, not a launch plus a ramp.  All
+// CTAs read the same inputs and run the same operation sequence, so they reach
+// the same coefficients and the same stop decision; CTA 0 ("leader") alone
+// writes the control block, the trace and the small-buffer copies.
+
+// stage_gram_finalize + stage_alpha (block_cg.hpp:165-218) on one warp.
+// alpha (row i = agent i) goes to coef[i * (P + 1) + j].  Returns false when
+// the iteration stops (stop already set, SPD violation, rank collapse).
 template <int P>
-__global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ small, Ctl* ctl) {
-    pdl_wait();
+__device__ bool alpha_solve_warp(double* __restrict__ small, Ctl* ctl, double* coef, bool leader) {
     __shared__ double lu[P][P + 1];
     __shared__ double rh[P][P + 1];
     __shared__ int perm[P];
@@ -631,7 +640,7 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
         }
         nsq = __ldcg(small + L.nsq_d() + lane);
     }
-    if (stop) return;
+    if (stop) return false;
     // M(i,j) = (raw(i,j) + raw(j,i)) / 2.0 (x * 0.5 is the same rounding)
     double m[P];
     double maxabs = 0.0, diag = 0.0;
@@ -659,23 +668,23 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
     // SPD guard (block_cg.hpp:196-202): nonpositive d_i^T A d_i with d_i != 0.
     const bool bad = (lane < p) && !(diag > 0.0) && (nsq > 0.0);
     if (__any_sync(0xffffffffu, bad)) {
-        if (lane == 0) {
+        if (leader && lane == 0) {
             ctl->err = 2;  // COOPCG_E_SPD_VIOLATION
             ctl->err_iter = ctl->k;
             ctl->stop = 1;
         }
-        return;
+        return false;
     }
     int pv;
     if (!lu_factor_regs<P>(m, pv, lane, p, floor)) {
-        if (lane == 0) {
+        if (leader && lane == 0) {
             // RankCollapse (solvers.hpp:117-123); steepest descent reports a
             // vanished gradient energy with r = 0 as Converged (solvers.hpp:588-594)
             ctl->status = (ctl->algo == 2) ? 0 : 1;
             if (ctl->algo == 2) ctl->converged_agent = 0;
             ctl->stop = 1;
         }
-        return;
+        return false;
     }
     if (lane < P) {
 #pragma unroll
@@ -687,22 +696,27 @@ __global__ void __launch_bounds__(32) solve_alpha_kernel(double* __restrict__ sm
         double x[P];
         lu_solve_regs<P>(lu, perm, p, rh[lane], x);
 #pragma unroll
-        for (int j = 0; j < P; ++j) small[L.alpha() + lane * P + j] = (j < p) ? x[j] : 0.0;
-        // keep the factorisation for the beta solve (same M, same pivots)
+        for (int j = 0; j < P; ++j) coef[lane * (P + 1) + j] = x[j];
+        if (leader) {
 #pragma unroll
-        for (int j = 0; j < P; ++j) ctl->lu[lane * P + j] = m[j];
-        ctl->perm[lane] = pv;
+            for (int j = 0; j < P; ++j) small[L.alpha() + lane * P + j] = (j < p) ? x[j] : 0.0;
+            // keep the factorisation for the beta solve (same M, same pivots)
+#pragma unroll
+            for (int j = 0; j < P; ++j) ctl->lu[lane * P + j] = m[j];
+            ctl->perm[lane] = pv;
+        }
     }
+    return true;
 }
 
 // stage_beta (block_cg.hpp:248-266) + the norms of stage_direction_and_norms
 // (:275-276) + the record / convergence part of end_of_iteration
-// (solvers.hpp:125-154).  One warp.
+// (solvers.hpp:125-154) on one warp.  beta goes to coef; returns false when
+// the iteration stops (stop already set, or an agent converged).
 template <int P>
-__global__ void __launch_bounds__(32)
-    solve_beta_kernel(double* __restrict__ small, Ctl* ctl, double* __restrict__ tr_norms,
-                      double* __restrict__ tr_minres, unsigned long long* __restrict__ tr_wall, int capacity) {
-    pdl_wait();
+__device__ bool beta_solve_warp(double* __restrict__ small, Ctl* ctl, double* coef, bool leader,
+                                double* __restrict__ tr_norms, double* __restrict__ tr_minres,
+                                unsigned long long* __restrict__ tr_wall, int capacity) {
     __shared__ double lu[P][P + 1];
     __shared__ double rh[P][P + 1];
     __shared__ int perm[P];
@@ -712,6 +726,7 @@ __global__ void __launch_bounds__(32)
     const int stop = __ldcg(&ctl->stop);
     const int p = __ldcg(&ctl->p);
     const int algo = __ldcg(&ctl->algo);
+    const double tol = __ldcg(&ctl->tol);
     double nsq = 0.0;
     if (lane < P) {
 #pragma unroll
@@ -722,7 +737,7 @@ __global__ void __launch_bounds__(32)
         perm[lane] = __ldcg(&ctl->perm[lane]);
         nsq = __ldcg(small + L.nsq_r() + lane);
     }
-    if (stop) return;
+    if (stop) return false;
     __syncwarp();
     if (lane < p) {
         double x[P];
@@ -733,110 +748,133 @@ __global__ void __launch_bounds__(32)
             lu_solve_regs<P>(lu, perm, p, rh[lane], x);
         }
 #pragma unroll
-        for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? x[j] : 0.0;
+        for (int j = 0; j < P; ++j) coef[lane * (P + 1) + j] = x[j];
         norms[lane] = __dsqrt_rn(nsq);
-        small[L.norm() + lane] = norms[lane];
+        if (leader) {
+#pragma unroll
+            for (int j = 0; j < P; ++j) small[L.beta() + lane * P + j] = (j < p) ? x[j] : 0.0;
+            small[L.norm() + lane] = norms[lane];
+        }
     }
     __syncwarp();
-    const int k = ctl->k;
-    const int p0 = ctl->p0;
-    if (k < capacity) {
-        // per-original-id record; ids that left the block (mccg) stay NaN
-        for (int j = lane; j < p0; j += 32) tr_norms[static_cast<size_t>(k) * p0 + j] = __longlong_as_double(0x7ff8000000000000ll);
-        __syncwarp();
-        if (lane < p) tr_norms[static_cast<size_t>(k) * p0 + ctl->ids[lane]] = norms[lane];
-    }
-    if (lane == 0) {
-        const unsigned long long now = globaltimer_ns();
-        double mn = norms[0];
-        int slot = -1;
-        const double tol = ctl->tol;
-        for (int j = 0; j < p; ++j) {
-            mn = (norms[j] < mn) ? norms[j] : mn;  // std::min (block_cg.hpp:297-303)
-            if (slot < 0 && norms[j] <= tol) slot = j;
-        }
+    // first agent at or below the tolerance (block_cg.hpp:297-303); every CTA
+    // computes it from the same norms
+    int slot = -1;
+    for (int j = 0; j < p; ++j)
+        if (slot < 0 && norms[j] <= tol) slot = j;
+    if (leader) {
+        const int k = ctl->k;
+        const int p0 = ctl->p0;
         if (k < capacity) {
-            tr_minres[k] = mn;
-            tr_wall[k] = now - ctl->t_last;
+            // per-original-id record; ids that left the block (mccg) stay NaN
+            for (int j = lane; j < p0; j += 32)
+                tr_norms[static_cast<size_t>(k) * p0 + j] = __longlong_as_double(0x7ff8000000000000ll);
+            __syncwarp();
+            if (lane < p) tr_norms[static_cast<size_t>(k) * p0 + ctl->ids[lane]] = norms[lane];
         }
-        ctl->t_last = now;
-        ctl->iterations = k + 1;
-        if (slot >= 0) {
-            ctl->status = 0;  // Converged
-            ctl->converged_agent = ctl->ids[slot];
-            ctl->stop = 1;
+        if (lane == 0) {
+            const unsigned long long now = globaltimer_ns();
+            double mn = norms[0];
+            for (int j = 0; j < p; ++j) mn = (norms[j] < mn) ? norms[j] : mn;  // std::min
+            if (k < capacity) {
+                tr_minres[k] = mn;
+                tr_wall[k] = now - ctl->t_last;
+            }
+            ctl->t_last = now;
+            ctl->iterations = k + 1;
+            if (slot >= 0) {
+                ctl->status = 0;  // Converged
+                ctl->converged_agent = ctl->ids[slot];
+                ctl->stop = 1;
+            }
         }
     }
+    return slot < 0;
 }
 
 // ---------------------------------------------------------------------------
 // (4) Elementwise block updates (kernels.hpp:36-49 combine_columns:
 // dest = base + sum_j coeff[j] * B(:, j), j ascending).  One thread per
-// (row, agent) element; the coefficient grid is staged with stride P+1.
+// (row, agent) element; a CTA step covers kUpdTiles tiles of 256 elements
+// (256 / P rows each) whose operands are staged in shared memory (coalesced:
+// thread t loads element t of each tile), so each thread keeps kUpdTiles
+// loads per operand in flight even when the solve's registers allow only one
+// CTA per SM.
 //
-// mode 0: R_i += sum_j alpha_ij Q_j ; X_i += sum_j alpha_ij D_j (recurrence)
-// mode 1: X_i += sum_j alpha_ij D_j only (recompute iterations: R is then
-//         recomputed as A X - b by ad_exact_kernel; block_cg.hpp:222-244)
-// mode 2: Dn_i = R_i + sum_j beta_ij D_j (block_cg.hpp:270-273), plus the
-//         fast (reordered) Gram partials Dn^T Dn used by the rank certificate.
+// alpha_update_kernel (alpha solve + block_cg.hpp:218-244):
+//   mode 0: R_i += sum_j alpha_ij Q_j ; X_i += sum_j alpha_ij D_j (recurrence)
+//   mode 1: X_i += sum_j alpha_ij D_j only (recompute iterations: R is then
+//           recomputed as A X - b by ad_exact_kernel; block_cg.hpp:222-244)
+constexpr int kUpdTiles = 4;
+template <int P>
 __global__ void __launch_bounds__(256)
-    update_kernel(double* __restrict__ R, double* __restrict__ X, const double* __restrict__ Q,
-                  const double* __restrict__ D, const double* __restrict__ small, int n, int p, int P,
-                  int mode, const int* __restrict__ stop) {
+    alpha_update_kernel(double* __restrict__ R, double* __restrict__ X, const double* __restrict__ Q,
+                        const double* __restrict__ D, double* __restrict__ small, int n, int p, int mode, Ctl* ctl) {
     pdl_wait();
-    if (*reinterpret_cast<volatile const int*>(stop)) return;
-    __shared__ double coef[kMaxP * (kMaxP + 1)];
-    const SmallLayout L{P};
-    for (int idx = threadIdx.x; idx < p * p; idx += blockDim.x) {
-        const int i = idx / p, j = idx % p;
-        coef[i * (kMaxP + 1) + j] = small[L.alpha() + i * P + j];
+    constexpr int U = kUpdTiles;
+    __shared__ double coef[P * (P + 1)];
+    __shared__ double tq[U * 256], td[U * 256];
+    __shared__ int go;
+    const int tid = threadIdx.x;
+    const int i = tid % P;
+    const int nel = n * P;
+    const int nblk = (nel + U * 256 - 1) / (U * 256);
+    double r[U], x[U];
+    auto stage = [&](int blk) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = (blk * U + u) * 256 + tid;
+            if (e < nel) {
+                if (mode == 0) {
+                    tq[u * 256 + tid] = Q[e];
+                    r[u] = R[e];
+                }
+                td[u * 256 + tid] = D[e];
+                x[u] = X[e];
+            }
+        }
+    };
+    int blk = blockIdx.x;
+    if (blk < nblk) stage(blk);
+    if (tid < 32) {
+        const bool ok = alpha_solve_warp<P>(small, ctl, coef, blockIdx.x == 0);
+        if (tid == 0) go = ok;
     }
     __syncthreads();
-    const size_t total = static_cast<size_t>(n) * P;
-    for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
-         e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int i = static_cast<int>(e % P);
-        if (i >= p) continue;
-        const size_t rowoff = e - i;
-        const double* a = coef + i * (kMaxP + 1);
-        if (mode == 0) {
-            double acc = R[e];
-            for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], Q[rowoff + j]);
-            R[e] = acc;
+    if (!go) return;
+    const double* a = coef + i * (P + 1);
+    const int rl = tid - i;  // first element of this thread's row in a tile
+    while (blk < nblk) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = (blk * U + u) * 256 + tid;
+            if (e < nel && i < p) {
+                if (mode == 0) {
+                    double acc = r[u];
+                    for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], tq[u * 256 + rl + j]);
+                    R[e] = acc;
+                }
+                double acc = x[u];
+                for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], td[u * 256 + rl + j]);
+                X[e] = acc;
+            }
         }
-        double acc = X[e];
-        for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], D[rowoff + j]);
-        X[e] = acc;
+        blk += gridDim.x;
+        if (blk >= nblk) break;
+        __syncthreads();
+        stage(blk);
+        __syncthreads();
     }
 }
 
-// Dn = R + D beta^T, plus per-CTA partial Grams of Dn for the rank
-// certificate (pairs i <= j < p).  Rows are processed in tiles of 256/P.
-__global__ void __launch_bounds__(256)
-    direction_kernel(const double* __restrict__ R, const double* __restrict__ D, double* __restrict__ Dn,
-                     const double* __restrict__ small, int n, int p, int P, double* __restrict__ partials,
-                     const int* __restrict__ stop, int sd_copy = 0) {
-    pdl_wait();
-    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
-    __shared__ double coef[kMaxP * (kMaxP + 1)];
-    __shared__ double tile[256];
-    const SmallLayout L{P};
-    const int tid = threadIdx.x;
-    const bool with_beta = (small != nullptr);
-    if (with_beta)
-        for (int idx = tid; idx < p * p; idx += blockDim.x) {
-            const int i = idx / p, j = idx % p;
-            coef[i * (kMaxP + 1) + j] = small[L.beta() + i * P + j];
-        }
-    const int npairs = p * (p + 1) / 2;
-    int pi[3], pj[3];
-    double part[3] = {0.0, 0.0, 0.0};
+// Pairs (i <= j < p) of the Gram Dn^T Dn handled by thread tid (up to 3).
+__device__ __forceinline__ void gram_pairs(int tid, int p, int (&pi)[3], int (&pj)[3]) {
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         int t = tid + q * 256;
         pi[q] = -1;
         pj[q] = -1;
-        if (t < npairs) {
+        if (t < p * (p + 1) / 2) {
             int i = 0;
             while (t >= p - i) {
                 t -= p - i;
@@ -846,45 +884,117 @@ __global__ void __launch_bounds__(256)
             pj[q] = i + t;
         }
     }
-    __syncthreads();
-    const int rows_per_tile = 256 / P;
-    const int ntiles = (n + rows_per_tile - 1) / rows_per_tile;
-    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const int row = t * rows_per_tile + tid / P;
-        const int i = tid % P;
-        double v = 0.0;
-        if (row < n) {
-            const size_t e = static_cast<size_t>(row) * P + i;
-            if (i < p) {
-                if (with_beta) {
-                    double acc = R[e];
-                    if (!sd_copy) {
-                        const double* a = coef + i * (kMaxP + 1);
-                        const size_t rowoff = e - i;
-                        for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], D[rowoff + j]);
-                    }
-                    v = acc;
-                    Dn[e] = v;
-                } else {
-                    v = D[e];
-                }
-            } else if (with_beta) {
-                Dn[e] = 0.0;
-            }
-        }
-        tile[tid] = v;
-        __syncthreads();
+}
+
+// Accumulate `rows` staged rows (tile[], row-major, stride P) into the pair
+// partials: fast (reordered, FMA) sums, used only by the rank certificate.
+template <int P>
+__device__ __forceinline__ void gram_tile(const double* tile, int rows, const int (&pi)[3], const int (&pj)[3],
+                                          double (&part)[3]) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            if (pi[q] >= 0) {
-                double s = part[q];
-                for (int rr = 0; rr < rows_per_tile; ++rr)
-                    s = fma(tile[rr * P + pi[q]], tile[rr * P + pj[q]], s);
-                part[q] = s;
+    for (int q = 0; q < 3; ++q) {
+        if (pi[q] >= 0) {
+            double s = part[q];
+            for (int rr = 0; rr < rows; ++rr) s = fma(tile[rr * P + pi[q]], tile[rr * P + pj[q]], s);
+            part[q] = s;
+        }
+    }
+}
+
+// beta solve + record, then Dn = R + D beta^T (block_cg.hpp:270-273; D' = R
+// for steepest descent, sd_copy) plus per-CTA partial Grams of Dn for the
+// rank certificate (rank_end_kernel sums gridDim.x partials).  Same staging
+// as alpha_update_kernel.
+template <int P>
+__global__ void __launch_bounds__(256)
+    beta_direction_kernel(const double* __restrict__ R, const double* __restrict__ D, double* __restrict__ Dn,
+                          double* __restrict__ small, int n, int p, double* __restrict__ partials, Ctl* ctl,
+                          double* __restrict__ tr_norms, double* __restrict__ tr_minres,
+                          unsigned long long* __restrict__ tr_wall, int capacity, int sd_copy) {
+    pdl_wait();
+    constexpr int U = kUpdTiles;
+    __shared__ double coef[P * (P + 1)];
+    __shared__ double td[U * 256], tile[U * 256];
+    __shared__ int go;
+    const int tid = threadIdx.x;
+    const int i = tid % P;
+    const int nel = n * P;
+    const int nblk = (nel + U * 256 - 1) / (U * 256);
+    double r[U];
+    auto stage = [&](int blk) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = (blk * U + u) * 256 + tid;
+            if (e < nel) {
+                r[u] = R[e];
+                td[u * 256 + tid] = D[e];
             }
         }
+    };
+    int blk = blockIdx.x;
+    if (blk < nblk) stage(blk);
+    if (tid < 32) {
+        const bool ok = beta_solve_warp<P>(small, ctl, coef, blockIdx.x == 0, tr_norms, tr_minres, tr_wall, capacity);
+        if (tid == 0) go = ok;
+    }
+    int pi[3], pj[3];
+    double part[3] = {0.0, 0.0, 0.0};
+    gram_pairs(tid, p, pi, pj);
+    __syncthreads();
+    if (!go) return;
+    const double* a = coef + i * (P + 1);
+    const int rl = tid - i;
+    while (blk < nblk) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = (blk * U + u) * 256 + tid;
+            double v = 0.0;
+            if (e < nel) {
+                if (i < p) {
+                    double acc = r[u];
+                    if (!sd_copy)
+                        for (int j = 0; j < p; ++j) acc = mac_exact(acc, a[j], td[u * 256 + rl + j]);
+                    v = acc;
+                }
+                Dn[e] = v;
+            }
+            tile[u * 256 + tid] = v;
+        }
+        __syncthreads();
+        gram_tile<P>(tile, U * (256 / P), pi, pj, part);
+        blk += gridDim.x;
+        if (blk < nblk) stage(blk);
         __syncthreads();
     }
+    const int npairs = p * (p + 1) / 2;
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+        if (pi[q] >= 0) partials[static_cast<size_t>(blockIdx.x) * npairs + tid + q * 256] = part[q];
+}
+
+// Partial Grams of an existing direction block (setup: D0 = R0; the
+// kernel-level rank entry point).  Same tiling and sums as above.
+template <int P>
+__global__ void __launch_bounds__(256)
+    gram_partials_kernel(const double* __restrict__ D, int n, int p, double* __restrict__ partials,
+                         const int* __restrict__ stop) {
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
+    __shared__ double tile[256];
+    const int tid = threadIdx.x;
+    const int i = tid % P;
+    constexpr int kRows = 256 / P;
+    const int ntiles = (n + kRows - 1) / kRows;
+    int pi[3], pj[3];
+    double part[3] = {0.0, 0.0, 0.0};
+    gram_pairs(tid, p, pi, pj);
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const int row = t * kRows + tid / P;
+        tile[tid] = (row < n && i < p) ? D[static_cast<size_t>(row) * P + i] : 0.0;
+        __syncthreads();
+        gram_tile<P>(tile, kRows, pi, pj, part);
+        __syncthreads();
+    }
+    const int npairs = p * (p + 1) / 2;
 #pragma unroll
     for (int q = 0; q < 3; ++q)
         if (pi[q] >= 0) partials[static_cast<size_t>(blockIdx.x) * npairs + tid + q * 256] = part[q];

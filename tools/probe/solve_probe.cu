@@ -1,6 +1,6 @@
 // Phase timing (clock64) of the one-warp alpha solve at P = 8: where do the
 // ~16k active cycles go?  Same code path as exact_kernels.cuh's
-// solve_alpha_kernel<8>, with timestamps between the phases.
+// alpha_solve_warp<8> (run by warp 0 of alpha_update_kernel), with timestamps between the phases.
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I../../paper_1204_0069_b200/csrc -o solve_probe solve_probe.cu
 #include <cstdio>
 #include <vector>
