@@ -198,17 +198,29 @@ size_t ad_smem() {
 // tools/probe/ad_probe.cu: -11% / -12% time at P = 16 / 32), 1 otherwise.
 template <int P>
 constexpr int ad_rpt() { return P >= 16 ? 2 : 1; }
+// the pipelined kernel (ad_exact_pipe_kernel) at P = 8 / BR = 128 and
+// P = 16 / BR = 64 (panel heights pick_ad_config chooses for large n)
+template <int P, int BR>
+constexpr bool ad_pipe() { return (P == 8 && BR == 128) || (P == 16 && BR == 64); }
+constexpr int kPipeT = 64, kPipeS = 3;
 
 template <int P, int CPT, int BR>
 cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop,
                         const PeerRows& peers) {
-    constexpr int RPT = ad_rpt<P>();
+    constexpr bool pipe = ad_pipe<P, BR>();
+    constexpr int RPT = pipe ? 2 : ad_rpt<P>();
     constexpr int T = ad_T<P>(), S = ad_S<P>();
     const bool push = peers.n > 0;
-    auto kern = (RPT == 1) ? (push ? ad_exact_kernel<P, CPT, BR, T, S, true> : ad_exact_kernel<P, CPT, BR, T, S, false>)
-                           : (push ? ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, true>
-                                   : ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, false>);
-    const size_t smem = ad_smem<P, CPT, BR>();
+    using Kern = void (*)(const double*, int, int, int, const double*, double*, const double*, int, const int*,
+                          PeerRows);
+    Kern kern;
+    if constexpr (pipe)
+        kern = push ? ad_exact_pipe_kernel<P, BR, kPipeT, kPipeS, true> : ad_exact_pipe_kernel<P, BR, kPipeT, kPipeS, false>;
+    else if constexpr (RPT == 1)
+        kern = push ? ad_exact_kernel<P, CPT, BR, T, S, true> : ad_exact_kernel<P, CPT, BR, T, S, false>;
+    else
+        kern = push ? ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, true> : ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, false>;
+    const size_t smem = pipe ? ad_pipe_smem(P, BR, kPipeT, kPipeS) : ad_smem<P, CPT, BR>();
     static bool attr_done[2][64] = {};
     const int dev = ctx->device & 63;
     if (!attr_done[push][dev]) {
@@ -229,6 +241,9 @@ cudaError_t ad_launch_br(coopcg_gpu_ctx* ctx, const double* src, double* dst, co
                          const PeerRows& peers) {
     switch (ctx->ad.BR) {
     case 32: return ad_launch_t<P, CPT, 32>(ctx, src, dst, b, stop, peers);
+    case 128:
+        if constexpr (P == 8) return ad_launch_t<P, CPT, 128>(ctx, src, dst, b, stop, peers);
+        return cudaErrorInvalidValue;
     default: return ad_launch_t<P, CPT, 64>(ctx, src, dst, b, stop, peers);
     }
 }
@@ -345,7 +360,10 @@ AdConfig pick_ad_config(int n_loc, int P) {
     // Measured sweep (tools/probe/ad_probe.cu, profiles/; ring shapes: ad_T / ad_S);
     // P=4: 2 cols/thread (7.1 TB/s at n=16384), P=8: 4 (5.0 TB/s),
     // P=16/32: 4 cols x 2 rows (FP64-issue bound in exact mode, ~13 of 18 T instr/s).
+    // Above one CTA per SM at BR = 64, P = 8 switches to 128-row panels for the
+    // pipelined kernel (tools/probe/ad_v3_probe.cu).
     c.BR = (n_loc >= 148 * 64) ? 64 : 32;
+    if (P == 8 && n_loc > 148 * 64) c.BR = 128;
     c.CPT = (P == 4) ? 2 : 4;  // with 2 rows per thread at P >= 16
     return c;
 }
@@ -657,7 +675,7 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         ctx->f_rgrid = std::min(rg, (ctx->n_loc + TR - 1) / TR);
         ctx->f_ugrid = std::min(rg, (n + TR - 1) / TR);
     } else {
-        ctx->brs = (ctx->ad.BR == 32) ? 5 : 6;
+        ctx->brs = (ctx->ad.BR == 32) ? 5 : (ctx->ad.BR == 64 ? 6 : 7);
         ctx->npanels = (ctx->n_loc + ctx->ad.BR - 1) / ctx->ad.BR;
         ctx->lay = ALay{0, ctx->brs, 0};
         ctx->ap_elems = (size_t)ctx->npanels * n * ctx->ad.BR;

@@ -351,6 +351,190 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
     if (PUSH) __threadfence_system();
 }
 
+// Pipelined variant (P = 8 / 16 at large n): thread = 2 rows x 4 columns,
+// operands software-pipelined two batches of U k-steps ahead in two register
+// sets (the chain kernel's scheme below), one straight-line body per tile, a
+// 3-stage ring (tile t+1 is waited for at the top of tile t).  Per warp and
+// k-step: one LDS.128 of A (two rows) and two broadcast LDS.128 of D feed 16
+// DMUL + 16 DADD, i.e. 8 shared-memory wavefronts per 256 MACs against 6 per
+// 128 in ad_exact_kernel, whose doubly-loaded SMs are shared-memory bound
+// (48 wavefronts vs 32 FP64-pipe cycles per k-step; profiles/).  One CTA of
+// 4 consumer warps per SM (P = 8 with BR = 128, P = 16 with BR = 64): a CTA's
+// warps map to SMSPs by warp index, so producer + 4 consumers keep one
+// consumer warp per SMSP (two co-resident 2-warp CTAs would stack theirs on
+// two SMSPs: 617 us in the probe).  tools/probe/ad_v3_probe.cu: n = 16384, P = 8:
+// 349 us vs 422 us; n = 65536, P = 16: 10.0 ms vs 11.1 ms.  Same arithmetic
+// and order as ad_exact_kernel.
+constexpr int kPipeU = 2;
+__host__ __device__ constexpr size_t ad_pipe_smem(int P, int BR, int T, int S) {
+    return static_cast<size_t>(S) * T * (BR + P) * sizeof(double) + 2 * S * sizeof(uint64_t);
+}
+template <int P, int BR, int T, int S, bool PUSH = false>
+__global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / 2, P / 4))
+    ad_exact_pipe_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
+                         const double* __restrict__ D, double* __restrict__ Y,
+                         const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers) {
+    pdl_wait();
+    constexpr int CPT = 4, RPT = 2, U = kPipeU;
+    constexpr int RG = BR / RPT;
+    constexpr int NW = ad_consumer_warps(RG, P / CPT);
+    constexpr int NBT = T / U;
+    static_assert(T % (2 * U) == 0, "even number of batches per tile");
+    static_assert((RG * (P / CPT)) % 32 == 0, "whole consumer warps");
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* As = reinterpret_cast<double*>(smem_raw);
+    double* Ds = As + S * T * BR;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Ds + S * T * P);
+    uint64_t* empty = full + S;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = (n + T - 1) / T;
+    const double* panel = Ap + static_cast<size_t>(blockIdx.x) * n * BR;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NW);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0) {
+        if (lane == 0) {
+            const uint64_t pol = l2_evict_first_policy();
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = 0; t < ntiles; ++t) {
+                if (t >= S) mbar_wait(&empty[s], ph ^ 1u);
+                const int k0 = t * T;
+                const int rows = min(T, n - k0);
+                mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
+                bulk_g2s_evict_first(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
+                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], pol);
+                bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
+                         &full[s]);
+                if (++s == S) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+    const int tid = threadIdx.x - 32;
+    const int rr = tid % RG, g = tid / RG;
+    const int aoff = rr * RPT, doff = g * CPT;
+    auto tile_wait = [&](int t) {
+        if (t < ntiles) mbar_wait(&full[t % S], static_cast<uint32_t>((t / S) & 1));
+    };
+    // batch j = k-steps j*U .. j*U+U-1: ring stage (j / NBT) % S.  Batches
+    // past the last tile read stale ring data that is multiplied, never added.
+    auto load = [&](int j, double (&a)[U][RPT], double (&d)[U][CPT]) {
+        const int st = (j / NBT) % S, kk = (j % NBT) * U;
+        const double* ab = As + st * T * BR + kk * BR + aoff;
+        const double* db = Ds + st * T * P + kk * P + doff;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const double2 av = *reinterpret_cast<const double2*>(ab + u * BR);
+            a[u][0] = av.x;
+            a[u][1] = av.y;
+#pragma unroll
+            for (int c = 0; c < CPT / 2; ++c) {
+                const double2 dv = reinterpret_cast<const double2*>(db + u * P)[c];
+                d[u][2 * c] = dv.x;
+                d[u][2 * c + 1] = dv.y;
+            }
+        }
+    };
+    double acc[RPT][CPT];
+#pragma unroll
+    for (int r = 0; r < RPT; ++r)
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) acc[r][c] = 0.0;
+    double pr[U][RPT][CPT];
+    double ae[U][RPT], ao[U][RPT], de[U][CPT], dq[U][CPT];
+    // add batch b, form batch b+1 (read set), load batch b+2 (write set)
+    auto step = [&](int b, const double (&ar)[U][RPT], const double (&dr)[U][CPT], double (&aw)[U][RPT],
+                    double (&dw)[U][CPT]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) {
+                    acc[r][c] = __dadd_rn(acc[r][c], pr[u][r][c]);
+                    pr[u][r][c] = __dmul_rn(ar[u][r], dr[u][c]);
+                }
+        load(b + 2, aw, dw);
+    };
+    tile_wait(0);
+    {
+        double a0[U][RPT], d0[U][CPT];
+        load(0, a0, d0);
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < RPT; ++r)
+#pragma unroll
+                for (int c = 0; c < CPT; ++c) pr[u][r][c] = __dmul_rn(a0[u][r], d0[u][c]);
+        load(1, ao, dq);
+    }
+    const int nb = (n + U - 1) / U;
+#pragma unroll 1
+    for (int t = 0; t < ntiles; ++t) {
+        tile_wait(t + 1);
+        const int b0 = t * NBT;
+        if ((t + 1) * T <= n) {
+#pragma unroll
+            for (int q = 0; q < NBT; q += 2) {
+                step(b0 + q, ao, dq, ae, de);
+                step(b0 + q + 1, ae, de, ao, dq);
+            }
+        } else {
+            // partial last tile: the batches that hold k-steps, the last masked
+            for (int q = 0; q < NBT && b0 + q < nb; ++q) {
+                const int b = b0 + q;
+                if (b == nb - 1) {
+                    const int rem = n - b * U;
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (u < rem)
+#pragma unroll
+                            for (int r = 0; r < RPT; ++r)
+#pragma unroll
+                                for (int c = 0; c < CPT; ++c) acc[r][c] = __dadd_rn(acc[r][c], pr[u][r][c]);
+                } else if (q & 1) {
+                    step(b, ae, de, ao, dq);
+                } else {
+                    step(b, ao, dq, ae, de);
+                }
+            }
+        }
+        __syncwarp();
+        mbar_arrive_lane0(&empty[t % S], lane);
+    }
+#pragma unroll
+    for (int r = 0; r < RPT; ++r) {
+        const int il = blockIdx.x * BR + aoff + r;
+        if (il < n_loc) {
+            const int row = row0 + il;
+            const double bb = (b != nullptr) ? b[row] : 0.0;
+            const size_t o = static_cast<size_t>(row) * P + doff;
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                double v = 0.0;
+                if (doff + c < p) v = (b != nullptr) ? __dsub_rn(acc[r][c], bb) : acc[r][c];
+                if (!PUSH) {
+                    Y[o + c] = v;
+                } else {
+                    for (int q = 0; q < peers.n; ++q) peers.dst[q][o + c] = v;
+                }
+            }
+        }
+    }
+    if (PUSH) __threadfence_system();
+}
+
 // ---------------------------------------------------------------------------
 // (2) Sequential dot-product chains: Gram rows, step right-hand sides and
 // norms (block_cg.hpp:153-160, :214-216, :262-264, :275-276; kernels.hpp:20-26).

@@ -121,9 +121,12 @@ def test_generated_problem_solves_like_oracle(m, po):
 
 
 # n >= 148 * 64 selects 64-row panels (and two rows per thread at P >= 16),
-# the A.D configurations of BASELINE configs 2-4 (coopcg_gpu.cu pick_ad_config).
+# n > 148 * 64 at P = 8 the 128-row panels of the pipelined kernel, as at
+# P = 16 (ad_exact_pipe_kernel): the A.D configurations of BASELINE configs
+# 2-4 (coopcg_gpu.cu pick_ad_config).  12345: partial last panel, partial
+# last k-tile and an odd k count (masked last batch).
 @pytest.mark.parametrize("n,p", [(1000, 3), (777, 17), (96, 32), (130, 1),
-                                 (9472, 8), (9473, 16), (9500, 24)])
+                                 (9472, 8), (9473, 8), (12345, 7), (9473, 16), (9500, 24)])
 def test_matvec_block_bitwise(m, po, n, p):
     rng = np.random.default_rng(n + p)
     A = po.gen_diagdom(n, 5) if n < 2000 else rng.uniform(-1, 1, (n, n))
@@ -136,6 +139,35 @@ def test_matvec_block_bitwise(m, po, n, p):
         ctx.set_A(A)
         out = ctx.matvec_block(D)
     assert np.array_equal(out, ref.T)
+
+
+def test_matvec_block_shard_rows_pipelined(m, po):
+    """A row shard large enough for the pipelined A.D (n_loc > 9472 at P = 8)
+    starting at a nonzero row offset, next to a small shard."""
+    n, p = 10007, 8
+    rng = np.random.default_rng(11)
+    A = rng.uniform(-1, 1, (n, n))
+    D = rng.uniform(-1, 1, (n, p))
+    ref = np.zeros((p, n))
+    Dc = np.ascontiguousarray(D.T)
+    po.oracle_lib().orc_matvec_block(A.ctypes.data, n, Dc.ctypes.data, p, ref.ctypes.data)
+    for r0, r1 in ((0, 407), (407, n)):
+        with m.GpuContext(n, p, row_begin=r0, row_end=r1) as ctx:
+            ctx.set_A(A[r0:r1])
+            out = ctx.matvec_block(D)
+        assert np.array_equal(out, ref.T[r0:r1])
+
+
+def test_pipelined_ad_solve_bitwise(m, po):
+    """A few exact iterations (with a residual recompute) on the pipelined A.D
+    path (n > 9472, p = 8): identical to the oracle."""
+    n, p = 9601, 8
+    A = po.gen_diagdom(n, 21)
+    b = po.gen_rhs(n, "uniform", 21)
+    X0 = po.gen_starts(n, p, 21)
+    ot = po.oracle_ccg(A, b, X0, tol=0.0, max_iters=6, recompute=4)
+    gt = m.ccg_solve(A, b, X0, m.SolveOptions(tol=0.0, max_iters=6, recompute_residual_every=4))
+    assert_same(gt, ot)
 
 
 def test_matvec_block_shard_rows(m, po):
