@@ -199,28 +199,40 @@ size_t ad_smem() {
 template <int P>
 constexpr int ad_rpt() { return P >= 16 ? 2 : 1; }
 // the pipelined kernel (ad_exact_pipe_kernel) at P = 8 / BR = 128 and
-// P = 16 / BR = 64 (panel heights pick_ad_config chooses for large n)
+// P = 16 / BR = 64 (panel heights pick_ad_config chooses for large n): 2 rows
+// x 4 columns per thread, 64-row tiles, 3 stages; at P = 4 / BR = 32 (small
+// n): 1 row x 2 columns, 128-row tiles, 4 stages (tools/probe/ad_v3_probe.cu)
 template <int P, int BR>
-constexpr bool ad_pipe() { return (P == 8 && BR == 128) || (P == 16 && BR == 64); }
-constexpr int kPipeT = 64, kPipeS = 3;
+constexpr bool ad_pipe() { return (P == 8 && BR == 128) || (P == 16 && BR == 64) || (P == 4 && BR == 32); }
+template <int P>
+constexpr int pipe_T() { return P == 4 ? 128 : 64; }
+template <int P>
+constexpr int pipe_S() { return P == 4 ? 4 : 3; }
+template <int P>
+constexpr int pipe_CPT() { return P == 4 ? 2 : 4; }
+template <int P>
+constexpr int pipe_RPT() { return P == 4 ? 1 : 2; }
 
 template <int P, int CPT, int BR>
 cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, const double* b, const int* stop,
                         const PeerRows& peers) {
     constexpr bool pipe = ad_pipe<P, BR>();
-    constexpr int RPT = pipe ? 2 : ad_rpt<P>();
+    constexpr int RPT = pipe ? pipe_RPT<P>() : ad_rpt<P>();
+    constexpr int KC = pipe ? pipe_CPT<P>() : CPT;  // columns per thread of the chosen kernel
+    constexpr int PT = pipe_T<P>(), PS = pipe_S<P>();
     constexpr int T = ad_T<P>(), S = ad_S<P>();
     const bool push = peers.n > 0;
     using Kern = void (*)(const double*, int, int, int, const double*, double*, const double*, int, const int*,
                           PeerRows);
     Kern kern;
     if constexpr (pipe)
-        kern = push ? ad_exact_pipe_kernel<P, BR, kPipeT, kPipeS, true> : ad_exact_pipe_kernel<P, BR, kPipeT, kPipeS, false>;
+        kern = push ? ad_exact_pipe_kernel<P, KC, RPT, BR, PT, PS, true>
+                    : ad_exact_pipe_kernel<P, KC, RPT, BR, PT, PS, false>;
     else if constexpr (RPT == 1)
         kern = push ? ad_exact_kernel<P, CPT, BR, T, S, true> : ad_exact_kernel<P, CPT, BR, T, S, false>;
     else
         kern = push ? ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, true> : ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, false>;
-    const size_t smem = pipe ? ad_pipe_smem(P, BR, kPipeT, kPipeS) : ad_smem<P, CPT, BR>();
+    const size_t smem = pipe ? ad_pipe_smem(P, BR, PT, PS) : ad_smem<P, CPT, BR>();
     static bool attr_done[2][64] = {};
     const int dev = ctx->device & 63;
     if (!attr_done[push][dev]) {
@@ -229,7 +241,7 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
         attr_done[push][dev] = true;
     }
     dim3 grid((ctx->n_loc + BR - 1) / BR);
-    dim3 block(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT));
+    dim3 block(32 + 32 * ad_consumer_warps(BR / RPT, P / KC));
     pdl_launch(kern, dim3(grid), dim3(block), smem, ctx->stream, ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop,
                peers);
     ++ctx->launches;

@@ -351,8 +351,9 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
     if (PUSH) __threadfence_system();
 }
 
-// Pipelined variant (P = 8 / 16 at large n): thread = 2 rows x 4 columns,
-// operands software-pipelined two batches of U k-steps ahead in two register
+// Pipelined variant (P = 8 / 16 at large n, P = 4 at small n): thread = RPT
+// rows x CPT columns, operands software-pipelined two batches of U k-steps
+// ahead in two register
 // sets (the chain kernel's scheme below), one straight-line body per tile, a
 // 3-stage ring (tile t+1 is waited for at the top of tile t).  Per warp and
 // k-step: one LDS.128 of A (two rows) and two broadcast LDS.128 of D feed 16
@@ -363,19 +364,23 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
 // warps map to SMSPs by warp index, so producer + 4 consumers keep one
 // consumer warp per SMSP (two co-resident 2-warp CTAs would stack theirs on
 // two SMSPs: 617 us in the probe).  tools/probe/ad_v3_probe.cu: n = 16384, P = 8:
-// 349 us vs 422 us; n = 65536, P = 16: 10.0 ms vs 11.1 ms.  Same arithmetic
-// and order as ad_exact_kernel.
-constexpr int kPipeU = 2;
+// 349 us vs 422 us; n = 65536, P = 16: 10.0 ms vs 11.1 ms.  At P = 4 and
+// n < 9472 (1 row x 2 columns, 32-row panels, 2 warps) a deeper ring keeps
+// enough bytes in flight for the latency-bound small case: n = 4096 34 us vs
+// 47 us.  Same arithmetic and order as ad_exact_kernel.
+constexpr int kPipeU = 2;  // k-steps per batch (deeper batches measured no better)
 __host__ __device__ constexpr size_t ad_pipe_smem(int P, int BR, int T, int S) {
     return static_cast<size_t>(S) * T * (BR + P) * sizeof(double) + 2 * S * sizeof(uint64_t);
 }
-template <int P, int BR, int T, int S, bool PUSH = false>
-__global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / 2, P / 4))
+template <int P, int CPT, int RPT, int BR, int T, int S, bool PUSH = false>
+__global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT))
     ad_exact_pipe_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                          const double* __restrict__ D, double* __restrict__ Y,
                          const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers) {
     pdl_wait();
-    constexpr int CPT = 4, RPT = 2, U = kPipeU;
+    constexpr int U = kPipeU;
+    static_assert(RPT == 1 || RPT == 2, "rows per thread");
+    static_assert(CPT % 2 == 0, "columns per thread come in double2 pairs");
     constexpr int RG = BR / RPT;
     constexpr int NW = ad_consumer_warps(RG, P / CPT);
     constexpr int NBT = T / U;
@@ -435,9 +440,13 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / 2, P / 4))
         const double* db = Ds + st * T * P + kk * P + doff;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const double2 av = *reinterpret_cast<const double2*>(ab + u * BR);
-            a[u][0] = av.x;
-            a[u][1] = av.y;
+            if constexpr (RPT == 2) {
+                const double2 av = *reinterpret_cast<const double2*>(ab + u * BR);
+                a[u][0] = av.x;
+                a[u][1] = av.y;
+            } else {
+                a[u][0] = ab[u * BR];
+            }
 #pragma unroll
             for (int c = 0; c < CPT / 2; ++c) {
                 const double2 dv = reinterpret_cast<const double2*>(db + u * P)[c];

@@ -322,6 +322,28 @@ int main(int argc, char** argv) {
         run<16, 4, 2, 64, 64, 3, 2>(n, "p16 rpt2 cpt4 4w");
         run<16, 4, 2, 112, 64, 3, 2>(n, "p16 rpt2 cpt4 7w");
         run<16, 8, 2, 128, 64, 3, 2>(n, "p16 rpt2 cpt8 4w");
+    } else if (mode == '4') {
+        for (int n : {4096, 1000}) {
+            setup<4>(n);
+            run_cur<4, 2, 32, 256, 3>(n);
+            run<4, 2, 1, 32, 128, 4, 2>(n, "p4 rpt1 cpt2 T128 S4 U2");
+            run<4, 2, 1, 32, 128, 4, 4>(n, "p4 rpt1 cpt2 T128 S4 U4");
+            run<4, 2, 1, 32, 128, 4, 8>(n, "p4 rpt1 cpt2 T128 S4 U8");
+            run<4, 2, 1, 16, 128, 4, 4>(n, "p4 rpt1 cpt2 BR16 T128 S4 U4");
+            run<4, 2, 1, 16, 128, 4, 8>(n, "p4 rpt1 cpt2 BR16 T128 S4 U8");
+            run<4, 4, 1, 32, 128, 4, 4>(n, "p4 rpt1 cpt4 1w T128 S4 U4");
+            run<4, 2, 1, 32, 64, 6, 4>(n, "p4 rpt1 cpt2 T64 S6 U4");
+        }
+    } else if (mode == 'c') {  // P = 8 at cfg-1-like small n: shapes for n <= 9472
+        for (int n : {4096, 9472}) {
+            setup<8>(n);
+            run_cur<8, 4, 32, 64, 2>(n);
+            run_cur<8, 4, 64, 64, 2>(n);
+            run<8, 4, 2, 64, 64, 3, 2>(n, "p8 rpt2 cpt4 BR64");
+            run<8, 4, 1, 32, 128, 4, 4>(n, "p8 rpt1 cpt4 BR32 T128 U4");
+            run<8, 2, 1, 32, 128, 4, 4>(n, "p8 rpt1 cpt2 BR32 T128 U4");
+            run<8, 4, 2, 128, 64, 3, 2>(n, "p8 rpt2 cpt4 BR128");
+        }
     } else {
         const int n = 131072;
         setup<32>(n);
