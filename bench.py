@@ -286,7 +286,9 @@ def _measure(m, torch, cfg, args, arith, dev):
         "clocks": clk.summary(),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": _profile_traffic(f"{cfg.name}_{arith}"),
-                     "kernel": "ad_exact_kernel (Q = A.D)" if arith == "exact" else "ad_fast_kernel (Q = A.D, DMMA)",
+                     "kernel": ("exact Q = A.D (ad_exact_pipe_kernel at the BASELINE configs with p <= 16, "
+                                "ad_exact_rpt_kernel at p = 32; DESIGN.md §5)") if arith == "exact"
+                     else "ad_fast_kernel (Q = A.D, DMMA)",
                      "ad_ms_per_launch": ad_ms, "ad_launches_timed": mv_n, "peak_source": peak_src,
                      "fp64": {"achieved_tflops": ad_flops / (ad_ms * 1e-3) / 1e12, "peak_tflops": fp64_peak,
                               "peak_source": "measured DFMA/DMMA probe (tools/probe/fp64_probe.cu)",
