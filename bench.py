@@ -260,12 +260,14 @@ def _measure(m, torch, cfg, args, arith, dev):
     torch.cuda.synchronize()
     e2e_iters = 0
     e2e_s = 0.0
-    for _ in range(args.steps):
-        flush_l2()
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        e2e_iters += e2e_once()  # returns after the final X and trace are on the host
-        e2e_s += time.perf_counter() - t0
+    # same host load as the timed loop (the clock sampler thread runs in both)
+    with ClockSampler(dev):
+        for _ in range(args.steps):
+            flush_l2()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_iters += e2e_once()  # returns after the final X and trace are on the host
+            e2e_s += time.perf_counter() - t0
     h2d = (n + n * p) * 8
     d2h = (n * p + tr.iterations * p) * 8
 
