@@ -103,6 +103,21 @@ __global__ void __launch_bounds__(kChainThreads)
                 xw[u] = b2z[xoff + u * P];
                 yw[u] = b2z[yoff + u * P];
             }
+        } else if (PIN == 3) {
+            // the add of (batch b, u) takes its operand through the product of
+            // (batch b+1, u): lo | (next.lo & kzero) == lo, so the DMUL of the
+            // next batch must be issued before this DADD (it cannot sink to its
+            // own consumer); the merge waits only where the DADD waits anyway
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const double nx = __dmul_rn(xr[u], yr[u]);
+                const double cur = __hiloint2double(__double2hiint(pr[u]),
+                                                    __double2loint(pr[u]) | (__double2loint(nx) & kzero));
+                acc = __dadd_rn(acc, cur);
+                pr[u] = nx;
+                xw[u] = b2[xoff + u * P];
+                yw[u] = b2[yoff + u * P];
+            }
         } else {
             // per step: load u of batch b+2 is addressed through product u
 #pragma unroll
@@ -213,10 +228,12 @@ int main() {
         cudaMemcpy(o1.data(), out, nch * 8, cudaMemcpyDeviceToHost);
         int bad = 0;
         for (int c = 0; c < nch; ++c) bad += o0[c] != o1[c];
-        float t2 = run<8, 384, 3, 2>(s[0], s[1], s[2], n, d, nch, out);
+        float t2 = run<8, 384, 3, 3>(s[0], s[1], s[2], n, d, nch, out);
         cudaMemcpy(o1.data(), out, nch * 8, cudaMemcpyDeviceToHost);
         for (int c = 0; c < nch; ++c) bad += o0[c] != o1[c];
-        std::printf("T=384 PIN=0: %.1f us   PIN=1: %.1f us   PIN=2: %.1f us   mismatches %d\n", t0 * 1e3, t1 * 1e3,
+        float t3 = run<8, 512, 3, 3>(s[0], s[1], s[2], n, d, nch, out);
+        std::printf("T=512 PIN=3: %.1f us\n", t3 * 1e3);
+        std::printf("T=384 PIN=0: %.1f us   PIN=1: %.1f us   PIN=3: %.1f us   mismatches %d\n", t0 * 1e3, t1 * 1e3,
                     t2 * 1e3, bad);
     }
     return 0;
