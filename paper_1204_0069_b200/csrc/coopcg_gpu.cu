@@ -98,6 +98,8 @@ struct coopcg_gpu_ctx {
     Ctl* ctl = nullptr;
     Ctl* ctl_host = nullptr;  // pinned snapshots [2]
     double* minres_host = nullptr;  // pinned [2][kChunkMax]: the chunk's recorded minres (enqueue sizing)
+    unsigned char* trace_host = nullptr;  // pinned staging of the trace copy-out (end_impl)
+    size_t trace_host_bytes = 0;
     ChainDesc* descs = nullptr;
     int desc_off[4] = {0, 0, 0, 0};
     int desc_cnt[4] = {0, 0, 0, 0};
@@ -567,6 +569,7 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaFree(ctx->stage);
     if (ctx->ctl_host) cudaFreeHost(ctx->ctl_host);
     if (ctx->minres_host) cudaFreeHost(ctx->minres_host);
+    if (ctx->trace_host) cudaFreeHost(ctx->trace_host);
     for (auto e : ctx->mv_ev) cudaEventDestroy(e);
     cudaEvent_t evs[] = {ctx->ev_run0,      ctx->ev_run1,      ctx->ev_loop0, ctx->ev_loop1,
                          ctx->ev_chunk[0], ctx->ev_chunk[1], ctx->ev_fork,  ctx->ev_join};
@@ -1298,7 +1301,9 @@ static int final_rest(coopcg_gpu_ctx* ctx) {
     return COOPCG_OK;
 }
 
-// Copy the trace out (after the stream is synchronised).
+// Copy the trace out: one read of the control block, then every trace piece
+// (and the final X) enqueued as async copies into pinned staging and a single
+// synchronisation (pageable cudaMemcpy calls cost a host round trip each).
 static int end_impl(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
     const int n = ctx->n, p = ctx->p, P = ctx->P;
     cudaStream_t st = ctx->stream;
@@ -1307,59 +1312,74 @@ static int end_impl(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
     const Ctl& fin = ctx->ctl_host[0];
     if (trace) {
         const int iters = fin.iterations;
+        const int p0 = ctx->p_orig;
         trace->status = fin.status;
         trace->converged_agent = fin.converged_agent;
         trace->iterations = iters;
         trace->exact_rank_checks = fin.exact_rank_checks;
         const int cap = std::min(iters, trace->capacity);
-        std::vector<unsigned long long> wall(std::max(iters, 1));
-        if (iters > 0)
-            CK(cudaMemcpy(wall.data(), ctx->tr_wall, sizeof(unsigned long long) * iters, cudaMemcpyDeviceToHost));
-        uint64_t total = 0;
-        for (int k = 0; k < iters; ++k) total += wall[k];
-        trace->loop_wall_ns = total;
-        if (cap > 0) {
-            if (trace->residual_norms)  // rows of p_orig, NaN for inactive agents
-                CK(cudaMemcpy(trace->residual_norms, ctx->tr_norms, sizeof(double) * (size_t)cap * ctx->p_orig,
-                              cudaMemcpyDeviceToHost));
-            if (trace->minres)
-                CK(cudaMemcpy(trace->minres, ctx->tr_minres, sizeof(double) * cap, cudaMemcpyDeviceToHost));
-            if (trace->wall_ns) std::memcpy(trace->wall_ns, wall.data(), sizeof(uint64_t) * cap);
+        // staging layout: wall[iters] | init[p0+1] | final[p+1] | norms[cap*p0] | minres[cap]
+        const size_t n_wall = (size_t)std::max(iters, 0), n_init = p0 + 1, n_fin = p + 1;
+        const size_t n_norm = (trace->residual_norms && cap > 0) ? (size_t)cap * p0 : 0;
+        const size_t n_min = (trace->minres && cap > 0) ? (size_t)cap : 0;
+        const size_t bytes = 8 * (n_wall + n_init + n_fin + n_norm + n_min);
+        if (bytes > ctx->trace_host_bytes) {
+            if (ctx->trace_host) cudaFreeHost(ctx->trace_host);
+            ctx->trace_host = nullptr;
+            ctx->trace_host_bytes = 0;
+            CK(cudaHostAlloc(&ctx->trace_host, bytes, cudaHostAllocDefault));
+            ctx->trace_host_bytes = bytes;
         }
-        std::vector<double> tmp(P + 1);
-        const int pi = ctx->p_orig;  // initial norms were recorded before any restriction
-        CK(cudaMemcpy(tmp.data(), ctx->init_norms, sizeof(double) * (pi + 1), cudaMemcpyDeviceToHost));
-        if (trace->initial_residual_norms) std::memcpy(trace->initial_residual_norms, tmp.data(), sizeof(double) * pi);
-        trace->initial_minres = tmp[pi];
-        CK(cudaMemcpy(tmp.data(), ctx->final_norms, sizeof(double) * (p + 1), cudaMemcpyDeviceToHost));
-        if (trace->final_residual_norms) std::memcpy(trace->final_residual_norms, tmp.data(), sizeof(double) * p);
-        trace->final_minres = tmp[p];
-        const int p0 = ctx->p_orig;
+        auto* wall = reinterpret_cast<unsigned long long*>(ctx->trace_host);
+        double* init = reinterpret_cast<double*>(wall + n_wall);
+        double* finl = init + n_init;
+        double* norms = finl + n_fin;
+        double* minres = norms + n_norm;
+        if (n_wall) CK(cudaMemcpyAsync(wall, ctx->tr_wall, 8 * n_wall, cudaMemcpyDeviceToHost, st));
+        // initial norms were recorded before any restriction (p_orig entries)
+        CK(cudaMemcpyAsync(init, ctx->init_norms, 8 * n_init, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(finl, ctx->final_norms, 8 * n_fin, cudaMemcpyDeviceToHost, st));
+        if (n_norm)  // rows of p_orig, NaN for inactive agents
+            CK(cudaMemcpyAsync(norms, ctx->tr_norms, 8 * n_norm, cudaMemcpyDeviceToHost, st));
+        if (n_min) CK(cudaMemcpyAsync(minres, ctx->tr_minres, 8 * n_min, cudaMemcpyDeviceToHost, st));
         const bool scatter = p != p0;
-        if (scatter) {  // mccg: per original agent id, NaN for dropped agents
-            std::vector<double> fr(p0, std::nan(""));
-            for (int j = 0; j < p; ++j) fr[ctx->ids[j]] = tmp[j];
-            if (trace->final_residual_norms) std::memcpy(trace->final_residual_norms, fr.data(), sizeof(double) * p0);
-        }
-        if (trace->active_agents)
-            for (int j = 0; j < p; ++j) trace->active_agents[j] = ctx->ids[j];
-        trace->n_active = p;
+        std::vector<double> xs;
         if (trace->final_x) {
             rowmajor_to_colmajor_kernel<<<grid_for((size_t)n * p, 256), 256, 0, st>>>(ctx->X, ctx->stage, n, p, P);
             CKL();
             if (!scatter) {
                 CK(cudaMemcpyAsync(trace->final_x, ctx->stage, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost,
                                    st));
-                CK(cudaStreamSynchronize(st));
             } else {
-                std::vector<double> xs((size_t)n * p);
+                xs.resize((size_t)n * p);
                 CK(cudaMemcpyAsync(xs.data(), ctx->stage, sizeof(double) * xs.size(), cudaMemcpyDeviceToHost, st));
-                CK(cudaStreamSynchronize(st));
-                for (size_t e = 0; e < (size_t)n * p0; ++e) trace->final_x[e] = std::nan("");
-                for (int j = 0; j < p; ++j)
-                    std::memcpy(trace->final_x + (size_t)ctx->ids[j] * n, xs.data() + (size_t)j * n,
-                                sizeof(double) * n);
             }
+        }
+        CK(cudaStreamSynchronize(st));
+        uint64_t total = 0;
+        for (int k = 0; k < iters; ++k) total += wall[k];
+        trace->loop_wall_ns = total;
+        if (n_norm) std::memcpy(trace->residual_norms, norms, 8 * n_norm);
+        if (n_min) std::memcpy(trace->minres, minres, 8 * n_min);
+        if (trace->wall_ns && cap > 0) std::memcpy(trace->wall_ns, wall, sizeof(uint64_t) * cap);
+        if (trace->initial_residual_norms) std::memcpy(trace->initial_residual_norms, init, sizeof(double) * p0);
+        trace->initial_minres = init[p0];
+        trace->final_minres = finl[p];
+        if (trace->final_residual_norms) {
+            if (!scatter) {
+                std::memcpy(trace->final_residual_norms, finl, sizeof(double) * p);
+            } else {  // mccg: per original agent id, NaN for dropped agents
+                for (int j = 0; j < p0; ++j) trace->final_residual_norms[j] = std::nan("");
+                for (int j = 0; j < p; ++j) trace->final_residual_norms[ctx->ids[j]] = finl[j];
+            }
+        }
+        if (trace->active_agents)
+            for (int j = 0; j < p; ++j) trace->active_agents[j] = ctx->ids[j];
+        trace->n_active = p;
+        if (trace->final_x && scatter) {
+            for (size_t e = 0; e < (size_t)n * p0; ++e) trace->final_x[e] = std::nan("");
+            for (int j = 0; j < p; ++j)
+                std::memcpy(trace->final_x + (size_t)ctx->ids[j] * n, xs.data() + (size_t)j * n, sizeof(double) * n);
         }
     }
     if (ctx->host_err) return fail(ctx, ctx->host_err, "%s", ctx->host_err_msg.c_str());
@@ -1388,10 +1408,10 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     } async_off{ctx};
 
     // ---- main loop, enqueued in chunks; device-side stop makes extras no-ops ----
-    // One host read after setup (the setup coordinator may already stop).
-    CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    bool stopped = ctx->ctl_host[0].stop != 0;
+    // No host read after setup: a stop raised by the setup coordinator turns
+    // the first chunk into no-ops and its snapshot ends the loop (mccg reads
+    // the control block in mccg_setup already).
+    bool stopped = false;
     int k_host = 0;
     int chunk_id = 0;
     double mv_total = 0.0;
