@@ -59,8 +59,11 @@ enum coopcg_status {
  * tree reductions, Cholesky) for the roofline. */
 enum coopcg_arith { COOPCG_ARITH_EXACT = 0, COOPCG_ARITH_FAST = 1 };
 
-/* On-device matrix generators. */
-enum coopcg_matrix_kind { COOPCG_MATRIX_DIAGDOM = 0, COOPCG_MATRIX_HOUSEHOLDER = 1 };
+/* On-device matrix generators.  RANDOM_SPD is the reference's
+ * own generator random_spd(n, cond = kappa, seed) (problem.hpp:118-152:
+ * Haar-orthogonal U by modified Gram-Schmidt, A = (U Lambda) U^T, SpdMatrix
+ * symmetrisation), bit-identical to it (m is ignored). */
+enum coopcg_matrix_kind { COOPCG_MATRIX_DIAGDOM = 0, COOPCG_MATRIX_HOUSEHOLDER = 1, COOPCG_MATRIX_RANDOM_SPD = 2 };
 enum coopcg_vector_kind { COOPCG_VEC_UNIFORM = 0, COOPCG_VEC_NORMAL = 1 };
 
 /* SolveOptions<double> (trace.hpp:74-88). keep_history / x_star are not
@@ -144,6 +147,12 @@ int coopcg_gen_starts(int n, int p, uint64_t seed, double* X0_colmajor);
  * the spectrum lambda (n). */
 int coopcg_gen_householder_factors(int n, int m, double kappa, uint64_t seed, double* V,
                                    double* lambda);
+
+/* Host parts of the reference's make_problem<double> (problem.hpp:219-230):
+ * the spectrum of random_spd_with_spectrum (problem.hpp:125-139) and
+ * random_rhs_and_starts (problem.hpp:187-200: b and X0 uniform on [-10, 10]). */
+int coopcg_gen_random_spd_spectrum(int n, double cond, uint64_t seed, double* lambda);
+int coopcg_gen_reference_rhs_starts(int n, int p, uint64_t seed, double* b, double* X0_colmajor);
 
 /* Upload b (n) and X0 (n x p column-major) into the context. */
 int coopcg_gpu_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0_colmajor);

@@ -109,6 +109,7 @@ def ref_lib() -> C.CDLL:
         lib.ref_sd_solve.argtypes = lib.ref_cg_solve.argtypes
         lib.ref_make_problem.argtypes = [C.c_int, C.c_int, C.c_double, C.c_ulonglong,
                                          C.c_void_p, C.c_void_p, C.c_void_p]
+        lib.ref_random_spd.argtypes = [C.c_int, C.c_double, C.c_ulonglong, C.c_void_p, C.c_void_p]
         lib.ref_matvec_block.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_gram.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_solve_small.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
@@ -192,6 +193,15 @@ def ref_cg(A, b, x0, tol=0.0, max_iters=-1, recompute=-1, algo="cg") -> Trace:
     o = _opts(tol, max_iters, recompute, 1e-10)
     fn = ref_lib().ref_cg_solve if algo == "cg" else ref_lib().ref_sd_solve
     return _run(fn, n, 1, cap, n, A.ctypes.data, b.ctypes.data, x0.ctypes.data, C.byref(o))
+
+
+def ref_random_spd(n, cond, seed):
+    """The reference's random_spd_with_spectrum: (A row-major, spectrum)."""
+    A = np.zeros((n, n))
+    lam = np.zeros(n)
+    if ref_lib().ref_random_spd(n, cond, seed, A.ctypes.data, lam.ctypes.data) != 0:
+        raise RuntimeError("ref_random_spd failed")
+    return A, lam
 
 
 def ref_make_problem(n, p, cond, seed):

@@ -185,6 +185,18 @@ int ref_make_problem(int n, int p, double cond, unsigned long long seed, double*
     }
 }
 
+// random_spd_with_spectrum(n, cond, seed) (problem.hpp:118-152): A and the spectrum.
+int ref_random_spd(int n, double cond, unsigned long long seed, double* A, double* lambda) {
+    try {
+        auto gen = random_spd_with_spectrum(n, cond, seed);
+        std::copy(gen.A.entries().begin(), gen.A.entries().end(), A);
+        std::copy(gen.spectrum.begin(), gen.spectrum.end(), lambda);
+        return 0;
+    } catch (...) {
+        return 1;
+    }
+}
+
 void ref_matvec_block(int n, int p, const double* A, const double* D, double* out) {
     auto Am = make_A(n, A);
     DenseBlock<double> d(n, p);

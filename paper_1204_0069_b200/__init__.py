@@ -22,9 +22,11 @@ from .solver import (  # noqa: F401
     cg_solve,
     steepest_descent_solve,
     gen_householder_factors,
+    gen_random_spd_spectrum,
+    gen_reference_rhs_starts,
     gen_rhs,
     gen_starts,
     iteration_mults,
     library_version,
 )
-from .configs import CONFIGS, make_problem_on_device  # noqa: F401
+from .configs import CONFIGS, make_problem_on_device, make_reference_problem_on_device  # noqa: F401

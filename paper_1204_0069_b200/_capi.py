@@ -55,6 +55,8 @@ SIGNATURES = [
     ("coopcg_gen_rhs", _I, [_I, _I, C.c_uint64, _VP]),
     ("coopcg_gen_starts", _I, [_I, _I, C.c_uint64, _VP]),
     ("coopcg_gen_householder_factors", _I, [_I, _I, C.c_double, C.c_uint64, _VP, _VP]),
+    ("coopcg_gen_random_spd_spectrum", _I, [_I, C.c_double, C.c_uint64, _VP]),
+    ("coopcg_gen_reference_rhs_starts", _I, [_I, _I, C.c_uint64, _VP, _VP]),
     ("coopcg_gpu_upload", _I, [_VP, _VP, _VP]),
     ("coopcg_gpu_run", _I, [_VP, C.POINTER(coopcg_opts), C.POINTER(coopcg_trace)]),
     ("coopcg_gpu_solve", _I, [_VP, _VP, _VP, C.POINTER(coopcg_opts), C.POINTER(coopcg_trace)]),

@@ -15,8 +15,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIBDIR, "libcoopcg_gpu.so")
-SOURCES = ["coopcg_gpu.cu"]
-DEPS = ["coopcg_gpu.cu", "common.cuh", "exact_kernels.cuh", "gen_kernels.cuh", "fast_kernels.cuh"]
+SOURCES = ["coopcg_gpu.cu", "refgen.cu"]
+DEPS = ["coopcg_gpu.cu", "common.cuh", "exact_kernels.cuh", "gen_kernels.cuh", "fast_kernels.cuh", "refgen.cu",
+        "host_rng.h"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

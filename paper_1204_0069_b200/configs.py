@@ -13,7 +13,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from .solver import GpuContext, SolveOptions, gen_rhs, gen_starts
+from .solver import GpuContext, SolveOptions, gen_reference_rhs_starts, gen_rhs, gen_starts
 
 
 @dataclass(frozen=True)
@@ -68,3 +68,12 @@ def make_problem_on_device(ctx: GpuContext, cfg: Config):
     ctx.gen_A(cfg.matrix, cfg.seed, cfg.reflectors, cfg.kappa)
     b, X0 = host_inputs(cfg, ctx.n, ctx.p)
     return b, X0, solve_options(cfg, b)
+
+
+def make_reference_problem_on_device(ctx: GpuContext, cond: float, seed: int):
+    """The reference's make_problem<double>(ProblemSpec{n, p, cond, seed})
+    (problem.hpp:219-230) with A generated on ctx's device: A = random_spd(n,
+    cond, seed) bit for bit, b / X0 = random_rhs_and_starts (host).  Returns
+    (b, X0) for ccg_solve's default options."""
+    ctx.gen_A("random_spd", seed, 0, cond)
+    return gen_reference_rhs_starts(ctx.n, ctx.p, seed)

@@ -31,6 +31,12 @@
 
 using namespace coopcg_gpu;
 
+namespace coopcg_gpu {
+// refgen.cu: the reference's random_spd (problem.hpp:118-152) on the device
+int refgen_random_spd(double* At, ALay L, size_t ap_elems, int n, double cond, uint64_t seed, cudaStream_t st,
+                      std::string& msg);
+}  // namespace coopcg_gpu
+
 namespace {
 
 // A.D ring shape (rows of k per stage x stages), tools/probe/ad_probe.cu at the
@@ -875,6 +881,11 @@ int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double
         cudaFree(dl);
         cudaFree(dw);
         cudaFree(dt);
+    } else if (kind == COOPCG_MATRIX_RANDOM_SPD) {
+        if (ctx->n_loc != n) return fail(ctx, COOPCG_E_INVALID, "random_spd generation needs the full matrix");
+        std::string msg;
+        if (int rc = refgen_random_spd(ctx->At, ctx->lay, ctx->ap_elems, n, kappa, seed, ctx->stream, msg))
+            return fail(ctx, rc, "%s", msg.c_str());
     } else {
         return fail(ctx, COOPCG_E_INVALID, "unknown matrix kind %d", kind);
     }

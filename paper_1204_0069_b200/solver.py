@@ -200,7 +200,10 @@ class GpuContext:
         _check(self._h, _capi.lib().coopcg_gpu_set_A(self._h, A_rows.ctypes.data))
 
     def gen_A(self, kind: str, seed: int, m: int = 0, kappa: float = 1.0) -> None:
-        k = {"diagdom": 0, "householder": 1}[kind]
+        """Generate A on the device: "diagdom" / "householder" (the BASELINE
+        generators) or "random_spd" (the reference's own
+        random_spd(n, cond=kappa, seed), problem.hpp:118-152, bit-identical)."""
+        k = {"diagdom": 0, "householder": 1, "random_spd": 2}[kind]
         _check(self._h, _capi.lib().coopcg_gpu_gen_A(self._h, k, seed, m, kappa))
 
     def get_A(self) -> np.ndarray:
@@ -404,6 +407,21 @@ def gen_starts(n: int, p: int, seed: int) -> np.ndarray:
     X0c = np.zeros((p, n))
     _check(None, _capi.lib().coopcg_gen_starts(n, p, seed, X0c.ctypes.data))
     return X0c.T.copy()
+
+
+def gen_random_spd_spectrum(n: int, cond: float, seed: int) -> np.ndarray:
+    """The spectrum of random_spd_with_spectrum (problem.hpp:125-139)."""
+    lam = np.zeros(n)
+    _check(None, _capi.lib().coopcg_gen_random_spd_spectrum(n, cond, seed, lam.ctypes.data))
+    return lam
+
+
+def gen_reference_rhs_starts(n: int, p: int, seed: int):
+    """random_rhs_and_starts<double> (problem.hpp:187-200): b, X0 ~ U[-10, 10]."""
+    b = np.zeros(n)
+    X0c = np.zeros((p, n))
+    _check(None, _capi.lib().coopcg_gen_reference_rhs_starts(n, p, seed, b.ctypes.data, X0c.ctypes.data))
+    return b, X0c.T.copy()
 
 
 def gen_householder_factors(n: int, m: int, kappa: float, seed: int):
