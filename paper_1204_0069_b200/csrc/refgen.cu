@@ -87,26 +87,18 @@ __global__ void __launch_bounds__(512) mgs_norm_kernel(double* __restrict__ W, i
     if (threadIdx.x == 0) {
         double acc = 0.0;
         int r = 0;
-        if (!pg) {  // shared memory: 16 squares per batch, the next batch in flight
+        if (!pg) {  // shared memory, 16 squares per batch (8.8 cycles/step, profiles/r01_probe_chain_split.txt)
             const double2* p2 = reinterpret_cast<const double2*>(sq);
             const int nb = n / 16;
-            double2 cur[8], nxt[8];
-            if (nb > 0) {
-#pragma unroll
-                for (int u = 0; u < 8; ++u) cur[u] = p2[u];
-            }
             for (int b = 0; b < nb; ++b) {
-                if (b + 1 < nb) {
+                double2 v[8];
 #pragma unroll
-                    for (int u = 0; u < 8; ++u) nxt[u] = p2[(b + 1) * 8 + u];
-                }
+                for (int u = 0; u < 8; ++u) v[u] = p2[b * 8 + u];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) {
-                    acc = __dadd_rn(acc, cur[u].x);
-                    acc = __dadd_rn(acc, cur[u].y);
+                    acc = __dadd_rn(acc, v[u].x);
+                    acc = __dadd_rn(acc, v[u].y);
                 }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) cur[u] = nxt[u];
             }
             r = nb * 16;
         }
