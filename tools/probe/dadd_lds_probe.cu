@@ -45,6 +45,34 @@ __global__ void k(double* out, long long* cyc) {
                 acc = __dadd_rn(acc, v[u].y);
             }
         }
+    } else if (V == 6 || V == 7) {
+        // products formed one loop iteration ahead (loop-carried registers, so
+        // ptxas cannot sink the DMULs next to their DADDs); V7 also carries
+        // the operands one more iteration ahead
+        double pr[U], xa[U], ya[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) pr[u] = __dmul_rn(sm[u], sm[u + 1 + (lane & 1)]);
+        if (V == 7) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) { xa[u] = sm[U + u]; ya[u] = sm[U + u + 1 + (lane & 1)]; }
+        }
+#pragma unroll 1
+        for (int b = 0; b < N / U - 2; ++b) {
+            double np[U];
+            if (V == 6) {
+#pragma unroll
+                for (int u = 0; u < U; ++u) np[u] = __dmul_rn(sm[(b + 1) * U + u], sm[(b + 1) * U + u + 1 + (lane & 1)]);
+            } else {
+#pragma unroll
+                for (int u = 0; u < U; ++u) np[u] = __dmul_rn(xa[u], ya[u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u) { xa[u] = sm[(b + 2) * U + u]; ya[u] = sm[(b + 2) * U + u + 1 + (lane & 1)]; }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc = __dadd_rn(acc, pr[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u) pr[u] = np[u];
+        }
     } else if (V == 3) {
         for (int b = 0; b < N / U; ++b) {
             double v[U];
@@ -65,9 +93,10 @@ int main() {
     cudaMalloc(&out, 1024 * 8);
     cudaMalloc(&cyc, 8);
     const char* names[] = {"register addend", "LDS batch of 16", "LDS.128 batch", "DMUL of LDS operands",
-                           "LDS batch + syncwarp", "LDS batch, bar.sync with a 2nd warp"};
+                           "LDS batch + syncwarp", "LDS batch, bar.sync with a 2nd warp",
+                           "DMUL products one iteration ahead", "... + operands two iterations ahead"};
     for (int rep = 0; rep < 2; ++rep) {
-        for (int v = 0; v < 6; ++v) {
+        for (int v = 0; v < 8; ++v) {
             long long h = 0;
             switch (v) {
             case 0: k<0><<<1, 32>>>(out, cyc); break;
@@ -76,6 +105,8 @@ int main() {
             case 3: k<3><<<1, 32>>>(out, cyc); break;
             case 4: k<4><<<1, 32>>>(out, cyc); break;
             case 5: k<5><<<1, 64>>>(out, cyc); break;
+            case 6: k<6><<<1, 32>>>(out, cyc); break;
+            case 7: k<7><<<1, 32>>>(out, cyc); break;
             }
             cudaMemcpy(&h, cyc, 8, cudaMemcpyDeviceToHost);
             if (rep) printf("%-38s %.2f cycles/step\n", names[v], (double)h / N);
