@@ -48,13 +48,11 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 
 // Column-block layout of the Gram-Schmidt working matrix W (n x n, np = n
 // rounded up to 32): block jb holds columns 32 jb .. 32 jb + 31 for all np
-// rows, row-major inside the block, so a 32-row x 32-column tile is one
-// contiguous 8 KB run (one bulk copy) and column t is a 256-byte stride.
-// Consecutive blocks are kWcbPad doubles (9472 B = 37 x 256 B) further apart
-// than np rows: every P CTA streams its own block at the same row position,
-// and with a power-of-two block stride those ~100 concurrent streams land on
-// the same HBM channels (measured 6.5 GB/s per CTA at n = 4096).
-constexpr int kWcbPad = 37 * 32;
+// rows, row-major inside the block, so a P stage (128 rows x 32 columns) is
+// one contiguous 32 KB run (one bulk copy) and column t is a 256-byte stride.
+// (A 9.5 KB gap between blocks, tried against HBM channel camping of the
+// ~100 concurrent block streams, changed nothing: kWcbPad = 0.)
+constexpr int kWcbPad = 0;
 __host__ __device__ __forceinline__ size_t wcb_stride(int np) { return static_cast<size_t>(np) * 32 + kWcbPad; }
 __host__ __device__ __forceinline__ size_t wcb(int np, int r, int j) {
     return static_cast<size_t>(j >> 5) * wcb_stride(np) + (static_cast<size_t>(r) << 5) + static_cast<size_t>(j & 31);
