@@ -18,8 +18,8 @@
 // so column j sees exactly the reference's operation sequence.  W (the
 // Gaussian sample, overwritten by U) is stored in 32-column blocks (wcb), so
 // a P warp's 32 columns x 128 rows are one 32 KB bulk copy through a 6-stage
-// ring.  U Lambda U^T is an n^3 product with a
-// sequential k-chain per entry (acc += (u_ik * l_k) * u_jk, k ascending).
+// ring.  U Lambda U^T is an n^3 product with a sequential k-chain per entry
+// (acc += (u_ik * l_k) * u_jk, k ascending).
 // The Gaussians come from glibc log/cos on the host (CUDA's are not
 // bit-identical to glibc) and are uploaded once, like the Householder vectors
 // of the BASELINE generator.
@@ -63,7 +63,7 @@ __host__ __device__ __forceinline__ size_t wcb(int np, int r, int j) {
 // W is in the column-block layout (wcb); u vectors are zero-padded to np rows.
 // All threads form v (kept in uout) and the squares (shared memory, or the
 // global scratch pg for n > kNormSmemMaxN); thread 0 then runs the one
-// sequential chain over the squares with loads a batch ahead.
+// sequential chain over the squares in 16-step batches.
 __global__ void __launch_bounds__(512) mgs_norm_kernel(double* __restrict__ W, int n, int np, int t,
                                                         const double* __restrict__ coef,
                                                         const double* __restrict__ uprev, double* __restrict__ uout,
