@@ -187,6 +187,11 @@ int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D_colmajor, 
  *          if recompute_at(k): <all-gather R rows>;  ITER_REST(k);
  *          (poll coopcg_gpu_state now and then; after a stop, phases are no-ops)
  *   FINAL_LOCAL; <all-gather S rows>; FINAL_REST; end.
+ * mccg_solve (opts.algo = 1) adds MCCG_SETUP right after SETUP_REST, and
+ * after a polled stop a call to coopcg_gpu_mccg_resume: when the stop was a
+ * rank drop it restricts the agents (solvers.hpp:156-175; every rank holds
+ * the same replicated blocks, so every rank restricts identically) and
+ * returns the iteration to continue from, else -1. 
  * A "local" phase writes only this context's rows of the named block;
  * coopcg_gpu_block returns the device pointer (row-major, leading dimension
  * `ld` doubles) for the exchange.  All work is ordered on the context stream
@@ -194,7 +199,8 @@ int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D_colmajor, 
 enum coopcg_phase {
     COOPCG_PH_SETUP_LOCAL = 0, COOPCG_PH_SETUP_REST = 1,
     COOPCG_PH_ITER_LOCAL = 2, COOPCG_PH_ITER_MID = 3, COOPCG_PH_ITER_REST = 4,
-    COOPCG_PH_FINAL_LOCAL = 5, COOPCG_PH_FINAL_REST = 6
+    COOPCG_PH_FINAL_LOCAL = 5, COOPCG_PH_FINAL_REST = 6,
+    COOPCG_PH_MCCG_SETUP = 7  /* mccg: setup_coordinator's restriction (solvers.hpp:63-91) */
 };
 enum coopcg_block { COOPCG_BLOCK_X = 0, COOPCG_BLOCK_R = 1, COOPCG_BLOCK_D = 2, COOPCG_BLOCK_Q = 3, COOPCG_BLOCK_S = 4 };
 int coopcg_gpu_begin(coopcg_gpu_ctx* ctx, const coopcg_opts* opts);
@@ -202,6 +208,9 @@ int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k);
 int coopcg_gpu_recompute_at(const coopcg_gpu_ctx* ctx, int k);
 int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int* ld);
 int coopcg_gpu_state(coopcg_gpu_ctx* ctx, int* stop, int* iterations);
+/* mccg after a polled stop: *next_k = iteration to resume from (the agents
+ * were restricted), or -1 (the solve is over). */
+int coopcg_gpu_mccg_resume(coopcg_gpu_ctx* ctx, int* next_k);
 int coopcg_gpu_end(coopcg_gpu_ctx* ctx, coopcg_trace* trace);
 
 /* ---- peer-memory Q exchange (one process per GPU, NVLink / NVSwitch) ------

@@ -70,12 +70,13 @@ SIGNATURES = [
     ("coopcg_gpu_recompute_at", _I, [_VP, _I]),
     ("coopcg_gpu_block", _I, [_VP, _I, _I, C.POINTER(_VP), C.POINTER(_I)]),
     ("coopcg_gpu_state", _I, [_VP, C.POINTER(_I), C.POINTER(_I)]),
+    ("coopcg_gpu_mccg_resume", _I, [_VP, C.POINTER(_I)]),
     ("coopcg_gpu_end", _I, [_VP, C.POINTER(coopcg_trace)]),
     ("coopcg_gpu_ipc_handles", _I, [_VP, _VP]),
     ("coopcg_gpu_set_peers", _I, [_VP, _I, _I, _VP]),
 ]
 
-PH_SETUP_LOCAL, PH_SETUP_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST, PH_FINAL_LOCAL, PH_FINAL_REST = range(7)
+PH_SETUP_LOCAL, PH_SETUP_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST, PH_FINAL_LOCAL, PH_FINAL_REST, PH_MCCG_SETUP = range(8)
 BLOCK_X, BLOCK_R, BLOCK_D, BLOCK_Q, BLOCK_S = range(5)
 
 _lib = None

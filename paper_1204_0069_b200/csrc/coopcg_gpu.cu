@@ -1101,8 +1101,6 @@ static int begin_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     ctx->every = o.recompute_residual_every >= 0 ? o.recompute_residual_every : 50;
     if (int rc = ensure_trace_capacity(ctx, std::max(ctx->max_iters, 1))) return rc;
     ctx->algo = (o.algo == 1 || o.algo == 2) ? o.algo : 0;
-    if (ctx->algo == 1 && sharded(ctx))
-        return fail(ctx, COOPCG_E_INVALID, "mccg_solve is single-GPU in this version");
     if (ctx->algo == 2 && (ctx->p != 1 || ctx->arith != COOPCG_ARITH_EXACT))
         return fail(ctx, COOPCG_E_INVALID, "steepest descent needs p = 1 and the exact mode");
     ctx->host_err = 0;
@@ -1585,8 +1583,20 @@ int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k) {
     case COOPCG_PH_ITER_REST: return iter_rest(ctx, k);
     case COOPCG_PH_FINAL_LOCAL: return final_local(ctx);
     case COOPCG_PH_FINAL_REST: return final_rest(ctx);
+    case COOPCG_PH_MCCG_SETUP: return ctx->algo == 1 ? mccg_setup(ctx) : COOPCG_OK;
     default: return fail(ctx, COOPCG_E_INVALID, "unknown phase %d", phase);
     }
+}
+
+int coopcg_gpu_mccg_resume(coopcg_gpu_ctx* ctx, int* next_k) {
+    if (!ctx || !next_k) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    *next_k = -1;
+    if (ctx->algo != 1) return COOPCG_OK;
+    CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    if (!ctx->ctl_host[0].restrict_pending) return COOPCG_OK;
+    return mccg_restrict(ctx, ctx->ctl_host[0].k, next_k);
 }
 
 int coopcg_gpu_recompute_at(const coopcg_gpu_ctx* ctx, int k) { return ctx ? (recompute_at(ctx, k) ? 1 : 0) : 0; }

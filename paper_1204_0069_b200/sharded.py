@@ -18,6 +18,7 @@ CPU engine of tests/test_sharded_gloo.py (gloo):
     engine.begin(opts); engine.phase(ph, k); engine.recompute_at(k) -> bool
     engine.block(which, k) -> torch tensor (n x P) view of that block
     engine.state() -> (stop, iterations); engine.end() -> SolveTrace
+    engine.mccg_resume() -> k to resume from after an mccg restriction, or -1
     engine.collective_stream() -> context manager ordering collectives with
                                   the engine's stream
 
@@ -40,7 +41,7 @@ import numpy as np
 from . import _capi
 from .solver import GpuContext, SolveOptions, _check, _dp
 
-PH_SETUP_LOCAL, PH_SETUP_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST, PH_FINAL_LOCAL, PH_FINAL_REST = range(7)
+PH_SETUP_LOCAL, PH_SETUP_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST, PH_FINAL_LOCAL, PH_FINAL_REST, PH_MCCG_SETUP = range(8)
 BLOCK_X, BLOCK_R, BLOCK_D, BLOCK_Q, BLOCK_S = range(5)
 
 
@@ -117,22 +118,35 @@ def solve_sharded(engine, exchange: RowExchange, opts: SolveOptions, poll_every:
     with engine.collective_stream():
         exchange.allgather(engine.block(BLOCK_R, 0))
     engine.phase(PH_SETUP_REST, 0)
+    mccg = opts.algo == "mccg"
+    if mccg:
+        engine.phase(PH_MCCG_SETUP, 0)
     stop, _ = engine.state()
     k = 0
-    while not stop and k < engine.max_iters:
-        engine.phase(PH_ITER_LOCAL, k)
-        with engine.collective_stream():
-            exchange.allgather_q(engine.block(BLOCK_Q, k))
-        engine.phase(PH_ITER_MID, k)
-        if engine.recompute_at(k):
+    while True:
+        while not stop and k < engine.max_iters:
+            engine.phase(PH_ITER_LOCAL, k)
             with engine.collective_stream():
-                exchange.allgather(engine.block(BLOCK_R, k))
-        engine.phase(PH_ITER_REST, k)
-        k += 1
-        # Every rank polls at the same k and, computing identical values,
-        # sees the same stop flag: the collectives stay matched.
-        if k % poll_every == 0 or k >= engine.max_iters:
-            stop, _ = engine.state()
+                exchange.allgather_q(engine.block(BLOCK_Q, k))
+            engine.phase(PH_ITER_MID, k)
+            if engine.recompute_at(k):
+                with engine.collective_stream():
+                    exchange.allgather(engine.block(BLOCK_R, k))
+            engine.phase(PH_ITER_REST, k)
+            k += 1
+            # Every rank polls at the same k and, computing identical values,
+            # sees the same stop flag: the collectives stay matched.
+            if k % poll_every == 0 or k >= engine.max_iters:
+                stop, _ = engine.state()
+        # mccg: a rank drop paused every rank at the same iteration; each
+        # restricts its replicated blocks identically and all resume together
+        # (the iterations enqueued after the pause were no-ops)
+        if not (mccg and stop):
+            break
+        k = engine.mccg_resume()
+        if k < 0:
+            break
+        stop = False
     engine.phase(PH_FINAL_LOCAL, 0)
     with engine.collective_stream():
         exchange.allgather(engine.block(BLOCK_S, 0))
@@ -205,6 +219,11 @@ class GpuShardEngine:
 
     def recompute_at(self, k: int) -> bool:
         return bool(_capi.lib().coopcg_gpu_recompute_at(self.ctx._h, k))
+
+    def mccg_resume(self) -> int:
+        nk = C.c_int()
+        _check(self.ctx._h, _capi.lib().coopcg_gpu_mccg_resume(self.ctx._h, C.byref(nk)))
+        return nk.value
 
     def state(self):
         stop = C.c_int()

@@ -19,7 +19,7 @@ import torch
 import pyoracle as po
 from paper_1204_0069_b200.sharded import (BLOCK_D, BLOCK_Q, BLOCK_R, BLOCK_S, BLOCK_X, PH_FINAL_LOCAL,
                                           PH_FINAL_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST,
-                                          PH_SETUP_LOCAL, PH_SETUP_REST, row_split)
+                                          PH_MCCG_SETUP, PH_SETUP_LOCAL, PH_SETUP_REST, row_split)
 
 
 def _dot(a, b):
@@ -40,7 +40,8 @@ class CpuShardEngine:
         self.A = np.ascontiguousarray(A)
         self.b = np.ascontiguousarray(b)
         self.n, self.p = X0.shape
-        self.P = self.p
+        self.P = self.p0 = self.p
+        self.X0 = np.array(X0, dtype=np.float64)
         self.row0, self.row1, _ = row_split(self.n, world, rank)
         z = lambda: torch.zeros((self.n, self.P), dtype=torch.float64)
         self.X = torch.from_numpy(np.array(X0, dtype=np.float64))
@@ -63,6 +64,12 @@ class CpuShardEngine:
         self.stop, self.status, self.k, self.err = False, "max-iterations", 0, None
         self.converged_agent = -1
         self.records = []
+        # mccg_solve (solvers.hpp:338-342): agents restricted on rank drops
+        self.mccg = opts.algo == "mccg"
+        self.p = self.p0
+        self.ids = list(range(self.p0))
+        self.pending = None
+        self.X.copy_(torch.from_numpy(self.X0))
 
     def recompute_at(self, k):
         return self.every > 0 and (k + 1) % self.every == 0
@@ -91,14 +98,22 @@ class CpuShardEngine:
             Rn = self.R.numpy()
             self.norms = [math.sqrt(_dot(Rn[:, j], Rn[:, j])) for j in range(p)]
             self.initial = list(self.norms)
+            rank0, cols = po.numerical_rank(self.Dblk[0].numpy(), self.rank_tol)
+            if self.mccg and 0 < rank0 < p:  # setup_coordinator's restriction (solvers.hpp:63-76)
+                self._restrict(sorted(int(c) for c in cols), self.Dblk[0])
+                Rn = self.R.numpy()
+                self.norms = [math.sqrt(_dot(Rn[:, j], Rn[:, j])) for j in range(self.p)]
             slot = self._first_converged(self.norms)
-            rank0 = po.numerical_rank(self.Dblk[0].numpy(), self.rank_tol)[0]
             if slot >= 0:
-                self.stop, self.status, self.converged_agent = True, "converged", slot
-            elif rank0 < p:
+                self.stop, self.status, self.converged_agent = True, "converged", self.ids[slot]
+            elif not self.mccg and rank0 < p:
                 self.stop, self.status = True, "rank-collapse"
+            elif self.mccg and rank0 == 0:
+                self.err, self.stop = "every starting direction is numerically zero", True
             if not self.stop and self.max_iters == 0:
                 self.stop = True
+        elif ph == PH_MCCG_SETUP:
+            pass  # done with SETUP_REST above
         elif ph in (PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST):
             if self.stop:
                 return
@@ -138,11 +153,19 @@ class CpuShardEngine:
                 m = norms[0]
                 for v in norms:
                     m = v if v < m else m
-                self.records.append((norms, m))
+                row = [math.nan] * self.p0  # per original agent id (IterationRecord::agents)
+                for j in range(p):
+                    row[self.ids[j]] = norms[j]
+                self.records.append((row, m))
                 slot = self._first_converged(norms)
+                rr = -1
+                if slot < 0:
+                    rr = po.numerical_rank(Dn[:, :p], self.rank_tol)[0]
                 if slot >= 0:
-                    self.stop, self.status, self.converged_agent = True, "converged", slot
-                elif po.numerical_rank(Dn, self.rank_tol)[0] < p:
+                    self.stop, self.status, self.converged_agent = True, "converged", self.ids[slot]
+                elif rr < p and self.mccg:  # pause for the restriction (mccg_resume)
+                    self.stop, self.pending = True, (k, rr)
+                elif rr < p:
                     self.stop, self.status = True, "rank-collapse"
                 elif k + 1 >= self.max_iters:
                     self.stop, self.status = True, "max-iterations"
@@ -150,7 +173,37 @@ class CpuShardEngine:
             self._local_residual(self.S.numpy())
         elif ph == PH_FINAL_REST:
             Sn = self.S.numpy()
-            self.final = [math.sqrt(_dot(Sn[:, j], Sn[:, j])) for j in range(p)]
+            self.final = [math.nan] * self.p0
+            for j in range(p):
+                self.final[self.ids[j]] = math.sqrt(_dot(Sn[:, j], Sn[:, j]))
+
+    def _restrict(self, keep, direction):
+        """BlockCgWorkspace::restrict_to (block_cg.hpp:84-96) on the replicated blocks."""
+        for blk in (self.X, self.R, direction):
+            a = blk.numpy()
+            kept = a[:, keep].copy()
+            a[:, :] = 0.0
+            a[:, :len(keep)] = kept
+        self.ids = [self.ids[c] for c in keep]
+        self.p = len(keep)
+
+    def mccg_resume(self):
+        """end_of_iteration's restriction (solvers.hpp:156-175) after a paused rank drop."""
+        if not self.pending:
+            return -1
+        k, rr = self.pending
+        self.pending = None
+        nsel, cols = po.numerical_rank(self.R.numpy()[:, :self.p], self.rank_tol)
+        pnext = min(rr, nsel)
+        if pnext == 0:
+            self.err = f"all agents degenerate at iteration {k} with residual above tolerance"
+            return -1
+        self._restrict(sorted(int(c) for c in cols[:pnext]), self.Dblk[(k + 1) & 1])
+        if k + 1 >= self.max_iters:
+            self.status = "max-iterations"
+            return -1
+        self.stop = False
+        return k + 1
 
     def _lu(self, M):
         p = self.p
@@ -175,6 +228,7 @@ class CpuShardEngine:
         if self.err:
             raise RuntimeError(self.err)
         return SimpleNamespace(status=self.status, iterations=len(self.records), converged_agent=self.converged_agent,
-                               residual_norms=np.array([r[0] for r in self.records]).reshape(-1, self.p),
-                               minres=np.array([r[1] for r in self.records]), final_x=self.X.numpy().copy(),
+                               residual_norms=np.array([r[0] for r in self.records]).reshape(-1, self.p0),
+                               minres=np.array([r[1] for r in self.records]),
+                               final_x=self.X.numpy()[:, :self.p].copy(), active_agents=list(self.ids),
                                final_residual_norms=np.array(self.final), initial=np.array(self.initial))

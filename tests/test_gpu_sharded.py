@@ -10,7 +10,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 from paper_1204_0069_b200.sharded import (BLOCK_Q, BLOCK_R, BLOCK_S, PH_FINAL_LOCAL, PH_FINAL_REST, PH_ITER_LOCAL,
-                                          PH_ITER_MID, PH_ITER_REST, PH_SETUP_LOCAL, PH_SETUP_REST,
+                                          PH_ITER_MID, PH_ITER_REST, PH_MCCG_SETUP, PH_SETUP_LOCAL, PH_SETUP_REST,
                                           GpuShardEngine)
 
 
@@ -32,22 +32,33 @@ def lockstep_solve(engines, opts):
     exchange(engines, BLOCK_R, 0)
     for e in engines:
         e.phase(PH_SETUP_REST, 0)
+    if opts.algo == "mccg":
+        for e in engines:
+            e.phase(PH_MCCG_SETUP, 0)
     stop = engines[0].state()[0]
     k = 0
-    while not stop and k < engines[0].max_iters:
-        for e in engines:
-            e.phase(PH_ITER_LOCAL, k)
-        exchange(engines, BLOCK_Q, k)
-        for e in engines:
-            e.phase(PH_ITER_MID, k)
-        if engines[0].recompute_at(k):
-            exchange(engines, BLOCK_R, k)
-        for e in engines:
-            e.phase(PH_ITER_REST, k)
-        k += 1
-        stops = [e.state()[0] for e in engines]
-        assert len(set(stops)) == 1  # replicated state => identical decisions
-        stop = stops[0]
+    while True:
+        while not stop and k < engines[0].max_iters:
+            for e in engines:
+                e.phase(PH_ITER_LOCAL, k)
+            exchange(engines, BLOCK_Q, k)
+            for e in engines:
+                e.phase(PH_ITER_MID, k)
+            if engines[0].recompute_at(k):
+                exchange(engines, BLOCK_R, k)
+            for e in engines:
+                e.phase(PH_ITER_REST, k)
+            k += 1
+            stops = [e.state()[0] for e in engines]
+            assert len(set(stops)) == 1  # replicated state => identical decisions
+            stop = stops[0]
+        if not (opts.algo == "mccg" and stop):
+            break
+        ks = [e.mccg_resume() for e in engines]  # every shard restricts identically
+        assert len(set(ks)) == 1
+        if ks[0] < 0:
+            break
+        k, stop = ks[0], False
     for e in engines:
         e.phase(PH_FINAL_LOCAL, 0)
     exchange(engines, BLOCK_S, 0)
@@ -118,5 +129,34 @@ def test_sharded_fast_within_tolerance(po):
         rel = np.linalg.norm(t.final_x - ref.final_x, axis=0) / np.linalg.norm(ref.final_x, axis=0)
         assert rel.max() < 1e-8
     assert np.array_equal(traces[0].final_x, traces[1].final_x)  # ranks agree bit for bit
+    for e in engines:
+        e.close()
+
+
+@pytest.mark.parametrize("name,world", [("mccg_n50_p8", 2), ("mccg_exhaustion_cliff", 3),
+                                        ("mccg_duplicate_columns", 2)])
+def test_sharded_mccg_matches_reference(name, world):
+    """mccg_solve on row-sharded contexts: each shard restricts its replicated
+    blocks on a rank drop (coopcg_gpu_mccg_resume) and the trace equals the
+    reference's own (golden fixture), NaN rows for dropped agents included."""
+    import paper_1204_0069_b200 as m
+    from conftest import load_golden
+    A, z = load_golden(name)
+    n, p = z["X0"].shape
+    opts = m.SolveOptions(tol=float(z["tol"]), max_iters=int(z["max_iters"]),
+                          recompute_residual_every=int(z["recompute"]), algo="mccg")
+    engines = [GpuShardEngine(n, p, r, world, 0, "exact") for r in range(world)]
+    for e in engines:
+        e.ctx.set_A(A[e.row0:e.row1])
+        e.ctx.upload(z["b"], z["X0"])
+    traces = lockstep_solve(engines, opts)
+    act = [int(a) for a in z["active_agents"]]
+    for t in traces:
+        assert str(t.status) == str(z["status"]) and t.iteration_count() == int(z["iterations"])
+        assert t.converged_agent == int(z["converged_agent"])
+        assert np.array_equal(t.residual_norms, z["residual_norms"], equal_nan=True)
+        assert t.active_agents == act
+        assert np.array_equal(t.final_x, z["final_x"][:, act])
+        assert np.array_equal(t.final_residual_norms_by_id, z["final_residual_norms"], equal_nan=True)
     for e in engines:
         e.close()
