@@ -22,8 +22,9 @@ def _cmp(m, po, A, b, X0, **kw):
 
 @pytest.mark.parametrize("n,p,kind,seed,tol", [
     (300, 3, "dd", 3, 1e-10),          # full rank: mccg == ccg
-    (120, 6, "hh", 4, 1e-13),          # tolerance below the floor: restrictions as agents exhaust
-    (96, 8, "hh", 7, 1e-14),
+    (120, 6, "hh", 4, 1e-13),          # Householder family, tight tolerance (converges before any
+    (96, 8, "hh", 7, 1e-14),           # rank drop; restrictions: the golden mccg_* fixtures in
+                                       # test_gpu_parity and the duplicate-column case below)
 ])
 def test_mccg_vs_oracle(po, n, p, kind, seed, tol):
     import paper_1204_0069_b200 as m
