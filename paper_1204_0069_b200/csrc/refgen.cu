@@ -26,6 +26,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -39,9 +40,10 @@ namespace coopcg_gpu {
 
 constexpr int kMgsTR = 32;   // rows per pipelined sub-tile
 constexpr int kMgsSR = 128;  // rows per ring stage (one bulk copy)
-constexpr int kMgsS = 6;     // ring stages
+constexpr int kMgsS = 6;     // ring stages (one CTA per SM)
+constexpr int kMgsS2 = 3;    // ring stages when the grid exceeds the SMs (two CTAs per SM)
 constexpr int kMgsStage = kMgsSR * 32 + 2 * kMgsSR;  // doubles: W rows + u_{t-1} + u_t
-constexpr size_t kMgsSmem = sizeof(double) * kMgsS * kMgsStage;
+constexpr size_t mgs_smem(int stages) { return sizeof(double) * stages * kMgsStage; }
 constexpr int kNormSmemMaxN = 24576;  // above this N(t) keeps the squares in global scratch
 
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
@@ -128,13 +130,13 @@ __global__ void __launch_bounds__(512) mgs_norm_kernel(double* __restrict__ W, i
 // (update, store, product), so the dependent DADD chain overlaps the
 // independent work.  Lanes outside (t, n) (first / last block) use c = 0 and
 // never store; their sums are discarded.
-template <bool PEND>
+template <bool PEND, int S>
 __global__ void __launch_bounds__(32) mgs_proj_kernel(double* __restrict__ W, int n, int np, int t,
                                                       double* __restrict__ coef, const double* __restrict__ uprev,
                                                       const double* __restrict__ ucur) {
     extern __shared__ __align__(128) double ring[];
-    __shared__ __align__(8) uint64_t full[kMgsS];
-    constexpr int TR = kMgsTR, SR = kMgsSR, SUB = SR / TR, S = kMgsS, STAGE = kMgsStage, AHEAD = S - 1;
+    __shared__ __align__(8) uint64_t full[S];
+    constexpr int TR = kMgsTR, SR = kMgsSR, SUB = SR / TR, STAGE = kMgsStage, AHEAD = S - 1;
     const int lane = threadIdx.x;
     const int jb = ((t + 1) >> 5) + blockIdx.x;
     const int j = jb * 32 + lane;
@@ -360,8 +362,16 @@ int refgen_random_spd(double* At, ALay L, size_t ap_elems, int n, double cond, u
     RG(cudaMemsetAsync(derr, 0, sizeof(int), st));
     const size_t norm_smem = norm_in_smem ? sizeof(double) * n : 0;
     RG(cudaFuncSetAttribute(mgs_norm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)norm_smem));
-    RG(cudaFuncSetAttribute(mgs_proj_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMgsSmem));
-    RG(cudaFuncSetAttribute(mgs_proj_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMgsSmem));
+    RG(cudaFuncSetAttribute(mgs_proj_kernel<false, kMgsS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mgs_smem(kMgsS)));
+    RG(cudaFuncSetAttribute(mgs_proj_kernel<true, kMgsS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mgs_smem(kMgsS)));
+    RG(cudaFuncSetAttribute(mgs_proj_kernel<false, kMgsS2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mgs_smem(kMgsS2)));
+    RG(cudaFuncSetAttribute(mgs_proj_kernel<true, kMgsS2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mgs_smem(kMgsS2)));
+    const bool force_two = std::getenv("COOPCG_REFGEN_TWO_PER_SM") != nullptr;  // tests: the 3-stage variant at small n
+    int nsm = 148;
+    {
+        int dev = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
 
     // Programmatic dependent launch: each step's kernel is scheduled while the
     // previous one drains and waits (griddepcontrol.wait) for its results.
@@ -377,20 +387,20 @@ int refgen_random_spd(double* At, ALay L, size_t ap_elems, int n, double cond, u
     cfg_n.numAttrs = 1;
     cfg_p = cfg_n;
     cfg_p.blockDim = dim3(32);
-    cfg_p.dynamicSmemBytes = kMgsSmem;
     for (int t = 0; t < n; ++t) {
         double* uprev = ubuf + (size_t)((t + 1) & 1) * np;  // u_{t-1}
         double* ucur = ubuf + (size_t)(t & 1) * np;          // u_t
         RG(cudaLaunchKernelEx(&cfg_n, mgs_norm_kernel, W, n, np, t, (const double*)coef, (const double*)uprev, ucur,
                               vg, derr));
         if (t + 1 < n) {
-            cfg_p.gridDim = dim3((unsigned)((n + 31) / 32 - (t + 1) / 32));
-            if (t == 0)
-                RG(cudaLaunchKernelEx(&cfg_p, mgs_proj_kernel<false>, W, n, np, t, coef, (const double*)uprev,
-                                      (const double*)ucur));
-            else
-                RG(cudaLaunchKernelEx(&cfg_p, mgs_proj_kernel<true>, W, n, np, t, coef, (const double*)uprev,
-                                      (const double*)ucur));
+            const int blocks = (n + 31) / 32 - (t + 1) / 32;
+            cfg_p.gridDim = dim3((unsigned)blocks);
+            // more column blocks than SMs: a 3-stage ring so two CTAs share an SM (one wave)
+            const bool two = blocks > nsm || force_two;
+            cfg_p.dynamicSmemBytes = mgs_smem(two ? kMgsS2 : kMgsS);
+            auto kern = t == 0 ? (two ? mgs_proj_kernel<false, kMgsS2> : mgs_proj_kernel<false, kMgsS>)
+                               : (two ? mgs_proj_kernel<true, kMgsS2> : mgs_proj_kernel<true, kMgsS>);
+            RG(cudaLaunchKernelEx(&cfg_p, kern, W, n, np, t, coef, (const double*)uprev, (const double*)ucur));
         }
     }
     RG(cudaMemsetAsync(At, 0, sizeof(double) * ap_elems, st));

@@ -32,6 +32,7 @@ CASES = [  # (n, p, cond, seed)
     (777, 4, 1e4, 5),       # n not a multiple of the 32-row ring / 64-entry tiles
     (1024, 8, 1e3, 7),
     (2048, 4, 1e2, 1204),
+    (4800, 4, 1e2, 3),      # 150 column blocks > 148 SMs: the two-CTAs-per-SM P kernel (~5 min here)
 ]
 
 
