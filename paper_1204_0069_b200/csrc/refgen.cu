@@ -353,7 +353,8 @@ int refgen_random_spd(double* At, ALay L, size_t ap_elems, int n, double cond, u
     RG(cudaMalloc(&coef, sizeof(double) * np));
     RG(cudaMalloc(&ubuf, sizeof(double) * (2 * np + kMgsSR)));
     RG(cudaMalloc(&derr, sizeof(int)));
-    const bool norm_in_smem = n <= kNormSmemMaxN;
+    // (tests force the global-scratch path at small n)
+    const bool norm_in_smem = n <= kNormSmemMaxN && std::getenv("COOPCG_REFGEN_NORM_GLOBAL") == nullptr;
     if (!norm_in_smem) RG(cudaMalloc(&vg, sizeof(double) * n));
     RG(cudaMemcpyAsync(W, Wh.data(), sizeof(double) * wel, cudaMemcpyHostToDevice, st));
     RG(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
