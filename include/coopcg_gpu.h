@@ -135,8 +135,17 @@ int coopcg_gpu_last_error(const coopcg_gpu_ctx* ctx, char* buf, size_t len);
  * row-major n x n matrix, i.e. (row_end - row_begin) x n doubles, host memory. */
 int coopcg_gpu_set_A(coopcg_gpu_ctx* ctx, const double* A_rows);
 /* Generate A on the device.  DIAGDOM ignores m, kappa.
- * HOUSEHOLDER needs the full matrix on this device (single-GPU contexts). */
+ * HOUSEHOLDER on a full context (row-sharded: the steps below). */
 int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double kappa);
+/* HOUSEHOLDER generation in steps, for row-sharded contexts (each owns its
+ * rows of A):
+ *   begin; for r = m-1 .. 0: { local(r); <all-gather the rows of w,
+ *   COOPCG_BLOCK_W>; rest(r) }; end.
+ * coopcg_gpu_gen_A(HOUSEHOLDER) runs the same steps on a full context. */
+int coopcg_gpu_gen_householder_begin(coopcg_gpu_ctx* ctx, uint64_t seed, int m, double kappa);
+int coopcg_gpu_gen_householder_local(coopcg_gpu_ctx* ctx, int r);
+int coopcg_gpu_gen_householder_rest(coopcg_gpu_ctx* ctx, int r);
+int coopcg_gpu_gen_householder_end(coopcg_gpu_ctx* ctx);
 /* Download this context's row block of A (row-major), for verification. */
 int coopcg_gpu_get_A(coopcg_gpu_ctx* ctx, double* A_rows);
 
@@ -202,7 +211,8 @@ enum coopcg_phase {
     COOPCG_PH_FINAL_LOCAL = 5, COOPCG_PH_FINAL_REST = 6,
     COOPCG_PH_MCCG_SETUP = 7  /* mccg: setup_coordinator's restriction (solvers.hpp:63-91) */
 };
-enum coopcg_block { COOPCG_BLOCK_X = 0, COOPCG_BLOCK_R = 1, COOPCG_BLOCK_D = 2, COOPCG_BLOCK_Q = 3, COOPCG_BLOCK_S = 4 };
+enum coopcg_block { COOPCG_BLOCK_X = 0, COOPCG_BLOCK_R = 1, COOPCG_BLOCK_D = 2, COOPCG_BLOCK_Q = 3, COOPCG_BLOCK_S = 4,
+                    COOPCG_BLOCK_W = 5 /* Householder generation's w vector (n x 1, ld 1) */ };
 int coopcg_gpu_begin(coopcg_gpu_ctx* ctx, const coopcg_opts* opts);
 int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k);
 int coopcg_gpu_recompute_at(const coopcg_gpu_ctx* ctx, int k);

@@ -52,6 +52,10 @@ SIGNATURES = [
     ("coopcg_gpu_set_A", _I, [_VP, _VP]),
     ("coopcg_gpu_gen_A", _I, [_VP, _I, C.c_uint64, _I, C.c_double]),
     ("coopcg_gpu_get_A", _I, [_VP, _VP]),
+    ("coopcg_gpu_gen_householder_begin", _I, [_VP, C.c_uint64, _I, C.c_double]),
+    ("coopcg_gpu_gen_householder_local", _I, [_VP, _I]),
+    ("coopcg_gpu_gen_householder_rest", _I, [_VP, _I]),
+    ("coopcg_gpu_gen_householder_end", _I, [_VP]),
     ("coopcg_gen_rhs", _I, [_I, _I, C.c_uint64, _VP]),
     ("coopcg_gen_starts", _I, [_I, _I, C.c_uint64, _VP]),
     ("coopcg_gen_householder_factors", _I, [_I, _I, C.c_double, C.c_uint64, _VP, _VP]),
@@ -77,7 +81,7 @@ SIGNATURES = [
 ]
 
 PH_SETUP_LOCAL, PH_SETUP_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST, PH_FINAL_LOCAL, PH_FINAL_REST, PH_MCCG_SETUP = range(8)
-BLOCK_X, BLOCK_R, BLOCK_D, BLOCK_Q, BLOCK_S = range(5)
+BLOCK_X, BLOCK_R, BLOCK_D, BLOCK_Q, BLOCK_S, BLOCK_W = range(6)
 
 _lib = None
 

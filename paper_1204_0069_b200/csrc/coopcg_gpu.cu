@@ -138,7 +138,20 @@ struct coopcg_gpu_ctx {
     int host_err = 0;               // error raised by the host-side mccg logic
     std::string host_err_msg;
     std::vector<int> ids;           // original id of each active slot
+    // Householder generation in steps (coopcg_gpu_gen_householder_*): factors,
+    // the vector w (all n rows; this context writes its own) and t1, t2
+    double *hh_V = nullptr, *hh_lam = nullptr, *hh_w = nullptr, *hh_t = nullptr;
+    int hh_m = -1;
 };
+
+static void hh_free(coopcg_gpu_ctx* ctx) {
+    cudaFree(ctx->hh_V);
+    cudaFree(ctx->hh_lam);
+    cudaFree(ctx->hh_w);
+    cudaFree(ctx->hh_t);
+    ctx->hh_V = ctx->hh_lam = ctx->hh_w = ctx->hh_t = nullptr;
+    ctx->hh_m = -1;
+}
 
 namespace {
 
@@ -561,6 +574,7 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaFree(ctx->b);
     cudaFree(ctx->qpart);
     cudaFree(ctx->gpart);
+    hh_free(ctx);
     cudaFree(ctx->npart);
     cudaFree(ctx->dtiles);
     cudaFree(ctx->small);
@@ -843,6 +857,63 @@ int coopcg_gen_starts(int n, int p, uint64_t seed, double* X0) {
     return COOPCG_OK;
 }
 
+int coopcg_gpu_gen_householder_begin(coopcg_gpu_ctx* ctx, uint64_t seed, int m, double kappa) {
+    if (!ctx || m < 0) return COOPCG_E_INVALID;
+    CK(cudaSetDevice(ctx->device));
+    const int n = ctx->n;
+    hh_free(ctx);
+    std::vector<double> V((size_t)std::max(m, 1) * n), lam(n);
+    coopcg_gen_householder_factors(n, m, kappa, seed, V.data(), lam.data());
+    CK(cudaMalloc(&ctx->hh_V, sizeof(double) * V.size()));
+    CK(cudaMalloc(&ctx->hh_lam, sizeof(double) * n));
+    CK(cudaMalloc(&ctx->hh_w, sizeof(double) * n));
+    CK(cudaMalloc(&ctx->hh_t, sizeof(double) * 2));
+    CK(cudaMemcpyAsync(ctx->hh_V, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(ctx->hh_lam, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    CK(cudaMemsetAsync(ctx->hh_w, 0, sizeof(double) * n, ctx->stream));
+    hh_init_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, ctx->n_loc, ctx->row0, ctx->hh_lam,
+                                                     ctx->ap_elems);
+    CKL();
+    CK(cudaStreamSynchronize(ctx->stream));  // the host factors are freed on return
+    ctx->hh_m = m;
+    ctx->a_ready = false;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_gen_householder_local(coopcg_gpu_ctx* ctx, int r) {
+    if (!ctx) return COOPCG_E_INVALID;
+    if (ctx->hh_m < 0 || r < 0 || r >= ctx->hh_m)
+        return fail(ctx, COOPCG_E_STATE, "gen_householder_local: reflector %d outside a begun generation", r);
+    CK(cudaSetDevice(ctx->device));
+    hh_w_kernel<<<(ctx->n_loc + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->lay, ctx->n, ctx->n_loc, ctx->row0,
+                                                                  ctx->hh_V + (size_t)r * ctx->n, ctx->hh_w);
+    CKL();
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_gen_householder_rest(coopcg_gpu_ctx* ctx, int r) {
+    if (!ctx) return COOPCG_E_INVALID;
+    if (ctx->hh_m < 0 || r < 0 || r >= ctx->hh_m)
+        return fail(ctx, COOPCG_E_STATE, "gen_householder_rest: reflector %d outside a begun generation", r);
+    CK(cudaSetDevice(ctx->device));
+    const double* v = ctx->hh_V + (size_t)r * ctx->n;
+    hh_scalars_kernel<<<1, 32, 0, ctx->stream>>>(ctx->n, v, ctx->hh_w, ctx->hh_t);
+    hh_update_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, ctx->n, ctx->n_loc, ctx->row0, v, ctx->hh_w,
+                                                       ctx->hh_t, ctx->ap_elems);
+    CKL();
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_gen_householder_end(coopcg_gpu_ctx* ctx) {
+    if (!ctx) return COOPCG_E_INVALID;
+    if (ctx->hh_m < 0) return fail(ctx, COOPCG_E_STATE, "gen_householder_end without begin");
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->stream));
+    hh_free(ctx);
+    ctx->a_ready = true;
+    return COOPCG_OK;
+}
+
 int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double kappa) {
     if (!ctx) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
@@ -856,31 +927,15 @@ int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double
                                                                              ctx->row0);
         CKL();
     } else if (kind == COOPCG_MATRIX_HOUSEHOLDER) {
-        if (ctx->n_loc != n) return fail(ctx, COOPCG_E_INVALID, "Householder generation needs the full matrix");
-        if (m < 0) return COOPCG_E_INVALID;
-        std::vector<double> V((size_t)std::max(m, 1) * n), lam(n);
-        coopcg_gen_householder_factors(n, m, kappa, seed, V.data(), lam.data());
-        double *dV = nullptr, *dl = nullptr, *dw = nullptr, *dt = nullptr;
-        CK(cudaMalloc(&dV, sizeof(double) * V.size()));
-        CK(cudaMalloc(&dl, sizeof(double) * n));
-        CK(cudaMalloc(&dw, sizeof(double) * n));
-        CK(cudaMalloc(&dt, sizeof(double) * 2));
-        CK(cudaMemcpyAsync(dV, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, ctx->stream));
-        CK(cudaMemcpyAsync(dl, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-        hh_init_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, dl, ctx->ap_elems);
-        CKL();
+        if (ctx->n_loc != n)
+            return fail(ctx, COOPCG_E_INVALID,
+                        "row-sharded Householder generation exchanges w: use coopcg_gpu_gen_householder_*");
+        if (int rc = coopcg_gpu_gen_householder_begin(ctx, seed, m, kappa)) return rc;
         for (int r = m - 1; r >= 0; --r) {
-            const double* v = dV + (size_t)r * n;
-            hh_w_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->lay, n, v, dw);
-            hh_scalars_kernel<<<1, 32, 0, ctx->stream>>>(n, v, dw, dt);
-            hh_update_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, v, dw, dt, ctx->ap_elems);
-            CKL();
+            if (int rc = coopcg_gpu_gen_householder_local(ctx, r)) return rc;
+            if (int rc = coopcg_gpu_gen_householder_rest(ctx, r)) return rc;
         }
-        CK(cudaStreamSynchronize(ctx->stream));
-        cudaFree(dV);
-        cudaFree(dl);
-        cudaFree(dw);
-        cudaFree(dt);
+        if (int rc = coopcg_gpu_gen_householder_end(ctx)) return rc;
     } else if (kind == COOPCG_MATRIX_RANDOM_SPD) {
         if (ctx->n_loc != n) return fail(ctx, COOPCG_E_INVALID, "random_spd generation needs the full matrix");
         std::string msg;
@@ -1657,6 +1712,11 @@ int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int*
     case COOPCG_BLOCK_D: b = ctx->Dblk[k & 1]; break;
     case COOPCG_BLOCK_Q: b = q_of(ctx, k); break;
     case COOPCG_BLOCK_S: b = ctx->S; break;
+    case COOPCG_BLOCK_W:
+        if (!ctx->hh_w) return fail(ctx, COOPCG_E_STATE, "no Householder generation in progress");
+        *dev_ptr = ctx->hh_w;
+        if (ld) *ld = 1;
+        return COOPCG_OK;
     default: return fail(ctx, COOPCG_E_INVALID, "unknown block %d", which);
     }
     *dev_ptr = b;

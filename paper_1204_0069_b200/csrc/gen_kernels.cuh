@@ -64,28 +64,33 @@ __global__ void gen_dd_diag_kernel(double* __restrict__ Ap, ALay L, int n, int n
     Ap[a_idx(L, n, i, il)] = __dadd_rn(acc, 1.0);
 }
 
-// Householder construction (single-GPU contexts hold the full matrix):
+// Householder construction on the context's rows [row0, row0 + n_loc):
 // M = diag(lambda); for r = m-1 .. 0: M <- H_r M H_r with
 //   s = v.v, w = M v, c = v.w, t1 = 2/s, t2 = (4 c)/(s s),
 //   M_ij <- (M_ij - t1 (v_i w_j + w_i v_j)) + t2 (v_i v_j)
-// (every sum sequential ascending, one rounding per op).
-__global__ void hh_init_kernel(double* __restrict__ Ap, ALay L, int n, const double* __restrict__ lambda,
-                               size_t total) {
+// (every sum sequential ascending, one rounding per op).  Row i of w needs
+// only row i of M, the update of row i needs all of w: a row-sharded context
+// computes its rows of w, the caller all-gathers w, every rank forms s, c
+// from the full vectors identically and updates its own rows.
+__global__ void hh_init_kernel(double* __restrict__ Ap, ALay L, int n, int n_loc, int row0,
+                               const double* __restrict__ lambda, size_t total) {
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        int k, i;
-        a_decode(L, n, e, k, i);
-        Ap[e] = (i == k && i < n) ? lambda[i] : 0.0;
+        int k, il;
+        a_decode(L, n, e, k, il);
+        const int i = row0 + il;
+        Ap[e] = (il < n_loc && k < n && i == k) ? lambda[i] : 0.0;
     }
 }
-__global__ void hh_w_kernel(const double* __restrict__ Ap, ALay L, int n, const double* __restrict__ v,
-                            double* __restrict__ w) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= n) return;
+// w[row0 + il] = sum_k M(il, k) v[k], k ascending
+__global__ void hh_w_kernel(const double* __restrict__ Ap, ALay L, int n, int n_loc, int row0,
+                            const double* __restrict__ v, double* __restrict__ w) {
+    const int il = blockIdx.x * blockDim.x + threadIdx.x;
+    if (il >= n_loc) return;
     double acc = 0.0;
 #pragma unroll 4
-    for (int k = 0; k < n; ++k) acc = mac_exact(acc, Ap[a_idx(L, n, k, i)], v[k]);
-    w[i] = acc;
+    for (int k = 0; k < n; ++k) acc = mac_exact(acc, Ap[a_idx(L, n, k, il)], v[k]);
+    w[row0 + il] = acc;
 }
 __global__ void hh_scalars_kernel(int n, const double* __restrict__ v, const double* __restrict__ w,
                                   double* __restrict__ t12) {
@@ -96,14 +101,16 @@ __global__ void hh_scalars_kernel(int n, const double* __restrict__ v, const dou
     t12[0] = __ddiv_rn(2.0, s);
     t12[1] = __ddiv_rn(__dmul_rn(4.0, c), __dmul_rn(s, s));
 }
-__global__ void hh_update_kernel(double* __restrict__ Ap, ALay L, int n, const double* __restrict__ v,
-                                 const double* __restrict__ w, const double* __restrict__ t12, size_t total) {
+__global__ void hh_update_kernel(double* __restrict__ Ap, ALay L, int n, int n_loc, int row0,
+                                 const double* __restrict__ v, const double* __restrict__ w,
+                                 const double* __restrict__ t12, size_t total) {
     const double t1 = t12[0], t2 = t12[1];
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
          e += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        int k, i;
-        a_decode(L, n, e, k, i);
-        if (i >= n || k >= n) continue;
+        int k, il;
+        a_decode(L, n, e, k, il);
+        if (il >= n_loc || k >= n) continue;
+        const int i = row0 + il;
         // element (i, k); the expression is symmetric in (i, k) bit for bit.
         const double q = __dadd_rn(__dmul_rn(v[i], w[k]), __dmul_rn(w[i], v[k]));
         const double m1 = __dsub_rn(Ap[e], __dmul_rn(t1, q));

@@ -42,7 +42,7 @@ from . import _capi
 from .solver import GpuContext, SolveOptions, _check, _dp
 
 PH_SETUP_LOCAL, PH_SETUP_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST, PH_FINAL_LOCAL, PH_FINAL_REST, PH_MCCG_SETUP = range(8)
-BLOCK_X, BLOCK_R, BLOCK_D, BLOCK_Q, BLOCK_S = range(5)
+BLOCK_X, BLOCK_R, BLOCK_D, BLOCK_Q, BLOCK_S, BLOCK_W = range(6)
 
 
 def row_split(n: int, world: int, rank: int):
@@ -109,6 +109,24 @@ class PeerQExchange(RowExchange):
         else:
             torch.cuda.current_stream().synchronize()
             dist.barrier(group=self.group)
+
+
+def gen_householder_sharded(engine, exchange_w: RowExchange, seed: int, m: int, kappa: float) -> None:
+    """The Householder generator on row-sharded contexts: each
+    rank computes its rows of w = M v, the ranks all-gather w (an n x 1
+    RowExchange), and each rank updates its own rows of M with the scalars
+    every rank forms identically from the full vectors
+    (include/coopcg_gpu.h, coopcg_gpu_gen_householder_*)."""
+    L = _capi.lib()
+    h = engine.ctx._h
+    _check(h, L.coopcg_gpu_gen_householder_begin(h, seed, m, kappa))
+    w = engine.vector(BLOCK_W)
+    for r in range(m - 1, -1, -1):
+        _check(h, L.coopcg_gpu_gen_householder_local(h, r))
+        with engine.collective_stream():
+            exchange_w.allgather(w)
+        _check(h, L.coopcg_gpu_gen_householder_rest(h, r))
+    _check(h, L.coopcg_gpu_gen_householder_end(h))
 
 
 def solve_sharded(engine, exchange: RowExchange, opts: SolveOptions, poll_every: int = 8):
@@ -205,6 +223,13 @@ class GpuShardEngine:
                                                      device=f"cuda:{self.device}")
         return self._views[key]
 
+    def vector(self, which: int):
+        """(n, 1) torch view of a device vector of the context (COOPCG_BLOCK_W)."""
+        ptr = C.c_void_p()
+        ld = C.c_int()
+        _check(self.ctx._h, _capi.lib().coopcg_gpu_block(self.ctx._h, which, 0, C.byref(ptr), C.byref(ld)))
+        return self._torch.as_tensor(_CudaArray(ptr.value, (self.n, 1), self.device), device=f"cuda:{self.device}")
+
     def collective_stream(self):
         return self._torch.cuda.stream(self._stream)
 
@@ -272,15 +297,12 @@ def bench_main(args, cfg, metric: str, clock_sampler=None, peaks=None) -> int:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    if cfg.matrix != "diagdom":
-        if rank == 0:
-            print(json.dumps({"metric": metric, "unavailable": "sharded Householder generation is not "
-                              "implemented this round (diag-dominant configs shard)"}))
-        dist.destroy_process_group()
-        return 0
     p2p = bool(getattr(args, "p2p", False))
     eng = GpuShardEngine(cfg.n, cfg.p, rank, world, local, arith=args.arith)
-    eng.ctx.gen_A(cfg.matrix, cfg.seed, cfg.reflectors, cfg.kappa)
+    if cfg.matrix == "householder":
+        gen_householder_sharded(eng, RowExchange(cfg.n, 1, world, rank), cfg.seed, cfg.reflectors, cfg.kappa)
+    else:
+        eng.ctx.gen_A(cfg.matrix, cfg.seed, cfg.reflectors, cfg.kappa)
     b, X0 = host_inputs(cfg)
     opts = solve_options(cfg, b)
     eng.ctx.upload(b, X0)

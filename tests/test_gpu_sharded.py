@@ -160,3 +160,59 @@ def test_sharded_mccg_matches_reference(name, world):
         assert np.array_equal(t.final_residual_norms_by_id, z["final_residual_norms"], equal_nan=True)
     for e in engines:
         e.close()
+
+
+class _LockstepW:
+    """In-process stand-in for the n x 1 all-gather of w between shards."""
+
+    def __init__(self, engines):
+        self.engines = engines
+
+    def run(self, seed, m, kappa):
+        from paper_1204_0069_b200 import _capi
+        from paper_1204_0069_b200.sharded import BLOCK_W
+        from paper_1204_0069_b200.solver import _check
+        L = _capi.lib()
+        for e in self.engines:
+            _check(e.ctx._h, L.coopcg_gpu_gen_householder_begin(e.ctx._h, seed, m, kappa))
+        ws = [e.vector(BLOCK_W) for e in self.engines]
+        for r in range(m - 1, -1, -1):
+            for e in self.engines:
+                _check(e.ctx._h, L.coopcg_gpu_gen_householder_local(e.ctx._h, r))
+            torch.cuda.synchronize()
+            for i, e in enumerate(self.engines):
+                for j in range(len(self.engines)):
+                    if i != j:
+                        ws[j][e.row0:e.row1].copy_(ws[i][e.row0:e.row1])
+            torch.cuda.synchronize()
+            for e in self.engines:
+                _check(e.ctx._h, L.coopcg_gpu_gen_householder_rest(e.ctx._h, r))
+        for e in self.engines:
+            _check(e.ctx._h, L.coopcg_gpu_gen_householder_end(e.ctx._h))
+
+
+@pytest.mark.parametrize("n,p,world,arith", [(517, 4, 3, "exact"), (256, 8, 2, "fast")])
+def test_sharded_householder_generation(po, n, p, world, arith):
+    """Row-sharded Householder generation (w all-gathered per reflector): every
+    shard's rows equal the oracle's full matrix bit for bit, and the sharded
+    solve on them equals the oracle solve (exact)."""
+    import paper_1204_0069_b200 as m
+    seed, refl, kappa = 11, 6, 1e3
+    A = po.gen_householder(n, refl, kappa, seed)
+    engines = [GpuShardEngine(n, p, r, world, 0, arith) for r in range(world)]
+    _LockstepW(engines).run(seed, refl, kappa)
+    for e in engines:
+        assert np.array_equal(e.ctx.get_A(), A[e.row0:e.row1])
+    if arith == "exact":
+        b = po.gen_rhs(n, "normal", seed)
+        X0 = po.gen_starts(n, p, seed)
+        opts = m.SolveOptions(tol=0.0, max_iters=40)
+        for e in engines:
+            e.ctx.upload(b, X0)
+        traces = lockstep_solve(engines, opts)
+        ot = po.oracle_ccg(A, b, X0, tol=0.0, max_iters=40)
+        for t in traces:
+            assert np.array_equal(t.residual_norms, ot.residual_norms)
+            assert np.array_equal(t.final_x, ot.final_x)
+    for e in engines:
+        e.close()
