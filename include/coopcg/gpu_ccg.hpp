@@ -17,14 +17,18 @@
 //
 // GpuSolver keeps A resident on the device between solves (SpdMatrix is
 // immutable, dense.hpp:95-96), the common "many right-hand sides" use.
+// gpu_make_problem is make_problem<double> with the matrix generated on the
+// device (the reference's Haar-MGS random_spd is O(n^3) and serial on a CPU).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
 #include <vector>
 
+#include "coopcg/problem.hpp"
 #include "coopcg/solvers.hpp"
 #include "coopcg_gpu.h"
 
@@ -176,6 +180,44 @@ inline SolveTrace<double> gpu_ccg(const SpdMatrix<double>& A, const Vec<double>&
     detail::check_block_inputs(A, b, X0);
     GpuSolver s(A, X0.cols(), g);
     return s.solve(b, X0, opts);
+}
+
+/// make_problem<double> (problem.hpp:219-230) with A = random_spd(n, cond, seed)
+/// generated on the device, bit-identical to the reference's:
+/// the reference's own ProblemInstance, so a benchmark harness switches with
+///     auto inst = coopcg::make_problem<double>(spec);      // CPU: O(n^3) serial MGS
+///     auto inst = coopcg::gpu_make_problem(spec);           // this library
+inline ProblemInstance<double> gpu_make_problem(const ProblemSpec& spec, bool with_oracle = false,
+                                                const GpuOptions& g = {}) {
+    spec.validate();
+    if (spec.n < 2) return make_problem<double>(spec, with_oracle);  // the 1 x 1 case: nothing to generate
+    const int n = spec.n, p = spec.p;
+    coopcg_gpu_ctx* ctx = nullptr;
+    int rc = coopcg_gpu_create(n, 1, g.device, COOPCG_ARITH_EXACT, &ctx);
+    if (rc != COOPCG_OK) gpu_detail::raise(rc, gpu_detail::last_error(nullptr));
+    std::vector<double> a(static_cast<size_t>(n) * n);
+    rc = coopcg_gpu_gen_A(ctx, COOPCG_MATRIX_RANDOM_SPD, spec.seed, 0, spec.cond);
+    if (rc == COOPCG_OK) rc = coopcg_gpu_get_A(ctx, a.data());
+    if (rc != COOPCG_OK) {
+        const std::string msg = gpu_detail::last_error(ctx);
+        coopcg_gpu_destroy(ctx);
+        gpu_detail::raise(rc, msg);
+    }
+    coopcg_gpu_destroy(ctx);
+    std::vector<double> lam(n), bh(n), x0(static_cast<size_t>(n) * p);
+    coopcg_gen_random_spd_spectrum(n, spec.cond, spec.seed, lam.data());
+    coopcg_gen_reference_rhs_starts(n, p, spec.seed, bh.data(), x0.data());
+    Vec<double> b(bh.begin(), bh.end());
+    DenseBlock<double> X0(n, p);
+    for (int j = 0; j < p; ++j)
+        for (int i = 0; i < n; ++i) X0(i, j) = x0[static_cast<size_t>(j) * n + i];
+    const auto [lo, hi] = std::minmax_element(lam.begin(), lam.end());
+    // SpdMatrix's float-mode construction symmetrises (already exact) and probes, as random_spd's does
+    ProblemInstance<double> inst{SpdMatrix<double>(n, std::move(a)), std::move(b), std::move(X0), std::nullopt,
+                                 *hi / *lo};
+    if (with_oracle)
+        inst.x_star = solve_dense(inst.A, inst.b);
+    return inst;
 }
 
 }  // namespace coopcg

@@ -99,6 +99,17 @@ int main() {
             compare(name, mccg_solve(inst.A, inst.b, inst.X0, o), gpu_mccg(inst.A, inst.b, inst.X0, o));
         }
     }
+    {   // gpu_make_problem == make_problem<double>, field by field
+        const ProblemSpec specs[] = {{2, 1, 3.0, 4}, {77, 3, 1e3, 9}, {300, 8, 1e4, 21}};
+        for (const auto& spec : specs) {
+            const auto r = make_problem<double>(spec);
+            const auto g = gpu_make_problem(spec);
+            bool ok = r.A == g.A && r.X0 == g.X0 && r.b.size() == g.b.size() && same(r.realized_cond, g.realized_cond);
+            for (size_t i = 0; ok && i < r.b.size(); ++i) ok = same(r.b[i], g.b[i]);
+            std::printf("gpu_make_problem n=%-4d p=%-2d        %s\n", spec.n, spec.p, ok ? "bit-identical" : "MISMATCH");
+            if (!ok) ++failures;
+        }
+    }
     {   // error behaviour: indefinite matrix -> SpdViolationError; bad shapes -> DimensionError
         const int n = 30;
         std::vector<double> e(static_cast<size_t>(n) * n, 0.0);
