@@ -182,6 +182,57 @@ inline SolveTrace<double> gpu_ccg(const SpdMatrix<double>& A, const Vec<double>&
     return s.solve(b, X0, opts);
 }
 
+namespace gpu_detail {
+
+// The scalar solvers on the p = 1 block kernels (algo 0: CG, 2: steepest
+// descent), with their own error text and per-iteration mult counting.
+inline SolveTrace<double> scalar_solve(const char* name, int algo, const SpdMatrix<double>& A, const Vec<double>& b,
+                                       const Vec<double>& x0, SolveOptions<double> opts, const GpuOptions& g) {
+    const int n = A.dim();
+    if (static_cast<int>(b.size()) != n || static_cast<int>(x0.size()) != n)
+        throw DimensionError(std::string(name) + ": operand shapes do not match");
+    if (opts.recompute_residual_every < 0) opts.recompute_residual_every = 1;  // solvers.hpp:399, :543
+    GpuOptions ge = g;
+    if (algo == 2) ge.arith = GpuOptions::Arith::exact;
+    SolveTrace<double> t;
+    try {
+        GpuSolver s(A, 1, ge);
+        t = s.solve(b, DenseBlock<double>::from_column(x0), opts, algo);
+    } catch (const SpdViolationError& ex) {  // "... at iteration k" from the block path
+        const std::string m = ex.what();
+        const std::string k = m.substr(m.find_last_of(' ') + 1);
+        throw SpdViolationError(std::string(name) + (algo == 2 ? ": nonpositive gradient energy at iteration "
+                                                               : ": nonpositive direction energy at iteration ") + k);
+    }
+    const auto un = static_cast<std::uint64_t>(n);
+    for (auto& rec : t.iterations) {  // solvers.hpp:438-486 (CG), :571-603 (SD)
+        const bool rc = detail::recompute_now(rec.k, opts.recompute_residual_every);
+        const std::uint64_t m = algo == 2 ? (rc ? 2 * un * un + 3 * un + 1 : un * un + 4 * un + 1)
+                                          : (rc ? 2 * un * un + 5 * un + 2 : un * un + 6 * un + 2);
+        rec.mults = m;
+        rec.mults_per_worker.assign(1, m);
+    }
+    return t;
+}
+
+}  // namespace gpu_detail
+
+/// cg_solve's signature plus GPU options (solvers.hpp:388-530): the p = 1 block
+/// solver with CG's residual policy reproduces it bit for bit
+/// (tests/test_solvers.cpp:176-201 in the reference).
+inline SolveTrace<double> gpu_cg_solve(const SpdMatrix<double>& A, const Vec<double>& b, const Vec<double>& x0,
+                                       const SolveOptions<double>& opts = {}, const GpuOptions& g = {}) {
+    return gpu_detail::scalar_solve("cg_solve", 0, A, b, x0, opts, g);
+}
+
+/// steepest_descent_solve's signature plus GPU options (solvers.hpp:532-646);
+/// exact arithmetic only.
+inline SolveTrace<double> gpu_steepest_descent_solve(const SpdMatrix<double>& A, const Vec<double>& b,
+                                                     const Vec<double>& x0, const SolveOptions<double>& opts = {},
+                                                     const GpuOptions& g = {}) {
+    return gpu_detail::scalar_solve("steepest_descent_solve", 2, A, b, x0, opts, g);
+}
+
 /// make_problem<double> (problem.hpp:219-230) with A = random_spd(n, cond, seed)
 /// generated on the device, bit-identical to the reference's:
 /// the reference's own ProblemInstance, so a benchmark harness switches with

@@ -99,6 +99,32 @@ int main() {
             compare(name, mccg_solve(inst.A, inst.b, inst.X0, o), gpu_mccg(inst.A, inst.b, inst.X0, o));
         }
     }
+    {   // cg_solve / steepest_descent_solve through the p = 1 block kernels
+        struct SCase { int n; double cond; unsigned long long seed; double tol; int max_iters; int recompute; };
+        const SCase sc[] = {{120, 1e3, 21, 1e-10, -1, -1}, {120, 1e3, 21, 1e-10, -1, 0}, {80, 30.0, 22, 1e-9, -1, -1},
+                            {64, 1e2, 5, 0.0, 25, 3}};
+        for (const auto& c : sc) {
+            ProblemSpec spec;
+            spec.n = c.n;
+            spec.p = 1;
+            spec.cond = c.cond;
+            spec.seed = c.seed;
+            auto inst = make_problem<double>(spec);
+            Vec<double> x0(inst.X0.col(0).begin(), inst.X0.col(0).end());
+            SolveOptions<double> o;
+            o.tol = c.tol;
+            o.max_iters = c.max_iters;
+            o.recompute_residual_every = c.recompute;
+            char name[64];
+            std::snprintf(name, sizeof name, "cg n=%d rec=%d", c.n, c.recompute);
+            compare(name, cg_solve(inst.A, inst.b, x0, o), gpu_cg_solve(inst.A, inst.b, x0, o));
+            std::snprintf(name, sizeof name, "steepest descent n=%d rec=%d", c.n, c.recompute);
+            SolveOptions<double> os = o;
+            if (os.max_iters < 0) os.max_iters = 400;
+            compare(name, steepest_descent_solve(inst.A, inst.b, x0, os),
+                    gpu_steepest_descent_solve(inst.A, inst.b, x0, os));
+        }
+    }
     {   // gpu_make_problem == make_problem<double>, field by field
         const ProblemSpec specs[] = {{2, 1, 3.0, 4}, {77, 3, 1e3, 9}, {300, 8, 1e4, 21}};
         for (const auto& spec : specs) {
