@@ -368,9 +368,15 @@ def _single_vector_solve(A, b, x0, opts, gpu, algo):
                              "operand shapes do not match")
     every = opts.recompute_residual_every if opts.recompute_residual_every >= 0 else 1
     o = dataclasses.replace(opts, recompute_residual_every=every, algo=algo)
+    name = "cg_solve" if algo == "ccg" else "steepest_descent_solve"
     with GpuContext(n, 1, gpu.device, gpu.arith if algo == "ccg" else "exact") as ctx:
         ctx.set_A(A)
-        t = ctx.solve(b, x0[:, None], o)
+        try:
+            t = ctx.solve(b, x0[:, None], o)
+        except SpdViolationError as ex:  # the scalar solvers' own text (solvers.hpp:448-449, :583-585)
+            k = str(ex).rsplit(" ", 1)[-1]
+            what = "direction" if algo == "ccg" else "gradient"
+            raise SpdViolationError(f"{name}: nonpositive {what} energy at iteration {k}") from None
     # the scalar solvers' own counting (solvers.hpp:438-486, :571-603)
     for rec in t.iterations:
         rc = every > 0 and (rec.k + 1) % every == 0
