@@ -256,3 +256,17 @@ def test_resident_reuse_is_deterministic(m, po):
         t2 = ctx.solve(b, X0, m.SolveOptions(max_iters=70))
     assert np.array_equal(t1.final_x, t2.final_x)
     assert np.array_equal(t1.residual_norms, t2.residual_norms)
+
+
+def test_scalar_solvers_raise_the_reference_texts(m):
+    """cg_solve / steepest_descent_solve on an indefinite matrix: SpdViolationError
+    with the scalar solvers' own messages (solvers.hpp:448-449, :583-585)."""
+    n = 24
+    A = -np.eye(n)
+    b = np.ones(n)
+    x0 = np.linspace(0.0, 1.0, n)
+    with pytest.raises(m.SpdViolationError, match=r"^cg_solve: nonpositive direction energy at iteration 0$"):
+        m.cg_solve(A, b, x0)
+    with pytest.raises(m.SpdViolationError,
+                       match=r"^steepest_descent_solve: nonpositive gradient energy at iteration 0$"):
+        m.steepest_descent_solve(A, b, x0)
