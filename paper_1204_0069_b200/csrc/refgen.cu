@@ -172,7 +172,9 @@ __global__ void __launch_bounds__(32) mgs_proj_kernel(double* __restrict__ W, in
         double x = st[o * 32 + lane];
         if (PEND) {
             x = __dsub_rn(x, __dmul_rn(c, st[SR * 32 + o]));
-            if (store) gblk[(static_cast<size_t>(g) * TR + rr) * 32 + lane] = x;
+            // st.global (not a generic store): a generic store may alias the
+            // shared ring, which would hold every later ring load behind it
+            if (store) __stcg(gblk + (static_cast<size_t>(g) * TR + rr) * 32 + lane, x);
         }
         return __dmul_rn(st[SR * 32 + SR + o], x);
     };
