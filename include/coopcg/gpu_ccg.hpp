@@ -13,7 +13,9 @@
 // (solvers.hpp:111-115), per-iteration records with the reference's mult
 // counting (workplan.hpp:693-715), final_residual_norms by true
 // recomputation (solvers.hpp:188-210).  In the default exact arithmetic mode
-// the trace is bit-identical to ccg_solve's.
+// the trace is bit-identical to ccg_solve's.  The
+// verification-only options keep_history / x_star (trace.hpp:84-85) are
+// rejected with std::invalid_argument rather than silently ignored.
 //
 // GpuSolver keeps A resident on the device between solves (SpdMatrix is
 // immutable, dense.hpp:95-96), the common "many right-hand sides" use.
@@ -38,6 +40,10 @@ struct GpuOptions {
     enum class Arith { exact, fast };
     int device = 0;
     Arith arith = Arith::exact;
+    /// More than one entry: A is row-block sharded over these devices, all
+    /// driven by this process (coopcg_gpu_create_multi; the A.D kernel stores
+    /// its Q rows into every device's Q over NVLink).  Empty: `device` alone.
+    std::vector<int> devices;
 };
 
 namespace gpu_detail {
@@ -74,7 +80,9 @@ public:
     GpuSolver(const SpdMatrix<double>& A, int p, const GpuOptions& g = {}) : n_(A.dim()), p_(p) {
         const int arith = g.arith == GpuOptions::Arith::fast ? COOPCG_ARITH_FAST : COOPCG_ARITH_EXACT;
         if (p < 1 || p >= n_) throw DimensionError("solver: need 1 <= p < n starting columns");
-        int rc = coopcg_gpu_create(n_, p, g.device, arith, &ctx_);
+        int rc = g.devices.size() > 1
+                     ? coopcg_gpu_create_multi(n_, p, static_cast<int>(g.devices.size()), g.devices.data(), arith, &ctx_)
+                     : coopcg_gpu_create(n_, p, g.devices.empty() ? g.device : g.devices[0], arith, &ctx_);
         if (rc != COOPCG_OK) gpu_detail::raise(rc, gpu_detail::last_error(nullptr));
         rc = coopcg_gpu_set_A(ctx_, A.entries().data());
         if (rc != COOPCG_OK) {
@@ -95,6 +103,12 @@ public:
             throw DimensionError("solver: operand shapes do not match the system matrix");
         if (X0.cols() < 1 || X0.cols() >= n_) throw DimensionError("solver: need 1 <= p < n starting columns");
         if (X0.cols() != p_) throw DimensionError("gpu_ccg: agent count differs from the solver's");
+        // The verification-only fields of SolveOptions (trace.hpp:84-85: history
+        // blocks, A-norm errors against an oracle solution) are not produced by
+        // the device solver; refuse them instead of returning an empty record.
+        if (opts.keep_history || opts.x_star != nullptr)
+            throw std::invalid_argument("gpu_ccg: keep_history / x_star (verification mode) are not supported "
+                                        "on the GPU backend; use ccg_solve for invariant checks");
         const int n = n_, p = p_;
         const int max_iters = opts.max_iters >= 0 ? opts.max_iters : 2 * n;  // solvers.hpp:18-23
         const int cap = max_iters > 0 ? max_iters : 1;

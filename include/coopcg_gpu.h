@@ -148,6 +148,9 @@ int coopcg_gpu_gen_householder_rest(coopcg_gpu_ctx* ctx, int r);
 int coopcg_gpu_gen_householder_end(coopcg_gpu_ctx* ctx);
 /* Download this context's row block of A (row-major), for verification. */
 int coopcg_gpu_get_A(coopcg_gpu_ctx* ctx, double* A_rows);
+/* Rows [row0, row0 + rows) of this context's row block (row-major,
+ * rows x n), e.g. to compare a 137 GB matrix with a host copy in slices. */
+int coopcg_gpu_get_A_rows(coopcg_gpu_ctx* ctx, int row0, int rows, double* A_rows);
 
 /* Host-side generators for b and X0. */
 int coopcg_gen_rhs(int n, int kind, uint64_t seed, double* b);
@@ -239,6 +242,41 @@ int coopcg_gpu_end(coopcg_gpu_ctx* ctx, coopcg_trace* trace);
 #define COOPCG_IPC_HANDLE_BYTES 64
 int coopcg_gpu_ipc_handles(coopcg_gpu_ctx* ctx, void* handles_out);
 int coopcg_gpu_set_peers(coopcg_gpu_ctx* ctx, int nranks, int self_rank, const void* handles);
+
+/* ---- multi-GPU inside the library --------------------------
+ * A is split into row blocks (coopcg_row_split: even blocks, rounded to 64-row
+ * panels); every n x p block and the p x p state are replicated, each shard
+ * computes its rows of Q = A_g D and the rows are exchanged once per
+ * iteration (plus R at setup / recompute iterations and S at finalize).  The
+ * run loop enqueues every shard's work and every exchange from the library:
+ * no per-iteration call from the host program.  In exact mode the result is
+ * bit-identical to one GPU for any split (each row's A-chain is local).
+ *
+ * coopcg_gpu_create_multi: ONE process drives ndev devices (a device may
+ *   repeat, e.g. two shards on one GPU).  The kernel that computes a shard's
+ *   rows of Q stores them into every shard's Q over NVLink / NVSwitch peer
+ *   memory (cudaDeviceEnablePeerAccess), so the exchange is a cross-stream
+ *   event barrier, not a collective.  The handle takes the whole-matrix calls:
+ *   set_A (all n rows), gen_A (DIAGDOM, HOUSEHOLDER), get_A[_rows], upload, run,
+ *   solve, timing, matvec_block, numerical_rank; not the phase API.
+ * coopcg_gpu_create_rank: ONE process per GPU (e.g. under torchrun); rank
+ *   `rank` of `nranks` owns coopcg_row_split's block `rank`, and the row
+ *   exchanges are NCCL collectives (grouped in-place broadcasts = an
+ *   all-gather of row blocks) on the context stream, enqueued by
+ *   coopcg_gpu_run.  Every rank calls create / gen_A or set_A (its own rows) /
+ *   upload / run with identical arguments.  `nccl_id` is
+ *   COOPCG_NCCL_ID_BYTES bytes from coopcg_nccl_unique_id on one rank,
+ *   distributed by the caller.  NCCL is loaded on first use (libnccl.so.2). */
+#define COOPCG_NCCL_ID_BYTES 128
+int coopcg_row_split(int n, int parts, int part, int* row_begin, int* row_end);
+int coopcg_gpu_create_multi(int n, int p, int ndev, const int* devices, int arith, coopcg_gpu_ctx** out);
+int coopcg_nccl_unique_id(void* id_out);
+int coopcg_gpu_create_rank(int n, int p, int device, int arith, int nranks, int rank, const void* nccl_id,
+                           coopcg_gpu_ctx** out);
+/* Shards of a context (1 for a single-device or rank context): count, and
+ * for the first `cap` shards their device and row block. */
+int coopcg_gpu_shards(const coopcg_gpu_ctx* ctx, int cap, int* nshards, int* devices, int* row_begin,
+                      int* row_end);
 
 #ifdef __cplusplus
 }

@@ -61,6 +61,8 @@ void orc_gen_diagdom(int n, uint64_t seed, double* A);
 void orc_gen_householder_factors(int n, int m, double kappa, uint64_t seed, double* V,
                                  double* lambda);
 void orc_gen_householder(int n, int m, const double* V, const double* lambda, double* A);
+void orc_gen_diagdom_rows(int n, uint64_t seed, int r0, int r1, double* out);
+void orc_gen_householder_par(int n, int m, const double* V, const double* lambda, double* A);
 void orc_gen_rhs(int n, int kind, uint64_t seed, double* b);
 void orc_gen_starts(int n, int p, uint64_t seed, double* X0_colmajor);
 

@@ -74,6 +74,16 @@ int main() {
         SolveOptions<double> o;
         o.tol = 1e-8;
         compare("degenerate x0 = 0", ccg_solve(inst.A, inst.b, z, o), gpu_ccg(inst.A, inst.b, z, o));
+        // A row-block sharded over two (here: the same) devices from this process
+        GpuOptions g2;
+        g2.devices = {0, 0};
+        SolveOptions<double> o2;
+        o2.tol = 1e-10;
+        compare("gpu_ccg devices={0,0}", ccg_solve(inst.A, inst.b, inst.X0, o2), gpu_ccg(inst.A, inst.b, inst.X0, o2, g2));
+        GpuOptions g3;
+        g3.devices = {0, 0, 0};
+        compare("gpu_mccg devices={0,0,0}", mccg_solve(inst.A, inst.b, inst.X0, o2),
+                gpu_mccg(inst.A, inst.b, inst.X0, o2, g3));
         // GpuSolver: A resident, two right-hand sides
         GpuSolver s(inst.A, 3);
         compare("GpuSolver reuse #1", ccg_solve(inst.A, inst.b, inst.X0, o), s.solve(inst.b, inst.X0, o));
@@ -150,6 +160,13 @@ int main() {
         const bool ok = !ref_msg.empty() && ref_msg == gpu_msg;
         std::printf("%-34s %s (\"%s\")\n", "SpdViolationError", ok ? "same exception" : "MISMATCH", gpu_msg.c_str());
         if (!ok) ++failures;
+        // verification-only options are refused, not silently dropped
+        bool refused = false;
+        SolveOptions<double> oh;
+        oh.keep_history = true;
+        try { gpu_ccg(A, b, X0, oh); } catch (const std::invalid_argument&) { refused = true; }
+        std::printf("%-34s %s\n", "keep_history refused", refused ? "invalid_argument" : "MISMATCH");
+        if (!refused) ++failures;
         bool dim = false;
         try { gpu_ccg(A, Vec<double>(n - 1, 1.0), X0, {}); } catch (const DimensionError&) { dim = true; }
         std::printf("%-34s %s\n", "DimensionError", dim ? "same exception" : "MISMATCH");

@@ -65,6 +65,33 @@ void orc_gen_diagdom(int n, uint64_t seed, double* A) {
     }
 }
 
+/* Rows [r0, r1) of the diagonally dominant A, row-major (r1 - r0) x n, each
+ * element the same pure function of its index as orc_gen_diagdom (the pair
+ * (min, max) draws the two uniforms; the diagonal is the ascending sum of the
+ * row's |off-diagonal| values plus one).  Rows are independent, so the rows
+ * run in parallel (OpenMP) with no change to any element's operation order:
+ * this is how the full-size configs (n = 16384 .. 131072) are generated on
+ * the host for the reference runs.  */
+void orc_gen_diagdom_rows(int n, uint64_t seed, int r0, int r1, double* out) {
+    const uint64_t key = stream_key(seed, SID_DD_MATRIX, (uint64_t)n);
+    const uint64_t un = (uint64_t)n;
+#pragma omp parallel for schedule(dynamic, 8)
+    for (int i = r0; i < r1; ++i) {
+        double* row = out + (size_t)(i - r0) * n;
+        for (int j = 0; j < n; ++j) {
+            if (j == i) continue;
+            const int lo = i < j ? i : j, hi = i < j ? j : i;
+            const double u1 = uniform_pm1(key, (uint64_t)lo * un + (uint64_t)hi + 1);
+            const double u2 = uniform_pm1(key, (uint64_t)hi * un + (uint64_t)lo + 1);
+            row[j] = (u1 + u2) * 0.5;
+        }
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j)
+            if (j != i) acc += fabs(row[j]);
+        row[i] = acc + 1.0;
+    }
+}
+
 void orc_gen_householder_factors(int n, int m, double kappa, uint64_t seed, double* V,
                                  double* lambda) {
     for (int i = 0; i < n; ++i) lambda[i] = pow(kappa, (double)i / (double)(n - 1));
@@ -97,6 +124,45 @@ void orc_gen_householder(int n, int m, const double* V, const double* lambda, do
                 const double m1 = A[(size_t)i * n + j] - t1 * q;
                 A[(size_t)i * n + j] = m1 + t2 * (v[i] * v[j]);
             }
+    }
+    free(w);
+}
+
+/* orc_gen_householder with the row loops in parallel (OpenMP): every w_i is
+ * still one sequential chain over k and every updated element the same
+ * operation sequence, so the result is bit-identical for any thread count. */
+void orc_gen_householder_par(int n, int m, const double* V, const double* lambda, double* A) {
+#pragma omp parallel for schedule(static)
+    for (int i = 0; i < n; ++i) {
+        memset(A + (size_t)i * n, 0, sizeof(double) * (size_t)n);
+        A[(size_t)i * n + i] = lambda[i];
+    }
+    double* w = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int r = m - 1; r >= 0; --r) {
+        const double* v = V + (size_t)r * n;
+        double s = 0.0;
+        for (int k = 0; k < n; ++k) s += v[k] * v[k];
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < n; ++i) {
+            double acc = 0.0;
+            const double* row = A + (size_t)i * n;
+            for (int k = 0; k < n; ++k) acc += row[k] * v[k];
+            w[i] = acc;
+        }
+        double c = 0.0;
+        for (int i = 0; i < n; ++i) c += v[i] * w[i];
+        const double t1 = 2.0 / s;
+        const double t2 = (4.0 * c) / (s * s);
+#pragma omp parallel for schedule(static)
+        for (int i = 0; i < n; ++i) {
+            double* row = A + (size_t)i * n;
+            const double vi = v[i], wi = w[i];
+            for (int j = 0; j < n; ++j) {
+                const double q = vi * w[j] + wi * v[j];
+                const double m1 = row[j] - t1 * q;
+                row[j] = m1 + t2 * (vi * v[j]);
+            }
+        }
     }
     free(w);
 }

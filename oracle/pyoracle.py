@@ -89,6 +89,8 @@ def oracle_lib() -> C.CDLL:
         lib.orc_solve_small.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
         lib.orc_gram.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
         lib.orc_matvec_block.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p]
+        lib.orc_gen_diagdom_rows.argtypes = [C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_void_p]
+        lib.orc_gen_householder_par.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p]
         _libs["orc"] = lib
     return _libs["orc"]
 
@@ -97,11 +99,14 @@ def ref_available() -> bool:
     return os.path.exists(REF_SO)
 
 
-def ref_lib() -> C.CDLL:
-    if "ref" not in _libs:
-        if not os.path.exists(REF_SO):
-            raise FileNotFoundError(f"{REF_SO} missing: run `make -C oracle ref` where /root/reference exists")
-        lib = C.CDLL(REF_SO)
+def ref_lib(path: str = REF_SO) -> C.CDLL:
+    """The compiled reference (path: another build of the same shim, e.g. the
+    FMA-contracted twin oracle/_ref/libccgref_fma.so of tests/golden/make_kdiv.py)."""
+    key = "ref" if path == REF_SO else path
+    if key not in _libs:
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `make -C oracle ref` where /root/reference exists")
+        lib = C.CDLL(path)
         lib.ref_block_solve.argtypes = [C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.POINTER(OrcOpts), C.POINTER(OrcTrace)]
         lib.ref_cg_solve.argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
@@ -114,8 +119,15 @@ def ref_lib() -> C.CDLL:
         lib.ref_gram.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         lib.ref_solve_small.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p]
         lib.ref_numerical_rank.argtypes = [C.c_int, C.c_int, C.c_void_p, C.c_double, C.c_void_p]
-        _libs["ref"] = lib
-    return _libs["ref"]
+        lib.ref_matrix_new.restype = C.c_void_p
+        lib.ref_matrix_new.argtypes = [C.c_int]
+        lib.ref_matrix_data.restype = C.POINTER(C.c_double)
+        lib.ref_matrix_data.argtypes = [C.c_void_p]
+        lib.ref_matrix_free.argtypes = [C.c_void_p]
+        lib.ref_block_solve_m.argtypes = [C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                          C.POINTER(OrcOpts), C.POINTER(OrcTrace)]
+        _libs[key] = lib
+    return _libs[key]
 
 
 def _run(fn, n, p, capacity, *args) -> Trace:
@@ -183,6 +195,45 @@ def ref_solve(A, b, X0, tol=0.0, max_iters=-1, recompute=-1, rank_tol=1e-10, alg
                 X0c.ctypes.data, C.byref(o))
 
 
+class RefMatrix:
+    """An n x n system matrix owned by the reference shim (one host copy: the
+    entries are written in place, then moved into the reference's SpdMatrix).
+    For the full-size BASELINE configs, where A is 2-137 GB."""
+
+    def __init__(self, n: int, lib_path: str = REF_SO):
+        self.n = n
+        self._lib = ref_lib(lib_path)
+        self._h = self._lib.ref_matrix_new(n)
+        if not self._h:
+            raise MemoryError(f"ref_matrix_new({n}) failed ({8 * n * n / 1e9:.1f} GB)")
+        ptr = self._lib.ref_matrix_data(self._h)
+        self.A = np.ctypeslib.as_array(ptr, shape=(n, n))  # writable view of the entries
+
+    def solve(self, b, X0, tol=0.0, max_iters=-1, recompute=-1, rank_tol=1e-10, algo="parallel") -> Trace:
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        X0 = np.asarray(X0, dtype=np.float64)
+        n, p = X0.shape
+        assert n == self.n
+        X0c = np.ascontiguousarray(X0.T)
+        cap = max_iters if max_iters >= 0 else 2 * n
+        o = _opts(tol, max_iters, recompute, rank_tol)
+        code = {"ccg": 0, "parallel": 1, "mccg": 2}[algo]
+        return _run(self._lib.ref_block_solve_m, n, p, cap, code, self._h, p, b.ctypes.data,
+                    X0c.ctypes.data, C.byref(o))
+
+    def close(self):
+        if self._h:
+            self.A = None
+            self._lib.ref_matrix_free(self._h)
+            self._h = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+
 def ref_cg(A, b, x0, tol=0.0, max_iters=-1, recompute=-1, algo="cg") -> Trace:
     """The reference's cg_solve (algo="sd": steepest_descent_solve)."""
     A = np.ascontiguousarray(A, dtype=np.float64)
@@ -220,6 +271,23 @@ def gen_diagdom(n, seed):
     A = np.zeros((n, n))
     oracle_lib().orc_gen_diagdom(n, seed, A.ctypes.data)
     return A
+
+
+def gen_diagdom_rows(n, seed, r0, r1, out=None):
+    """Rows [r0, r1) of gen_diagdom(n, seed) (OpenMP over rows, same bits)."""
+    if out is None:
+        out = np.empty((r1 - r0, n))
+    assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == (r1 - r0) * n
+    oracle_lib().orc_gen_diagdom_rows(n, seed, r0, r1, out.ctypes.data)
+    return out
+
+
+def gen_householder_into(n, m, kappa, seed, out):
+    """gen_householder(n, m, kappa, seed) written into `out` (OpenMP over rows, same bits)."""
+    V, lam = gen_householder_factors(n, m, kappa, seed)
+    assert out.dtype == np.float64 and out.flags.c_contiguous and out.size == n * n
+    oracle_lib().orc_gen_householder_par(n, m, V.ctypes.data, lam.ctypes.data, out.ctypes.data)
+    return out
 
 
 def gen_householder_factors(n, m, kappa, seed):

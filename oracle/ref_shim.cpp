@@ -17,7 +17,11 @@
 #include <cstdio>
 #include <cstring>
 #include <exception>
+#include <memory>
+#include <optional>
 #include <vector>
+
+#include <sys/mman.h>
 
 #include "coopcg/parallel.hpp"
 #include "coopcg/problem.hpp"
@@ -105,31 +109,98 @@ SpdMatrix<double> make_A(int n, const double* A) {
     return SpdMatrix<double>(n, std::vector<double>(A, A + (size_t)n * n), SpdCheck::skip);
 }
 
+// A system matrix owned by the shim, for the full-size BASELINE configs
+// (A = 34 / 137 GB at cfg 3 / 4): the caller fills the entries in place
+// (ref_matrix_data) and the vector is then MOVED into the reference's
+// SpdMatrix (SpdCheck::skip: the generators are exactly symmetric, so the
+// float-mode symmetrisation would be the identity, dense.hpp:104-122), so
+// the host holds one copy of A, not two as make_A does.
+struct RefMatrix {
+    int n = 0;
+    double* data = nullptr;
+    std::vector<double> v;
+    std::optional<SpdMatrix<double>> m;
+    const SpdMatrix<double>& sealed() {
+        if (!m) {
+            m.emplace(n, std::move(v), SpdCheck::skip);
+            data = const_cast<double*>(m->entries().data());
+        }
+        return *m;
+    }
+};
+
+int block_solve(int algo, const SpdMatrix<double>& Am, int n, int p, const double* b, const double* X0,
+                const orc_opts* o, orc_trace* tr) {
+    std::vector<double> bv(b, b + n);
+    DenseBlock<double> x0(n, p);
+    for (int j = 0; j < p; ++j)
+        for (int i = 0; i < n; ++i) x0(i, j) = X0[(size_t)j * n + i];
+    SolveOptions<double> opts;
+    opts.tol = o->tol;
+    opts.max_iters = o->max_iters;
+    opts.recompute_residual_every = o->recompute_residual_every;
+    opts.rank_rel_tol = o->rank_rel_tol;
+    SolveTrace<double> t;
+    if (algo == 0) t = ccg_solve(Am, bv, x0, opts);
+    else if (algo == 1) t = parallel_ccg(Am, bv, x0, opts, p);
+    else t = mccg_solve(Am, bv, x0, opts);
+    fill_trace(t, n, tr);
+    return 0;
+}
+
 } // namespace
 
 extern "C" {
+
+/// A shim-owned n x n matrix (row-major entries, filled by the caller through
+/// ref_matrix_data before the first solve).  NULL if the allocation fails.
+void* ref_matrix_new(int n) {
+    try {
+        auto* h = new RefMatrix;
+        h->n = n;
+        const size_t N = static_cast<size_t>(n) * n;
+        // reserve (mmap, untouched), ask for transparent huge pages and fault
+        // the pages in from every core: resize()'s single-threaded zero fill
+        // of up to 137 GB then runs on mapped memory instead of taking 4 KB
+        // page faults one at a time
+        h->v.reserve(N);
+        {
+            const uintptr_t a = reinterpret_cast<uintptr_t>(h->v.data());
+            const uintptr_t lo = (a + 4095) & ~uintptr_t(4095), hi = (a + N * sizeof(double)) & ~uintptr_t(4095);
+            if (hi > lo) madvise(reinterpret_cast<void*>(lo), hi - lo, MADV_HUGEPAGE);
+            char* base = reinterpret_cast<char*>(h->v.data());
+            const size_t bytes = N * sizeof(double), chunk = size_t(64) << 20;
+#pragma omp parallel for schedule(dynamic, 1)
+            for (long long c = 0; c < (long long)((bytes + chunk - 1) / chunk); ++c) {
+                const size_t o = (size_t)c * chunk;
+                std::memset(base + o, 0, std::min(chunk, bytes - o));
+            }
+        }
+        h->v.resize(N);
+        h->data = h->v.data();
+        return h;
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+double* ref_matrix_data(void* h) { return static_cast<RefMatrix*>(h)->data; }
+
+void ref_matrix_free(void* h) { delete static_cast<RefMatrix*>(h); }
+
+/// ref_block_solve on a shim-owned matrix (no copy of A).
+int ref_block_solve_m(int algo, void* h, int p, const double* b, const double* X0, const orc_opts* o,
+                      orc_trace* tr) {
+    tr->error_msg[0] = '\0';
+    auto* rm = static_cast<RefMatrix*>(h);
+    return guarded(tr, [&] { block_solve(algo, rm->sealed(), rm->n, p, b, X0, o, tr); });
+}
 
 /// algo: 0 = ccg_solve, 1 = parallel_ccg (p OpenMP threads), 2 = mccg_solve.
 int ref_block_solve(int algo, int n, int p, const double* A, const double* b, const double* X0,
                     const orc_opts* o, orc_trace* tr) {
     tr->error_msg[0] = '\0';
-    return guarded(tr, [&] {
-        auto Am = make_A(n, A);
-        std::vector<double> bv(b, b + n);
-        DenseBlock<double> x0(n, p);
-        for (int j = 0; j < p; ++j)
-            for (int i = 0; i < n; ++i) x0(i, j) = X0[(size_t)j * n + i];
-        SolveOptions<double> opts;
-        opts.tol = o->tol;
-        opts.max_iters = o->max_iters;
-        opts.recompute_residual_every = o->recompute_residual_every;
-        opts.rank_rel_tol = o->rank_rel_tol;
-        SolveTrace<double> t;
-        if (algo == 0) t = ccg_solve(Am, bv, x0, opts);
-        else if (algo == 1) t = parallel_ccg(Am, bv, x0, opts, p);
-        else t = mccg_solve(Am, bv, x0, opts);
-        fill_trace(t, n, tr);
-    });
+    return guarded(tr, [&] { block_solve(algo, make_A(n, A), n, p, b, X0, o, tr); });
 }
 
 int ref_cg_solve(int n, const double* A, const double* b, const double* x0, const orc_opts* o,

@@ -28,5 +28,7 @@ from .solver import (  # noqa: F401
     gen_starts,
     iteration_mults,
     library_version,
+    nccl_unique_id,
+    row_split,
 )
 from .configs import CONFIGS, make_problem_on_device, make_reference_problem_on_device  # noqa: F401

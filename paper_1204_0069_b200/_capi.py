@@ -52,6 +52,7 @@ SIGNATURES = [
     ("coopcg_gpu_set_A", _I, [_VP, _VP]),
     ("coopcg_gpu_gen_A", _I, [_VP, _I, C.c_uint64, _I, C.c_double]),
     ("coopcg_gpu_get_A", _I, [_VP, _VP]),
+    ("coopcg_gpu_get_A_rows", _I, [_VP, _I, _I, _VP]),
     ("coopcg_gpu_gen_householder_begin", _I, [_VP, C.c_uint64, _I, C.c_double]),
     ("coopcg_gpu_gen_householder_local", _I, [_VP, _I]),
     ("coopcg_gpu_gen_householder_rest", _I, [_VP, _I]),
@@ -78,7 +79,13 @@ SIGNATURES = [
     ("coopcg_gpu_end", _I, [_VP, C.POINTER(coopcg_trace)]),
     ("coopcg_gpu_ipc_handles", _I, [_VP, _VP]),
     ("coopcg_gpu_set_peers", _I, [_VP, _I, _I, _VP]),
+    ("coopcg_row_split", _I, [_I, _I, _I, C.POINTER(_I), C.POINTER(_I)]),
+    ("coopcg_gpu_create_multi", _I, [_I, _I, _I, C.POINTER(_I), _I, C.POINTER(_VP)]),
+    ("coopcg_nccl_unique_id", _I, [_VP]),
+    ("coopcg_gpu_create_rank", _I, [_I, _I, _I, _I, _I, _I, _VP, C.POINTER(_VP)]),
+    ("coopcg_gpu_shards", _I, [_VP, _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
 ]
+NCCL_ID_BYTES = 128
 
 PH_SETUP_LOCAL, PH_SETUP_REST, PH_ITER_LOCAL, PH_ITER_MID, PH_ITER_REST, PH_FINAL_LOCAL, PH_FINAL_REST, PH_MCCG_SETUP = range(8)
 BLOCK_X, BLOCK_R, BLOCK_D, BLOCK_Q, BLOCK_S, BLOCK_W = range(6)

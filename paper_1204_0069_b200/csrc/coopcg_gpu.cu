@@ -21,7 +21,12 @@
 #include <string>
 #include <vector>
 #include <cstdlib>
+#include <mutex>
+#include <type_traits>
 #include <utility>
+
+#include <dlfcn.h>
+#include <nccl.h>  // types only: the library is dlopen'ed on first use (nccl_api)
 
 #include "../../include/coopcg_gpu.h"
 #include "common.cuh"
@@ -47,7 +52,8 @@ constexpr int ad_T() { return P >= 8 ? 64 : 32; }
 template <int P>
 constexpr int ad_S() { return P >= 8 ? 2 : 4; }
 constexpr int kChunkMax = 16;
-constexpr int kMaxParts = 296;  // 2 x 148 SMs
+constexpr int kMaxParts = 296;  // cap on per-CTA partial slots (2 x 148 SMs on a B200)
+constexpr int kMaxDevices = 64;
 
 int grid_for(size_t elems, int block) {
     size_t g = (elems + block - 1) / block;
@@ -59,6 +65,62 @@ int pad_cols(int p) {
     return P;
 }
 
+// NCCL, loaded on first use by a rank context (coopcg_gpu_create_rank): the
+// copy already mapped into the process (torch's) if there is one, else the
+// system's libnccl.so.2.  Single-process contexts never load it.  The loaded
+// table is the library's only process-wide state (initialised once).
+struct NcclApi {
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+    std::string err;
+};
+
+const NcclApi& nccl_api() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            const char* e = dlerror();
+            api.err = std::string("dlopen(libnccl.so.2): ") + (e ? e : "?");
+            return;
+        }
+        bool ok = true;
+        auto sym = [&](auto& fp, const char* name) {
+            fp = reinterpret_cast<std::remove_reference_t<decltype(fp)>>(dlsym(h, name));
+            if (!fp) {
+                ok = false;
+                api.err += std::string(api.err.empty() ? "" : "; ") + "missing " + name;
+            }
+        };
+        sym(api.getUniqueId, "ncclGetUniqueId");
+        sym(api.commInitRank, "ncclCommInitRank");
+        sym(api.commDestroy, "ncclCommDestroy");
+        sym(api.broadcast, "ncclBroadcast");
+        sym(api.groupStart, "ncclGroupStart");
+        sym(api.groupEnd, "ncclGroupEnd");
+        sym(api.errorString, "ncclGetErrorString");
+        if (!ok) api.getUniqueId = nullptr;
+    });
+    return api;
+}
+
+// Even row blocks for `parts` shards, rounded up to 64-row panels when every
+// shard keeps rows (coopcg_row_split; identical on every rank).
+void row_split(int n, int parts, int part, int* r0, int* r1) {
+    int per = (n + parts - 1) / parts;
+    const int aligned = (per + 63) / 64 * 64;
+    if ((long long)aligned * (parts - 1) < n) per = aligned;
+    *r0 = std::min(n, part * per);
+    *r1 = std::min(n, *r0 + per);
+}
+
 struct AdConfig {
     int BR = 64;
     int CPT = 4;
@@ -68,6 +130,7 @@ struct AdConfig {
 
 struct coopcg_gpu_ctx {
     int n = 0, p = 0, P = 0, device = 0, arith = 0;
+    int sms = 148;  // multiprocessors of `device` (queried at creation)
     int row0 = 0, row1 = 0, n_loc = 0, brs = 6, npanels = 0;
     size_t ap_elems = 0;
     ALay lay{0, 6, 0};
@@ -142,6 +205,17 @@ struct coopcg_gpu_ctx {
     // the vector w (all n rows; this context writes its own) and t1, t2
     double *hh_V = nullptr, *hh_lam = nullptr, *hh_w = nullptr, *hh_t = nullptr;
     int hh_m = -1;
+    // ---- multi-GPU ---------------------------------------
+    // A group handle (coopcg_gpu_create_multi): one process drives the row
+    // shards `shards` (one per listed device; a device may repeat).  The
+    // handle owns no device memory of its own; every call is routed to the
+    // shards and the run loop enqueues every shard's work from this thread.
+    std::vector<coopcg_gpu_ctx*> shards;
+    std::vector<cudaEvent_t> gev;   // one cross-stream barrier event per shard
+    // A rank context (coopcg_gpu_create_rank): one process per GPU, the row
+    // exchanges are NCCL collectives on this context's stream.
+    void* nccl = nullptr;           // ncclComm_t
+    int nranks = 1, rank = 0;
 };
 
 static void hh_free(coopcg_gpu_ctx* ctx) {
@@ -254,13 +328,13 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
     else
         kern = push ? ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, true> : ad_exact_rpt_kernel<P, CPT, BR, T, S, 2, false>;
     const size_t smem = pipe ? ad_pipe_smem(P, BR, PT, PS) : ad_smem<P, CPT, BR>();
-    static bool attr_done[2][64] = {};
-    const int dev = ctx->device & 63;
-    if (!attr_done[push][dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_done[push][dev] = true;
-    }
+    // the shared-memory opt-in, once per (instantiation, device); thread-safe
+    static std::once_flag attr_once[2][kMaxDevices];
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once[push][ctx->device % kMaxDevices], [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
     dim3 grid((ctx->n_loc + BR - 1) / BR);
     dim3 block(32 + 32 * ad_consumer_warps(BR / RPT, P / KC));
     pdl_launch(kern, dim3(grid), dim3(block), smem, ctx->stream, ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop,
@@ -306,13 +380,12 @@ cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
     constexpr int WN = fast_wn<P>();
     constexpr bool TR = P >= 16;
     auto kern = ad_fast_kernel<P, WN, TR>;
-    static bool attr_done[64] = {};
-    const int dev = ctx->device & 63;
-    if (!attr_done[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_ad_smem<P>());
-        if (e != cudaSuccess) return e;
-        attr_done[dev] = true;
-    }
+    static std::once_flag attr_once[kMaxDevices];
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once[ctx->device % kMaxDevices], [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fast_ad_smem<P>());
+    });
+    if (attr_err != cudaSuccess) return attr_err;
     const double* operand = src;
     if (TR) {  // operand -> [col][kk] k-tiles (conflict-free B fragments at P >= 16)
         const size_t tot = (size_t)ctx->lay.ntiles * P * kFastT;
@@ -388,15 +461,15 @@ cudaError_t fast_solve(coopcg_gpu_ctx* ctx, int mode) {
     }
 }
 
-AdConfig pick_ad_config(int n_loc, int P) {
+AdConfig pick_ad_config(int n_loc, int P, int sms) {
     AdConfig c;
     // Measured sweep (tools/probe/ad_probe.cu, profiles/; ring shapes: ad_T / ad_S);
     // P=4: 2 cols/thread (7.1 TB/s at n=16384), P=8: 4 (5.0 TB/s),
     // P=16/32: 4 cols x 2 rows (FP64-issue bound in exact mode, ~13 of 18 T instr/s).
     // Above one CTA per SM at BR = 64, P = 8 switches to 128-row panels for the
     // pipelined kernel (tools/probe/ad_v3_probe.cu).
-    c.BR = (n_loc >= 148 * 64) ? 64 : 32;
-    if (P == 8 && n_loc > 148 * 64) c.BR = 128;
+    c.BR = (n_loc >= sms * 64) ? 64 : 32;
+    if (P == 8 && n_loc > sms * 64) c.BR = 128;
     c.CPT = (P == 4) ? 2 : 4;  // with 2 rows per thread at P >= 16
     return c;
 }
@@ -558,8 +631,14 @@ size_t rank_smem(int P) { return 2ull * kRankTile * P * sizeof(double) + 2 * siz
 
 int destroy_impl(coopcg_gpu_ctx* ctx) {
     if (!ctx) return COOPCG_OK;
+    for (size_t g = 0; g < ctx->gev.size(); ++g) {
+        cudaSetDevice(ctx->shards[g]->device);
+        if (ctx->gev[g]) cudaEventDestroy(ctx->gev[g]);
+    }
+    for (coopcg_gpu_ctx* c : ctx->shards) destroy_impl(c);
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    if (ctx->nccl) nccl_api().commDestroy(static_cast<ncclComm_t>(ctx->nccl));
     cudaFree(ctx->At);
     cudaFree(ctx->X);
     cudaFree(ctx->X0);
@@ -612,7 +691,9 @@ int ensure_trace_capacity(coopcg_gpu_ctx* ctx, int cap) {
     ctx->tr_norms = nullptr;
     ctx->tr_minres = nullptr;
     ctx->tr_wall = nullptr;
-    CK(cudaMalloc(&ctx->tr_norms, sizeof(double) * (size_t)cap * ctx->p));
+    // rows are p_orig wide (the kernels write tr_norms[k * p0 + j]; a previous
+    // mccg solve may have left ctx->p reduced)
+    CK(cudaMalloc(&ctx->tr_norms, sizeof(double) * (size_t)cap * ctx->p_orig));
     CK(cudaMalloc(&ctx->tr_minres, sizeof(double) * (size_t)cap));
     CK(cudaMalloc(&ctx->tr_wall, sizeof(unsigned long long) * (size_t)cap));
     ctx->tr_capacity = cap;
@@ -640,6 +721,16 @@ double host_normal(uint64_t key, uint64_t t) {
 }
 
 }  // namespace
+
+// Group handles (coopcg_gpu_create_multi) route the C ABI to their shards;
+// defined at the end of this file.
+static bool is_group(const coopcg_gpu_ctx* ctx) { return ctx && !ctx->shards.empty(); }
+static int group_set_A(coopcg_gpu_ctx* ctx, const double* A_rows);
+static int group_get_A_rows(coopcg_gpu_ctx* ctx, int row0, int rows, double* A_rows);
+static int group_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double kappa);
+static int group_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0);
+static int group_matvec_block(coopcg_gpu_ctx* ctx, const double* D, double* out);
+static int rank_gen_householder(coopcg_gpu_ctx* ctx, uint64_t seed, int m, double kappa);
 
 // =============================================================================
 // C ABI
@@ -677,7 +768,12 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
     ctx->row0 = row_begin;
     ctx->row1 = row_end;
     ctx->n_loc = row_end - row_begin;
-    ctx->ad = pick_ad_config(ctx->n_loc, ctx->P);
+    {
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && sms > 0)
+            ctx->sms = sms;
+    }
+    ctx->ad = pick_ad_config(ctx->n_loc, ctx->P, ctx->sms);
     if (arith == COOPCG_ARITH_FAST) {
         const int ntiles = (n + kFastT - 1) / kFastT;
         ctx->npanels = (ctx->n_loc + kFastBR - 1) / kFastBR;
@@ -686,7 +782,7 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         // Work units = (panel, k-chunk) on persistent CTAs (2 per SM).  Pick the
         // k-split with the best wave efficiency units/slots / ceil(units/slots)
         // (one wave for small n; e.g. n=65536: 1024 panels x 2 = 6.92 waves).
-        const int slots = 2 * 148;
+        const int slots = std::min(2 * ctx->sms, kMaxParts);
         int best_k = 1;
         double best_eff = -1.0;
         for (int kc = 1; kc <= std::min(16, ntiles); ++kc) {
@@ -793,6 +889,7 @@ int coopcg_gpu_create(int n, int p, int device, int arith, coopcg_gpu_ctx** out)
 int coopcg_gpu_destroy(coopcg_gpu_ctx* ctx) { return destroy_impl(ctx); }
 
 int coopcg_gpu_set_A(coopcg_gpu_ctx* ctx, const double* A_rows) {
+    if (is_group(ctx)) return A_rows ? group_set_A(ctx, A_rows) : COOPCG_E_INVALID;
     if (!ctx || !A_rows) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     const int n = ctx->n;
@@ -811,22 +908,31 @@ int coopcg_gpu_set_A(coopcg_gpu_ctx* ctx, const double* A_rows) {
     return COOPCG_OK;
 }
 
-int coopcg_gpu_get_A(coopcg_gpu_ctx* ctx, double* A_rows) {
+int coopcg_gpu_get_A_rows(coopcg_gpu_ctx* ctx, int row0, int rows, double* A_rows) {
+    if (is_group(ctx)) return A_rows ? group_get_A_rows(ctx, row0, rows, A_rows) : COOPCG_E_INVALID;
     if (!ctx || !A_rows) return COOPCG_E_INVALID;
     if (!ctx->a_ready) return fail(ctx, COOPCG_E_STATE, "A not set");
+    if (row0 < 0 || rows < 0 || row0 + rows > ctx->n_loc)
+        return fail(ctx, COOPCG_E_DIMENSION, "get_A_rows: row range outside this context's rows");
     CK(cudaSetDevice(ctx->device));
     const int n = ctx->n;
     const int chunk = (int)std::max<size_t>(1, std::min<size_t>(ctx->stage_elems / n, 4096));
-    for (int r0 = 0; r0 < ctx->n_loc; r0 += chunk) {
-        const int rows = std::min(chunk, ctx->n_loc - r0);
-        dim3 grid((n + 31) / 32, (rows + 31) / 32);
-        untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->lay, r0, rows, n, ctx->stage);
+    for (int r = 0; r < rows; r += chunk) {
+        const int m = std::min(chunk, rows - r);
+        dim3 grid((n + 31) / 32, (m + 31) / 32);
+        untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->lay, row0 + r, m, n,
+                                                                      ctx->stage);
         CKL();
-        CK(cudaMemcpyAsync(A_rows + (size_t)r0 * n, ctx->stage, sizeof(double) * (size_t)rows * n,
+        CK(cudaMemcpyAsync(A_rows + (size_t)r * n, ctx->stage, sizeof(double) * (size_t)m * n,
                            cudaMemcpyDeviceToHost, ctx->stream));
         CK(cudaStreamSynchronize(ctx->stream));
     }
     return COOPCG_OK;
+}
+
+int coopcg_gpu_get_A(coopcg_gpu_ctx* ctx, double* A_rows) {
+    if (!ctx || !A_rows) return COOPCG_E_INVALID;
+    return coopcg_gpu_get_A_rows(ctx, 0, ctx->n_loc, A_rows);
 }
 
 int coopcg_gen_householder_factors(int n, int m, double kappa, uint64_t seed, double* V, double* lambda) {
@@ -858,6 +964,8 @@ int coopcg_gen_starts(int n, int p, uint64_t seed, double* X0) {
 }
 
 int coopcg_gpu_gen_householder_begin(coopcg_gpu_ctx* ctx, uint64_t seed, int m, double kappa) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx || m < 0) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     const int n = ctx->n;
@@ -871,7 +979,7 @@ int coopcg_gpu_gen_householder_begin(coopcg_gpu_ctx* ctx, uint64_t seed, int m, 
     CK(cudaMemcpyAsync(ctx->hh_V, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->hh_lam, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(ctx->hh_w, 0, sizeof(double) * n, ctx->stream));
-    hh_init_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, ctx->n_loc, ctx->row0, ctx->hh_lam,
+    hh_init_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, ctx->n_loc, ctx->row0, ctx->hh_lam,
                                                      ctx->ap_elems);
     CKL();
     CK(cudaStreamSynchronize(ctx->stream));  // the host factors are freed on return
@@ -881,6 +989,8 @@ int coopcg_gpu_gen_householder_begin(coopcg_gpu_ctx* ctx, uint64_t seed, int m, 
 }
 
 int coopcg_gpu_gen_householder_local(coopcg_gpu_ctx* ctx, int r) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx) return COOPCG_E_INVALID;
     if (ctx->hh_m < 0 || r < 0 || r >= ctx->hh_m)
         return fail(ctx, COOPCG_E_STATE, "gen_householder_local: reflector %d outside a begun generation", r);
@@ -892,19 +1002,23 @@ int coopcg_gpu_gen_householder_local(coopcg_gpu_ctx* ctx, int r) {
 }
 
 int coopcg_gpu_gen_householder_rest(coopcg_gpu_ctx* ctx, int r) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx) return COOPCG_E_INVALID;
     if (ctx->hh_m < 0 || r < 0 || r >= ctx->hh_m)
         return fail(ctx, COOPCG_E_STATE, "gen_householder_rest: reflector %d outside a begun generation", r);
     CK(cudaSetDevice(ctx->device));
     const double* v = ctx->hh_V + (size_t)r * ctx->n;
     hh_scalars_kernel<<<1, 32, 0, ctx->stream>>>(ctx->n, v, ctx->hh_w, ctx->hh_t);
-    hh_update_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, ctx->n, ctx->n_loc, ctx->row0, v, ctx->hh_w,
+    hh_update_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, ctx->n, ctx->n_loc, ctx->row0, v, ctx->hh_w,
                                                        ctx->hh_t, ctx->ap_elems);
     CKL();
     return COOPCG_OK;
 }
 
 int coopcg_gpu_gen_householder_end(coopcg_gpu_ctx* ctx) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx) return COOPCG_E_INVALID;
     if (ctx->hh_m < 0) return fail(ctx, COOPCG_E_STATE, "gen_householder_end without begin");
     CK(cudaSetDevice(ctx->device));
@@ -915,18 +1029,20 @@ int coopcg_gpu_gen_householder_end(coopcg_gpu_ctx* ctx) {
 }
 
 int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double kappa) {
+    if (is_group(ctx)) return group_gen_A(ctx, kind, seed, m, kappa);
     if (!ctx) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     const int n = ctx->n;
     if (kind == COOPCG_MATRIX_DIAGDOM) {
         const uint64_t key = stream_key(seed, 101, (uint64_t)n);
-        gen_dd_offdiag_kernel<<<148 * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, ctx->n_loc, ctx->row0, key,
+        gen_dd_offdiag_kernel<<<ctx->sms * 8, 256, 0, ctx->stream>>>(ctx->At, ctx->lay, n, ctx->n_loc, ctx->row0, key,
                                                                  ctx->ap_elems);
         CKL();
         gen_dd_diag_kernel<<<(ctx->n_loc + 127) / 128, 128, 0, ctx->stream>>>(ctx->At, ctx->lay, n, ctx->n_loc,
                                                                              ctx->row0);
         CKL();
     } else if (kind == COOPCG_MATRIX_HOUSEHOLDER) {
+        if (ctx->n_loc != n && ctx->nccl) return rank_gen_householder(ctx, seed, m, kappa);
         if (ctx->n_loc != n)
             return fail(ctx, COOPCG_E_INVALID,
                         "row-sharded Householder generation exchanges w: use coopcg_gpu_gen_householder_*");
@@ -950,6 +1066,7 @@ int coopcg_gpu_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double
 }
 
 int coopcg_gpu_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0) {
+    if (is_group(ctx)) return (b && X0) ? group_upload(ctx, b, X0) : COOPCG_E_INVALID;
     if (!ctx || !b || !X0) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     const int n = ctx->n, p = ctx->p_orig, P = ctx->P;
@@ -999,6 +1116,24 @@ static int restrict_to(coopcg_gpu_ctx* ctx, const std::vector<int>& keep, double
     for (double* b : blks) {
         compact_columns_kernel<<<(n + 127) / 128, 128, 0, ctx->stream>>>(b, n, ctx->P, kl, pk);
         CKL();
+    }
+    // The per-agent vectors of the small state (|D_j|^2 from the last rank
+    // check, |R_j|^2, norms) are still in the old slot order: compact them
+    // too, so the fast mode's SPD guard pairs each new slot's Gram diagonal
+    // with its own direction norm on the first iteration after a restriction.
+    {
+        const SmallLayout L{ctx->P};
+        const int P = ctx->P;
+        std::vector<double> vec(4 * (size_t)P);
+        CK(cudaMemcpyAsync(vec.data(), ctx->small + L.nsq_d(), sizeof(double) * 4 * P, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+        std::vector<double> out(vec);
+        for (int v = 0; v < 4; ++v)
+            for (int c = 0; c < pk; ++c) out[(size_t)v * P + c] = vec[(size_t)v * P + keep[c]];
+        CK(cudaMemcpyAsync(ctx->small + L.nsq_d(), out.data(), sizeof(double) * 4 * P, cudaMemcpyHostToDevice,
+                           ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
     }
     std::vector<int> nid(pk);
     for (int c = 0; c < pk; ++c) nid[c] = ctx->ids[keep[c]];
@@ -1453,28 +1588,168 @@ static int end_impl(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
     return COOPCG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Row exchanges between the shards of a solve.  One solve is
+// run by a set of LOCAL contexts (the shards this process drives) under one of
+//   mode 0  one context holding every row (nothing to exchange),
+//   mode 1  shards of one process (coopcg_gpu_create_multi): Q rows are pushed
+//           into every shard's Q by the kernel that computes them (peer
+//           stores over NVLink, or plain stores when shards share a device)
+//           and the exchange is a cross-stream event barrier; R / S / w rows
+//           are peer copies between two barriers,
+//   mode 2  one rank context per process (coopcg_gpu_create_rank): every row
+//           exchange is an all-gather of the row blocks (grouped in-place NCCL
+//           broadcasts, one per rank) on the context stream.
+// Everything is stream-ordered: the host enqueues whole chunks of iterations
+// for every shard and reads one control snapshot per chunk, as for one GPU.
+struct Exch {
+    int mode = 0;
+    std::vector<coopcg_gpu_ctx*> s;        // local shards, rank order (s[0] records the trace)
+    std::vector<cudaEvent_t>* ev = nullptr; // mode 1: one barrier event per shard
+};
+
+static Exch exch_of(coopcg_gpu_ctx* ctx) {
+    Exch X;
+    if (!ctx->shards.empty()) {
+        X.mode = 1;
+        X.s = ctx->shards;
+        X.ev = &ctx->gev;
+    } else {
+        X.mode = ctx->nccl ? 2 : 0;
+        X.s = {ctx};
+    }
+    return X;
+}
+
+// Run f on every local shard (its device current); a failure's message is
+// copied to the handle h.
+template <typename F>
+static int each(coopcg_gpu_ctx* h, const Exch& X, F&& f) {
+    for (coopcg_gpu_ctx* c : X.s) {
+        if (X.s.size() > 1 || c != h) {
+            cudaError_t e = cudaSetDevice(c->device);
+            if (e != cudaSuccess) return fail(h, COOPCG_E_CUDA, "cudaSetDevice(%d): %s", c->device, cudaGetErrorString(e));
+        }
+        if (int rc = f(c)) {
+            if (c != h) h->msg = c->msg;
+            return rc;
+        }
+    }
+    return COOPCG_OK;
+}
+
+// mode 1: every shard's stream waits for every other shard's current position.
+static int xbarrier(coopcg_gpu_ctx* ctx, const Exch& X) {
+    if (X.mode != 1 || X.s.size() < 2) return COOPCG_OK;
+    for (size_t g = 0; g < X.s.size(); ++g) {
+        CK(cudaSetDevice(X.s[g]->device));
+        CK(cudaEventRecord((*X.ev)[g], X.s[g]->stream));
+    }
+    for (size_t h = 0; h < X.s.size(); ++h) {
+        CK(cudaSetDevice(X.s[h]->device));
+        for (size_t g = 0; g < X.s.size(); ++g)
+            if (g != h) CK(cudaStreamWaitEvent(X.s[h]->stream, (*X.ev)[g], 0));
+    }
+    return COOPCG_OK;
+}
+
+// Device buffer of block `which` (n rows, ld doubles per row) on shard c.
+static double* block_of(coopcg_gpu_ctx* c, int which, int k, int* ld) {
+    *ld = c->P;
+    switch (which) {
+    case COOPCG_BLOCK_R: return c->R;
+    case COOPCG_BLOCK_Q: return (c->p2p && (k & 1)) ? c->Qalt : c->Q;
+    case COOPCG_BLOCK_S: return c->S;
+    case COOPCG_BLOCK_W: *ld = 1; return c->hh_w;
+    default: return nullptr;
+    }
+}
+
+static const char* nccl_err(ncclResult_t r) {
+    const NcclApi& api = nccl_api();
+    return api.errorString ? api.errorString(r) : "nccl error";
+}
+
+// All-gather of the row blocks of `which`: afterwards every shard holds every
+// shard's rows [row0, row1).
+static int xrows(coopcg_gpu_ctx* ctx, const Exch& X, int which, int k) {
+    if (X.mode == 0) return COOPCG_OK;
+    if (X.mode == 2) {
+        coopcg_gpu_ctx* c = X.s[0];
+        const NcclApi& api = nccl_api();
+        int ld = 0;
+        double* buf = block_of(c, which, k, &ld);
+        ncclResult_t r = api.groupStart();
+        for (int q = 0; q < c->nranks && r == ncclSuccess; ++q) {
+            int r0 = 0, r1 = 0;
+            row_split(c->n, c->nranks, q, &r0, &r1);
+            if (r1 > r0)
+                r = api.broadcast(buf + (size_t)r0 * ld, buf + (size_t)r0 * ld, (size_t)(r1 - r0) * ld, ncclFloat64,
+                                  q, static_cast<ncclComm_t>(c->nccl), c->stream);
+        }
+        ncclResult_t r2 = api.groupEnd();
+        if (r != ncclSuccess || r2 != ncclSuccess)
+            return fail(ctx, COOPCG_E_CUDA, "NCCL all-gather of rows: %s", nccl_err(r != ncclSuccess ? r : r2));
+        return COOPCG_OK;
+    }
+    if (X.s.size() < 2) return COOPCG_OK;
+    // every shard has reached the exchange (no later write of a peer's rows
+    // can race with the copies), copies, and every copy has landed
+    if (int rc = xbarrier(ctx, X)) return rc;
+    for (coopcg_gpu_ctx* g : X.s) {
+        CK(cudaSetDevice(g->device));
+        int ld = 0;
+        const double* src = block_of(g, which, k, &ld) + (size_t)g->row0 * ld;
+        const size_t bytes = sizeof(double) * (size_t)g->n_loc * ld;
+        for (coopcg_gpu_ctx* h : X.s)
+            if (h != g)
+                CK(cudaMemcpyPeerAsync(block_of(h, which, k, &ld) + (size_t)g->row0 * ld, h->device, src, g->device,
+                                       bytes, g->stream));
+    }
+    return xbarrier(ctx, X);
+}
+
+// After every shard's iter_local(k): the full Q of iteration k everywhere.
+static int xq(coopcg_gpu_ctx* ctx, const Exch& X, int k) {
+    if (X.mode == 1) return xbarrier(ctx, X);  // the rows were pushed by the producing kernel
+    return xrows(ctx, X, COOPCG_BLOCK_Q, k);
+}
+
 static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* trace) {
-    if (sharded(ctx))
-        return fail(ctx, COOPCG_E_STATE, "row-sharded contexts are driven phase by phase (coopcg_gpu_phase)");
-    if (int rc = begin_impl(ctx, opts)) return rc;
-    cudaStream_t st = ctx->stream;
-    const int max_iters = ctx->max_iters;
-    CK(cudaEventRecord(ctx->ev_run0, st));
-    if (int rc = setup_local(ctx)) return rc;
-    if (int rc = setup_rest(ctx)) return rc;
-    if (ctx->algo == 1)
-        if (int rc = mccg_setup(ctx)) return rc;
-    CK(cudaEventRecord(ctx->ev_loop0, st));
-    ctx->rank_async = true;
+    const Exch X = exch_of(ctx);
+    coopcg_gpu_ctx* c0 = X.s[0];
+    if (X.mode == 0 && sharded(c0))
+        return fail(ctx, COOPCG_E_STATE,
+                    "a row shard without an exchange is driven phase by phase (coopcg_gpu_phase); "
+                    "use coopcg_gpu_create_multi / coopcg_gpu_create_rank for a multi-GPU run");
+    if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) { return begin_impl(c, opts); })) return rc;
+    auto on0 = [&]() -> int {
+        CK(cudaSetDevice(c0->device));
+        return COOPCG_OK;
+    };
+    const int max_iters = c0->max_iters;
+    if (int rc = on0()) return rc;
+    CK(cudaEventRecord(c0->ev_run0, c0->stream));
+    if (int rc = each(ctx, X, setup_local)) return rc;
+    if (int rc = xrows(ctx, X, COOPCG_BLOCK_R, 0)) return rc;
+    if (int rc = each(ctx, X, setup_rest)) return rc;
+    if (c0->algo == 1)
+        if (int rc = each(ctx, X, mccg_setup)) return rc;
+    if (int rc = on0()) return rc;
+    CK(cudaEventRecord(c0->ev_loop0, c0->stream));
+    for (coopcg_gpu_ctx* c : X.s) c->rank_async = true;
     struct AsyncOff {
-        coopcg_gpu_ctx* c;
-        ~AsyncOff() { c->rank_async = false; }
-    } async_off{ctx};
+        const Exch& X;
+        ~AsyncOff() {
+            for (coopcg_gpu_ctx* c : X.s) c->rank_async = false;
+        }
+    } async_off{X};
 
     // ---- main loop, enqueued in chunks; device-side stop makes extras no-ops ----
     // No host read after setup: a stop raised by the setup coordinator turns
     // the first chunk into no-ops and its snapshot ends the loop (mccg reads
-    // the control block in mccg_setup already).
+    // the control block in mccg_setup already).  Every shard holds the same
+    // control state (replicated), so shard 0's snapshot decides.
     bool stopped = false;
     int k_host = 0;
     int chunk_id = 0;
@@ -1485,9 +1760,10 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     int trend_k = -1;
     bool chunk_rec[2][kChunkMax] = {};
     // A.D launch timing (coopcg_timing, the bench roofline): CUDA events around
-    // every mv_every-th A.D only -- an event between two kernels costs the
-    // programmatic-launch overlap there (+1.3% exact / +2.4% fast it/s at cfg 2
-    // with 8 vs 1, tools/mv_events_ab.sh).  COOPCG_MV_EVERY overrides (0 = off).
+    // every mv_every-th A.D of shard 0 only -- an event between two kernels
+    // costs the programmatic-launch overlap there (+1.3% exact / +2.4% fast it/s
+    // at cfg 2 with 8 vs 1, tools/mv_events_ab.sh).  COOPCG_MV_EVERY overrides
+    // (0 = off).
     static const int mv_every = [] {
         const char* e = std::getenv("COOPCG_MV_EVERY");
         return e ? std::atoi(e) : 8;
@@ -1497,15 +1773,15 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     int npending = 0;
     auto read_chunk = [&](int c) -> int {
         const int slot = c & 1;
-        CK(cudaEventSynchronize(ctx->ev_chunk[slot]));
-        const Ctl& snap = ctx->ctl_host[slot];
+        CK(cudaEventSynchronize(c0->ev_chunk[slot]));
+        const Ctl& snap = c0->ctl_host[slot];
         for (int u = 0; u < chunk_iters[slot]; ++u) {
             const int kk = chunk_k0[slot] + u;
             if (kk >= snap.iterations) break;  // launches after the stop were no-ops
             if (!chunk_rec[slot][u]) continue;
             float ms = 0.f;
-            if (cudaEventElapsedTime(&ms, ctx->mv_ev[(slot * kChunkMax + u) * 2],
-                                     ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1]) == cudaSuccess) {
+            if (cudaEventElapsedTime(&ms, c0->mv_ev[(slot * kChunkMax + u) * 2],
+                                     c0->mv_ev[(slot * kChunkMax + u) * 2 + 1]) == cudaSuccess) {
                 mv_total += ms;
                 ++mv_count;
             }
@@ -1513,9 +1789,9 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
         if (snap.stop) stopped = true;
         // residual trend of the chunk (recorded minres), for sizing what to enqueue next
         const int n_done = std::min(chunk_iters[slot], snap.iterations - chunk_k0[slot]);
-        if (n_done >= 2 && chunk_k0[slot] + n_done <= ctx->tr_capacity) {
-            const double first = ctx->minres_host[slot * kChunkMax];
-            trend_last = ctx->minres_host[slot * kChunkMax + n_done - 1];
+        if (n_done >= 2 && chunk_k0[slot] + n_done <= c0->tr_capacity) {
+            const double first = c0->minres_host[slot * kChunkMax];
+            trend_last = c0->minres_host[slot * kChunkMax + n_done - 1];
             // geometric-mean decay per iteration over the chunk
             trend_rate = (first > 0.0 && trend_last > 0.0) ? std::pow(trend_last / first, 1.0 / (n_done - 1)) : 1.0;
             trend_k = chunk_k0[slot] + n_done - 1;
@@ -1538,7 +1814,7 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
         }
         const int slot = chunk_id & 1;
         int U = std::min(chunk, max_iters - k_host);
-        const double tol = ctx->ctl_host[0].tol;
+        const double tol = c0->ctl_host[0].tol;
         if (tol > 0.0 && trend_k >= 0 && trend_last > tol && trend_rate > 0.0 && trend_rate < 0.9) {
             // clear geometric convergence: enqueue about what is still needed
             const double need = std::ceil(std::log(tol / trend_last) / std::log(trend_rate));
@@ -1551,18 +1827,26 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
         for (int u = 0; u < U; ++u, ++k_host) {
             const bool rec = mv_every > 0 && k_host % mv_every == 0;
             chunk_rec[slot][u] = rec;
-            if (int rc = iter_local(ctx, k_host, rec ? ctx->mv_ev[(slot * kChunkMax + u) * 2] : nullptr,
-                                    rec ? ctx->mv_ev[(slot * kChunkMax + u) * 2 + 1] : nullptr))
+            const int k = k_host;
+            if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) {
+                    const bool r = rec && c == c0;
+                    return iter_local(c, k, r ? c->mv_ev[(slot * kChunkMax + u) * 2] : nullptr,
+                                      r ? c->mv_ev[(slot * kChunkMax + u) * 2 + 1] : nullptr);
+                }))
                 return rc;
-            if (int rc = iter_mid(ctx, k_host)) return rc;
-            if (int rc = iter_rest(ctx, k_host)) return rc;
+            if (int rc = xq(ctx, X, k)) return rc;
+            if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) { return iter_mid(c, k); })) return rc;
+            if (recompute_at(c0, k))
+                if (int rc = xrows(ctx, X, COOPCG_BLOCK_R, k)) return rc;
+            if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) { return iter_rest(c, k); })) return rc;
         }
-        if (int rc = join_rank(ctx)) return rc;
-        CK(cudaMemcpyAsync(&ctx->ctl_host[slot], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-        if (chunk_k0[slot] + U <= ctx->tr_capacity)
-            CK(cudaMemcpyAsync(ctx->minres_host + slot * kChunkMax, ctx->tr_minres + chunk_k0[slot],
-                               sizeof(double) * U, cudaMemcpyDeviceToHost, st));
-        CK(cudaEventRecord(ctx->ev_chunk[slot], st));
+        if (int rc = each(ctx, X, join_rank)) return rc;
+        if (int rc = on0()) return rc;
+        CK(cudaMemcpyAsync(&c0->ctl_host[slot], c0->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c0->stream));
+        if (chunk_k0[slot] + U <= c0->tr_capacity)
+            CK(cudaMemcpyAsync(c0->minres_host + slot * kChunkMax, c0->tr_minres + chunk_k0[slot],
+                               sizeof(double) * U, cudaMemcpyDeviceToHost, c0->stream));
+        CK(cudaEventRecord(c0->ev_chunk[slot], c0->stream));
         pending[npending++] = chunk_id;
         ++chunk_id;
         if (++same == 2) {
@@ -1573,13 +1857,16 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
       for (int q = 0; q < npending; ++q)
           if (int rc = read_chunk(pending[q])) return rc;
       npending = 0;
-      // mccg: the device paused on a rank drop (restrict_pending); restrict and resume.
-      if (ctx->algo != 1) break;
-      CK(cudaMemcpyAsync(&ctx->ctl_host[0], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (!ctx->ctl_host[0].restrict_pending) break;
+      // mccg: the device paused on a rank drop (restrict_pending); every shard
+      // holds the same replicated blocks and takes the same decision.
+      if (c0->algo != 1) break;
+      if (int rc = on0()) return rc;
+      CK(cudaMemcpyAsync(&c0->ctl_host[0], c0->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, c0->stream));
+      CK(cudaStreamSynchronize(c0->stream));
+      if (!c0->ctl_host[0].restrict_pending) break;
+      const int kr = c0->ctl_host[0].k;
       int next_k = -1;
-      if (int rc = mccg_restrict(ctx, ctx->ctl_host[0].k, &next_k)) return rc;
+      if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) { return mccg_restrict(c, kr, &next_k); })) return rc;
       if (next_k < 0) break;
       k_host = next_k;
       stopped = false;
@@ -1587,39 +1874,60 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
       same = 0;
       trend_k = -1;
     }
-    if (int rc = join_rank(ctx)) return rc;
-    ctx->rank_async = false;
-    CK(cudaEventRecord(ctx->ev_loop1, st));
-    if (int rc = final_local(ctx)) return rc;
-    if (int rc = final_rest(ctx)) return rc;
-    CK(cudaEventRecord(ctx->ev_run1, st));
-    CK(cudaStreamSynchronize(st));
+    if (int rc = each(ctx, X, join_rank)) return rc;
+    for (coopcg_gpu_ctx* c : X.s) c->rank_async = false;
+    if (int rc = on0()) return rc;
+    CK(cudaEventRecord(c0->ev_loop1, c0->stream));
+    if (int rc = each(ctx, X, final_local)) return rc;
+    if (int rc = xrows(ctx, X, COOPCG_BLOCK_S, 0)) return rc;
+    if (int rc = each(ctx, X, final_rest)) return rc;
+    if (int rc = xbarrier(ctx, X)) return rc;  // shard 0's end event after every shard's work
+    if (int rc = on0()) return rc;
+    CK(cudaEventRecord(c0->ev_run1, c0->stream));
+    if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) -> int {
+            cudaError_t e = cudaStreamSynchronize(c->stream);
+            return e == cudaSuccess ? COOPCG_OK
+                                    : fail(c, COOPCG_E_CUDA, "stream synchronize: %s", cudaGetErrorString(e));
+        }))
+        return rc;
+    if (int rc = on0()) return rc;
     float run_ms = 0.f, loop_ms = 0.f;
-    CK(cudaEventElapsedTime(&run_ms, ctx->ev_run0, ctx->ev_run1));
-    CK(cudaEventElapsedTime(&loop_ms, ctx->ev_loop0, ctx->ev_loop1));
-    ctx->timing.run_ms = run_ms;
-    ctx->timing.loop_ms = loop_ms;
-    ctx->timing.matvec_ms_total = mv_total;
-    ctx->timing.matvec_launches = mv_count;
-    ctx->timing.kernel_launches = ctx->launches;
-    return end_impl(ctx, trace);
+    CK(cudaEventElapsedTime(&run_ms, c0->ev_run0, c0->ev_run1));
+    CK(cudaEventElapsedTime(&loop_ms, c0->ev_loop0, c0->ev_loop1));
+    long long launches = 0;
+    for (coopcg_gpu_ctx* c : X.s) launches += c->launches;
+    coopcg_timing tm{};
+    tm.run_ms = run_ms;
+    tm.loop_ms = loop_ms;
+    tm.matvec_ms_total = mv_total;
+    tm.matvec_launches = mv_count;
+    tm.kernel_launches = launches;
+    c0->timing = tm;
+    ctx->timing = tm;
+    const int rc = end_impl(c0, trace);
+    if (rc != COOPCG_OK && c0 != ctx) ctx->msg = c0->msg;
+    return rc;
 }
 
 extern "C" {
 
 int coopcg_gpu_run(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* trace) {
     if (!ctx) return COOPCG_E_INVALID;
-    CK(cudaSetDevice(ctx->device));
+    if (!is_group(ctx)) CK(cudaSetDevice(ctx->device));
     return run_impl(ctx, opts, trace);
 }
 
 int coopcg_gpu_begin(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     return begin_impl(ctx, opts);
 }
 
 int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     switch (phase) {
@@ -1644,6 +1952,8 @@ int coopcg_gpu_phase(coopcg_gpu_ctx* ctx, int phase, int k) {
 }
 
 int coopcg_gpu_mccg_resume(coopcg_gpu_ctx* ctx, int* next_k) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx || !next_k) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     *next_k = -1;
@@ -1654,9 +1964,14 @@ int coopcg_gpu_mccg_resume(coopcg_gpu_ctx* ctx, int* next_k) {
     return mccg_restrict(ctx, ctx->ctl_host[0].k, next_k);
 }
 
-int coopcg_gpu_recompute_at(const coopcg_gpu_ctx* ctx, int k) { return ctx ? (recompute_at(ctx, k) ? 1 : 0) : 0; }
+int coopcg_gpu_recompute_at(const coopcg_gpu_ctx* ctx, int k) {
+    if (is_group(ctx)) ctx = ctx->shards[0];
+    return ctx ? (recompute_at(ctx, k) ? 1 : 0) : 0;
+}
 
 int coopcg_gpu_ipc_handles(coopcg_gpu_ctx* ctx, void* handles_out) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx || !handles_out) return COOPCG_E_INVALID;
     if (!sharded(ctx)) return fail(ctx, COOPCG_E_STATE, "peer exchange is for row-sharded contexts");
     CK(cudaSetDevice(ctx->device));
@@ -1674,6 +1989,8 @@ int coopcg_gpu_ipc_handles(coopcg_gpu_ctx* ctx, void* handles_out) {
 }
 
 int coopcg_gpu_set_peers(coopcg_gpu_ctx* ctx, int nranks, int self_rank, const void* handles) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx || !handles) return COOPCG_E_INVALID;
     if (nranks < 1 || nranks > kMaxPeers || self_rank < 0 || self_rank >= nranks)
         return fail(ctx, COOPCG_E_INVALID, "set_peers: nranks %d (max %d), self %d", nranks, kMaxPeers, self_rank);
@@ -1704,6 +2021,8 @@ int coopcg_gpu_set_peers(coopcg_gpu_ctx* ctx, int nranks, int self_rank, const v
 }
 
 int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int* ld) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx || !dev_ptr) return COOPCG_E_INVALID;
     double* b = nullptr;
     switch (which) {
@@ -1725,6 +2044,8 @@ int coopcg_gpu_block(coopcg_gpu_ctx* ctx, int which, int k, void** dev_ptr, int*
 }
 
 int coopcg_gpu_state(coopcg_gpu_ctx* ctx, int* stop, int* iterations) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     CK(cudaMemcpyAsync(&ctx->ctl_host[1], ctx->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, ctx->stream));
@@ -1735,6 +2056,8 @@ int coopcg_gpu_state(coopcg_gpu_ctx* ctx, int* stop, int* iterations) {
 }
 
 int coopcg_gpu_end(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
+    if (is_group(ctx))
+        return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     ctx->timing.kernel_launches = ctx->launches;
@@ -1767,9 +2090,13 @@ int coopcg_gpu_timing(const coopcg_gpu_ctx* ctx, coopcg_timing* out) {
     return COOPCG_OK;
 }
 
-void* coopcg_gpu_stream(const coopcg_gpu_ctx* ctx) { return ctx ? (void*)ctx->stream : nullptr; }
+void* coopcg_gpu_stream(const coopcg_gpu_ctx* ctx) {
+    if (is_group(ctx)) return (void*)ctx->shards[0]->stream;
+    return ctx ? (void*)ctx->stream : nullptr;
+}
 
 int coopcg_gpu_matvec_block(coopcg_gpu_ctx* ctx, const double* D, double* out) {
+    if (is_group(ctx)) return (D && out) ? group_matvec_block(ctx, D, out) : COOPCG_E_INVALID;
     if (!ctx || !D || !out) return COOPCG_E_INVALID;
     if (!ctx->a_ready) return fail(ctx, COOPCG_E_STATE, "A not set");
     CK(cudaSetDevice(ctx->device));
@@ -1795,6 +2122,7 @@ int coopcg_gpu_matvec_block(coopcg_gpu_ctx* ctx, const double* D, double* out) {
 }
 
 int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D, double tol, int force_exact, int* rank) {
+    if (is_group(ctx)) return coopcg_gpu_numerical_rank_ex(ctx->shards[0], D, tol, force_exact, rank);
     if (!ctx || !D || !rank) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     if (ctx->p != ctx->p_orig)
@@ -1824,6 +2152,222 @@ int coopcg_gpu_numerical_rank_ex(coopcg_gpu_ctx* ctx, const double* D, double to
 
 int coopcg_gpu_numerical_rank(coopcg_gpu_ctx* ctx, const double* D, double tol, int* rank) {
     return coopcg_gpu_numerical_rank_ex(ctx, D, tol, 0, rank);
+}
+
+}  // extern "C"
+
+// =============================================================================
+// Multi-GPU contexts: a group handle over in-process row shards
+// and rank contexts with NCCL row exchanges.
+// =============================================================================
+static int group_set_A(coopcg_gpu_ctx* ctx, const double* A_rows) {
+    const Exch X = exch_of(ctx);
+    return each(ctx, X, [&](coopcg_gpu_ctx* c) { return coopcg_gpu_set_A(c, A_rows + (size_t)c->row0 * c->n); });
+}
+
+static int group_get_A_rows(coopcg_gpu_ctx* ctx, int row0, int rows, double* A_rows) {
+    if (row0 < 0 || rows < 0 || row0 + rows > ctx->n)
+        return fail(ctx, COOPCG_E_DIMENSION, "get_A_rows: row range outside the matrix");
+    const Exch X = exch_of(ctx);
+    return each(ctx, X, [&](coopcg_gpu_ctx* c) {
+        const int a = std::max(row0, c->row0), b = std::min(row0 + rows, c->row1);
+        if (a >= b) return (int)COOPCG_OK;
+        return coopcg_gpu_get_A_rows(c, a - c->row0, b - a, A_rows + (size_t)(a - row0) * c->n);
+    });
+}
+
+// The Householder generator over row shards: each shard computes its rows of
+// w = M v, the rows are exchanged, every shard forms the scalars from the full
+// vectors identically and updates its rows.
+static int gen_householder_x(coopcg_gpu_ctx* ctx, const Exch& X, uint64_t seed, int m, double kappa) {
+    for (coopcg_gpu_ctx* c : X.s) c->a_ready = false;
+    if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) { return coopcg_gpu_gen_householder_begin(c, seed, m, kappa); }))
+        return rc;
+    for (int r = m - 1; r >= 0; --r) {
+        if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) { return coopcg_gpu_gen_householder_local(c, r); }))
+            return rc;
+        if (int rc = xrows(ctx, X, COOPCG_BLOCK_W, 0)) return rc;
+        if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) { return coopcg_gpu_gen_householder_rest(c, r); }))
+            return rc;
+    }
+    return each(ctx, X, [&](coopcg_gpu_ctx* c) { return coopcg_gpu_gen_householder_end(c); });
+}
+
+static int rank_gen_householder(coopcg_gpu_ctx* ctx, uint64_t seed, int m, double kappa) {
+    return gen_householder_x(ctx, exch_of(ctx), seed, m, kappa);
+}
+
+static int group_gen_A(coopcg_gpu_ctx* ctx, int kind, uint64_t seed, int m, double kappa) {
+    const Exch X = exch_of(ctx);
+    if (kind == COOPCG_MATRIX_DIAGDOM)
+        return each(ctx, X, [&](coopcg_gpu_ctx* c) { return coopcg_gpu_gen_A(c, kind, seed, m, kappa); });
+    if (kind == COOPCG_MATRIX_HOUSEHOLDER) return gen_householder_x(ctx, X, seed, m, kappa);
+    return fail(ctx, COOPCG_E_INVALID, "matrix kind %d needs the whole matrix on one device", kind);
+}
+
+static int group_upload(coopcg_gpu_ctx* ctx, const double* b, const double* X0) {
+    const Exch X = exch_of(ctx);
+    return each(ctx, X, [&](coopcg_gpu_ctx* c) { return coopcg_gpu_upload(c, b, X0); });
+}
+
+static int group_matvec_block(coopcg_gpu_ctx* ctx, const double* D, double* out) {
+    const Exch X = exch_of(ctx);
+    const int n = ctx->n, p = ctx->p_orig;
+    std::vector<double> part;
+    return each(ctx, X, [&](coopcg_gpu_ctx* c) {
+        part.resize((size_t)c->n_loc * p);
+        if (int rc = coopcg_gpu_matvec_block(c, D, part.data())) return rc;
+        for (int j = 0; j < p; ++j)  // column-major n_loc x p -> rows [row0, row1) of the n x p output
+            std::memcpy(out + (size_t)j * n + c->row0, part.data() + (size_t)j * c->n_loc, sizeof(double) * c->n_loc);
+        return (int)COOPCG_OK;
+    });
+}
+
+extern "C" {
+
+int coopcg_row_split(int n, int parts, int part, int* row_begin, int* row_end) {
+    if (n < 1 || parts < 1 || part < 0 || part >= parts || !row_begin || !row_end) return COOPCG_E_INVALID;
+    row_split(n, parts, part, row_begin, row_end);
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_create_multi(int n, int p, int ndev, const int* devices, int arith, coopcg_gpu_ctx** out) {
+    if (!out || !devices || ndev < 1) return COOPCG_E_INVALID;
+    *out = nullptr;
+    g_create_error.clear();
+    if (ndev > kMaxPeers) return fail(nullptr, COOPCG_E_INVALID, "ndev %d > %d", ndev, kMaxPeers);
+    if (ndev == 1) return coopcg_gpu_create(n, p, devices[0], arith, out);
+    for (int g = 0; g < ndev; ++g) {
+        int r0 = 0, r1 = 0;
+        row_split(n, ndev, g, &r0, &r1);
+        if (r1 <= r0) return fail(nullptr, COOPCG_E_DIMENSION, "n = %d rows cannot be split over %d devices", n, ndev);
+    }
+    auto* ctx = new coopcg_gpu_ctx();
+    ctx->n = n;
+    ctx->p = ctx->p_orig = p;
+    ctx->device = devices[0];
+    ctx->arith = arith;
+    ctx->row0 = 0;
+    ctx->row1 = ctx->n_loc = n;
+    auto bail = [&](int code) {
+        const std::string m = ctx->msg.empty() ? g_create_error : ctx->msg;
+        destroy_impl(ctx);
+        g_create_error = m;
+        return code;
+    };
+    for (int g = 0; g < ndev; ++g) {
+        int r0 = 0, r1 = 0;
+        row_split(n, ndev, g, &r0, &r1);
+        coopcg_gpu_ctx* c = nullptr;
+        if (int rc = coopcg_gpu_create_shard(n, p, devices[g], arith, r0, r1, &c)) return bail(rc);
+        ctx->shards.push_back(c);
+    }
+    ctx->P = ctx->shards[0]->P;
+    // peer access between distinct devices (the Q rows are stored straight
+    // into every shard's Q by the kernel that computes them)
+    for (int g = 0; g < ndev; ++g)
+        for (int h = 0; h < ndev; ++h) {
+            if (devices[g] == devices[h]) continue;
+            int can = 0;
+            cudaDeviceCanAccessPeer(&can, devices[g], devices[h]);
+            if (!can) {
+                fail(ctx, COOPCG_E_CUDA, "device %d cannot access device %d (peer access)", devices[g], devices[h]);
+                return bail(COOPCG_E_CUDA);
+            }
+            cudaSetDevice(devices[g]);
+            cudaError_t e = cudaDeviceEnablePeerAccess(devices[h], 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) {
+                cudaGetLastError();
+            } else if (e != cudaSuccess) {
+                fail(ctx, COOPCG_E_CUDA, "cudaDeviceEnablePeerAccess(%d -> %d): %s", devices[g], devices[h],
+                     cudaGetErrorString(e));
+                return bail(COOPCG_E_CUDA);
+            }
+        }
+    // Q double-buffered by iteration parity (a shard pushing iteration k+1
+    // never overwrites rows a slower shard still reads in k)
+    for (coopcg_gpu_ctx* c : ctx->shards) {
+        cudaSetDevice(c->device);
+        const size_t bytes = sizeof(double) * (size_t)n * c->P;
+        if (cudaMalloc(&c->Qalt, bytes) != cudaSuccess || cudaMemset(c->Qalt, 0, bytes) != cudaSuccess) {
+            fail(ctx, COOPCG_E_CUDA, "allocating the second Q buffer on device %d", c->device);
+            return bail(COOPCG_E_CUDA);
+        }
+    }
+    for (coopcg_gpu_ctx* c : ctx->shards) {
+        PeerRows pr[2] = {};
+        for (int h = 0; h < ndev; ++h) {
+            pr[0].dst[h] = ctx->shards[h]->Q;
+            pr[1].dst[h] = ctx->shards[h]->Qalt;
+        }
+        pr[0].n = pr[1].n = ndev;
+        c->peers[0] = pr[0];
+        c->peers[1] = pr[1];
+        c->p2p = true;
+    }
+    ctx->gev.assign(ndev, nullptr);
+    for (int g = 0; g < ndev; ++g) {
+        cudaSetDevice(devices[g]);
+        if (cudaEventCreateWithFlags(&ctx->gev[g], cudaEventDisableTiming) != cudaSuccess) {
+            fail(ctx, COOPCG_E_CUDA, "event creation on device %d", devices[g]);
+            return bail(COOPCG_E_CUDA);
+        }
+    }
+    cudaSetDevice(devices[0]);
+    *out = ctx;
+    return COOPCG_OK;
+}
+
+int coopcg_nccl_unique_id(void* id_out) {
+    if (!id_out) return COOPCG_E_INVALID;
+    const NcclApi& api = nccl_api();
+    if (!api.getUniqueId) return fail(nullptr, COOPCG_E_CUDA, "NCCL unavailable: %s", api.err.c_str());
+    static_assert(sizeof(ncclUniqueId) == COOPCG_NCCL_ID_BYTES, "ncclUniqueId size");
+    ncclUniqueId id;
+    ncclResult_t r = api.getUniqueId(&id);
+    if (r != ncclSuccess) return fail(nullptr, COOPCG_E_CUDA, "ncclGetUniqueId: %s", nccl_err(r));
+    std::memcpy(id_out, &id, sizeof id);
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_create_rank(int n, int p, int device, int arith, int nranks, int rank, const void* nccl_id,
+                           coopcg_gpu_ctx** out) {
+    if (!out || !nccl_id || nranks < 1 || rank < 0 || rank >= nranks) return COOPCG_E_INVALID;
+    *out = nullptr;
+    int r0 = 0, r1 = 0;
+    row_split(n, nranks, rank, &r0, &r1);
+    if (r1 <= r0) return fail(nullptr, COOPCG_E_DIMENSION, "n = %d rows cannot be split over %d ranks", n, nranks);
+    const NcclApi& api = nccl_api();
+    if (!api.getUniqueId) return fail(nullptr, COOPCG_E_CUDA, "NCCL unavailable: %s", api.err.c_str());
+    coopcg_gpu_ctx* ctx = nullptr;
+    if (int rc = coopcg_gpu_create_shard(n, p, device, arith, r0, r1, &ctx)) return rc;
+    ncclUniqueId id;
+    std::memcpy(&id, nccl_id, sizeof id);
+    ncclComm_t comm = nullptr;
+    cudaSetDevice(device);
+    ncclResult_t r = api.commInitRank(&comm, nranks, id, rank);
+    if (r != ncclSuccess) {
+        destroy_impl(ctx);
+        return fail(nullptr, COOPCG_E_CUDA, "ncclCommInitRank(%d of %d): %s", rank, nranks, nccl_err(r));
+    }
+    ctx->nccl = comm;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    *out = ctx;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_shards(const coopcg_gpu_ctx* ctx, int cap, int* nshards, int* devices, int* row_begin, int* row_end) {
+    if (!ctx || !nshards) return COOPCG_E_INVALID;
+    const int ns = is_group(ctx) ? (int)ctx->shards.size() : 1;
+    *nshards = ns;
+    for (int g = 0; g < ns && g < cap; ++g) {
+        const coopcg_gpu_ctx* c = is_group(ctx) ? ctx->shards[g] : ctx;
+        if (devices) devices[g] = c->device;
+        if (row_begin) row_begin[g] = c->row0;
+        if (row_end) row_end[g] = c->row1;
+    }
+    return COOPCG_OK;
 }
 
 }  // extern "C"

@@ -180,7 +180,9 @@ __global__ void __launch_bounds__(32 + 64 * WN)
 // Rows are processed in tiles of 256/P (thread per element).
 template <int P, bool PUSH = false>
 __global__ void __launch_bounds__(256)
-    fast_rows_kernel(const double* __restrict__ Qpart, int kchunks, int n_loc, int row0, double* __restrict__ dst,
+    // Qpart and dst may alias (kchunks == 1: the row pass rewrites the block it
+    // sums in place), so neither is __restrict__.
+    fast_rows_kernel(const double* Qpart, int kchunks, int n_loc, int row0, double* dst,
                      const double* __restrict__ b, const double* __restrict__ D, const double* __restrict__ R,
                      const double* __restrict__ Qfull, int p, int mode, double* __restrict__ partials,
                      const int* __restrict__ stop, PeerRows peers) {

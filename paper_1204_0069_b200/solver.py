@@ -83,6 +83,9 @@ class SolveOptions:
 class GpuOptions:
     device: int = 0
     arith: str = "exact"  # "exact" (bit-identical to the reference) | "fast"
+    # several devices: A row-block sharded over them, one process driving all
+    # (coopcg_gpu_create_multi; a device may repeat).  None: `device` alone.
+    devices: Optional[List[int]] = None
 
 
 @dataclass
@@ -139,8 +142,7 @@ def _check(ctx_handle, rc: int) -> None:
     if rc == 0:
         return
     buf = C.create_string_buffer(512)
-    if ctx_handle is not None:
-        _capi.lib().coopcg_gpu_last_error(ctx_handle, buf, 512)
+    _capi.lib().coopcg_gpu_last_error(ctx_handle, buf, 512)  # None: the thread's last create/host error
     msg = buf.value.decode() or f"coopcg error code {rc}"
     raise _ERRORS.get(rc, Error)(msg)
 
@@ -157,22 +159,47 @@ class GpuContext:
     """
 
     def __init__(self, n: int, p: int, device: int = 0, arith: str = "exact",
-                 row_begin: int = 0, row_end: Optional[int] = None):
+                 row_begin: int = 0, row_end: Optional[int] = None, devices: Optional[List[int]] = None,
+                 nccl: Optional[tuple] = None):
+        """devices: row-shard A over these devices, one process driving all
+        (coopcg_gpu_create_multi).  nccl = (nranks, rank, unique_id_bytes):
+        this process's rank context (coopcg_gpu_create_rank) with the NCCL row
+        exchanges inside the library; its rows are row_split(n, nranks, rank)."""
         L = _capi.lib()
         self.n, self.p, self.device, self.arith = n, p, device, arith
+        self.devices = list(devices) if devices else [device]
         self.row_begin = row_begin
         self.row_end = n if row_end is None else row_end
         h = C.c_void_p()
         if arith not in _ARITH:
             raise Error(f"unknown arith mode {arith!r}")
-        rc = L.coopcg_gpu_create_shard(n, p, device, _ARITH[arith], self.row_begin, self.row_end,
-                                       C.byref(h))
+        if nccl is not None:
+            nranks, rank, uid = nccl
+            if len(uid) != _capi.NCCL_ID_BYTES:
+                raise Error("nccl unique id must be 128 bytes (nccl_unique_id())")
+            self.row_begin, self.row_end = row_split(n, nranks, rank)
+            idbuf = C.create_string_buffer(bytes(uid), _capi.NCCL_ID_BYTES)
+            rc = L.coopcg_gpu_create_rank(n, p, device, _ARITH[arith], nranks, rank, idbuf, C.byref(h))
+        elif devices is not None and len(devices) > 1:
+            arr = (C.c_int * len(devices))(*devices)
+            rc = L.coopcg_gpu_create_multi(n, p, len(devices), arr, _ARITH[arith], C.byref(h))
+        else:
+            rc = L.coopcg_gpu_create_shard(n, p, device, _ARITH[arith], self.row_begin, self.row_end,
+                                           C.byref(h))
         if rc != 0:
             buf = C.create_string_buffer(512)
             L.coopcg_gpu_last_error(None, buf, 512)
             raise _ERRORS.get(rc, Error)(buf.value.decode() or f"create failed ({rc})")
         self._h = h
         self._timing = _capi.coopcg_timing()
+
+    def shards(self) -> list:
+        """[(device, row_begin, row_end)] of the context's row shards."""
+        ns = C.c_int()
+        cap = 16
+        dev, r0, r1 = (C.c_int * cap)(), (C.c_int * cap)(), (C.c_int * cap)()
+        _check(self._h, _capi.lib().coopcg_gpu_shards(self._h, cap, C.byref(ns), dev, r0, r1))
+        return [(dev[g], r0[g], r1[g]) for g in range(min(ns.value, cap))]
 
     # -- lifecycle --
     def close(self) -> None:
@@ -206,9 +233,15 @@ class GpuContext:
         k = {"diagdom": 0, "householder": 1, "random_spd": 2}[kind]
         _check(self._h, _capi.lib().coopcg_gpu_gen_A(self._h, k, seed, m, kappa))
 
-    def get_A(self) -> np.ndarray:
-        out = np.empty((self.row_end - self.row_begin, self.n))
-        _check(self._h, _capi.lib().coopcg_gpu_get_A(self._h, out.ctypes.data))
+    def get_A(self, row0: int = 0, rows: Optional[int] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
+        """Rows [row0, row0 + rows) of this context's row block (default: all)."""
+        if rows is None:
+            rows = self.row_end - self.row_begin - row0
+        if out is None:
+            out = np.empty((rows, self.n))
+        elif out.dtype != np.float64 or not out.flags.c_contiguous or out.size != rows * self.n:
+            raise DimensionError("get_A: output buffer does not match the row range")
+        _check(self._h, _capi.lib().coopcg_gpu_get_A_rows(self._h, row0, rows, out.ctypes.data))
         return out
 
     # -- inputs / solve --
@@ -350,7 +383,7 @@ def ccg_solve(A: np.ndarray, b: np.ndarray, X0: np.ndarray, opts: Optional[Solve
     p = X0.shape[1]
     if p < 1 or p >= n:
         raise DimensionError("solver: need 1 <= p < n starting columns")
-    with GpuContext(n, p, gpu.device, gpu.arith) as ctx:
+    with GpuContext(n, p, gpu.device, gpu.arith, devices=gpu.devices) as ctx:
         ctx.set_A(A)
         return ctx.solve(b, X0, opts)
 
@@ -436,6 +469,20 @@ def gen_householder_factors(n: int, m: int, kappa: float, seed: int):
     _check(None, _capi.lib().coopcg_gen_householder_factors(n, m, kappa, seed, V.ctypes.data,
                                                               lam.ctypes.data))
     return V[:m], lam
+
+
+def row_split(n: int, parts: int, part: int) -> tuple:
+    """The library's row blocks (coopcg_row_split): rows [r0, r1) of shard `part`."""
+    r0, r1 = C.c_int(), C.c_int()
+    _check(None, _capi.lib().coopcg_row_split(n, parts, part, C.byref(r0), C.byref(r1)))
+    return r0.value, r1.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for GpuContext(..., nccl=(nranks, rank, id))."""
+    buf = C.create_string_buffer(_capi.NCCL_ID_BYTES)
+    _check(None, _capi.lib().coopcg_nccl_unique_id(buf))
+    return buf.raw
 
 
 def library_version() -> str:

@@ -9,6 +9,11 @@ import sys
 import numpy as np
 import pytest
 
+# The reference's OpenMP solver (oracle/_ref) runs one thread per agent, up to
+# p = 32 threads on the box's 16 cores: passive waiting keeps oversubscribed
+# barriers from spinning.  Must be set before libgomp loads.
+os.environ.setdefault("OMP_WAIT_POLICY", "passive")
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))

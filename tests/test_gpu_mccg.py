@@ -75,3 +75,29 @@ def test_mccg_fast_mode_converges(po):
     assert str(t.status) == "converged" and t.active_agents == ot.extra["active_agents"]
     rel = np.linalg.norm(t.final_x - ot.final_x[:, t.active_agents], axis=0) / np.linalg.norm(t.final_x, axis=0)
     assert rel.max() < 1e-8
+
+
+def test_mccg_restricted_then_larger_trace(po):
+    """after a restricted mccg solve the next solve on the
+    same context asks for a larger trace; the trace buffers must be sized for
+    the context's original agent count, not the restricted one."""
+    import paper_1204_0069_b200 as m
+    n, p = 240, 6
+    A = po.gen_householder(n, 6, 1e3, 11)
+    b = po.gen_rhs(n, "normal", 11)
+    X0 = po.gen_starts(n, p, 11)
+    Xd = X0.copy()
+    Xd[:, 4] = Xd[:, 2]
+    Xd[:, 5] = Xd[:, 1]   # rank(D0) = 4: restricted at setup
+    with m.GpuContext(n, p) as ctx:
+        ctx.set_A(A)
+        t1 = ctx.solve(b, Xd, m.SolveOptions(tol=0.0, max_iters=3, algo="mccg"))
+        assert len(t1.active_agents) == 4
+        t2 = ctx.solve(b, X0, m.SolveOptions(tol=1e-9 * po.seq_norm(b)))   # 2n-row trace
+        t3 = ctx.solve(b, Xd, m.SolveOptions(tol=1e-9 * po.seq_norm(b), max_iters=3 * n, algo="mccg"))
+    ref = po.oracle_ccg(A, b, X0, tol=1e-9 * po.seq_norm(b))
+    assert t2.iteration_count() == ref.iterations
+    assert np.array_equal(t2.final_x, ref.final_x) and np.array_equal(t2.residual_norms, ref.residual_norms)
+    ref3 = po.oracle_ccg(A, b, Xd, tol=1e-9 * po.seq_norm(b), max_iters=3 * n, algo="mccg")
+    assert np.array_equal(t3.residual_norms, ref3.residual_norms, equal_nan=True)
+    assert np.array_equal(t3.final_x, ref3.final_x[:, t3.active_agents])
