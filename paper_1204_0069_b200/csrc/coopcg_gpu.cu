@@ -22,6 +22,7 @@
 #include <vector>
 #include <cstdlib>
 #include <mutex>
+#include <thread>
 #include <type_traits>
 #include <utility>
 
@@ -178,6 +179,12 @@ struct coopcg_gpu_ctx {
     int tr_capacity = 0;
     double* stage = nullptr;  // host<->device staging, n * P doubles
     size_t stage_elems = 0;
+    // A's host transfers (set_A / get_A_rows): two pinned + two device slots,
+    // allocated on first use, so host copies overlap the PCIe copies
+    double* pin[2] = {nullptr, nullptr};
+    double* dslot[2] = {nullptr, nullptr};
+    cudaEvent_t pin_ev[2] = {nullptr, nullptr};
+    size_t pin_elems = 0;
 
     AdConfig ad;
     int nparts = 0;
@@ -441,13 +448,12 @@ cudaError_t fast_update(coopcg_gpu_ctx* ctx, const double* Q, const double* D, d
 template <int P>
 cudaError_t fast_solve_t(coopcg_gpu_ctx* ctx, int mode) {
     const size_t smem = (size_t)(4 * P * P + 1024) * sizeof(double);
-    static bool attr_done[64] = {};
-    const int dev = ctx->device & 63;
-    if (!attr_done[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(fast_solve_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr_done[dev] = true;
-    }
+    static std::once_flag attr_once[kMaxDevices];
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once[ctx->device % kMaxDevices], [&] {
+        attr_err = cudaFuncSetAttribute(fast_solve_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
     return pdl_launch(fast_solve_kernel<P>, dim3(1), dim3(1024), smem, ctx->stream, ctx->gpart, ctx->f_rgrid, ctx->small,
                       ctx->ctl, mode);
 }
@@ -557,13 +563,12 @@ cudaError_t chains_launch_t(coopcg_gpu_ctx* ctx, int phase, const double* s0, co
                             int nsrc, const int* stop) {
     auto kern = chain_kernel<P, T, S>;
     const size_t smem_max = chain_smem_bytes(P, T, S, NSRC_MAX);
-    static bool attr_done[64] = {};
-    const int dev = ctx->device & 63;
-    if (!attr_done[dev]) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
-        if (e != cudaSuccess) return e;
-        attr_done[dev] = true;
-    }
+    static std::once_flag attr_once[kMaxDevices];
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once[ctx->device % kMaxDevices], [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
     const int cnt = ctx->desc_cnt[phase];
     const size_t smem = chain_smem_bytes(P, T, S, nsrc);
     pdl_launch(kern, dim3((cnt + 63) / 64), dim3(kChainThreads), smem, ctx->stream, s0, s1, s2, nsrc, ctx->n, ctx->descs + ctx->desc_off[phase],
@@ -666,6 +671,11 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaFree(ctx->tr_minres);
     cudaFree(ctx->tr_wall);
     cudaFree(ctx->stage);
+    for (int q = 0; q < 2; ++q) {
+        if (ctx->pin[q]) cudaFreeHost(ctx->pin[q]);
+        cudaFree(ctx->dslot[q]);
+        if (ctx->pin_ev[q]) cudaEventDestroy(ctx->pin_ev[q]);
+    }
     if (ctx->ctl_host) cudaFreeHost(ctx->ctl_host);
     if (ctx->minres_host) cudaFreeHost(ctx->minres_host);
     if (ctx->trace_host) cudaFreeHost(ctx->trace_host);
@@ -721,6 +731,38 @@ double host_normal(uint64_t key, uint64_t t) {
 }
 
 }  // namespace
+
+// memcpy on several host threads (a single core copies ~10 GB/s; the
+// PCIe 5 link and host DRAM take several times that).
+static void par_memcpy(void* dst, const void* src, size_t bytes) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned T = bytes >= (size_t(4) << 20) ? std::min(8u, hw) : 1u;
+    if (T <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t per = ((bytes + T - 1) / T + 4095) & ~size_t(4095);
+    std::vector<std::thread> th;
+    for (unsigned t = 0; t < T; ++t) {
+        const size_t o = t * per;
+        if (o >= bytes) break;
+        th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + o, static_cast<const char*>(src) + o,
+                                          std::min(per, bytes - o)); });
+    }
+    for (auto& x : th) x.join();
+}
+
+static int ensure_pinned(coopcg_gpu_ctx* ctx) {
+    if (ctx->pin[0]) return COOPCG_OK;
+    const size_t slot_bytes = size_t(32) << 20;
+    ctx->pin_elems = std::max<size_t>(slot_bytes / sizeof(double), (size_t)ctx->n);
+    for (int q = 0; q < 2; ++q) {
+        CK(cudaHostAlloc(&ctx->pin[q], sizeof(double) * ctx->pin_elems, cudaHostAllocDefault));
+        CK(cudaMalloc(&ctx->dslot[q], sizeof(double) * ctx->pin_elems));
+        CK(cudaEventCreateWithFlags(&ctx->pin_ev[q], cudaEventDisableTiming));
+    }
+    return COOPCG_OK;
+}
 
 // Group handles (coopcg_gpu_create_multi) route the C ABI to their shards;
 // defined at the end of this file.
@@ -893,15 +935,21 @@ int coopcg_gpu_set_A(coopcg_gpu_ctx* ctx, const double* A_rows) {
     if (!ctx || !A_rows) return COOPCG_E_INVALID;
     CK(cudaSetDevice(ctx->device));
     const int n = ctx->n;
-    // Stage row chunks (pinned bounce is implicit in cudaMemcpy from pageable).
-    const int chunk = (int)std::max<size_t>(1, std::min<size_t>(ctx->stage_elems / n, 4096));
-    for (int r0 = 0; r0 < ctx->n_loc; r0 += chunk) {
+    if (int rc = ensure_pinned(ctx)) return rc;
+    // Row chunks through two pinned slots: host threads fill slot s while the
+    // device copies and re-lays out the chunk in slot s ^ 1.
+    const int chunk = (int)std::max<size_t>(1, ctx->pin_elems / n);
+    for (int c = 0, r0 = 0; r0 < ctx->n_loc; ++c, r0 += chunk) {
+        const int s = c & 1;
         const int rows = std::min(chunk, ctx->n_loc - r0);
-        CK(cudaMemcpyAsync(ctx->stage, A_rows + (size_t)r0 * n, sizeof(double) * (size_t)rows * n,
-                           cudaMemcpyHostToDevice, ctx->stream));
+        if (c >= 2) CK(cudaEventSynchronize(ctx->pin_ev[s]));
+        par_memcpy(ctx->pin[s], A_rows + (size_t)r0 * n, sizeof(double) * (size_t)rows * n);
+        CK(cudaMemcpyAsync(ctx->dslot[s], ctx->pin[s], sizeof(double) * (size_t)rows * n, cudaMemcpyHostToDevice,
+                           ctx->stream));
         dim3 grid((n + 31) / 32, (rows + 31) / 32);
-        transpose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->stage, rows, n, ctx->At, ctx->lay, r0);
+        transpose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->dslot[s], rows, n, ctx->At, ctx->lay, r0);
         CKL();
+        CK(cudaEventRecord(ctx->pin_ev[s], ctx->stream));
     }
     CK(cudaStreamSynchronize(ctx->stream));
     ctx->a_ready = true;
@@ -916,16 +964,27 @@ int coopcg_gpu_get_A_rows(coopcg_gpu_ctx* ctx, int row0, int rows, double* A_row
         return fail(ctx, COOPCG_E_DIMENSION, "get_A_rows: row range outside this context's rows");
     CK(cudaSetDevice(ctx->device));
     const int n = ctx->n;
-    const int chunk = (int)std::max<size_t>(1, std::min<size_t>(ctx->stage_elems / n, 4096));
-    for (int r = 0; r < rows; r += chunk) {
-        const int m = std::min(chunk, rows - r);
-        dim3 grid((n + 31) / 32, (m + 31) / 32);
-        untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->lay, row0 + r, m, n,
-                                                                      ctx->stage);
-        CKL();
-        CK(cudaMemcpyAsync(A_rows + (size_t)r * n, ctx->stage, sizeof(double) * (size_t)m * n,
-                           cudaMemcpyDeviceToHost, ctx->stream));
-        CK(cudaStreamSynchronize(ctx->stream));
+    if (int rc = ensure_pinned(ctx)) return rc;
+    // chunk c is re-laid out and copied into pinned slot c & 1 while the host
+    // threads drain chunk c - 1 from the other slot
+    const int chunk = (int)std::max<size_t>(1, ctx->pin_elems / n);
+    const int nch = (rows + chunk - 1) / chunk;
+    for (int c = 0; c <= nch; ++c) {
+        if (c < nch) {
+            const int s = c & 1, r = c * chunk, m = std::min(chunk, rows - r);
+            dim3 grid((n + 31) / 32, (m + 31) / 32);
+            untranspose_rows_kernel<<<grid, dim3(32, 8), 0, ctx->stream>>>(ctx->At, ctx->lay, row0 + r, m, n,
+                                                                          ctx->dslot[s]);
+            CKL();
+            CK(cudaMemcpyAsync(ctx->pin[s], ctx->dslot[s], sizeof(double) * (size_t)m * n, cudaMemcpyDeviceToHost,
+                               ctx->stream));
+            CK(cudaEventRecord(ctx->pin_ev[s], ctx->stream));
+        }
+        if (c >= 1) {
+            const int s = (c - 1) & 1, r = (c - 1) * chunk, m = std::min(chunk, rows - r);
+            CK(cudaEventSynchronize(ctx->pin_ev[s]));
+            par_memcpy(A_rows + (size_t)r * n, ctx->pin[s], sizeof(double) * (size_t)m * n);
+        }
     }
     return COOPCG_OK;
 }
@@ -1399,8 +1458,7 @@ static bool recompute_at(const coopcg_gpu_ctx* ctx, int k) {
 // R_loc = A_loc X - b (the caller exchanges R before iter_rest).
 static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
     double* Qk = q_of(ctx, k);
-    const int n = ctx->n, P = ctx->P;
-    cudaStream_t st = ctx->stream;
+    const int n = ctx->n;
     int* stop = &ctx->ctl->stop;
     double* D = ctx->Dblk[k & 1];
     double* Dn = ctx->Dblk[(k + 1) & 1];
@@ -1414,10 +1472,7 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
             CK(fast_rows_any(ctx, Qk, 1, n, 0, Qk, nullptr, D, ctx->R, nullptr, 0, stop));
         if (!rec) {
             CK(fast_solve(ctx, 0));
-            CK(fast_update(ctx, Qk, D, Dn, 0, stop));
-            pdl_launch(fast_record_kernel, dim3(1), dim3(256), 0, st, ctx->npart, ctx->f_ugrid, P, 0, 1, ctx->small, ctx->ctl,
-                                                  ctx->tr_norms, ctx->tr_minres, ctx->tr_wall, ctx->tr_capacity);
-            LAUNCHED();
+            CK(fast_update(ctx, Qk, D, Dn, 0, stop));  // the record follows in iter_rest
         } else {
             CK(fast_solve(ctx, 1));
             CK(fast_update(ctx, Qk, D, Dn, 1, stop));
@@ -1447,21 +1502,27 @@ static int iter_rest(coopcg_gpu_ctx* ctx, int k) {
             CK(fast_rows_any(ctx, ctx->R, 1, n, 0, ctx->R, nullptr, nullptr, nullptr, Qk, 1, stop));
         CK(fast_solve(ctx, 2));
         CK(fast_update(ctx, Qk, D, Dn, 2, stop));
-        pdl_launch(fast_record_kernel, dim3(1), dim3(256), 0, st, ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1, ctx->small,
-                                              ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall,
-                                              ctx->tr_capacity);
-        LAUNCHED();
     }
-    // The rank certificate of D' gates only what comes after the next A.D
-    // (which reads D' and nothing rank_end writes): in run_impl it runs on
-    // the side stream, concurrently with that A.D.  A stop it raises turns
-    // the rest of the iteration into no-ops as before; the A.D it overlapped
-    // only wrote the scratch Q.
+    // The record (fast mode) and the rank certificate of D' gate only what
+    // comes after the next A.D (which reads D' and nothing they write): in
+    // run_impl they run on the side stream, concurrently with that A.D.  A
+    // stop they raise turns the rest of the iteration into no-ops as before;
+    // the A.D they overlapped only wrote scratch.
     cudaStream_t rs = st;
     if (ctx->rank_async) {
         CK(cudaEventRecord(ctx->ev_fork, st));
         CK(cudaStreamWaitEvent(ctx->side, ctx->ev_fork, 0));
         rs = ctx->side;
+    }
+    if (fast) {
+        // norms -> record + convergence (solvers.hpp:125-154), then k++ in rank_end
+        if (!rec)
+            pdl_launch(fast_record_kernel, dim3(1), dim3(256), 0, rs, ctx->npart, ctx->f_ugrid, P, 0, 1, ctx->small,
+                       ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall, ctx->tr_capacity);
+        else
+            pdl_launch(fast_record_kernel, dim3(1), dim3(256), 0, rs, ctx->gpart, ctx->f_rgrid, 4 * P * P, P * P, P + 1,
+                       ctx->small, ctx->ctl, ctx->tr_norms, ctx->tr_minres, ctx->tr_wall, ctx->tr_capacity);
+        LAUNCHED();
     }
     pdl_launch(rank_end_kernel, dim3(1), dim3(1024), rank_smem(P), rs, ctx->partials, dgrid_of(ctx), Dn, ctx->V, n, ctx->ctl, 0,
                                                    fast ? ctx->small : nullptr);

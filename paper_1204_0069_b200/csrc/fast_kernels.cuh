@@ -252,23 +252,29 @@ __global__ void __launch_bounds__(256)
             const int o = tid + q * 256;
             if (o < NOUT) {
                 const int gsel = o / (P * P), a = (o / P) % P, c2 = o % P;
-                double s = acc[q];
+                // four independent accumulators over the tile rows (r mod 4),
+                // added in a fixed order at the end of the tile
+                const double(*xs)[P] = nullptr;
+                const double(*ys)[P] = nullptr;
                 if (mode == 0) {
-                    if (gsel == 0)
-                        for (int r = 0; r < TR; ++r) s = fma(td[r][a], tq[r][c2], s);
-                    else if (gsel == 1)
-                        for (int r = 0; r < TR; ++r) s = fma(trr[r][a], td[r][c2], s);
-                    else if (gsel == 2)
-                        for (int r = 0; r < TR; ++r) s = fma(trr[r][a], tq[r][c2], s);
-                    else
-                        for (int r = 0; r < TR; ++r) s = fma(tq[r][a], tq[r][c2], s);
-                } else {
-                    if (gsel == 0 && Qfull != nullptr)
-                        for (int r = 0; r < TR; ++r) s = fma(tq[r][a], td[r][c2], s);
-                    else if (gsel == 1 && a == c2)
-                        for (int r = 0; r < TR; ++r) s = fma(tq[r][a], tq[r][a], s);
+                    xs = gsel == 0 ? td : (gsel == 3 ? tq : trr);
+                    ys = (gsel == 1) ? td : tq;
+                } else if (gsel == 0 && Qfull != nullptr) {
+                    xs = tq;
+                    ys = td;
+                } else if (gsel == 1 && a == c2) {
+                    xs = tq;
+                    ys = tq;
                 }
-                acc[q] = s;
+                if (xs != nullptr) {
+                    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+                    for (int r = 0; r < TR; r += 4) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) s4[u] = fma(xs[r + u][a], ys[r + u][c2], s4[u]);
+                    }
+                    acc[q] += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                }
             }
         }
         __syncthreads();
@@ -474,14 +480,22 @@ __global__ void __launch_bounds__(256)
         al[idx / p][idx % p] = small[L.alpha() + (idx / p) * P + idx % p];
         be[idx / p][idx % p] = small[L.beta() + (idx / p) * P + idx % p];
     }
+    // D'^T D' pair partials: item (pair, g) sums the tile rows r = g, g + G, ...
+    // (G = 256 / npairs row groups per pair when the pairs are fewer than the
+    // threads), so no thread walks a whole tile in one dependent chain; the G
+    // group sums are added in a fixed order at the end (deterministic).
     const int npairs = p * (p + 1) / 2;
-    int pi[3], pj[3];
+    const int G = npairs < 256 ? 256 / npairs : 1;
+    int pi[3], pj[3], pg[3];
     double part[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
         int t = tid + q * 256;
         pi[q] = pj[q] = -1;
-        if (t < npairs) {
+        pg[q] = 0;
+        if (t < npairs * G) {
+            pg[q] = t % G;
+            t /= G;
             int i = 0;
             while (t >= p - i) {
                 t -= p - i;
@@ -557,7 +571,7 @@ __global__ void __launch_bounds__(256)
             for (int q = 0; q < 3; ++q)
                 if (pi[q] >= 0) {
                     double s = part[q];
-                    for (int r = 0; r < TR; ++r) s = fma(tdn[r][pi[q]], tdn[r][pj[q]], s);
+                    for (int r = pg[q]; r < TR; r += G) s = fma(tdn[r][pi[q]], tdn[r][pj[q]], s);
                     part[q] = s;
                 }
         }
@@ -574,9 +588,20 @@ __global__ void __launch_bounds__(256)
         if (mode == 0) norm_part[static_cast<size_t>(blockIdx.x) * P + tid] = s;
     }
     if (mode != 1) {
+        if (G == 1) {
 #pragma unroll
-        for (int q = 0; q < 3; ++q)
-            if (pi[q] >= 0) pair_part[static_cast<size_t>(blockIdx.x) * npairs + tid + q * 256] = part[q];
+            for (int q = 0; q < 3; ++q)
+                if (pi[q] >= 0) pair_part[static_cast<size_t>(blockIdx.x) * npairs + tid + q * 256] = part[q];
+        } else {  // one item per thread: add the G group sums of each pair in order
+            __syncthreads();
+            nred[tid] = part[0];
+            __syncthreads();
+            if (tid < npairs) {
+                double t = 0.0;
+                for (int g = 0; g < G; ++g) t += nred[tid * G + g];
+                pair_part[static_cast<size_t>(blockIdx.x) * npairs + tid] = t;
+            }
+        }
     }
 }
 
