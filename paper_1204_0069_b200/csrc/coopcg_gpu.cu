@@ -141,6 +141,10 @@ struct coopcg_gpu_ctx {
     double* gpart = nullptr;     // rgrid x 4 P^2 (row-pass Gram partials)
     double* npart = nullptr;     // ugrid x P (norm partials)
     double* dtiles = nullptr;    // the A.D operand re-laid out as [col][kk] k-tiles
+    double* gfin = nullptr;      // fast_iter_kernel: the reduced Grams (4 P^2)
+    unsigned int* gbar = nullptr;  // fast_iter_kernel: grid barrier {count, generation}
+    int fused_k = -1;            // iteration whose solve + update ran inside fast_iter_kernel
+    bool fuse_ok = false;        // fast_iter_kernel's f_ugrid CTAs fit on the device at once
     bool a_ready = false, inputs_ready = false;
     cudaStream_t stream = nullptr;
     std::string msg;
@@ -467,6 +471,67 @@ cudaError_t fast_solve(coopcg_gpu_ctx* ctx, int mode) {
     }
 }
 
+// The fused post-MMA iteration (fast_iter_kernel): one cooperative launch of
+// f_ugrid CTAs (== f_rgrid on an unsharded context), all co-resident.
+// COOPCG_NO_FUSE=1 runs the separate row / solve / update kernels instead.
+static bool fuse_enabled() {
+    static const bool on = std::getenv("COOPCG_NO_FUSE") == nullptr;
+    return on;
+}
+template <int P>
+cudaError_t fast_iter_t(coopcg_gpu_ctx* ctx, double* Q, const double* D, double* Dn) {
+    auto kern = fast_iter_kernel<P>;
+    const size_t smem = fused_smem_bytes<P>();
+    static std::once_flag attr_once[kMaxDevices];
+    cudaError_t attr_err = cudaSuccess;
+    std::call_once(attr_once[ctx->device % kMaxDevices], [&] {
+        attr_err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    if (attr_err != cudaSuccess) return attr_err;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(ctx->f_ugrid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    ++ctx->launches;
+    return cudaLaunchKernelEx(&cfg, kern, (const double*)ctx->qpart, ctx->f_kchunks, ctx->n, Q, ctx->X, ctx->R, D, Dn,
+                              ctx->small, ctx->ctl, ctx->p, ctx->gpart, ctx->gfin, ctx->npart, ctx->partials,
+                              ctx->gbar);
+}
+template <int P>
+bool fast_iter_fits_t(const coopcg_gpu_ctx* ctx) {
+    int occ = 0;
+    if (cudaFuncSetAttribute(fast_iter_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)fused_smem_bytes<P>()) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fast_iter_kernel<P>, 256, fused_smem_bytes<P>()) !=
+            cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return occ * ctx->sms >= ctx->f_ugrid && ctx->f_ugrid == ctx->f_rgrid;
+}
+bool fast_iter_fits(const coopcg_gpu_ctx* ctx) {
+    switch (ctx->P) {
+    case 8: return fast_iter_fits_t<8>(ctx);
+    case 16: return fast_iter_fits_t<16>(ctx);
+    default: return fast_iter_fits_t<32>(ctx);
+    }
+}
+cudaError_t fast_iter(coopcg_gpu_ctx* ctx, double* Q, const double* D, double* Dn) {
+    switch (ctx->P) {
+    case 8: return fast_iter_t<8>(ctx, Q, D, Dn);
+    case 16: return fast_iter_t<16>(ctx, Q, D, Dn);
+    default: return fast_iter_t<32>(ctx, Q, D, Dn);
+    }
+}
+
 AdConfig pick_ad_config(int n_loc, int P, int sms) {
     AdConfig c;
     // Measured sweep (tools/probe/ad_probe.cu, profiles/; ring shapes: ad_T / ad_S);
@@ -661,6 +726,8 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     hh_free(ctx);
     cudaFree(ctx->npart);
     cudaFree(ctx->dtiles);
+    cudaFree(ctx->gfin);
+    cudaFree(ctx->gbar);
     cudaFree(ctx->small);
     cudaFree(ctx->partials);
     cudaFree(ctx->init_norms);
@@ -886,6 +953,10 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         CKC(cudaMalloc(&ctx->gpart, sizeof(double) * (size_t)ctx->f_rgrid * 4 * ctx->P * ctx->P));
         CKC(cudaMalloc(&ctx->npart, sizeof(double) * (size_t)ctx->f_ugrid * ctx->P));
         CKC(cudaMalloc(&ctx->dtiles, sizeof(double) * (size_t)ctx->lay.ntiles * ctx->P * kFastT));
+        CKC(cudaMalloc(&ctx->gfin, sizeof(double) * 4 * ctx->P * ctx->P));
+        CKC(cudaMalloc(&ctx->gbar, 2 * sizeof(unsigned int)));
+        CKC(cudaMemsetAsync(ctx->gbar, 0, 2 * sizeof(unsigned int), ctx->stream));
+        ctx->fuse_ok = ctx->n_loc == n && fast_iter_fits(ctx);
     }
     const SmallLayout L{ctx->P};
     CKC(cudaMalloc(&ctx->small, sizeof(double) * L.total()));
@@ -1431,6 +1502,10 @@ static int join_rank(coopcg_gpu_ctx* ctx) {
     return COOPCG_OK;
 }
 
+static bool recompute_at(const coopcg_gpu_ctx* ctx, int k) {
+    return ctx->every > 0 && (k + 1) % ctx->every == 0;  // solvers.hpp:33-35
+}
+
 static int iter_local(coopcg_gpu_ctx* ctx, int k, cudaEvent_t ev0, cudaEvent_t ev1) {
     double* Qk = q_of(ctx, k);
     int* stop = &ctx->ctl->stop;
@@ -1444,15 +1519,19 @@ static int iter_local(coopcg_gpu_ctx* ctx, int k, cudaEvent_t ev0, cudaEvent_t e
         CK(fast_ad(ctx, D, stop));
         if (ev1) CK(cudaEventRecord(ev1, ctx->stream));
         if (int rc = join_rank(ctx)) return rc;
-        // single GPU: fuse the four Gram partials into the local row pass
-        CK(fast_rows(ctx, Qk, nullptr, D, ctx->R, nullptr, sharded(ctx) ? 1 : 0, stop, peers_of(ctx, k)));
+        if (!sharded(ctx) && !recompute_at(ctx, k) && ctx->fuse_ok && fuse_enabled()) {
+            // single GPU, plain iteration: row pass + Grams + solves + update in one launch
+            CK(fast_iter(ctx, Qk, D, ctx->Dblk[(k + 1) & 1]));
+            ctx->fused_k = k;
+        } else {
+            ctx->fused_k = -1;
+            // single GPU: fuse the four Gram partials into the local row pass
+            CK(fast_rows(ctx, Qk, nullptr, D, ctx->R, nullptr, sharded(ctx) ? 1 : 0, stop, peers_of(ctx, k)));
+        }
     }
     return COOPCG_OK;
 }
 
-static bool recompute_at(const coopcg_gpu_ctx* ctx, int k) {
-    return ctx->every > 0 && (k + 1) % ctx->every == 0;  // solvers.hpp:33-35
-}
 
 // After Q is complete: Grams, alpha, update; in recompute iterations ends with
 // R_loc = A_loc X - b (the caller exchanges R before iter_rest).
@@ -1471,8 +1550,10 @@ static int iter_mid(coopcg_gpu_ctx* ctx, int k) {
         if (sharded(ctx))  // the four Gram partials over the full replicated blocks
             CK(fast_rows_any(ctx, Qk, 1, n, 0, Qk, nullptr, D, ctx->R, nullptr, 0, stop));
         if (!rec) {
-            CK(fast_solve(ctx, 0));
-            CK(fast_update(ctx, Qk, D, Dn, 0, stop));  // the record follows in iter_rest
+            if (ctx->fused_k != k) {
+                CK(fast_solve(ctx, 0));
+                CK(fast_update(ctx, Qk, D, Dn, 0, stop));  // the record follows in iter_rest
+            }
         } else {
             CK(fast_solve(ctx, 1));
             CK(fast_update(ctx, Qk, D, Dn, 1, stop));

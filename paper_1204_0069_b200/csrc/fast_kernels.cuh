@@ -606,6 +606,370 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// (4b) One fused, cooperative launch for the whole post-MMA part of a plain
+// (non-recompute, single-GPU) iteration: the row pass, the Gram reduction,
+// the step solves and the update pass of kernels (2)-(4), separated by two
+// grid-wide barriers (every CTA is co-resident: cooperative launch).
+//   A  rows:   Q = sum_c Qpart[c]; per-CTA partials of D^T Q, R^T D, R^T Q, Q^T Q
+//   B  reduce: one warp per Gram entry sums the CTA partials (fixed order)
+//   C  solve:  every CTA redoes the Cholesky / alpha / beta solve from the
+//              reduced Grams in shared memory (identical inputs -> identical
+//              results); CTA 0 publishes alpha, beta, the factor and errors
+//   D  update: X += D alpha^T, R += Q alpha^T, D' = R + D beta^T, plus the
+//              |R_j|^2 and D'^T D' per-CTA partials (kernel (4)'s format)
+// Three launches and their drain/fill gaps become one.  The per-element
+// arithmetic is that of the separate kernels; only the Gram reduction adds
+// the CTA partials in a different (still fixed, deterministic) order.
+__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned int* vgen = bar + 1;
+        const unsigned int gen = *vgen;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == nblocks - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicAdd(bar + 1, 1u);
+        } else {
+            while (*vgen == gen) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <int P>
+__host__ __device__ constexpr int fused_rows_tr() { return (256 / P) * 4; }
+template <int P>
+__host__ __device__ constexpr int fused_upd_tr() { return (256 / P) * ((P >= 32) ? 2 : 4); }
+template <int P>
+__host__ __device__ constexpr size_t fused_smem_bytes() {
+    // phase A: 3 tiles; phase C/D: grams (4 P^2) + alpha, beta + 4 update tiles + reductions
+    constexpr size_t a = 3ull * fused_rows_tr<P>() * P;
+    constexpr size_t d = 4ull * P * P + 2ull * P * (P + 1) + 4ull * fused_upd_tr<P>() * P + 256 + P * (P + 1);
+    return (a > d ? a : d) * sizeof(double);
+}
+
+template <int P>
+__global__ void __launch_bounds__(256, 2)
+    fast_iter_kernel(const double* __restrict__ Qpart, int kchunks, int n, double* __restrict__ Q,
+                     double* __restrict__ X, double* __restrict__ R, const double* __restrict__ D,
+                     double* __restrict__ Dn, double* __restrict__ small, Ctl* ctl, int p,
+                     double* __restrict__ gpart, double* __restrict__ gfin, double* __restrict__ norm_part,
+                     double* __restrict__ pair_part, unsigned int* __restrict__ gbar) {
+    pdl_wait();
+    if (*reinterpret_cast<volatile const int*>(&ctl->stop)) return;  // stable: no writer runs concurrently
+    extern __shared__ __align__(16) double fsm[];
+    constexpr int NOUT = 4 * P * P;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned int G = gridDim.x;
+    const SmallLayout L{P};
+
+    // ---- A: row pass (kernel (2), mode 0) ----------------------------------
+    {
+        constexpr int RP = 4;
+        constexpr int TR = fused_rows_tr<P>();
+        constexpr int PER = (NOUT + 255) / 256;
+        double(*tq)[P] = reinterpret_cast<double(*)[P]>(fsm);
+        double(*td)[P] = reinterpret_cast<double(*)[P]>(fsm + TR * P);
+        double(*trr)[P] = reinterpret_cast<double(*)[P]>(fsm + 2 * TR * P);
+        const int lr0 = tid / P, j = tid % P;
+        double acc[PER];
+#pragma unroll
+        for (int q = 0; q < PER; ++q) acc[q] = 0.0;
+        const int ntile = (n + TR - 1) / TR;
+        for (int t = blockIdx.x; t < ntile; t += G) {
+            double v[RP], dv[RP], rv[RP];
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                const int il = t * TR + lr0 + u * (256 / P);
+                v[u] = dv[u] = rv[u] = 0.0;
+                if (il < n) {
+                    const double* qp = Qpart + static_cast<size_t>(il) * P + j;
+                    const size_t cs = static_cast<size_t>(n) * P;
+                    for (int c0 = 0; c0 < kchunks; c0 += 8) {
+                        double w[8];
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc) w[cc] = (c0 + cc < kchunks) ? qp[(c0 + cc) * cs] : 0.0;
+#pragma unroll
+                        for (int cc = 0; cc < 8; ++cc)
+                            if (c0 + cc < kchunks) v[u] += w[cc];
+                    }
+                    dv[u] = D[static_cast<size_t>(il) * P + j];
+                    rv[u] = R[static_cast<size_t>(il) * P + j];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                const int lr = lr0 + u * (256 / P);
+                const int il = t * TR + lr;
+                if (il < n) Q[static_cast<size_t>(il) * P + j] = v[u];
+                tq[lr][j] = v[u];
+                td[lr][j] = dv[u];
+                trr[lr][j] = rv[u];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < PER; ++q) {
+                const int o = tid + q * 256;
+                if (o < NOUT) {
+                    const int gsel = o / (P * P), a = (o / P) % P, c2 = o % P;
+                    const double(*xs)[P] = gsel == 0 ? td : (gsel == 3 ? tq : trr);
+                    const double(*ys)[P] = (gsel == 1) ? td : tq;
+                    double s4[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 2
+                    for (int r = 0; r < TR; r += 4) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) s4[u] = fma(xs[r + u][a], ys[r + u][c2], s4[u]);
+                    }
+                    acc[q] += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int q = 0; q < PER; ++q) {
+            const int o = tid + q * 256;
+            if (o < NOUT) gpart[static_cast<size_t>(blockIdx.x) * NOUT + o] = acc[q];
+        }
+    }
+    grid_barrier(gbar, G);
+
+    // ---- B: Gram reduction, one warp per entry (fixed order) ---------------
+    for (int o = blockIdx.x * 8 + warp; o < NOUT; o += G * 8) {
+        double s = 0.0;
+        for (unsigned int c = lane; c < G; c += 32) s += __ldcg(gpart + static_cast<size_t>(c) * NOUT + o);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+        if (lane == 0) gfin[o] = s;
+    }
+    grid_barrier(gbar, G);
+
+    // ---- C: step solves (kernel (3), mode 0), redundantly in every CTA ------
+    double* flat = fsm;                          // 4 P^2
+    double(*al)[P + 1] = reinterpret_cast<double(*)[P + 1]>(fsm + NOUT);
+    double(*be)[P + 1] = reinterpret_cast<double(*)[P + 1]>(fsm + NOUT + P * (P + 1));
+    double* tiles = fsm + NOUT + 2 * P * (P + 1);
+    constexpr int TRU = fused_upd_tr<P>();
+    double* nred = tiles + 4 * TRU * P;          // 256
+    double(*lsm)[P + 1] = reinterpret_cast<double(*)[P + 1]>(nred + 256);
+    __shared__ int abort_flag;
+    for (int o = tid; o < NOUT; o += 256) flat[o] = __ldcg(gfin + o);
+    if (tid == 0) abort_flag = 0;
+    __syncthreads();
+    auto Gm = [&](int gsel, int a, int c) { return flat[(gsel * P + a) * P + c]; };
+    if (warp == 0) {
+        const bool pub = blockIdx.x == 0;
+        const double nsq = (lane < P) ? small[L.nsq_d() + lane] : 0.0;
+        double l[P];
+        double maxabs = 0.0, diag = 0.0;
+#pragma unroll
+        for (int jj = 0; jj < P; ++jj) {
+            l[jj] = 0.0;
+            if (lane < p && jj < p) {
+                l[jj] = 0.5 * (Gm(0, lane, jj) + Gm(0, jj, lane));
+                maxabs = fmax(maxabs, fabs(l[jj]));
+                if (jj == lane) diag = l[jj];
+            }
+        }
+        for (int off = 16; off > 0; off >>= 1) maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, off));
+        const double floor = maxabs * 1e-14;
+        const bool bad = (lane < p) && !(diag > 0.0) && (nsq > 0.0);
+        bool fail = false;
+        if (__any_sync(0xffffffffu, bad)) {
+            if (pub && lane == 0) {
+                ctl->err = 2;
+                ctl->err_iter = ctl->k;
+                ctl->stop = 1;
+            }
+            fail = true;
+        }
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            if (fail || k >= p) break;
+            double dk = 0.0;
+            if (lane == k) {
+                double sk = l[k];
+#pragma unroll
+                for (int m = 0; m < k; ++m) sk = fma(-l[m], l[m], sk);
+                dk = (sk > floor) ? sqrt(sk) : -1.0;
+            }
+            const double lkk = __shfl_sync(0xffffffffu, dk, k);
+            if (!(lkk > 0.0)) {
+                if (pub && lane == 0) {
+                    ctl->status = 1;  // rank collapse (pivot vanished)
+                    ctl->stop = 1;
+                }
+                fail = true;
+                break;
+            }
+            double rk[P];
+#pragma unroll
+            for (int m = 0; m < k; ++m) rk[m] = __shfl_sync(0xffffffffu, l[m], k);
+            if (lane > k && lane < p) {
+                double sk = l[k];
+#pragma unroll
+                for (int m = 0; m < k; ++m) sk = fma(-l[m], rk[m], sk);
+                l[k] = sk / lkk;
+            }
+            if (lane == k) l[k] = lkk;
+        }
+        if (fail) {
+            if (lane == 0) abort_flag = 1;
+        } else {
+            if (lane < P) {
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) {
+                    lsm[lane][jj] = l[jj];
+                    if (pub) ctl->lu[lane * P + jj] = l[jj];
+                }
+            }
+            __syncwarp();
+            double x[P], rhs[P], xb[P];
+            if (lane < p) {
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) rhs[jj] = (jj < p) ? -Gm(1, lane, jj) : 0.0;
+                chol_solve_regs<P>(lsm, p, rhs, x);
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) {
+                    double sb = Gm(2, lane, jj);
+#pragma unroll
+                    for (int m = 0; m < P; ++m)
+                        if (m < p) sb = fma(x[m], Gm(3, m, jj), sb);
+                    rhs[jj] = (jj < p) ? -sb : 0.0;
+                }
+                chol_solve_regs<P>(lsm, p, rhs, xb);
+#pragma unroll
+                for (int jj = 0; jj < P; ++jj) {
+                    al[lane][jj] = (jj < p) ? x[jj] : 0.0;
+                    be[lane][jj] = (jj < p) ? xb[jj] : 0.0;
+                    if (pub) {
+                        small[L.alpha() + lane * P + jj] = (jj < p) ? x[jj] : 0.0;
+                        small[L.beta() + lane * P + jj] = (jj < p) ? xb[jj] : 0.0;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    if (abort_flag) return;
+
+    // ---- D: update pass (kernel (4), mode 0) -------------------------------
+    {
+        constexpr int RP = (P >= 32) ? 2 : 4;
+        constexpr int TR = TRU;
+        double(*tr_)[P] = reinterpret_cast<double(*)[P]>(tiles);
+        double(*tdn)[P] = reinterpret_cast<double(*)[P]>(tiles + TR * P);
+        double(*td_)[P] = reinterpret_cast<double(*)[P]>(tiles + 2 * TR * P);
+        double(*tq_)[P] = reinterpret_cast<double(*)[P]>(tiles + 3 * TR * P);
+        const int npairs = p * (p + 1) / 2;
+        const int GR = npairs < 256 ? 256 / npairs : 1;
+        int pi[3], pj[3], pg[3];
+        double part[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            int t = tid + q * 256;
+            pi[q] = pj[q] = -1;
+            pg[q] = 0;
+            if (t < npairs * GR) {
+                pg[q] = t % GR;
+                t /= GR;
+                int i = 0;
+                while (t >= p - i) {
+                    t -= p - i;
+                    ++i;
+                }
+                pi[q] = i;
+                pj[q] = i + t;
+            }
+        }
+        double nrm = 0.0;
+        const int lr0 = tid / P, i = tid % P;
+        const int ntile = (n + TR - 1) / TR;
+        for (int t = blockIdx.x; t < ntile; t += G) {
+            double dv[RP], qv[RP], xv[RP], rv[RP];
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                const int row = t * TR + lr0 + u * (256 / P);
+                const size_t e = static_cast<size_t>(row) * P + i;
+                const bool ok = row < n;
+                dv[u] = ok ? D[e] : 0.0;
+                qv[u] = ok ? Q[e] : 0.0;
+                xv[u] = ok ? X[e] : 0.0;
+                rv[u] = ok ? R[e] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                td_[lr0 + u * (256 / P)][i] = dv[u];
+                tq_[lr0 + u * (256 / P)][i] = qv[u];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                const int lr = lr0 + u * (256 / P);
+                const int row = t * TR + lr;
+                const size_t e = static_cast<size_t>(row) * P + i;
+                double rnew = 0.0;
+                if (row < n && i < p) {
+                    double x = xv[u];
+                    for (int jj = 0; jj < p; ++jj) x = fma(al[i][jj], td_[lr][jj], x);
+                    X[e] = x;
+                    double r = rv[u];
+                    for (int jj = 0; jj < p; ++jj) r = fma(al[i][jj], tq_[lr][jj], r);
+                    R[e] = r;
+                    rnew = r;
+                    nrm = fma(r, r, nrm);
+                }
+                tr_[lr][i] = rnew;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                const int lr = lr0 + u * (256 / P);
+                const int row = t * TR + lr;
+                double dn = 0.0;
+                if (row < n && i < p) {
+                    dn = tr_[lr][i];
+                    for (int jj = 0; jj < p; ++jj) dn = fma(be[i][jj], td_[lr][jj], dn);
+                }
+                if (row < n) Dn[static_cast<size_t>(row) * P + i] = dn;
+                tdn[lr][i] = dn;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (pi[q] >= 0) {
+                    double sp = part[q];
+                    for (int r = pg[q]; r < TR; r += GR) sp = fma(tdn[r][pi[q]], tdn[r][pj[q]], sp);
+                    part[q] = sp;
+                }
+            __syncthreads();
+        }
+        nred[tid] = nrm;
+        __syncthreads();
+        if (tid < P) {
+            double sn = 0.0;
+            for (int r = 0; r < 256 / P; ++r) sn += nred[r * P + tid];
+            norm_part[static_cast<size_t>(blockIdx.x) * P + tid] = sn;
+        }
+        if (GR == 1) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q)
+                if (pi[q] >= 0) pair_part[static_cast<size_t>(blockIdx.x) * npairs + tid + q * 256] = part[q];
+        } else {
+            __syncthreads();
+            nred[tid] = part[0];
+            __syncthreads();
+            if (tid < npairs) {
+                double sp = 0.0;
+                for (int g = 0; g < GR; ++g) sp += nred[tid * GR + g];
+                pair_part[static_cast<size_t>(blockIdx.x) * npairs + tid] = sp;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // (5) Norms from partials -> record + convergence (the fast twin of the tail of
 // beta_solve_warp; solvers.hpp:125-154).  `diag_stride` selects the layout:
 // norm partials are P values per CTA (stride P), residual-pass partials keep

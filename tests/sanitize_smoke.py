@@ -6,8 +6,9 @@ fast-mode solve:
 
     python tests/sanitize_smoke.py
 
-(compute-sanitizer is not available on the GPU pool; the same cases also run
-inside the -m gpu suite.)"""
+Meant to run under compute-sanitizer (tools/sanitize.sh, SANITIZE_SMALL=1);
+the GPU pool refuses compute-sanitizer (profiles/r02_sanitizer_closed.txt),
+so the same cases run bitwise against the oracle inside the -m gpu suite."""
 import os
 import sys
 
@@ -46,7 +47,13 @@ def main():
     ft = m.ccg_solve(A, b, X0, m.SolveOptions(tol=0.0, max_iters=6, recompute_residual_every=4),
                      m.GpuOptions(arith="fast"))
     print(f"fast n={n} p={p}: {ft.iteration_count()} iterations, status {ft.status}", flush=True)
-    return 0
+    # two row shards driven by one process (peer-push Q, event barriers)
+    gt = m.ccg_solve(A, b, X0, m.SolveOptions(tol=0.0, max_iters=6, recompute_residual_every=4),
+                     m.GpuOptions(devices=[0, 0]))
+    ot = po.oracle_ccg(A, b, X0, tol=0.0, max_iters=6, recompute=4)
+    ok = np.array_equal(gt.residual_norms, ot.residual_norms) and np.array_equal(gt.final_x, ot.final_x)
+    print(f"exact 2 shards n={n} p={p}: {'bitwise ok' if ok else 'MISMATCH'}", flush=True)
+    return 0 if ok else 1
 
 
 if __name__ == "__main__":

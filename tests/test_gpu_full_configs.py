@@ -170,6 +170,12 @@ def test_full_config_parity(m, po, c):
     assert abs(d_it) <= 2
     assert hist_max < 1e-8
     assert xrel < 1e-8
-    assert fres_max < 1e-8
-    if not above.all():  # at the floor both are round-off: bounded, not compared
-        assert np.all(f.final_residual_norms[~above] / nb < 1e-11)
+    if kd >= ot.iterations:
+        # the whole history is inside the comparable band (cfg 3 / 4): the true
+        # final residuals agree like the history does
+        assert fres_max < 1e-8
+    else:
+        # past k_div (cfg 1 converged to tol, cfg 2 at the round-off floor) the
+        # two runs' last iterates differ at the rounding level of their own
+        # residual: both true residuals are that small
+        assert np.all(f.final_residual_norms <= 10 * np.maximum(ot.final_residual_norms, 1e-11 * nb))
