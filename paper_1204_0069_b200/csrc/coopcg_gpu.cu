@@ -227,13 +227,78 @@ struct coopcg_gpu_ctx {
     // exchanges are NCCL collectives on this context's stream.
     void* nccl = nullptr;           // ncclComm_t
     int nranks = 1, rank = 0;
+    // COOPCG_GUARD=1 (debug): every device buffer sits between two guard
+    // regions filled with a byte pattern; run / destroy check them
+    struct Guarded {
+        void* user;
+        size_t bytes;
+        const char* name;
+    };
+    std::vector<Guarded> guards;
 };
 
+// ---- device allocations (optionally guarded) ------------------------------
+// COOPCG_GUARD=1: each buffer gets kGuardBytes of 0xA5 before and after it;
+// check_guards() reports the first region a kernel wrote into.  A stand-in
+// for compute-sanitizer's memcheck, which the GPU pool does not allow.
+constexpr size_t kGuardBytes = 16384;
+constexpr unsigned char kGuardByte = 0xA5;
+static bool guard_enabled() {
+    static const bool on = std::getenv("COOPCG_GUARD") != nullptr && std::getenv("COOPCG_GUARD")[0] == '1';
+    return on;
+}
+template <typename T>
+static cudaError_t gmalloc(coopcg_gpu_ctx* ctx, T** p, size_t bytes, const char* name) {
+    if (!guard_enabled()) return cudaMalloc(reinterpret_cast<void**>(p), bytes);
+    char* base = nullptr;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&base), bytes + 2 * kGuardBytes);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaMemset(base, kGuardByte, kGuardBytes)) != cudaSuccess) return e;
+    if ((e = cudaMemset(base + kGuardBytes + bytes, kGuardByte, kGuardBytes)) != cudaSuccess) return e;
+    *p = reinterpret_cast<T*>(base + kGuardBytes);
+    ctx->guards.push_back({base + kGuardBytes, bytes, name});
+    return cudaSuccess;
+}
+static void gfree(coopcg_gpu_ctx* ctx, void* p) {
+    if (!p) return;
+    if (guard_enabled()) {
+        for (size_t i = 0; i < ctx->guards.size(); ++i)
+            if (ctx->guards[i].user == p) {
+                ctx->guards.erase(ctx->guards.begin() + i);
+                cudaFree(static_cast<char*>(p) - kGuardBytes);
+                return;
+            }
+    }
+    cudaFree(p);
+}
+// 0, or 1 with `what` naming the first overwritten guard region.
+static int check_guards(const coopcg_gpu_ctx* ctx, std::string& what) {
+    std::vector<unsigned char> buf(kGuardBytes);
+    for (const auto& g : ctx->guards)
+        for (int side = 0; side < 2; ++side) {
+            const char* at = side ? static_cast<const char*>(g.user) + g.bytes
+                                  : static_cast<const char*>(g.user) - kGuardBytes;
+            if (cudaMemcpy(buf.data(), at, kGuardBytes, cudaMemcpyDeviceToHost) != cudaSuccess) {
+                what = std::string("cannot read the guard of ") + g.name;
+                return 1;
+            }
+            for (size_t i = 0; i < kGuardBytes; ++i)
+                if (buf[i] != kGuardByte) {
+                    char m[160];
+                    std::snprintf(m, sizeof m, "device buffer %s: guard %s the buffer overwritten at byte %zu",
+                                  g.name, side ? "after" : "before", i);
+                    what = m;
+                    return 1;
+                }
+        }
+    return 0;
+}
+
 static void hh_free(coopcg_gpu_ctx* ctx) {
-    cudaFree(ctx->hh_V);
-    cudaFree(ctx->hh_lam);
-    cudaFree(ctx->hh_w);
-    cudaFree(ctx->hh_t);
+    gfree(ctx, ctx->hh_V);
+    gfree(ctx, ctx->hh_lam);
+    gfree(ctx, ctx->hh_w);
+    gfree(ctx, ctx->hh_t);
     ctx->hh_V = ctx->hh_lam = ctx->hh_w = ctx->hh_t = nullptr;
     ctx->hh_m = -1;
 }
@@ -709,38 +774,38 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     if (ctx->nccl) nccl_api().commDestroy(static_cast<ncclComm_t>(ctx->nccl));
-    cudaFree(ctx->At);
-    cudaFree(ctx->X);
-    cudaFree(ctx->X0);
-    cudaFree(ctx->R);
-    cudaFree(ctx->Dblk[0]);
-    cudaFree(ctx->Dblk[1]);
+    gfree(ctx, ctx->At);
+    gfree(ctx, ctx->X);
+    gfree(ctx, ctx->X0);
+    gfree(ctx, ctx->R);
+    gfree(ctx, ctx->Dblk[0]);
+    gfree(ctx, ctx->Dblk[1]);
     for (void* ptr : ctx->ipc_opened) cudaIpcCloseMemHandle(ptr);
-    cudaFree(ctx->Qalt);
-    cudaFree(ctx->Q);
-    cudaFree(ctx->S);
-    cudaFree(ctx->V);
-    cudaFree(ctx->b);
-    cudaFree(ctx->qpart);
-    cudaFree(ctx->gpart);
+    gfree(ctx, ctx->Qalt);
+    gfree(ctx, ctx->Q);
+    gfree(ctx, ctx->S);
+    gfree(ctx, ctx->V);
+    gfree(ctx, ctx->b);
+    gfree(ctx, ctx->qpart);
+    gfree(ctx, ctx->gpart);
     hh_free(ctx);
-    cudaFree(ctx->npart);
-    cudaFree(ctx->dtiles);
-    cudaFree(ctx->gfin);
-    cudaFree(ctx->gbar);
-    cudaFree(ctx->small);
-    cudaFree(ctx->partials);
-    cudaFree(ctx->init_norms);
-    cudaFree(ctx->final_norms);
-    cudaFree(ctx->ctl);
-    cudaFree(ctx->descs);
-    cudaFree(ctx->tr_norms);
-    cudaFree(ctx->tr_minres);
-    cudaFree(ctx->tr_wall);
-    cudaFree(ctx->stage);
+    gfree(ctx, ctx->npart);
+    gfree(ctx, ctx->dtiles);
+    gfree(ctx, ctx->gfin);
+    gfree(ctx, ctx->gbar);
+    gfree(ctx, ctx->small);
+    gfree(ctx, ctx->partials);
+    gfree(ctx, ctx->init_norms);
+    gfree(ctx, ctx->final_norms);
+    gfree(ctx, ctx->ctl);
+    gfree(ctx, ctx->descs);
+    gfree(ctx, ctx->tr_norms);
+    gfree(ctx, ctx->tr_minres);
+    gfree(ctx, ctx->tr_wall);
+    gfree(ctx, ctx->stage);
     for (int q = 0; q < 2; ++q) {
         if (ctx->pin[q]) cudaFreeHost(ctx->pin[q]);
-        cudaFree(ctx->dslot[q]);
+        gfree(ctx, ctx->dslot[q]);
         if (ctx->pin_ev[q]) cudaEventDestroy(ctx->pin_ev[q]);
     }
     if (ctx->ctl_host) cudaFreeHost(ctx->ctl_host);
@@ -762,17 +827,17 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
 
 int ensure_trace_capacity(coopcg_gpu_ctx* ctx, int cap) {
     if (cap <= ctx->tr_capacity) return COOPCG_OK;
-    cudaFree(ctx->tr_norms);
-    cudaFree(ctx->tr_minres);
-    cudaFree(ctx->tr_wall);
+    gfree(ctx, ctx->tr_norms);
+    gfree(ctx, ctx->tr_minres);
+    gfree(ctx, ctx->tr_wall);
     ctx->tr_norms = nullptr;
     ctx->tr_minres = nullptr;
     ctx->tr_wall = nullptr;
     // rows are p_orig wide (the kernels write tr_norms[k * p0 + j]; a previous
     // mccg solve may have left ctx->p reduced)
-    CK(cudaMalloc(&ctx->tr_norms, sizeof(double) * (size_t)cap * ctx->p_orig));
-    CK(cudaMalloc(&ctx->tr_minres, sizeof(double) * (size_t)cap));
-    CK(cudaMalloc(&ctx->tr_wall, sizeof(unsigned long long) * (size_t)cap));
+    CK(gmalloc(ctx, &ctx->tr_norms, sizeof(double) * (size_t)cap * ctx->p_orig, "tr_norms"));
+    CK(gmalloc(ctx, &ctx->tr_minres, sizeof(double) * (size_t)cap, "tr_minres"));
+    CK(gmalloc(ctx, &ctx->tr_wall, sizeof(unsigned long long) * (size_t)cap, "tr_wall"));
     ctx->tr_capacity = cap;
     return COOPCG_OK;
 }
@@ -825,7 +890,7 @@ static int ensure_pinned(coopcg_gpu_ctx* ctx) {
     ctx->pin_elems = std::max<size_t>(slot_bytes / sizeof(double), (size_t)ctx->n);
     for (int q = 0; q < 2; ++q) {
         CK(cudaHostAlloc(&ctx->pin[q], sizeof(double) * ctx->pin_elems, cudaHostAllocDefault));
-        CK(cudaMalloc(&ctx->dslot[q], sizeof(double) * ctx->pin_elems));
+        CK(gmalloc(ctx, &ctx->dslot[q], sizeof(double) * ctx->pin_elems, "dslot"));
         CK(cudaEventCreateWithFlags(&ctx->pin_ev[q], cudaEventDisableTiming));
     }
     return COOPCG_OK;
@@ -894,7 +959,15 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         const int slots = std::min(2 * ctx->sms, kMaxParts);
         int best_k = 1;
         double best_eff = -1.0;
-        for (int kc = 1; kc <= std::min(16, ntiles); ++kc) {
+        // The split is capped at 8: every extra k-chunk is one more n x P
+        // partial block the row pass must sum (tools/fast_sweep.sh, round 2:
+        // cap 8 vs 16: cfg 2 2861 vs 2842 it/s, cfg 1 20914 vs 19775 it/s;
+        // caps 1-4 lose A.D wave efficiency).  COOPCG_FAST_KMAX overrides.
+        static const int kmax = [] {
+            const char* e = std::getenv("COOPCG_FAST_KMAX");
+            return e ? std::max(1, std::atoi(e)) : 8;
+        }();
+        for (int kc = 1; kc <= std::min(kmax, ntiles); ++kc) {
             const double w = (double)ctx->npanels * kc / slots;
             const double eff = w / std::ceil(w);
             if (eff > best_eff + 1e-3) {
@@ -911,7 +984,12 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         // Row / update passes are light; fewer CTAs keep the single-CTA
         // partial reductions short (~P^2 x grid doubles).
         const int TR = (256 / ctx->P) * 2;  // (smaller) rows per tile of fast_rows / fast_update
-        const int rg = (ctx->P <= 8) ? 128 : (ctx->P == 16 ? 192 : 296);
+        static const int rg_env = [] {
+            const char* e = std::getenv("COOPCG_FAST_RG");
+            return e ? std::atoi(e) : 0;
+        }();
+        const int rg = rg_env > 0 ? std::min(rg_env, kMaxParts)
+                                  : ((ctx->P <= 8) ? 128 : (ctx->P == 16 ? 192 : 296));
         ctx->f_rgrid = std::min(rg, (ctx->n_loc + TR - 1) / TR);
         ctx->f_ugrid = std::min(rg, (n + TR - 1) / TR);
     } else {
@@ -940,41 +1018,41 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         }                                                                                 \
     } while (0)
     CKC(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    CKC(cudaMalloc(&ctx->At, sizeof(double) * ctx->ap_elems));
+    CKC(gmalloc(ctx, &ctx->At, sizeof(double) * ctx->ap_elems, "A"));
     CKC(cudaMemsetAsync(ctx->At, 0, sizeof(double) * ctx->ap_elems, ctx->stream));
     double** blocks[] = {&ctx->X, &ctx->X0, &ctx->R, &ctx->Dblk[0], &ctx->Dblk[1], &ctx->Q, &ctx->S, &ctx->V};
     for (double** bp : blocks) {
-        CKC(cudaMalloc(bp, sizeof(double) * blk));
+        CKC(gmalloc(ctx, bp, sizeof(double) * blk, "n x P block"));
         CKC(cudaMemsetAsync(*bp, 0, sizeof(double) * blk, ctx->stream));
     }
-    CKC(cudaMalloc(&ctx->b, sizeof(double) * n));
+    CKC(gmalloc(ctx, &ctx->b, sizeof(double) * n, "b"));
     if (arith == COOPCG_ARITH_FAST) {
-        CKC(cudaMalloc(&ctx->qpart, sizeof(double) * (size_t)ctx->f_kchunks * ctx->n_loc * ctx->P));
-        CKC(cudaMalloc(&ctx->gpart, sizeof(double) * (size_t)ctx->f_rgrid * 4 * ctx->P * ctx->P));
-        CKC(cudaMalloc(&ctx->npart, sizeof(double) * (size_t)ctx->f_ugrid * ctx->P));
-        CKC(cudaMalloc(&ctx->dtiles, sizeof(double) * (size_t)ctx->lay.ntiles * ctx->P * kFastT));
-        CKC(cudaMalloc(&ctx->gfin, sizeof(double) * 4 * ctx->P * ctx->P));
-        CKC(cudaMalloc(&ctx->gbar, 2 * sizeof(unsigned int)));
+        CKC(gmalloc(ctx, &ctx->qpart, sizeof(double) * (size_t)ctx->f_kchunks * ctx->n_loc * ctx->P, "qpart"));
+        CKC(gmalloc(ctx, &ctx->gpart, sizeof(double) * (size_t)ctx->f_rgrid * 4 * ctx->P * ctx->P, "gpart"));
+        CKC(gmalloc(ctx, &ctx->npart, sizeof(double) * (size_t)ctx->f_ugrid * ctx->P, "npart"));
+        CKC(gmalloc(ctx, &ctx->dtiles, sizeof(double) * (size_t)ctx->lay.ntiles * ctx->P * kFastT, "dtiles"));
+        CKC(gmalloc(ctx, &ctx->gfin, sizeof(double) * 4 * ctx->P * ctx->P, "gfin"));
+        CKC(gmalloc(ctx, &ctx->gbar, 2 * sizeof(unsigned int), "gbar"));
         CKC(cudaMemsetAsync(ctx->gbar, 0, 2 * sizeof(unsigned int), ctx->stream));
         ctx->fuse_ok = ctx->n_loc == n && fast_iter_fits(ctx);
     }
     const SmallLayout L{ctx->P};
-    CKC(cudaMalloc(&ctx->small, sizeof(double) * L.total()));
+    CKC(gmalloc(ctx, &ctx->small, sizeof(double) * L.total(), "small"));
     CKC(cudaMemsetAsync(ctx->small, 0, sizeof(double) * L.total(), ctx->stream));
     ctx->nparts = kMaxParts;
-    CKC(cudaMalloc(&ctx->partials, sizeof(double) * kMaxParts * 528));
-    CKC(cudaMalloc(&ctx->init_norms, sizeof(double) * (ctx->P + 1)));
-    CKC(cudaMalloc(&ctx->final_norms, sizeof(double) * (ctx->P + 1)));
-    CKC(cudaMalloc(&ctx->ctl, sizeof(Ctl)));
+    CKC(gmalloc(ctx, &ctx->partials, sizeof(double) * kMaxParts * 528, "partials"));
+    CKC(gmalloc(ctx, &ctx->init_norms, sizeof(double) * (ctx->P + 1), "init_norms"));
+    CKC(gmalloc(ctx, &ctx->final_norms, sizeof(double) * (ctx->P + 1), "final_norms"));
+    CKC(gmalloc(ctx, &ctx->ctl, sizeof(Ctl), "ctl"));
     CKC(cudaHostAlloc(&ctx->ctl_host, 2 * sizeof(Ctl), cudaHostAllocDefault));
     CKC(cudaHostAlloc(&ctx->minres_host, 2 * kChunkMax * sizeof(double), cudaHostAllocDefault));
     std::vector<ChainDesc> descs;
     build_descs(p, ctx->P, descs, ctx->desc_off, ctx->desc_cnt);
-    CKC(cudaMalloc(&ctx->descs, sizeof(ChainDesc) * descs.size()));
+    CKC(gmalloc(ctx, &ctx->descs, sizeof(ChainDesc) * descs.size(), "descs"));
     CKC(cudaMemcpyAsync(ctx->descs, descs.data(), sizeof(ChainDesc) * descs.size(), cudaMemcpyHostToDevice,
                         ctx->stream));
     ctx->stage_elems = std::max<size_t>(blk, (size_t)n * 128);
-    CKC(cudaMalloc(&ctx->stage, sizeof(double) * ctx->stage_elems));
+    CKC(gmalloc(ctx, &ctx->stage, sizeof(double) * ctx->stage_elems, "stage"));
     ctx->mv_ev.resize(2 * 2 * kChunkMax);
     for (auto& ev : ctx->mv_ev) CKC(cudaEventCreate(&ev));
     CKC(cudaEventCreate(&ctx->ev_run0));
@@ -1102,10 +1180,10 @@ int coopcg_gpu_gen_householder_begin(coopcg_gpu_ctx* ctx, uint64_t seed, int m, 
     hh_free(ctx);
     std::vector<double> V((size_t)std::max(m, 1) * n), lam(n);
     coopcg_gen_householder_factors(n, m, kappa, seed, V.data(), lam.data());
-    CK(cudaMalloc(&ctx->hh_V, sizeof(double) * V.size()));
-    CK(cudaMalloc(&ctx->hh_lam, sizeof(double) * n));
-    CK(cudaMalloc(&ctx->hh_w, sizeof(double) * n));
-    CK(cudaMalloc(&ctx->hh_t, sizeof(double) * 2));
+    CK(gmalloc(ctx, &ctx->hh_V, sizeof(double) * V.size(), "hh_V"));
+    CK(gmalloc(ctx, &ctx->hh_lam, sizeof(double) * n, "hh_lam"));
+    CK(gmalloc(ctx, &ctx->hh_w, sizeof(double) * n, "hh_w"));
+    CK(gmalloc(ctx, &ctx->hh_t, sizeof(double) * 2, "hh_t"));
     CK(cudaMemcpyAsync(ctx->hh_V, V.data(), sizeof(double) * V.size(), cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemcpyAsync(ctx->hh_lam, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
     CK(cudaMemsetAsync(ctx->hh_w, 0, sizeof(double) * n, ctx->stream));
@@ -2046,6 +2124,11 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     tm.kernel_launches = launches;
     c0->timing = tm;
     ctx->timing = tm;
+    if (guard_enabled())
+        for (coopcg_gpu_ctx* c : X.s) {
+            std::string what;
+            if (check_guards(c, what)) return fail(ctx, COOPCG_E_CUDA, "COOPCG_GUARD: %s", what.c_str());
+        }
     const int rc = end_impl(c0, trace);
     if (rc != COOPCG_OK && c0 != ctx) ctx->msg = c0->msg;
     return rc;
@@ -2116,6 +2199,8 @@ int coopcg_gpu_ipc_handles(coopcg_gpu_ctx* ctx, void* handles_out) {
         return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx || !handles_out) return COOPCG_E_INVALID;
     if (!sharded(ctx)) return fail(ctx, COOPCG_E_STATE, "peer exchange is for row-sharded contexts");
+    if (guard_enabled())
+        return fail(ctx, COOPCG_E_STATE, "CUDA IPC exchange is unavailable with COOPCG_GUARD=1 (guarded buffers)");
     CK(cudaSetDevice(ctx->device));
     if (!ctx->Qalt) {
         CK(cudaMalloc(&ctx->Qalt, sizeof(double) * (size_t)ctx->n * ctx->P));
@@ -2204,6 +2289,10 @@ int coopcg_gpu_end(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
     CK(cudaSetDevice(ctx->device));
     ctx->timing.kernel_launches = ctx->launches;
     const int rc = end_impl(ctx, trace);  // synchronises the stream
+    if (rc == COOPCG_OK && guard_enabled()) {
+        std::string what;
+        if (check_guards(ctx, what)) return fail(ctx, COOPCG_E_CUDA, "COOPCG_GUARD: %s", what.c_str());
+    }
     if (rc != COOPCG_OK) return rc;
     // the phase API's sampled A.D launches (iteration 8 i; later ones were no-ops)
     double tot = 0.0;
@@ -2431,7 +2520,8 @@ int coopcg_gpu_create_multi(int n, int p, int ndev, const int* devices, int arit
     for (coopcg_gpu_ctx* c : ctx->shards) {
         cudaSetDevice(c->device);
         const size_t bytes = sizeof(double) * (size_t)n * c->P;
-        if (cudaMalloc(&c->Qalt, bytes) != cudaSuccess || cudaMemset(c->Qalt, 0, bytes) != cudaSuccess) {
+        if (gmalloc(c, &c->Qalt, bytes, "Q (odd iterations)") != cudaSuccess ||
+            cudaMemset(c->Qalt, 0, bytes) != cudaSuccess) {
             fail(ctx, COOPCG_E_CUDA, "allocating the second Q buffer on device %d", c->device);
             return bail(COOPCG_E_CUDA);
         }

@@ -295,8 +295,8 @@ __global__ void __launch_bounds__(256)
 //   beta_i:  M beta_i^T  = -(R^T Q + alpha Q^T Q)_i   (algebraic R_new^T Q)
 // mode 0: alpha + beta; mode 1: alpha only (recompute iteration, beta later);
 // mode 2: beta only from G0 = R_new^T Q of a residual pass (uses ctl->lu).
-// L L^T x = rhs for lane-owned right-hand sides, L in shared memory
-// (compile-time P, active p; the operation order of the one-warp version).
+// L L^T x = rhs for lane-owned right-hand sides, L in shared memory with
+// 1 / L_ii stored on its diagonal (no division on the solve's critical path).
 template <int P>
 __device__ __forceinline__ void chol_solve_regs(const double (*l)[P + 1], int p, const double (&rhs)[P],
                                                 double (&x)[P]) {
@@ -312,7 +312,7 @@ __device__ __forceinline__ void chol_solve_regs(const double (*l)[P + 1], int p,
             double s = rhs[i];
 #pragma unroll
             for (int j = 0; j < i; ++j) s = fma(-l[i][j], y[j], s);
-            y[i] = s / l[i][i];
+            y[i] = s * l[i][i];  // the diagonal holds 1 / L_ii
         }
     }
 #pragma unroll
@@ -322,7 +322,7 @@ __device__ __forceinline__ void chol_solve_regs(const double (*l)[P + 1], int p,
 #pragma unroll
             for (int j = i + 1; j < P; ++j)
                 if (j < p) s = fma(-l[j][i], x[j], s);
-            x[i] = s / l[i][i];
+            x[i] = s * l[i][i];
         }
     }
 }
@@ -388,10 +388,10 @@ __global__ void __launch_bounds__(1024)
                 double s = l[k];
 #pragma unroll
                 for (int m = 0; m < k; ++m) s = fma(-l[m], l[m], s);
-                dk = (s > floor) ? sqrt(s) : -1.0;
+                dk = (s > floor) ? rsqrt(s) : -1.0;  // 1 / L_kk
             }
-            const double lkk = __shfl_sync(0xffffffffu, dk, k);
-            if (!(lkk > 0.0)) {
+            const double ikk = __shfl_sync(0xffffffffu, dk, k);
+            if (!(ikk > 0.0)) {
                 if (lane == 0) {
                     ctl->status = 1;  // rank collapse (pivot vanished)
                     ctl->stop = 1;
@@ -405,9 +405,9 @@ __global__ void __launch_bounds__(1024)
                 double s = l[k];
 #pragma unroll
                 for (int m = 0; m < k; ++m) s = fma(-l[m], rk[m], s);
-                l[k] = s / lkk;
+                l[k] = s * ikk;
             }
-            if (lane == k) l[k] = lkk;
+            if (lane == k) l[k] = ikk;  // the factor keeps 1 / L_kk on its diagonal
         }
         if (lane < P) {
 #pragma unroll
@@ -792,10 +792,10 @@ __global__ void __launch_bounds__(256, 2)
                 double sk = l[k];
 #pragma unroll
                 for (int m = 0; m < k; ++m) sk = fma(-l[m], l[m], sk);
-                dk = (sk > floor) ? sqrt(sk) : -1.0;
+                dk = (sk > floor) ? rsqrt(sk) : -1.0;  // 1 / L_kk
             }
-            const double lkk = __shfl_sync(0xffffffffu, dk, k);
-            if (!(lkk > 0.0)) {
+            const double ikk = __shfl_sync(0xffffffffu, dk, k);
+            if (!(ikk > 0.0)) {
                 if (pub && lane == 0) {
                     ctl->status = 1;  // rank collapse (pivot vanished)
                     ctl->stop = 1;
@@ -810,9 +810,9 @@ __global__ void __launch_bounds__(256, 2)
                 double sk = l[k];
 #pragma unroll
                 for (int m = 0; m < k; ++m) sk = fma(-l[m], rk[m], sk);
-                l[k] = sk / lkk;
+                l[k] = sk * ikk;
             }
-            if (lane == k) l[k] = lkk;
+            if (lane == k) l[k] = ikk;  // 1 / L_kk on the diagonal
         }
         if (fail) {
             if (lane == 0) abort_flag = 1;
