@@ -73,3 +73,35 @@ def test_fast_fused_iteration_matches_separate_kernels():
         assert fused[key]["it"] == sep[key]["it"] == 30
         a, b = np.array(fused[key]["x"]), np.array(sep[key]["x"])
         assert np.max(np.linalg.norm(a - b, axis=0) / np.linalg.norm(b, axis=0)) < 1e-12, key
+
+
+GUARD_SCRIPT = r"""
+import ctypes as C, numpy as np, paper_1204_0069_b200 as m
+from paper_1204_0069_b200 import _capi
+from cuda.bindings import runtime as rt
+n, p = 300, 4
+ctx = m.GpuContext(n, p)
+ctx.gen_A("diagdom", 3)
+ctx.upload(m.gen_rhs(n, "uniform", 3), m.gen_starts(n, p, 3))
+t = ctx.run(m.SolveOptions(tol=0.0, max_iters=5))          # clean run: guards intact
+ptr, ld = C.c_void_p(), C.c_int()
+assert _capi.lib().coopcg_gpu_block(ctx._h, _capi.BLOCK_X, 0, C.byref(ptr), C.byref(ld)) == 0
+# one double just past the end of X, as an off-by-one-row kernel would write
+err, = rt.cudaMemset(ptr.value + n * ld.value * 8, 0x11, 8)
+assert err == rt.cudaError_t.cudaSuccess
+try:
+    ctx.run(m.SolveOptions(tol=0.0, max_iters=5))
+    print("NOT DETECTED")
+except m.CudaError as e:
+    print("DETECTED", e)
+"""
+
+
+def test_guard_mode_detects_an_overflow():
+    """COOPCG_GUARD=1 (the memcheck stand-in: compute-sanitizer is refused on
+    the GPU pool) reports a write past the end of a device buffer."""
+    env = dict(os.environ, COOPCG_GUARD="1")
+    r = subprocess.run([sys.executable, "-c", GUARD_SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert "DETECTED" in r.stdout and "guard after the buffer" in r.stdout, r.stdout
