@@ -644,10 +644,11 @@ template <int P>
 __host__ __device__ constexpr int fused_upd_tr() { return (256 / P) * ((P >= 32) ? 2 : 4); }
 template <int P>
 __host__ __device__ constexpr size_t fused_smem_bytes() {
-    // phase A: 3 tiles; phase C/D: grams (4 P^2) + alpha, beta + 4 update tiles + reductions
+    // phase A's three tiles (kept for phase D when the tilings agree), then phase
+    // C/D: grams (4 P^2) + alpha, beta + 4 update tiles + reductions + the factor
     constexpr size_t a = 3ull * fused_rows_tr<P>() * P;
     constexpr size_t d = 4ull * P * P + 2ull * P * (P + 1) + 4ull * fused_upd_tr<P>() * P + 256 + P * (P + 1);
-    return (a > d ? a : d) * sizeof(double);
+    return (a + d) * sizeof(double);
 }
 
 template <int P>
@@ -665,38 +666,73 @@ __global__ void __launch_bounds__(256, 2)
     const unsigned int G = gridDim.x;
     const SmallLayout L{P};
 
+    // When the row pass and the update pass tile the rows alike and every CTA
+    // owns at most one tile, the update reuses the row pass's D, Q, R tiles
+    // (still in shared memory) and X is fetched during the row pass.
+    constexpr int TRA = fused_rows_tr<P>();
+    constexpr bool SAME_TILING = TRA == fused_upd_tr<P>();
+    const bool reuse = SAME_TILING && (n + TRA - 1) / TRA <= static_cast<int>(gridDim.x);
+    double xpre[4] = {0.0, 0.0, 0.0, 0.0};
     // ---- A: row pass (kernel (2), mode 0) ----------------------------------
     {
         constexpr int RP = 4;
-        constexpr int TR = fused_rows_tr<P>();
+        constexpr int TR = TRA;
         constexpr int PER = (NOUT + 255) / 256;
         double(*tq)[P] = reinterpret_cast<double(*)[P]>(fsm);
         double(*td)[P] = reinterpret_cast<double(*)[P]>(fsm + TR * P);
         double(*trr)[P] = reinterpret_cast<double(*)[P]>(fsm + 2 * TR * P);
         const int lr0 = tid / P, j = tid % P;
+        if (reuse) {
+#pragma unroll
+            for (int u = 0; u < RP; ++u) {
+                const int il = blockIdx.x * TR + lr0 + u * (256 / P);
+                if (il < n) xpre[u] = X[static_cast<size_t>(il) * P + j];
+            }
+        }
         double acc[PER];
 #pragma unroll
         for (int q = 0; q < PER; ++q) acc[q] = 0.0;
         const int ntile = (n + TR - 1) / TR;
         for (int t = blockIdx.x; t < ntile; t += G) {
             double v[RP], dv[RP], rv[RP];
+            const size_t cs = static_cast<size_t>(n) * P;
+            if (kchunks <= 8) {
+                // every row's chunk partials in flight together, then summed in chunk order
+                double w[RP][8];
 #pragma unroll
-            for (int u = 0; u < RP; ++u) {
-                const int il = t * TR + lr0 + u * (256 / P);
-                v[u] = dv[u] = rv[u] = 0.0;
-                if (il < n) {
+                for (int u = 0; u < RP; ++u) {
+                    const int il = t * TR + lr0 + u * (256 / P);
                     const double* qp = Qpart + static_cast<size_t>(il) * P + j;
-                    const size_t cs = static_cast<size_t>(n) * P;
-                    for (int c0 = 0; c0 < kchunks; c0 += 8) {
-                        double w[8];
 #pragma unroll
-                        for (int cc = 0; cc < 8; ++cc) w[cc] = (c0 + cc < kchunks) ? qp[(c0 + cc) * cs] : 0.0;
+                    for (int cc = 0; cc < 8; ++cc) w[u][cc] = (il < n && cc < kchunks) ? qp[cc * cs] : 0.0;
+                    dv[u] = (il < n) ? D[static_cast<size_t>(il) * P + j] : 0.0;
+                    rv[u] = (il < n) ? R[static_cast<size_t>(il) * P + j] : 0.0;
+                }
 #pragma unroll
-                        for (int cc = 0; cc < 8; ++cc)
-                            if (c0 + cc < kchunks) v[u] += w[cc];
+                for (int u = 0; u < RP; ++u) {
+                    v[u] = 0.0;
+#pragma unroll
+                    for (int cc = 0; cc < 8; ++cc)
+                        if (cc < kchunks) v[u] += w[u][cc];
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < RP; ++u) {
+                    const int il = t * TR + lr0 + u * (256 / P);
+                    v[u] = dv[u] = rv[u] = 0.0;
+                    if (il < n) {
+                        const double* qp = Qpart + static_cast<size_t>(il) * P + j;
+                        for (int c0 = 0; c0 < kchunks; c0 += 8) {
+                            double w[8];
+#pragma unroll
+                            for (int cc = 0; cc < 8; ++cc) w[cc] = (c0 + cc < kchunks) ? qp[(c0 + cc) * cs] : 0.0;
+#pragma unroll
+                            for (int cc = 0; cc < 8; ++cc)
+                                if (c0 + cc < kchunks) v[u] += w[cc];
+                        }
+                        dv[u] = D[static_cast<size_t>(il) * P + j];
+                        rv[u] = R[static_cast<size_t>(il) * P + j];
                     }
-                    dv[u] = D[static_cast<size_t>(il) * P + j];
-                    rv[u] = R[static_cast<size_t>(il) * P + j];
                 }
             }
 #pragma unroll
@@ -746,10 +782,10 @@ __global__ void __launch_bounds__(256, 2)
     grid_barrier(gbar, G);
 
     // ---- C: step solves (kernel (3), mode 0), redundantly in every CTA ------
-    double* flat = fsm;                          // 4 P^2
-    double(*al)[P + 1] = reinterpret_cast<double(*)[P + 1]>(fsm + NOUT);
-    double(*be)[P + 1] = reinterpret_cast<double(*)[P + 1]>(fsm + NOUT + P * (P + 1));
-    double* tiles = fsm + NOUT + 2 * P * (P + 1);
+    double* flat = fsm + 3 * TRA * P;            // 4 P^2 (after phase A's tiles)
+    double(*al)[P + 1] = reinterpret_cast<double(*)[P + 1]>(flat + NOUT);
+    double(*be)[P + 1] = reinterpret_cast<double(*)[P + 1]>(flat + NOUT + P * (P + 1));
+    double* tiles = flat + NOUT + 2 * P * (P + 1);
     constexpr int TRU = fused_upd_tr<P>();
     double* nred = tiles + 4 * TRU * P;          // 256
     double(*lsm)[P + 1] = reinterpret_cast<double(*)[P + 1]>(nred + 256);
@@ -860,8 +896,10 @@ __global__ void __launch_bounds__(256, 2)
         constexpr int TR = TRU;
         double(*tr_)[P] = reinterpret_cast<double(*)[P]>(tiles);
         double(*tdn)[P] = reinterpret_cast<double(*)[P]>(tiles + TR * P);
-        double(*td_)[P] = reinterpret_cast<double(*)[P]>(tiles + 2 * TR * P);
-        double(*tq_)[P] = reinterpret_cast<double(*)[P]>(tiles + 3 * TR * P);
+        // with `reuse`, D and Q are phase A's tiles (tq at fsm, td after it)
+        double(*td_)[P] = reinterpret_cast<double(*)[P]>(reuse ? fsm + TRA * P : tiles + 2 * TR * P);
+        double(*tq_)[P] = reinterpret_cast<double(*)[P]>(reuse ? fsm : tiles + 3 * TR * P);
+        const double(*trA)[P] = reinterpret_cast<const double(*)[P]>(fsm + 2 * TRA * P);
         const int npairs = p * (p + 1) / 2;
         const int GR = npairs < 256 ? 256 / npairs : 1;
         int pi[3], pj[3], pg[3];
@@ -888,20 +926,28 @@ __global__ void __launch_bounds__(256, 2)
         const int ntile = (n + TR - 1) / TR;
         for (int t = blockIdx.x; t < ntile; t += G) {
             double dv[RP], qv[RP], xv[RP], rv[RP];
+            if (reuse) {  // one tile per CTA: the row pass's tiles and the prefetched X
 #pragma unroll
-            for (int u = 0; u < RP; ++u) {
-                const int row = t * TR + lr0 + u * (256 / P);
-                const size_t e = static_cast<size_t>(row) * P + i;
-                const bool ok = row < n;
-                dv[u] = ok ? D[e] : 0.0;
-                qv[u] = ok ? Q[e] : 0.0;
-                xv[u] = ok ? X[e] : 0.0;
-                rv[u] = ok ? R[e] : 0.0;
-            }
+                for (int u = 0; u < RP; ++u) {
+                    xv[u] = xpre[u];
+                    rv[u] = trA[lr0 + u * (256 / P)][i];
+                }
+            } else {
 #pragma unroll
-            for (int u = 0; u < RP; ++u) {
-                td_[lr0 + u * (256 / P)][i] = dv[u];
-                tq_[lr0 + u * (256 / P)][i] = qv[u];
+                for (int u = 0; u < RP; ++u) {
+                    const int row = t * TR + lr0 + u * (256 / P);
+                    const size_t e = static_cast<size_t>(row) * P + i;
+                    const bool ok = row < n;
+                    dv[u] = ok ? D[e] : 0.0;
+                    qv[u] = ok ? Q[e] : 0.0;
+                    xv[u] = ok ? X[e] : 0.0;
+                    rv[u] = ok ? R[e] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < RP; ++u) {
+                    td_[lr0 + u * (256 / P)][i] = dv[u];
+                    tq_[lr0 + u * (256 / P)][i] = qv[u];
+                }
             }
             __syncthreads();
 #pragma unroll
