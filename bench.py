@@ -293,6 +293,8 @@ def _measure(m, torch, cfg, args, arith, steps, warmup, ctx_kw, e2e=True, clock_
     from paper_1204_0069_b200.configs import CONFIGS, make_problem_on_device
 
     pcfg = CONFIGS[cfg.idx]
+    if callable(ctx_kw.get("nccl")):  # rank contexts: a fresh NCCL id per communicator
+        ctx_kw = dict(ctx_kw, nccl=ctx_kw["nccl"]())
     ctx = m.GpuContext(cfg.n, cfg.p, arith=arith, **ctx_kw)
     b, X0, opts = make_problem_on_device(ctx, pcfg)
     ctx.upload(b, X0)
@@ -423,9 +425,11 @@ def run_ours(args, cfg):
         import torch.distributed as dist
         torch.cuda.set_device(local)
         dist.init_process_group("gloo")  # control plane only; the row exchanges are NCCL inside the library
-        uid = [m.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        ctx_kw = {"device": local, "nccl": (ws, rank, uid[0])}
+        def fresh_id():
+            uid = [m.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            return (ws, rank, uid[0])
+        ctx_kw = {"device": local, "nccl": fresh_id}
         barrier = dist.barrier
 
         def reduce_max(x):
