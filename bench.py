@@ -419,7 +419,7 @@ def run_ours(args, cfg):
 
     ws, rank, local = _dist()
     barrier = reduce_max = None
-    if ws > 1:
+    if ws > 1 or args.rank_path:
         if args.gpus not in (1, ws):
             raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
         import torch.distributed as dist
@@ -473,7 +473,7 @@ def run_ours(args, cfg):
         "roofline": main["roofline"], "e2e": main["e2e"], "gpu_launches": main["gpu_launches"],
         "clocks": main["clocks"],
     }
-    big_ok = ws == 1 and n_gpus == 1
+    big_ok = ws == 1 and n_gpus == 1 and not args.rank_path
     if not args.no_secondary:
         other = "fast" if args.arith == "exact" else "exact"
         r2, _ = _measure(m, torch, cfg, args, other, args.steps, args.warmup, ctx_kw, clock_dev=clock_dev,
@@ -504,7 +504,7 @@ def run_ours(args, cfg):
                                           "agent; the reference's per-iteration wall times)"}
     if rank == 0:
         print(json.dumps(line))
-    if ws > 1:
+    if ws > 1 or args.rank_path:
         import torch.distributed as dist
         dist.destroy_process_group()
     return 0
@@ -526,6 +526,8 @@ def main():
     ap.add_argument("--no-oneshot", action="store_true", help="skip the one-shot e2e (A uploaded every call)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the other arithmetic mode")
+    ap.add_argument("--rank-path", action="store_true",
+                    help="(testing) take the one-process-per-GPU rank-context path even with one rank under torchrun")
     args = ap.parse_args()
     cfg = Cfg(args.config)
     if args.impl == "reference":
