@@ -445,7 +445,8 @@ cudaError_t ad_launch(coopcg_gpu_ctx* ctx, const double* src, double* dst, const
 // ---- fast-mode launchers ------------------------------------------------------
 template <int P>
 size_t fast_ad_smem() {
-    return (size_t)kFastS * (kFastBR * kFastT + kFastT * P) * sizeof(double) + 2 * kFastS * sizeof(uint64_t);
+    return (size_t)fast_stages<P>() * (kFastBR * kFastT + kFastT * P) * sizeof(double) +
+           2 * fast_stages<P>() * sizeof(uint64_t);
 }
 // column groups per CTA: P=8 -> 1 (2 DMMA warps), P=16/32 -> 2 (4 DMMA warps)
 template <int P>

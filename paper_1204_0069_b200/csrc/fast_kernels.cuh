@@ -17,7 +17,10 @@ namespace coopcg_gpu {
 
 constexpr int kFastBR = 64;   // rows per A panel (2 consumer warps x 32 rows)
 constexpr int kFastT = 36;    // k per A tile; 36*8 B row stride keeps DMMA A-fragment loads conflict-free
-constexpr int kFastS = 4;     // ring stages
+constexpr int kFastS = 4;     // ring stages (two CTAs per SM; 5 stages at P = 8 measured slower:
+                              // cfg 2 A.D 340 vs 314 us, cfg 1 unchanged -- round 2)
+template <int P>
+__host__ __device__ constexpr int fast_stages() { return kFastS; }
 
 // Fast A layout ("tiles"): panel q (kFastBR rows), k-tile t: a contiguous
 // [r][kk] block of kFastBR x kFastT doubles at ((q*ntiles + t)*BR + r)*T + kk.
@@ -69,7 +72,7 @@ __global__ void __launch_bounds__(32 + 64 * WN)
     static_assert(P % (8 * WN) == 0, "fast contexts pad p to a multiple of 8 per column group");
     constexpr int NT = P / 8 / WN;  // N tiles of 8 columns per warp
     constexpr int NCW = 2 * WN;     // consumer warps
-    constexpr int BR = kFastBR, T = kFastT, S = kFastS;
+    constexpr int BR = kFastBR, T = kFastT, S = fast_stages<P>();
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);  // S x BR x T
