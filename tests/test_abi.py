@@ -97,3 +97,21 @@ def test_mult_counting_matches_workplan():
     for n, p in ((100, 3), (4096, 4), (7, 1)):
         assert iteration_mults(n, p, False) == n * n + 6 * n * p + p * (p + 1) * (2 * p + 1) // 3
         assert iteration_mults(n, p, True) == 2 * n * n + 5 * n * p + p * (p + 1) * (2 * p + 1) // 3
+
+
+def test_row_split_and_multi_argument_checks():
+    """Host-side logic of the in-library multi-GPU paths (no GPU needed): the
+    row split every rank computes identically, and the dimension checks that
+    run before any device call."""
+    import paper_1204_0069_b200 as m
+    for n, parts in ((1000, 3), (131072, 8), (65536, 8), (100, 7), (64, 2), (16384, 4)):
+        rows = [m.row_split(n, parts, g) for g in range(parts)]
+        assert rows[0][0] == 0 and rows[-1][1] == n
+        assert all(rows[g][1] == rows[g + 1][0] for g in range(parts - 1))
+        assert all(r1 > r0 for r0, r1 in rows)
+        if n >= 64 * parts * 2:
+            assert all(r0 % 64 == 0 for r0, _ in rows)  # 64-row panel boundaries
+    with pytest.raises(m.DimensionError, match="cannot be split"):
+        m.GpuContext(3, 1, devices=[0, 0, 0, 0])
+    with pytest.raises(m.Error):
+        m.GpuContext(100, 2, nccl=(2, 0, b"short"))
