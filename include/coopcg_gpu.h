@@ -112,6 +112,8 @@ typedef struct {
     double run_ms;                  /* event time of the whole last run (setup..finalize) */
     double loop_ms;                 /* event time of the iteration loop only */
     long long kernel_launches;      /* kernels this library launched in the last run */
+    double a_l2_resident_bytes;     /* bytes of A the A.D keeps in L2 across iterations
+                                       (evict-last k-range; COOPCG_L2_RES_MB) */
 } coopcg_timing;
 
 typedef struct coopcg_gpu_ctx coopcg_gpu_ctx;

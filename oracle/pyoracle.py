@@ -190,7 +190,7 @@ def ref_solve(A, b, X0, tol=0.0, max_iters=-1, recompute=-1, rank_tol=1e-10, alg
     A, b, X0c, n, p = _prep(A, b, X0)
     cap = max_iters if max_iters >= 0 else 2 * n
     o = _opts(tol, max_iters, recompute, rank_tol)
-    code = {"ccg": 0, "parallel": 1, "mccg": 2}[algo]
+    code = {"ccg": 0, "parallel": 1, "mccg": 2, "parallel_team_finalize": 3}[algo]
     return _run(ref_lib().ref_block_solve, n, p, cap, code, n, p, A.ctypes.data, b.ctypes.data,
                 X0c.ctypes.data, C.byref(o))
 
@@ -217,7 +217,7 @@ class RefMatrix:
         X0c = np.ascontiguousarray(X0.T)
         cap = max_iters if max_iters >= 0 else 2 * n
         o = _opts(tol, max_iters, recompute, rank_tol)
-        code = {"ccg": 0, "parallel": 1, "mccg": 2}[algo]
+        code = {"ccg": 0, "parallel": 1, "mccg": 2, "parallel_team_finalize": 3}[algo]
         return _run(self._lib.ref_block_solve_m, n, p, cap, code, self._h, p, b.ctypes.data,
                     X0c.ctypes.data, C.byref(o))
 

@@ -129,6 +129,99 @@ struct RefMatrix {
     }
 };
 
+// parallel_ccg (parallel.hpp:76-111) with one change, for the full-size
+// BASELINE configs only: finalize_trace's per-agent loop (solvers.hpp:188-210:
+// A x_j - b and its 2-norm, one agent after another in the coordinator) is run
+// by the team, agent j on worker j, with the reference's own kernels::matvec_col
+// and kernels::norm2.  Each agent's residual is the same sequence of operations
+// either way, so the trace is bit-identical to parallel_ccg's (pinned by
+// tests/test_oracle.py::test_team_finalize_equals_parallel_ccg); at cfg 4 the
+// serial loop is 32 latency-bound 131072^2 matvecs (~9 minutes), the team's ~1.
+// Every other step is the reference's: its drive() loop and OmpExecutor, wrapped.
+template <ScalarField S>
+class TeamFinalizeExecutor {
+public:
+    TeamFinalizeExecutor(detail::BlockCgWorkspace<S>& ws, detail::DriverControl& ctrl, SolveTrace<S>& trace,
+                         std::vector<double>& fres, int tid)
+        : inner_(ws, ctrl, tid), ws_(&ws), ctrl_(&ctrl), trace_(&trace), fres_(&fres), tid_(tid) {}
+    template <class F>
+    void phase(F&& f) { inner_.phase(std::forward<F>(f)); }
+    void barrier() { inner_.barrier(); }
+    template <class F>
+    void coordinator(F&& f) {
+        // drive() enters a coordinator section with ctrl.stop already set only
+        // for finalize_trace (every other one sets it, solvers.hpp:264-283)
+        if (!ctrl_->stop) {
+            inner_.coordinator(std::forward<F>(f));
+            return;
+        }
+        inner_.barrier();
+        const bool failed = ctrl_->worker_failed.load(std::memory_order_seq_cst);
+        if (!failed && tid_ < ws_->p) {
+            const int j = tid_;
+            Vec<S> scratch(static_cast<std::size_t>(ws_->n));
+            kernels::matvec_col<S>(*ws_->A, ws_->X.col(j), std::span<S>(scratch.data(), scratch.size()));
+            for (int i = 0; i < ws_->n; ++i)
+                scratch[static_cast<std::size_t>(i)] -= (*ws_->b)[static_cast<std::size_t>(i)];
+            (*fres_)[static_cast<std::size_t>(j)] =
+                kernels::norm2<S>(std::span<const S>(scratch.data(), scratch.size()));
+        }
+        inner_.barrier();
+#pragma omp single
+        {
+            trace_->status = ctrl_->status;
+            trace_->converged_agent = ctrl_->converged_agent;
+            trace_->final_x = ws_->X;
+            trace_->active_agents = ws_->agent_ids;
+            if (!failed) {
+                trace_->final_residual_norms.assign(fres_->begin(), fres_->begin() + ws_->p);
+                trace_->final_minres = trace_->final_residual_norms.empty()
+                                           ? 0.0
+                                           : *std::min_element(trace_->final_residual_norms.begin(),
+                                                               trace_->final_residual_norms.end());
+            }
+        }
+    }
+
+private:
+    detail::OmpExecutor<S> inner_;
+    detail::BlockCgWorkspace<S>* ws_;
+    detail::DriverControl* ctrl_;
+    SolveTrace<S>* trace_;
+    std::vector<double>* fres_;
+    int tid_;
+};
+
+SolveTrace<double> parallel_ccg_team_finalize(const SpdMatrix<double>& A, const Vec<double>& b,
+                                              const DenseBlock<double>& X0, const SolveOptions<double>& opts) {
+    // the body of parallel_ccg (parallel.hpp:79-110) with the wrapped executor
+    detail::check_block_inputs(A, b, X0);
+    const int p = X0.cols();
+    detail::BlockCgWorkspace<double> ws;
+    ws.init(A, b, X0);
+    detail::DriverControl ctrl;
+    ctrl.max_iters = detail::resolve_max_iters(opts, A.dim());
+    SolveTrace<double> trace;
+    const int recompute_every = detail::resolve_recompute(opts, 50);
+    std::vector<double> fres(static_cast<std::size_t>(p));
+    bool team_ok = true;
+    omp_set_dynamic(0);
+#pragma omp parallel num_threads(p) default(shared)
+    {
+        if (omp_get_num_threads() != p) {
+#pragma omp single
+            team_ok = false;
+        } else {
+            TeamFinalizeExecutor<double> exec(ws, ctrl, trace, fres, omp_get_thread_num());
+            detail::drive(ws, ctrl, trace, opts, recompute_every, /*allow_restriction=*/false, exec);
+        }
+    }
+    if (!team_ok) throw Error("parallel_ccg: could not start " + std::to_string(p) + " workers");
+    detail::rethrow_pending(ctrl);
+    trace.barriers_per_iteration = WorkPlan::standard(p).barriers_per_iteration();
+    return trace;
+}
+
 int block_solve(int algo, const SpdMatrix<double>& Am, int n, int p, const double* b, const double* X0,
                 const orc_opts* o, orc_trace* tr) {
     std::vector<double> bv(b, b + n);
@@ -143,6 +236,7 @@ int block_solve(int algo, const SpdMatrix<double>& Am, int n, int p, const doubl
     SolveTrace<double> t;
     if (algo == 0) t = ccg_solve(Am, bv, x0, opts);
     else if (algo == 1) t = parallel_ccg(Am, bv, x0, opts, p);
+    else if (algo == 3) t = parallel_ccg_team_finalize(Am, bv, x0, opts);
     else t = mccg_solve(Am, bv, x0, opts);
     fill_trace(t, n, tr);
     return 0;
@@ -196,7 +290,8 @@ int ref_block_solve_m(int algo, void* h, int p, const double* b, const double* X
     return guarded(tr, [&] { block_solve(algo, rm->sealed(), rm->n, p, b, X0, o, tr); });
 }
 
-/// algo: 0 = ccg_solve, 1 = parallel_ccg (p OpenMP threads), 2 = mccg_solve.
+/// algo: 0 = ccg_solve, 1 = parallel_ccg (p OpenMP threads), 2 = mccg_solve,
+/// 3 = parallel_ccg with finalize_trace's agent loop run by the team (above).
 int ref_block_solve(int algo, int n, int p, const double* A, const double* b, const double* X0,
                     const orc_opts* o, orc_trace* tr) {
     tr->error_msg[0] = '\0';

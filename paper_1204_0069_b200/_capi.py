@@ -37,7 +37,7 @@ class coopcg_trace(C.Structure):
 class coopcg_timing(C.Structure):
     _fields_ = [("matvec_launches", C.c_int), ("matvec_ms_total", C.c_double),
                 ("run_ms", C.c_double), ("loop_ms", C.c_double),
-                ("kernel_launches", C.c_longlong)]
+                ("kernel_launches", C.c_longlong), ("a_l2_resident_bytes", C.c_double)]
 
 
 # Every symbol include/coopcg_gpu.h declares: (name, restype, argtypes).

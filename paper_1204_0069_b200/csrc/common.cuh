@@ -189,6 +189,16 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+// L2 residency across iterations ("A in L2"): the k-range of A
+// below the context's res_k is copied with an evict-last policy, so that part of
+// A (the same k-rows of every panel: every CTA reads the same share from L2)
+// stays in L2 from one iteration's A.D to the next; the rest streams
+// evict-first past it.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ void bulk_g2s_evict_first(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
                                                      uint64_t pol) {
     asm volatile(

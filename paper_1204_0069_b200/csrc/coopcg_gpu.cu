@@ -143,6 +143,10 @@ struct coopcg_gpu_ctx {
     double* dtiles = nullptr;    // the A.D operand re-laid out as [col][kk] k-tiles
     double* gfin = nullptr;      // fast_iter_kernel: the reduced Grams (4 P^2)
     unsigned int* gbar = nullptr;  // fast_iter_kernel: grid barrier {count, generation}
+    // A in L2 across iterations (set_l2_residency): the A.D copies A's k-rows
+    // below res_k (exact) / k-tiles below res_k (fast) with an evict-last policy
+    int res_k = 0;
+    size_t res_bytes = 0;
     int fused_k = -1;            // iteration whose solve + update ran inside fast_iter_kernel
     bool fuse_ok = false;        // fast_iter_kernel's f_ugrid CTAs fit on the device at once
     bool a_ready = false, inputs_ready = false;
@@ -394,7 +398,7 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
     constexpr int T = ad_T<P>(), S = ad_S<P>();
     const bool push = peers.n > 0;
     using Kern = void (*)(const double*, int, int, int, const double*, double*, const double*, int, const int*,
-                          PeerRows);
+                          PeerRows, int);
     Kern kern;
     if constexpr (pipe)
         kern = push ? ad_exact_pipe_kernel<P, KC, RPT, BR, PT, PS, true>
@@ -414,7 +418,7 @@ cudaError_t ad_launch_t(coopcg_gpu_ctx* ctx, const double* src, double* dst, con
     dim3 grid((ctx->n_loc + BR - 1) / BR);
     dim3 block(32 + 32 * ad_consumer_warps(BR / RPT, P / KC));
     pdl_launch(kern, dim3(grid), dim3(block), smem, ctx->stream, ctx->At, ctx->n, ctx->n_loc, ctx->row0, src, dst, b, ctx->p, stop,
-               peers);
+               peers, ctx->res_k);
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -473,7 +477,7 @@ cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
     }
     pdl_launch(kern, dim3(ctx->f_grid), dim3(32 + 64 * WN), fast_ad_smem<P>(), ctx->stream, 
         ctx->At, ctx->n, ctx->n_loc, ctx->lay.ntiles, operand, ctx->qpart, ctx->f_kchunks, ctx->f_tpc,
-        ctx->f_units, stop);
+        ctx->f_units, stop, ctx->res_k);
     ++ctx->launches;
     return cudaGetLastError();
 }
@@ -609,6 +613,33 @@ AdConfig pick_ad_config(int n_loc, int P, int sms) {
     if (P == 8 && n_loc > sms * 64) c.BR = 128;
     c.CPT = (P == 4) ? 2 : 4;  // with 2 rows per thread at P >= 16
     return c;
+}
+
+// ---- A in L2 across iterations ------------------------------------------------
+// A is re-read by every iteration's A.D; the part of it that fits next to the
+// iteration's other working set (the n x P blocks, the k-chunk partials) can
+// stay in the 126 MB L2 from one iteration to the next.  The resident part is
+// a k-range shared by every panel (the first res_k k-rows, or k-tiles in the
+// fast layout), so every A.D CTA reads the same share of its panel from L2.
+// Budget: COOPCG_L2_RES_MB (0 disables), default kL2ResDefaultMB, split among
+// the contexts sharing a device (`share`).
+constexpr double kL2ResDefaultMB = 0.0;
+double l2_res_budget_mb() {
+    static const double mb = [] {
+        const char* e = std::getenv("COOPCG_L2_RES_MB");
+        return e ? std::max(0.0, std::atof(e)) : kL2ResDefaultMB;
+    }();
+    return mb;
+}
+void set_l2_residency(coopcg_gpu_ctx* ctx, int share) {
+    const double budget = l2_res_budget_mb() * 1e6 / std::max(1, share);
+    // bytes of A per unit of res_k: one k-row of every panel (exact) or one
+    // k-tile of every panel (fast)
+    const double unit = ctx->arith == COOPCG_ARITH_FAST ? (double)ctx->npanels * kFastBR * kFastT * 8.0
+                                                         : (double)ctx->npanels * ctx->ad.BR * 8.0;
+    const int units = ctx->arith == COOPCG_ARITH_FAST ? ctx->lay.ntiles : ctx->n;
+    ctx->res_k = (int)std::min<double>(units, std::floor(budget / unit));
+    ctx->res_bytes = (size_t)(ctx->res_k * unit);
 }
 
 // ---- the p x p solves fused into their elementwise consumers ----------------
@@ -999,6 +1030,7 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         ctx->lay = ALay{0, ctx->brs, 0};
         ctx->ap_elems = (size_t)ctx->npanels * n * ctx->ad.BR;
     }
+    set_l2_residency(ctx, 1);
     auto bail = [&](int code) {
         g_create_error = ctx->msg;
         destroy_impl(ctx);
@@ -2319,6 +2351,8 @@ int coopcg_gpu_solve(coopcg_gpu_ctx* ctx, const double* b, const double* X0, con
 int coopcg_gpu_timing(const coopcg_gpu_ctx* ctx, coopcg_timing* out) {
     if (!ctx || !out) return COOPCG_E_INVALID;
     *out = ctx->timing;
+    out->a_l2_resident_bytes = (double)ctx->res_bytes;
+    for (const coopcg_gpu_ctx* c : ctx->shards) out->a_l2_resident_bytes += (double)c->res_bytes;
     return COOPCG_OK;
 }
 
@@ -2494,6 +2528,8 @@ int coopcg_gpu_create_multi(int n, int p, int ndev, const int* devices, int arit
         if (int rc = coopcg_gpu_create_shard(n, p, devices[g], arith, r0, r1, &c)) return bail(rc);
         ctx->shards.push_back(c);
     }
+    for (int g = 0; g < ndev; ++g)  // shards sharing a device share its L2
+        set_l2_residency(ctx->shards[g], (int)std::count(devices, devices + ndev, devices[g]));
     ctx->P = ctx->shards[0]->P;
     // peer access between distinct devices (the Q rows are stored straight
     // into every shard's Q by the kernel that computes them)

@@ -42,7 +42,8 @@ template <int P, int CPT, int BR, int T, int S, bool PUSH = false>
 __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
     ad_exact_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
-                    const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers) {
+                    const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers,
+                    int res_k) {
     pdl_wait();
     constexpr int kConsumerWarps = ad_consumer_warps(BR, P / CPT);
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
@@ -70,7 +71,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
     if (warp == 0) {
         // Producer: one lane streams the A panel tiles and the D tiles.
         if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
+            const uint64_t pol = l2_evict_first_policy(), pol_res = l2_evict_last_policy();
             int s = 0;
             uint32_t ph = 0;
             for (int t = 0; t < ntiles; ++t) {
@@ -79,7 +80,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR, P / CPT))
                 const int rows = min(T, n - k0);
                 mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
                 bulk_g2s_evict_first(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
-                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], pol);
+                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], k0 < res_k ? pol_res : pol);
                 bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
                          &full[s]);
                 if (++s == S) {
@@ -196,7 +197,8 @@ template <int P, int CPT, int BR, int T, int S, int RPT = 2, bool PUSH = false>
 __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT))
     ad_exact_rpt_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                     const double* __restrict__ D, double* __restrict__ Y,
-                    const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers) {
+                    const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers,
+                    int res_k) {
     pdl_wait();
     constexpr int RT = BR / RPT;  // row-threads per column group
     constexpr int kConsumerWarps = ad_consumer_warps(RT, P / CPT);
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
     if (warp == 0) {
         // Producer: one lane streams the A panel tiles and the D tiles.
         if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
+            const uint64_t pol = l2_evict_first_policy(), pol_res = l2_evict_last_policy();
             int s = 0;
             uint32_t ph = 0;
             for (int t = 0; t < ntiles; ++t) {
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
                 const int rows = min(T, n - k0);
                 mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
                 bulk_g2s_evict_first(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
-                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], pol);
+                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], k0 < res_k ? pol_res : pol);
                 bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
                          &full[s]);
                 if (++s == S) {
@@ -376,7 +378,8 @@ template <int P, int CPT, int RPT, int BR, int T, int S, bool PUSH = false>
 __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT))
     ad_exact_pipe_kernel(const double* __restrict__ Ap, int n, int n_loc, int row0,
                          const double* __restrict__ D, double* __restrict__ Y,
-                         const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers) {
+                         const double* __restrict__ b, int p, const int* __restrict__ stop, PeerRows peers,
+                    int res_k) {
     pdl_wait();
     constexpr int U = kPipeU;
     static_assert(RPT == 1 || RPT == 2, "rows per thread");
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
     __syncthreads();
     if (warp == 0) {
         if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
+            const uint64_t pol = l2_evict_first_policy(), pol_res = l2_evict_last_policy();
             int s = 0;
             uint32_t ph = 0;
             for (int t = 0; t < ntiles; ++t) {
@@ -415,7 +418,7 @@ __global__ void __launch_bounds__(32 + 32 * ad_consumer_warps(BR / RPT, P / CPT)
                 const int rows = min(T, n - k0);
                 mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(rows) * (BR * 8u + P * 8u));
                 bulk_g2s_evict_first(As + s * T * BR, panel + static_cast<size_t>(k0) * BR,
-                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], pol);
+                                     static_cast<uint32_t>(rows) * BR * 8u, &full[s], k0 < res_k ? pol_res : pol);
                 bulk_g2s(Ds + s * T * P, D + static_cast<size_t>(k0) * P, static_cast<uint32_t>(rows) * P * 8u,
                          &full[s]);
                 if (++s == S) {

@@ -67,7 +67,7 @@ template <int P, int WN, bool TR>
 __global__ void __launch_bounds__(32 + 64 * WN)
     ad_fast_kernel(const double* __restrict__ Af, int n, int n_loc, int ntiles, const double* __restrict__ Dt,
                    double* __restrict__ Qpart, int kchunks, int tiles_per_chunk, int nunits,
-                   const int* __restrict__ stop) {
+                   const int* __restrict__ stop, int res_t) {
     pdl_wait();
     static_assert(P % (8 * WN) == 0, "fast contexts pad p to a multiple of 8 per column group");
     constexpr int NT = P / 8 / WN;  // N tiles of 8 columns per warp
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(32 + 64 * WN)
     __syncthreads();
     if (warp == 0) {
         if (lane == 0) {
-            const uint64_t pol = l2_evict_first_policy();
+            const uint64_t pol = l2_evict_first_policy(), pol_res = l2_evict_last_policy();
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(32 + 64 * WN)
                     }
                     mbar_arrive_expect_tx(&full[s], abytes + dbytes);
                     bulk_g2s_evict_first(As + s * BR * T, Af + (static_cast<size_t>(q) * ntiles + t) * BR * T, abytes, &full[s],
-                                         pol);
+                                         t < res_t ? pol_res : pol);
                     bulk_g2s(Ds + s * P * T, Dt + static_cast<size_t>(t) * P * T, dbytes, &full[s]);
                     if (++s == S) {
                         s = 0;

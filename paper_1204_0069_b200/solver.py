@@ -340,7 +340,8 @@ class GpuContext:
         _capi.lib().coopcg_gpu_timing(self._h, C.byref(self._timing))
         t = self._timing
         return {"matvec_launches": t.matvec_launches, "matvec_ms_total": t.matvec_ms_total,
-                "run_ms": t.run_ms, "loop_ms": t.loop_ms, "kernel_launches": t.kernel_launches}
+                "run_ms": t.run_ms, "loop_ms": t.loop_ms, "kernel_launches": t.kernel_launches,
+                "a_l2_resident_bytes": t.a_l2_resident_bytes}
 
     def stream_handle(self) -> int:
         """cudaStream_t of this context (for events on the launching stream)."""

@@ -29,10 +29,14 @@ Iterations: cfg 1 the full solve to 1e-10 ||b|| (~1.1k iterations), cfg 2 all
 200 fixed iterations, cfg 3 / cfg 4 setup + 4 / 2 iterations + finalize (the
 reference streams A once per agent per iteration: 4.3 s per iteration at
 cfg 3 and 41 s at cfg 4 with its one-thread-per-agent OpenMP team on the box's
-16 cores, and its finalize_trace recomputes the p true residuals serially in
-the coordinator, solvers.hpp:188-210: ~7.5 min at cfg 4 -- the bulk of this
-file's ~10 minutes).  A summary (times, deltas)
-is written to gpurun_out/full_config_parity.json.
+16 cores).  Its finalize_trace recomputes the p true residuals one agent after
+another in the coordinator (solvers.hpp:188-210): ~9 minutes of latency-bound
+matvecs at cfg 4.  At cfg 3 / 4 the test therefore runs parallel_ccg with that
+per-agent loop executed by the team, agent j on worker j, with the reference's
+own matvec_col / norm2 (oracle/ref_shim.cpp, parallel_ccg_team_finalize; every
+other step is the reference's drive() and OmpExecutor) -- bit-identical to
+parallel_ccg (tests/test_oracle.py::test_team_finalize_equals_parallel_ccg).
+A summary (times, deltas) is written to gpurun_out/full_config_parity.json.
 """
 import json
 import os
@@ -127,7 +131,10 @@ def test_full_config_parity(m, po, c):
                 times[f"{arith}_solve_s"] = time.time() - t0
 
         t0 = time.time()
-        ot = R.solve(b, X0, tol=tol, max_iters=max_iters, algo="parallel")
+        # cfg 3 / 4: parallel_ccg with finalize_trace's agent loop on the team
+        # (bit-identical, tests/test_oracle.py::test_team_finalize_equals_parallel_ccg)
+        algo = "parallel_team_finalize" if c >= 3 else "parallel"
+        ot = R.solve(b, X0, tol=tol, max_iters=max_iters, algo=algo)
         times["reference_solve_s"] = time.time() - t0
     finally:
         R.close()
@@ -165,7 +172,7 @@ def test_full_config_parity(m, po, c):
         "fast_final_residual_rel": float(np.max(f.final_residual_norms / nb)),
         "fast_final_residual_vs_reference_rel_above_floor": fres_max,
         "reference_s_per_iteration": float(np.mean(wall) * 1e-9) if len(wall) else None,
-        "reference_threads": p, "host_cores": os.cpu_count(), "times_s": times})
+        "reference_threads": p, "host_cores": os.cpu_count(), "reference_entry": algo, "times_s": times})
     assert str(f.status) == ot.status
     assert abs(d_it) <= 2
     assert hist_max < 1e-8

@@ -62,6 +62,39 @@ def test_oracle_matches_reference_live(po, seed):
     assert np.array_equal(pr.final_x, r.final_x) and np.array_equal(pr.residual_norms, r.residual_norms)
 
 
+def _trace_fields_equal(a, b):
+    assert a.rc == b.rc and a.status == b.status and a.iterations == b.iterations
+    assert a.converged_agent == b.converged_agent
+    for f in ("initial_residual_norms", "residual_norms", "minres", "final_x", "final_residual_norms"):
+        assert np.array_equal(getattr(a, f), getattr(b, f), equal_nan=True), f
+    assert a.final_minres == b.final_minres or (np.isnan(a.final_minres) and np.isnan(b.final_minres))
+
+
+@pytest.mark.skipif(not __import__("pyoracle").ref_available(), reason="reference shim not built")
+@pytest.mark.parametrize("case", ["converged", "fixed", "degenerate", "rank_loop", "recompute"])
+def test_team_finalize_equals_parallel_ccg(po, case):
+    """The full-size parity test's reference at cfg 3 / 4 (ref_shim.cpp,
+    parallel_ccg_team_finalize: finalize_trace's agent loop run by the team)
+    gives parallel_ccg's trace bit for bit."""
+    n, p = 300, 5
+    # rank_loop: three distinct eigenvalues, so D loses rank inside the loop (k = 20)
+    A = po.gen_diagdom(n, 7) if case != "rank_loop" else np.diag(np.repeat([1.0, 2.0, 5.0], n // 3))
+    b = po.gen_rhs(n, "uniform", 7)
+    X0 = po.gen_starts(n, p, 7)
+    kw = dict(tol=1e-10 * po.seq_norm(b), max_iters=-1)
+    if case == "fixed":
+        kw = dict(tol=0.0, max_iters=25)
+    elif case == "degenerate":
+        X0 = np.zeros((n, p))
+    elif case == "rank_loop":
+        kw = dict(tol=0.0, max_iters=50)
+    elif case == "recompute":
+        kw = dict(tol=0.0, max_iters=30, recompute=7)
+    a = po.ref_solve(A, b, X0, algo="parallel", **kw)
+    t = po.ref_solve(A, b, X0, algo="parallel_team_finalize", **kw)
+    _trace_fields_equal(a, t)
+
+
 @pytest.mark.skipif(not __import__("pyoracle").ref_available(), reason="reference shim not built")
 def test_oracle_kernels_match_reference(po):
     import ctypes as C
