@@ -12,7 +12,9 @@ import os
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+# COOPCG_LIB_PATH: an alternative build of the same library (A/B timing of
+# build-time variants, tools/variants.sh); the default is the in-tree build.
+LIB_PATH = os.environ.get("COOPCG_LIB_PATH") or _build.LIB
 
 
 class coopcg_opts(C.Structure):
