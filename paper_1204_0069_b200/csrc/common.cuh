@@ -122,6 +122,12 @@ __host__ __device__ __forceinline__ void a_decode(const ALay& L, int n, size_t e
 // kernel has completed and its memory is visible.  Every kernel of the
 // iteration loop calls it before reading anything (a no-op otherwise).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the next kernel of the stream be scheduled now (each CTA of this grid
+// triggers; the dependent grid launches once all have).  Called by the
+// fast-mode iteration-tail kernels, right after their own wait, so the next
+// A.D can request its first A tiles (A is read-only during a solve) while the
+// tail runs; the dependent still waits in griddepcontrol.wait for the rest.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
     unsigned long long t;

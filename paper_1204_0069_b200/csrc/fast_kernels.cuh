@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(256)
     operand_tiles_kernel(const double* __restrict__ src, int n, int ntiles, double* __restrict__ dst,
                          const int* __restrict__ stop) {
     pdl_wait();
+    pdl_trigger();  // after the wait: no chain of early launches reaches past this kernel
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     const size_t total = static_cast<size_t>(ntiles) * P * kFastT;
     for (size_t e = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
@@ -68,12 +69,10 @@ __global__ void __launch_bounds__(32 + 64 * WN)
     ad_fast_kernel(const double* __restrict__ Af, int n, int n_loc, int ntiles, const double* __restrict__ Dt,
                    double* __restrict__ Qpart, int kchunks, int tiles_per_chunk, int nunits,
                    const int* __restrict__ stop, int res_t) {
-    pdl_wait();
     static_assert(P % (8 * WN) == 0, "fast contexts pad p to a multiple of 8 per column group");
     constexpr int NT = P / 8 / WN;  // N tiles of 8 columns per warp
     constexpr int NCW = 2 * WN;     // consumer warps
     constexpr int BR = kFastBR, T = kFastT, S = fast_stages<P>();
-    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);  // S x BR x T
     double* Ds = As + S * BR * T;                       // S x P x T
@@ -89,37 +88,73 @@ __global__ void __launch_bounds__(32 + 64 * WN)
     }
     __syncthreads();
     if (warp == 0) {
+        // Producer.  A does not change during a solve, so the first S A tiles
+        // are requested BEFORE griddepcontrol.wait, while the previous kernel
+        // (the iteration's tail, which triggers its dependents at its start)
+        // is still running; the operand tiles (the previous kernel's output)
+        // and everything after them follow the wait.  A stopped solve still
+        // issues the operand copies of the prefetched stages and waits for
+        // them, so no bulk copy is in flight when the CTA exits.
         if (lane == 0) {
             const uint64_t pol = l2_evict_first_policy(), pol_res = l2_evict_last_policy();
             int s = 0;
             uint32_t ph = 0;
             int it = 0;
+            bool waited = false;
+            int pend_t[S];
+            auto d_bytes = [&](int t) {
+                return TR ? P * T * 8u : static_cast<uint32_t>(min(T, n - t * T)) * P * 8u;
+            };
+            // pdl_wait, then the operand copies of the prefetched stages;
+            // false: the solve has stopped (the CTA drains and exits)
+            auto release = [&](int npre) {
+                pdl_wait();
+                waited = true;
+                for (int i = 0; i < npre; ++i)
+                    bulk_g2s(Ds + i * P * T, Dt + static_cast<size_t>(pend_t[i]) * P * T, d_bytes(pend_t[i]), &full[i]);
+                if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) {
+                    for (int i = 0; i < npre; ++i) mbar_wait(&full[i], 0u);
+                    return false;
+                }
+                return true;
+            };
+            // only the in-loop launches (stop != nullptr) prefetch: A is stable
+            // across an iteration; setup / finalize / matvec_block launches may
+            // follow a kernel that wrote A
+            if (stop == nullptr) {
+                pdl_wait();
+                waited = true;
+            }
             for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
                 const int q = u / kchunks, c = u % kchunks;
                 const int t0 = c * tiles_per_chunk, t1 = min(ntiles, t0 + tiles_per_chunk);
                 for (int t = t0; t < t1; ++t, ++it) {
+                    if (it == S && !waited && !release(S)) return;
                     if (it >= S) mbar_wait(&empty[s], ph ^ 1u);
                     const uint32_t abytes = BR * T * 8u;
-                    uint32_t dbytes = P * T * 8u;
+                    const uint32_t dbytes = d_bytes(t);
                     if (!TR) {  // row-major operand: copy the valid rows, zero the tail
                         const int rows = min(T, n - t * T);
                         double* ds = Ds + s * P * T;
                         for (int e = rows * P; e < T * P; ++e) ds[e] = 0.0;
-                        dbytes = static_cast<uint32_t>(rows) * P * 8u;
                     }
                     mbar_arrive_expect_tx(&full[s], abytes + dbytes);
                     bulk_g2s_evict_first(As + s * BR * T, Af + (static_cast<size_t>(q) * ntiles + t) * BR * T, abytes, &full[s],
                                          t < res_t ? pol_res : pol);
-                    bulk_g2s(Ds + s * P * T, Dt + static_cast<size_t>(t) * P * T, dbytes, &full[s]);
+                    if (waited) bulk_g2s(Ds + s * P * T, Dt + static_cast<size_t>(t) * P * T, dbytes, &full[s]);
+                    else pend_t[it] = t;
                     if (++s == S) {
                         s = 0;
                         ph ^= 1u;
                     }
                 }
             }
+            if (!waited) release(it);
         }
         return;
     }
+    pdl_wait();
+    if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     const int cw = warp - 1;
     const int rb = cw / WN;          // row block: rows [32 rb, 32 rb + 32)
     const int cg = cw % WN;          // column group: N tiles [cg*NT, cg*NT + NT)
@@ -472,6 +507,7 @@ __global__ void __launch_bounds__(256)
                        int p, int mode, double* __restrict__ norm_part, double* __restrict__ pair_part,
                        const int* __restrict__ stop) {
     pdl_wait();
+    pdl_trigger();  // after the wait: no chain of early launches reaches past this kernel
     if (*reinterpret_cast<volatile const int*>(stop)) return;
     constexpr int RP = (P >= 32) ? 2 : 4;
     constexpr int TR = (256 / P) * RP;
@@ -662,6 +698,7 @@ __global__ void __launch_bounds__(256, 2)
                      double* __restrict__ gpart, double* __restrict__ gfin, double* __restrict__ norm_part,
                      double* __restrict__ pair_part, unsigned int* __restrict__ gbar) {
     pdl_wait();
+    pdl_trigger();  // after the wait: no chain of early launches reaches past this kernel
     if (*reinterpret_cast<volatile const int*>(&ctl->stop)) return;  // stable: no writer runs concurrently
     extern __shared__ __align__(16) double fsm[];
     constexpr int NOUT = 4 * P * P;

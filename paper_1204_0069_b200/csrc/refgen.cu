@@ -46,8 +46,6 @@ constexpr int kMgsStage = kMgsSR * 32 + 2 * kMgsSR;  // doubles: W rows + u_{t-1
 constexpr size_t mgs_smem(int stages) { return sizeof(double) * stages * kMgsStage; }
 constexpr int kNormSmemMaxN = 24576;  // above this N(t) keeps the squares in global scratch
 
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
-
 // Column-block layout of the Gram-Schmidt working matrix W (n x n, np = n
 // rounded up to 32): block jb holds columns 32 jb .. 32 jb + 31 for all np
 // rows, row-major inside the block, so a P stage (128 rows x 32 columns) is

@@ -43,7 +43,7 @@ def loops(ins):
     by_addr = {x["addr"]: i for i, x in enumerate(ins)}
     out = []
     for i, x in enumerate(ins):
-        m = re.search(r"BRA(?:\.\S+)? (0x[0-9a-f]+)", x["op"])
+        m = re.search(r"BRA\S*\s+(?:!?U?P\d+,\s*)?(0x[0-9a-f]+)", x["op"])
         if m:
             tgt = int(m.group(1), 16)
             if tgt < x["addr"] and tgt in by_addr:
@@ -94,3 +94,25 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def load_use(run):
+    """For every LDS / LDG in a straight run: static cycles until the first
+    instruction that waits on its write barrier (the load-to-use distance
+    ptxas planned; shared loads take ~30 cycles, so shorter distances stall)."""
+    out = []
+    for i, x in enumerate(run):
+        op = re.sub(r"^@!?U?P\d+\s+", "", x["op"])
+        if not (op.startswith("LDS") or op.startswith("LDG")) or x["wb"] == 7:
+            continue
+        cyc = 0
+        for y in run[i + 1:]:
+            cyc += max(1, run[run.index(y) - 1]["stall"]) if False else 0
+        # cycles = sum of stalls from this instruction up to the waiter
+        c = 0
+        for j in range(i, len(run) - 1):
+            c += max(1, run[j]["stall"])
+            if run[j + 1]["wait"] & (1 << x["wb"]):
+                out.append((x["addr"], op[:30], c))
+                break
+    return out
