@@ -137,12 +137,13 @@ struct coopcg_gpu_ctx {
     ALay lay{0, 6, 0};
     // fast mode work decomposition (ad_fast_kernel): units = panels x kchunks
     int f_kchunks = 1, f_tpc = 1, f_units = 0, f_grid = 0, f_rgrid = 0, f_ugrid = 0;
+    int f_rp = 4;  // fast_iter_kernel's rows per thread (fast_iter_rp)
     double* qpart = nullptr;     // kchunks x n_loc x P
     double* gpart = nullptr;     // rgrid x 4 P^2 (row-pass Gram partials)
     double* npart = nullptr;     // ugrid x P (norm partials)
     double* dtiles = nullptr;    // the A.D operand re-laid out as [col][kk] k-tiles
     double* gfin = nullptr;      // fast_iter_kernel: the reduced Grams (4 P^2)
-    unsigned int* gbar = nullptr;  // fast_iter_kernel: grid barrier {count, generation}
+    unsigned long long* gbar = nullptr;  // fast_iter_kernel: grid barrier arrival counter (monotonic)
     // A in L2 across iterations (set_l2_residency): the A.D copies A's k-rows
     // below res_k (exact) / k-tiles below res_k (fast) with an evict-last policy
     int res_k = 0;
@@ -548,10 +549,10 @@ static bool fuse_enabled() {
     static const bool on = std::getenv("COOPCG_NO_FUSE") == nullptr;
     return on;
 }
-template <int P>
+template <int P, int RP>
 cudaError_t fast_iter_t(coopcg_gpu_ctx* ctx, double* Q, const double* D, double* Dn) {
-    auto kern = fast_iter_kernel<P>;
-    const size_t smem = fused_smem_bytes<P>();
+    auto kern = fast_iter_kernel<P, RP>;
+    const size_t smem = fused_smem_bytes<P, RP>();
     static std::once_flag attr_once[kMaxDevices];
     cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once[ctx->device % kMaxDevices], [&] {
@@ -575,30 +576,46 @@ cudaError_t fast_iter_t(coopcg_gpu_ctx* ctx, double* Q, const double* D, double*
                               ctx->small, ctx->ctl, ctx->p, ctx->gpart, ctx->gfin, ctx->npart, ctx->partials,
                               ctx->gbar);
 }
-template <int P>
+template <int P, int RP>
 bool fast_iter_fits_t(const coopcg_gpu_ctx* ctx) {
     int occ = 0;
-    if (cudaFuncSetAttribute(fast_iter_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)fused_smem_bytes<P>()) != cudaSuccess ||
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fast_iter_kernel<P>, 256, fused_smem_bytes<P>()) !=
+    if (cudaFuncSetAttribute(fast_iter_kernel<P, RP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)fused_smem_bytes<P, RP>()) != cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fast_iter_kernel<P, RP>, 256, fused_smem_bytes<P, RP>()) !=
             cudaSuccess) {
         cudaGetLastError();
         return false;
     }
     return occ * ctx->sms >= ctx->f_ugrid && ctx->f_ugrid == ctx->f_rgrid;
 }
+template <int P>
+bool fast_iter_fits_p(const coopcg_gpu_ctx* ctx) {
+    switch (ctx->f_rp) {
+    case 1: return fast_iter_fits_t<P, 1>(ctx);
+    case 2: return fast_iter_fits_t<P, 2>(ctx);
+    default: return fast_iter_fits_t<P, 4>(ctx);
+    }
+}
 bool fast_iter_fits(const coopcg_gpu_ctx* ctx) {
     switch (ctx->P) {
-    case 8: return fast_iter_fits_t<8>(ctx);
-    case 16: return fast_iter_fits_t<16>(ctx);
-    default: return fast_iter_fits_t<32>(ctx);
+    case 8: return fast_iter_fits_p<8>(ctx);
+    case 16: return fast_iter_fits_p<16>(ctx);
+    default: return fast_iter_fits_p<32>(ctx);
+    }
+}
+template <int P>
+cudaError_t fast_iter_p(coopcg_gpu_ctx* ctx, double* Q, const double* D, double* Dn) {
+    switch (ctx->f_rp) {
+    case 1: return fast_iter_t<P, 1>(ctx, Q, D, Dn);
+    case 2: return fast_iter_t<P, 2>(ctx, Q, D, Dn);
+    default: return fast_iter_t<P, 4>(ctx, Q, D, Dn);
     }
 }
 cudaError_t fast_iter(coopcg_gpu_ctx* ctx, double* Q, const double* D, double* Dn) {
     switch (ctx->P) {
-    case 8: return fast_iter_t<8>(ctx, Q, D, Dn);
-    case 16: return fast_iter_t<16>(ctx, Q, D, Dn);
-    default: return fast_iter_t<32>(ctx, Q, D, Dn);
+    case 8: return fast_iter_p<8>(ctx, Q, D, Dn);
+    case 16: return fast_iter_p<16>(ctx, Q, D, Dn);
+    default: return fast_iter_p<32>(ctx, Q, D, Dn);
     }
 }
 
@@ -798,6 +815,22 @@ size_t rank_smem(int P) { return 2ull * kRankTile * P * sizeof(double) + 2 * siz
 
 int destroy_impl(coopcg_gpu_ctx* ctx) {
     if (!ctx) return COOPCG_OK;
+#ifdef COOPCG_PHASE_TIMES
+    {
+        unsigned long long h[8] = {0};
+        cudaSetDevice(ctx->device);
+        cudaDeviceSynchronize();
+        cudaMemcpyFromSymbol(h, g_phase_ns, sizeof h);
+        if (h[7])
+            std::fprintf(stderr,
+                         "fast_iter phases (CTA 0, mean over %llu): A %.2f  bar1 %.2f  B %.2f  bar2 %.2f  C-load %.2f  "
+                         "C-solve %.2f  D %.2f us\n",
+                         h[7], h[0] * 1e-3 / h[7], h[1] * 1e-3 / h[7], h[2] * 1e-3 / h[7], h[3] * 1e-3 / h[7],
+                         h[4] * 1e-3 / h[7], h[5] * 1e-3 / h[7], h[6] * 1e-3 / h[7]);
+        const unsigned long long z[8] = {0};
+        cudaMemcpyToSymbol(g_phase_ns, z, sizeof z);
+    }
+#endif
     for (size_t g = 0; g < ctx->gev.size(); ++g) {
         cudaSetDevice(ctx->shards[g]->device);
         if (ctx->gev[g]) cudaEventDestroy(ctx->gev[g]);
@@ -1024,6 +1057,26 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
                                   : ((ctx->P <= 8) ? 128 : (ctx->P == 16 ? 192 : 296));
         ctx->f_rgrid = std::min(rg, (ctx->n_loc + TR - 1) / TR);
         ctx->f_ugrid = std::min(rg, (n + TR - 1) / TR);
+        if (ctx->n_loc == n) {
+            // single GPU (the fused iteration kernel): the smallest rows-per-thread
+            // whose tiles fit two co-resident CTAs per SM, one tile per CTA when
+            // they do (COOPCG_FAST_RP forces 1 / 2 / 4)
+            static const int rp_env = [] {
+                const char* e = std::getenv("COOPCG_FAST_RP");
+                return e ? std::atoi(e) : 0;
+            }();
+            const int slots = std::min(2 * ctx->sms, kMaxParts);
+            int rp = 4;
+            for (int c : {1, 2, 4})
+                if ((n + (256 / ctx->P) * c - 1) / ((256 / ctx->P) * c) <= slots) {
+                    rp = c;
+                    break;
+                }
+            if (rp_env == 1 || rp_env == 2 || rp_env == 4) rp = rp_env;
+            ctx->f_rp = rp;
+            const int tiles = (n + (256 / ctx->P) * rp - 1) / ((256 / ctx->P) * rp);
+            ctx->f_rgrid = ctx->f_ugrid = std::min(tiles, slots);
+        }
     } else {
         ctx->brs = (ctx->ad.BR == 32) ? 5 : (ctx->ad.BR == 64 ? 6 : 7);
         ctx->npanels = (ctx->n_loc + ctx->ad.BR - 1) / ctx->ad.BR;
@@ -1065,8 +1118,8 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         CKC(gmalloc(ctx, &ctx->npart, sizeof(double) * (size_t)ctx->f_ugrid * ctx->P, "npart"));
         CKC(gmalloc(ctx, &ctx->dtiles, sizeof(double) * (size_t)ctx->lay.ntiles * ctx->P * kFastT, "dtiles"));
         CKC(gmalloc(ctx, &ctx->gfin, sizeof(double) * 4 * ctx->P * ctx->P, "gfin"));
-        CKC(gmalloc(ctx, &ctx->gbar, 2 * sizeof(unsigned int), "gbar"));
-        CKC(cudaMemsetAsync(ctx->gbar, 0, 2 * sizeof(unsigned int), ctx->stream));
+        CKC(gmalloc(ctx, &ctx->gbar, sizeof(unsigned long long), "gbar"));
+        CKC(cudaMemsetAsync(ctx->gbar, 0, sizeof(unsigned long long), ctx->stream));
         ctx->fuse_ok = ctx->n_loc == n && fast_iter_fits(ctx);
     }
     const SmallLayout L{ctx->P};

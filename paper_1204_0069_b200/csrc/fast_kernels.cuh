@@ -659,47 +659,69 @@ __global__ void __launch_bounds__(256)
 // Three launches and their drain/fill gaps become one.  The per-element
 // arithmetic is that of the separate kernels; only the Gram reduction adds
 // the CTA partials in a different (still fixed, deterministic) order.
-__device__ __forceinline__ void grid_barrier(unsigned int* bar, unsigned int nblocks) {
+// COOPCG_PHASE_TIMES (measurement builds only, tools/variants.sh): CTA 0's
+// thread 0 accumulates the globaltimer time of each phase of fast_iter_kernel
+// into g_phase_ns[0..6] (entry->A end, barrier 1, B, barrier 2, C loads,
+// C solve + sync, D), g_phase_ns[7] = launches; printed at context destroy.
+#ifdef COOPCG_PHASE_TIMES
+__device__ unsigned long long g_phase_ns[8];
+#define PHASE_MARK(i)                                                                  \
+    do {                                                                               \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                     \
+            const unsigned long long now_ = globaltimer_ns();                          \
+            if ((i) > 0) atomicAdd(&g_phase_ns[(i) - 1], now_ - t_prev_);              \
+            t_prev_ = now_;                                                            \
+        }                                                                              \
+    } while (0)
+#else
+#define PHASE_MARK(i) \
+    do {              \
+    } while (0)
+#endif
+// Grid barrier on a monotonic 64-bit arrival counter (never reset): CTA
+// arrival j of a barrier round returns old = r * G + j, so the round ends
+// when the counter reaches (r + 1) * G.  One release atomic per CTA, then
+// acquire polls; no reset atomics on the last arriver's critical path.
+__device__ __forceinline__ void grid_barrier(unsigned long long* bar, unsigned int nblocks) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned int* vgen = bar + 1;
-        const unsigned int gen = *vgen;
-        __threadfence();
-        if (atomicAdd(bar, 1u) == nblocks - 1) {
-            atomicExch(bar, 0u);
-            __threadfence();
-            atomicAdd(bar + 1, 1u);
-        } else {
-            while (*vgen == gen) __nanosleep(32);
-        }
-        __threadfence();
+        unsigned long long old;
+        asm volatile("atom.add.release.gpu.u64 %0, [%1], 1;" : "=l"(old) : "l"(bar) : "memory");
+        const unsigned long long target = (old / nblocks + 1) * nblocks;
+        unsigned long long cur;
+        do {
+            asm volatile("ld.acquire.gpu.u64 %0, [%1];" : "=l"(cur) : "l"(bar) : "memory");
+        } while (cur < target);
     }
     __syncthreads();
 }
 
-template <int P>
-__host__ __device__ constexpr int fused_rows_tr() { return (256 / P) * 4; }
-template <int P>
-__host__ __device__ constexpr int fused_upd_tr() { return (256 / P) * ((P >= 32) ? 2 : 4); }
-template <int P>
+template <int P, int RP>
+__host__ __device__ constexpr int fused_rows_tr() { return (256 / P) * RP; }
+template <int P, int RP>
+__host__ __device__ constexpr int fused_upd_tr() { return (256 / P) * RP; }
+template <int P, int RP>
 __host__ __device__ constexpr size_t fused_smem_bytes() {
     // phase A's three tiles (kept for phase D when the tilings agree), then phase
     // C/D: grams (4 P^2) + alpha, beta + 4 update tiles + reductions + the factor
-    constexpr size_t a = 3ull * fused_rows_tr<P>() * P;
-    constexpr size_t d = 4ull * P * P + 2ull * P * (P + 1) + 4ull * fused_upd_tr<P>() * P + 256 + P * (P + 1);
+    constexpr size_t a = 3ull * fused_rows_tr<P, RP>() * P;
+    constexpr size_t d = 4ull * P * P + 2ull * P * (P + 1) + 4ull * fused_upd_tr<P, RP>() * P + 256 + P * (P + 1);
     return (a + d) * sizeof(double);
 }
 
-template <int P>
+template <int P, int RP>
 __global__ void __launch_bounds__(256, 2)
     fast_iter_kernel(const double* __restrict__ Qpart, int kchunks, int n, double* __restrict__ Q,
                      double* __restrict__ X, double* __restrict__ R, const double* __restrict__ D,
                      double* __restrict__ Dn, double* __restrict__ small, Ctl* ctl, int p,
                      double* __restrict__ gpart, double* __restrict__ gfin, double* __restrict__ norm_part,
-                     double* __restrict__ pair_part, unsigned int* __restrict__ gbar) {
+                     double* __restrict__ pair_part, unsigned long long* __restrict__ gbar) {
     pdl_wait();
     pdl_trigger();  // after the wait: no chain of early launches reaches past this kernel
     if (*reinterpret_cast<volatile const int*>(&ctl->stop)) return;  // stable: no writer runs concurrently
+    unsigned long long t_prev_ = 0;
+    (void)t_prev_;
+    PHASE_MARK(0);
     extern __shared__ __align__(16) double fsm[];
     constexpr int NOUT = 4 * P * P;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -709,13 +731,14 @@ __global__ void __launch_bounds__(256, 2)
     // When the row pass and the update pass tile the rows alike and every CTA
     // owns at most one tile, the update reuses the row pass's D, Q, R tiles
     // (still in shared memory) and X is fetched during the row pass.
-    constexpr int TRA = fused_rows_tr<P>();
-    constexpr bool SAME_TILING = TRA == fused_upd_tr<P>();
+    constexpr int TRA = fused_rows_tr<P, RP>();
+    constexpr bool SAME_TILING = TRA == fused_upd_tr<P, RP>();
     const bool reuse = SAME_TILING && (n + TRA - 1) / TRA <= static_cast<int>(gridDim.x);
-    double xpre[4] = {0.0, 0.0, 0.0, 0.0};
+    double xpre[RP];
+#pragma unroll
+    for (int u = 0; u < RP; ++u) xpre[u] = 0.0;
     // ---- A: row pass (kernel (2), mode 0) ----------------------------------
     {
-        constexpr int RP = 4;
         constexpr int TR = TRA;
         constexpr int PER = (NOUT + 255) / 256;
         double(*tq)[P] = reinterpret_cast<double(*)[P]>(fsm);
@@ -809,32 +832,51 @@ __global__ void __launch_bounds__(256, 2)
             if (o < NOUT) gpart[static_cast<size_t>(blockIdx.x) * NOUT + o] = acc[q];
         }
     }
+    PHASE_MARK(1);
     grid_barrier(gbar, G);
+    PHASE_MARK(2);
 
     // ---- B: Gram reduction, one warp per entry (fixed order) ---------------
     for (int o = blockIdx.x * 8 + warp; o < NOUT; o += G * 8) {
+        // lane l sums partials l, l+32, ... (G <= 296: at most 10), loads first
+        double v[10];
+#pragma unroll
+        for (int q = 0; q < 10; ++q) {
+            const unsigned int c = lane + 32u * q;
+            v[q] = (c < G) ? __ldcg(gpart + static_cast<size_t>(c) * NOUT + o) : 0.0;
+        }
         double s = 0.0;
-        for (unsigned int c = lane; c < G; c += 32) s += __ldcg(gpart + static_cast<size_t>(c) * NOUT + o);
+#pragma unroll
+        for (int q = 0; q < 10; ++q) s += v[q];
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
         if (lane == 0) gfin[o] = s;
     }
+    PHASE_MARK(3);
     grid_barrier(gbar, G);
+    PHASE_MARK(4);
 
     // ---- C: step solves (kernel (3), mode 0), redundantly in every CTA ------
     double* flat = fsm + 3 * TRA * P;            // 4 P^2 (after phase A's tiles)
     double(*al)[P + 1] = reinterpret_cast<double(*)[P + 1]>(flat + NOUT);
     double(*be)[P + 1] = reinterpret_cast<double(*)[P + 1]>(flat + NOUT + P * (P + 1));
     double* tiles = flat + NOUT + 2 * P * (P + 1);
-    constexpr int TRU = fused_upd_tr<P>();
+    constexpr int TRU = fused_upd_tr<P, RP>();
     double* nred = tiles + 4 * TRU * P;          // 256
     double(*lsm)[P + 1] = reinterpret_cast<double(*)[P + 1]>(nred + 256);
     __shared__ int abort_flag;
     for (int o = tid; o < NOUT; o += 256) flat[o] = __ldcg(gfin + o);
     if (tid == 0) abort_flag = 0;
     __syncthreads();
+    PHASE_MARK(5);
     auto Gm = [&](int gsel, int a, int c) { return flat[(gsel * P + a) * P + c]; };
-    if (warp == 0) {
+    // The solve runs on one warp; the two CTAs an SM hosts (blocks b and
+    // b + #SMs under the usual placement) use warps 0 and 1, i.e. different
+    // SMSPs, so their serial FP64 chains do not share an issue port.
+    unsigned int nsm;
+    asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+    const int solver = static_cast<int>((blockIdx.x / nsm) & 1u);
+    if (warp == solver) {
         const bool pub = blockIdx.x == 0;
         const double nsq = (lane < P) ? small[L.nsq_d() + lane] : 0.0;
         double l[P];
@@ -928,11 +970,11 @@ __global__ void __launch_bounds__(256, 2)
         }
     }
     __syncthreads();
+    PHASE_MARK(6);
     if (abort_flag) return;
 
     // ---- D: update pass (kernel (4), mode 0) -------------------------------
     {
-        constexpr int RP = (P >= 32) ? 2 : 4;
         constexpr int TR = TRU;
         double(*tr_)[P] = reinterpret_cast<double(*)[P]>(tiles);
         double(*tdn)[P] = reinterpret_cast<double(*)[P]>(tiles + TR * P);
@@ -1038,6 +1080,10 @@ __global__ void __launch_bounds__(256, 2)
             for (int r = 0; r < 256 / P; ++r) sn += nred[r * P + tid];
             norm_part[static_cast<size_t>(blockIdx.x) * P + tid] = sn;
         }
+#ifdef COOPCG_PHASE_TIMES
+        PHASE_MARK(7);
+        if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g_phase_ns[7], 1ull);
+#endif
         if (GR == 1) {
 #pragma unroll
             for (int q = 0; q < 3; ++q)
