@@ -68,11 +68,15 @@ def test_fast_fused_iteration_matches_separate_kernels():
         assert r.returncode == 0, r.stderr[-2000:]
         return json.loads(r.stdout.strip().splitlines()[-1])
     import numpy as np
-    fused, sep = run({}), run({"COOPCG_NO_FUSE": "1"})
-    for key in fused:
-        assert fused[key]["it"] == sep[key]["it"] == 30
-        a, b = np.array(fused[key]["x"]), np.array(sep[key]["x"])
-        assert np.max(np.linalg.norm(a - b, axis=0) / np.linalg.norm(b, axis=0)) < 1e-12, key
+    sep = run({"COOPCG_NO_FUSE": "1"})
+    # the default tiling and every rows-per-thread tile shape (COOPCG_FAST_RP;
+    # 4 gives fewer tiles than CTAs at these sizes, 1 the one-tile-per-CTA path)
+    for extra in ({}, {"COOPCG_FAST_RP": "1"}, {"COOPCG_FAST_RP": "2"}, {"COOPCG_FAST_RP": "4"}):
+        fused = run(extra)
+        for key in fused:
+            assert fused[key]["it"] == sep[key]["it"] == 30
+            a, b = np.array(fused[key]["x"]), np.array(sep[key]["x"])
+            assert np.max(np.linalg.norm(a - b, axis=0) / np.linalg.norm(b, axis=0)) < 1e-12, (key, extra)
 
 
 GUARD_SCRIPT = r"""
