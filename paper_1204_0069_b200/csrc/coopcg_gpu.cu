@@ -522,7 +522,8 @@ cudaError_t fast_update(coopcg_gpu_ctx* ctx, const double* Q, const double* D, d
 }
 template <int P>
 cudaError_t fast_solve_t(coopcg_gpu_ctx* ctx, int mode) {
-    const size_t smem = (size_t)(4 * P * P + 1024) * sizeof(double);
+    // flat Grams + the reduction scratch (+ solve_cta's five P x (P+1) buffers at P >= 16)
+    const size_t smem = (size_t)(4 * P * P + 1024 + (P >= 16 ? 5 * P * (P + 1) : 0)) * sizeof(double);
     static std::once_flag attr_once[kMaxDevices];
     cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once[ctx->device % kMaxDevices], [&] {
@@ -817,7 +818,7 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     if (!ctx) return COOPCG_OK;
 #ifdef COOPCG_PHASE_TIMES
     {
-        unsigned long long h[8] = {0};
+        unsigned long long h[16] = {0};
         cudaSetDevice(ctx->device);
         cudaDeviceSynchronize();
         cudaMemcpyFromSymbol(h, g_phase_ns, sizeof h);
@@ -827,7 +828,9 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
                          "C-solve %.2f  D %.2f us\n",
                          h[7], h[0] * 1e-3 / h[7], h[1] * 1e-3 / h[7], h[2] * 1e-3 / h[7], h[3] * 1e-3 / h[7],
                          h[4] * 1e-3 / h[7], h[5] * 1e-3 / h[7], h[6] * 1e-3 / h[7]);
-        const unsigned long long z[8] = {0};
+        std::fprintf(stderr, "  C-solve: setup %.2f  cholesky %.2f  alpha %.2f  beta %.2f us\n", h[8] * 1e-3 / h[7],
+                     h[9] * 1e-3 / h[7], h[10] * 1e-3 / h[7], h[11] * 1e-3 / h[7]);
+        const unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(g_phase_ns, z, sizeof z);
     }
 #endif
@@ -1072,6 +1075,9 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
                     rp = c;
                     break;
                 }
+            // no tiling gives one tile per CTA: P = 32 takes the smallest tiles (the
+            // only shape whose shared memory fits two CTAs per SM), P <= 16 the largest
+            if ((n + (256 / ctx->P) * rp - 1) / ((256 / ctx->P) * rp) > slots && ctx->P >= 32) rp = 1;
             if (rp_env == 1 || rp_env == 2 || rp_env == 4) rp = rp_env;
             ctx->f_rp = rp;
             const int tiles = (n + (256 / ctx->P) * rp - 1) / ((256 / ctx->P) * rp);

@@ -335,6 +335,130 @@ __global__ void __launch_bounds__(256)
 // mode 2: beta only from G0 = R_new^T Q of a residual pass (uses ctl->lu).
 // L L^T x = rhs for lane-owned right-hand sides, L in shared memory with
 // 1 / L_ii stored on its diagonal (no division on the solve's critical path).
+// The step solves on a whole CTA in shared memory (P >= 16, where one warp
+// holding P-wide register rows spills and serialises: 27 us at P = 16 in the
+// fused kernel, 394 us at P = 32 in fast_solve_kernel, round 2).
+//   M = sym(G0) (identity on the padded rows), SPD guard, right-looking
+//   Cholesky by warp 0 (lane = row; the factor keeps 1 / L_kk on its
+//   diagonal, the format of ctl->lu), W = L^-1 column by column, Minv = W^T W,
+//   then alpha_i = Minv (-G1_i), rhs_beta = -(G2 + alpha G3), beta_i = Minv rhs_i
+//   as CTA-wide products.  mode 0: alpha + beta; 1: alpha; 2: beta from the
+//   stored factor `lf` (filled by the caller) with rhs -G0.
+// Returns 0, 1 (pivot vanished: rank collapse) or 2 (SPD guard); every
+// thread of the CTA must call it.  Shared buffers: lf, W, Mi, al, be (P x P+1).
+template <int P>
+__device__ int solve_cta(const double* G, int p, int mode, const double* __restrict__ nsq,
+                         double (*lf)[P + 1], double (*W)[P + 1], double (*Mi)[P + 1], double (*al)[P + 1],
+                         double (*be)[P + 1], double* red) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ int flag;
+    auto g = [&](int gsel, int a, int c) { return G[(gsel * P + a) * P + c]; };
+    if (mode != 2) {
+        double mx = 0.0;
+        for (int e = tid; e < P * P; e += nt) {
+            const int i = e / P, j = e % P;
+            double v = (i == j) ? 1.0 : 0.0;
+            if (i < p && j < p) {
+                v = 0.5 * (g(0, i, j) + g(0, j, i));
+                mx = fmax(mx, fabs(v));
+            }
+            lf[i][j] = v;
+        }
+        for (int off = 16; off > 0; off >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, off));
+        if (lane == 0) red[warp] = mx;
+        if (tid == 0) flag = 0;
+        __syncthreads();
+        if (tid < p && !(lf[tid][tid] > 0.0) && nsq[tid] > 0.0) atomicOr(&flag, 2);  // block_cg.hpp:196-202
+        if (warp == 0) {
+            double m2 = (lane < nt / 32) ? red[lane] : 0.0;
+            for (int off = 16; off > 0; off >>= 1) m2 = fmax(m2, __shfl_xor_sync(0xffffffffu, m2, off));
+            const double floor = m2 * 1e-14;  // the reference's pivot floor (block_cg.hpp:180-190)
+            __syncwarp();
+            if (flag == 0) {
+                for (int k = 0; k < p; ++k) {
+                    const double d = lf[k][k];
+                    if (!(d > floor)) {
+                        if (lane == 0) flag = 1;
+                        break;
+                    }
+                    const double inv = rsqrt(d);
+                    if (lane > k && lane < p) lf[lane][k] *= inv;
+                    __syncwarp();
+                    if (lane > k && lane < p) {
+                        const double lik = lf[lane][k];
+                        for (int j = k + 1; j <= lane; ++j) lf[lane][j] = fma(-lik, lf[j][k], lf[lane][j]);
+                    }
+                    if (lane == k) lf[k][k] = inv;
+                    __syncwarp();
+                }
+            }
+        }
+        __syncthreads();
+        if (flag) return flag;
+    }
+    // W = L^-1 (lower), one column per thread of warp 0
+    if (warp == 0) {
+        const int j = lane;
+        for (int i = 0; i < P; ++i) {
+            double w = 0.0;
+            if (j < p && i < p && i >= j) {
+                double s = (i == j) ? 1.0 : 0.0;
+                for (int m = j; m < i; ++m) s = fma(-lf[i][m], W[m][j], s);
+                w = s * lf[i][i];
+            }
+            if (j < P) W[i][j] = w;
+            __syncwarp();
+        }
+    }
+    __syncthreads();
+    // Minv = W^T W
+    for (int e = tid; e < P * P; e += nt) {
+        const int a = e / P, b = e % P;
+        double s = 0.0;
+        if (a < p && b < p)
+            for (int m = (a > b ? a : b); m < p; ++m) s = fma(W[m][a], W[m][b], s);
+        Mi[a][b] = s;
+    }
+    __syncthreads();
+    if (mode != 2) {
+        // alpha_i = Minv (-G1_i)   (block_cg.hpp:203-217)
+        for (int e = tid; e < P * P; e += nt) {
+            const int i = e / P, j = e % P;
+            double s = 0.0;
+            if (i < p && j < p)
+                for (int m = 0; m < p; ++m) s = fma(Mi[j][m], -g(1, i, m), s);
+            al[i][j] = s;
+        }
+        __syncthreads();
+    }
+    if (mode == 1) return 0;
+    // rhs_beta (W reused): -(G2 + alpha G3), or -G0 from a residual pass (mode 2)
+    for (int e = tid; e < P * P; e += nt) {
+        const int i = e / P, j = e % P;
+        double s = 0.0;
+        if (i < p && j < p) {
+            if (mode == 2) {
+                s = -g(0, i, j);
+            } else {
+                s = g(2, i, j);
+                for (int m = 0; m < p; ++m) s = fma(al[i][m], g(3, m, j), s);
+                s = -s;
+            }
+        }
+        W[i][j] = s;
+    }
+    __syncthreads();
+    for (int e = tid; e < P * P; e += nt) {
+        const int i = e / P, j = e % P;
+        double s = 0.0;
+        if (i < p && j < p)
+            for (int m = 0; m < p; ++m) s = fma(Mi[j][m], W[i][m], s);
+        be[i][j] = s;
+    }
+    __syncthreads();
+    return 0;
+}
+
 template <int P>
 __device__ __forceinline__ void chol_solve_regs(const double (*l)[P + 1], int p, const double (&rhs)[P],
                                                 double (&x)[P]) {
@@ -388,6 +512,40 @@ __global__ void __launch_bounds__(1024)
     }
     cta_reduce_fixed(partials, nparts, 4 * P * P, 0, 1, nout, flat, red);
     __syncthreads();
+    if constexpr (P >= 16) {
+        // the whole CTA solves in shared memory (solve_cta); buffers after red[]
+        double(*lf)[P + 1] = reinterpret_cast<double(*)[P + 1]>(red + blockDim.x);
+        double(*Wb)[P + 1] = lf + P;
+        double(*Mib)[P + 1] = lf + 2 * P;
+        double(*al)[P + 1] = lf + 3 * P;
+        double(*be)[P + 1] = lf + 4 * P;
+        if (mode == 2) {
+            for (int e = tid; e < P * P; e += blockDim.x) lf[e / P][e % P] = ctl->lu[e];
+            __syncthreads();
+        }
+        const int rc = solve_cta<P>(flat, p, mode, small + L.nsq_d(), lf, Wb, Mib, al, be, red);
+        if (rc) {
+            if (tid == 0) {
+                if (rc == 2) {
+                    ctl->err = 2;
+                    ctl->err_iter = ctl->k;
+                } else {
+                    ctl->status = 1;  // rank collapse (pivot vanished)
+                }
+                ctl->stop = 1;
+            }
+            return;
+        }
+        for (int e = tid; e < P * P; e += blockDim.x) {
+            const int i = e / P, j = e % P;
+            if (mode != 2) {
+                ctl->lu[e] = lf[i][j];
+                small[L.alpha() + e] = al[i][j];
+            }
+            if (mode != 1) small[L.beta() + e] = be[i][j];
+        }
+        return;
+    }
     // G[gsel][a][c] = flat[(gsel * P + a) * P + c]
     auto G = [&](int gsel, int a, int c) { return flat[(gsel * P + a) * P + c]; };
     if (tid >= 32) return;
@@ -664,16 +822,27 @@ __global__ void __launch_bounds__(256)
 // into g_phase_ns[0..6] (entry->A end, barrier 1, B, barrier 2, C loads,
 // C solve + sync, D), g_phase_ns[7] = launches; printed at context destroy.
 #ifdef COOPCG_PHASE_TIMES
-__device__ unsigned long long g_phase_ns[8];
+__device__ unsigned long long g_phase_ns[16];
 #define PHASE_MARK(i)                                                                  \
     do {                                                                               \
         if (blockIdx.x == 0 && threadIdx.x == 0) {                                     \
             const unsigned long long now_ = globaltimer_ns();                          \
-            if ((i) > 0) atomicAdd(&g_phase_ns[(i) - 1], now_ - t_prev_);              \
+            if ((i) > 0) atomicAdd(&g_phase_ns[(i) > 7 ? (i) : (i) - 1], now_ - t_prev_);\
             t_prev_ = now_;                                                            \
         }                                                                              \
     } while (0)
+#define PHASE_SUB(i)                                                                   \
+    do {                                                                               \
+        if (blockIdx.x == 0 && threadIdx.x == 0) {                                     \
+            const unsigned long long now_ = globaltimer_ns();                          \
+            atomicAdd(&g_phase_ns[i], now_ - t_sub_);                                  \
+            t_sub_ = now_;                                                             \
+        }                                                                              \
+    } while (0)
 #else
+#define PHASE_SUB(i) \
+    do {             \
+    } while (0)
 #define PHASE_MARK(i) \
     do {              \
     } while (0)
@@ -706,7 +875,8 @@ __host__ __device__ constexpr size_t fused_smem_bytes() {
     // C/D: grams (4 P^2) + alpha, beta + 4 update tiles + reductions + the factor
     constexpr size_t a = 3ull * fused_rows_tr<P, RP>() * P;
     constexpr size_t d = 4ull * P * P + 2ull * P * (P + 1) + 4ull * fused_upd_tr<P, RP>() * P + 256 + P * (P + 1);
-    return (a + d) * sizeof(double);
+    constexpr size_t e = P >= 16 ? 2ull * P * (P + 1) : 0;  // solve_cta's W and Minv
+    return (a + d + e) * sizeof(double);
 }
 
 template <int P, int RP>
@@ -719,8 +889,9 @@ __global__ void __launch_bounds__(256, 2)
     pdl_wait();
     pdl_trigger();  // after the wait: no chain of early launches reaches past this kernel
     if (*reinterpret_cast<volatile const int*>(&ctl->stop)) return;  // stable: no writer runs concurrently
-    unsigned long long t_prev_ = 0;
+    unsigned long long t_prev_ = 0, t_sub_ = 0;
     (void)t_prev_;
+    (void)t_sub_;
     PHASE_MARK(0);
     extern __shared__ __align__(16) double fsm[];
     constexpr int NOUT = 4 * P * P;
@@ -869,101 +1040,133 @@ __global__ void __launch_bounds__(256, 2)
     if (tid == 0) abort_flag = 0;
     __syncthreads();
     PHASE_MARK(5);
+#ifdef COOPCG_PHASE_TIMES
+    if (blockIdx.x == 0 && threadIdx.x == 0) t_sub_ = t_prev_;
+#endif
     auto Gm = [&](int gsel, int a, int c) { return flat[(gsel * P + a) * P + c]; };
-    // The solve runs on one warp; the two CTAs an SM hosts (blocks b and
-    // b + #SMs under the usual placement) use warps 0 and 1, i.e. different
-    // SMSPs, so their serial FP64 chains do not share an issue port.
-    unsigned int nsm;
-    asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
-    const int solver = static_cast<int>((blockIdx.x / nsm) & 1u);
-    if (warp == solver) {
-        const bool pub = blockIdx.x == 0;
-        const double nsq = (lane < P) ? small[L.nsq_d() + lane] : 0.0;
-        double l[P];
-        double maxabs = 0.0, diag = 0.0;
-#pragma unroll
-        for (int jj = 0; jj < P; ++jj) {
-            l[jj] = 0.0;
-            if (lane < p && jj < p) {
-                l[jj] = 0.5 * (Gm(0, lane, jj) + Gm(0, jj, lane));
-                maxabs = fmax(maxabs, fabs(l[jj]));
-                if (jj == lane) diag = l[jj];
-            }
-        }
-        for (int off = 16; off > 0; off >>= 1) maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, off));
-        const double floor = maxabs * 1e-14;
-        const bool bad = (lane < p) && !(diag > 0.0) && (nsq > 0.0);
-        bool fail = false;
-        if (__any_sync(0xffffffffu, bad)) {
-            if (pub && lane == 0) {
-                ctl->err = 2;
-                ctl->err_iter = ctl->k;
+    if constexpr (P >= 16) {
+        double(*Wb)[P + 1] = reinterpret_cast<double(*)[P + 1]>(&lsm[P][0]);
+        double(*Mib)[P + 1] = reinterpret_cast<double(*)[P + 1]>(&lsm[2 * P][0]);
+        const int rc = solve_cta<P>(flat, p, 0, small + L.nsq_d(), lsm, Wb, Mib, al, be, nred);
+        if (rc) {
+            if (blockIdx.x == 0 && tid == 0) {
+                if (rc == 2) {
+                    ctl->err = 2;
+                    ctl->err_iter = ctl->k;
+                } else {
+                    ctl->status = 1;  // rank collapse (pivot vanished)
+                }
                 ctl->stop = 1;
             }
-            fail = true;
+            return;
         }
-#pragma unroll
-        for (int k = 0; k < P; ++k) {
-            if (fail || k >= p) break;
-            double dk = 0.0;
-            if (lane == k) {
-                double sk = l[k];
-#pragma unroll
-                for (int m = 0; m < k; ++m) sk = fma(-l[m], l[m], sk);
-                dk = (sk > floor) ? rsqrt(sk) : -1.0;  // 1 / L_kk
+        if (blockIdx.x == 0)
+            for (int e = tid; e < P * P; e += 256) {
+                const int i = e / P, j = e % P;
+                ctl->lu[e] = lsm[i][j];
+                small[L.alpha() + e] = al[i][j];
+                small[L.beta() + e] = be[i][j];
             }
-            const double ikk = __shfl_sync(0xffffffffu, dk, k);
-            if (!(ikk > 0.0)) {
+    } else {
+        // The solve runs on one warp; the two CTAs an SM hosts (blocks b and
+        // b + #SMs under the usual placement) use warps 0 and 1, i.e. different
+        // SMSPs, so their serial FP64 chains do not share an issue port.
+        unsigned int nsm;
+        asm("mov.u32 %0, %%nsmid;" : "=r"(nsm));
+        const int solver = static_cast<int>((blockIdx.x / nsm) & 1u);
+        if (warp == solver) {
+            const bool pub = blockIdx.x == 0;
+            const double nsq = (lane < P) ? small[L.nsq_d() + lane] : 0.0;
+            double l[P];
+            double maxabs = 0.0, diag = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < P; ++jj) {
+                l[jj] = 0.0;
+                if (lane < p && jj < p) {
+                    l[jj] = 0.5 * (Gm(0, lane, jj) + Gm(0, jj, lane));
+                    maxabs = fmax(maxabs, fabs(l[jj]));
+                    if (jj == lane) diag = l[jj];
+                }
+            }
+            for (int off = 16; off > 0; off >>= 1) maxabs = fmax(maxabs, __shfl_xor_sync(0xffffffffu, maxabs, off));
+            const double floor = maxabs * 1e-14;
+            PHASE_SUB(8);
+            const bool bad = (lane < p) && !(diag > 0.0) && (nsq > 0.0);
+            bool fail = false;
+            if (__any_sync(0xffffffffu, bad)) {
                 if (pub && lane == 0) {
-                    ctl->status = 1;  // rank collapse (pivot vanished)
+                    ctl->err = 2;
+                    ctl->err_iter = ctl->k;
                     ctl->stop = 1;
                 }
                 fail = true;
-                break;
             }
-            double rk[P];
 #pragma unroll
-            for (int m = 0; m < k; ++m) rk[m] = __shfl_sync(0xffffffffu, l[m], k);
-            if (lane > k && lane < p) {
-                double sk = l[k];
+            for (int k = 0; k < P; ++k) {
+                if (fail || k >= p) break;
+                double dk = 0.0;
+                if (lane == k) {
+                    double sk = l[k];
 #pragma unroll
-                for (int m = 0; m < k; ++m) sk = fma(-l[m], rk[m], sk);
-                l[k] = sk * ikk;
-            }
-            if (lane == k) l[k] = ikk;  // 1 / L_kk on the diagonal
-        }
-        if (fail) {
-            if (lane == 0) abort_flag = 1;
-        } else {
-            if (lane < P) {
-#pragma unroll
-                for (int jj = 0; jj < P; ++jj) {
-                    lsm[lane][jj] = l[jj];
-                    if (pub) ctl->lu[lane * P + jj] = l[jj];
+                    for (int m = 0; m < k; ++m) sk = fma(-l[m], l[m], sk);
+                    dk = (sk > floor) ? rsqrt(sk) : -1.0;  // 1 / L_kk
                 }
-            }
-            __syncwarp();
-            double x[P], rhs[P], xb[P];
-            if (lane < p) {
-#pragma unroll
-                for (int jj = 0; jj < P; ++jj) rhs[jj] = (jj < p) ? -Gm(1, lane, jj) : 0.0;
-                chol_solve_regs<P>(lsm, p, rhs, x);
-#pragma unroll
-                for (int jj = 0; jj < P; ++jj) {
-                    double sb = Gm(2, lane, jj);
-#pragma unroll
-                    for (int m = 0; m < P; ++m)
-                        if (m < p) sb = fma(x[m], Gm(3, m, jj), sb);
-                    rhs[jj] = (jj < p) ? -sb : 0.0;
+                const double ikk = __shfl_sync(0xffffffffu, dk, k);
+                if (!(ikk > 0.0)) {
+                    if (pub && lane == 0) {
+                        ctl->status = 1;  // rank collapse (pivot vanished)
+                        ctl->stop = 1;
+                    }
+                    fail = true;
+                    break;
                 }
-                chol_solve_regs<P>(lsm, p, rhs, xb);
+                double rk[P];
 #pragma unroll
-                for (int jj = 0; jj < P; ++jj) {
-                    al[lane][jj] = (jj < p) ? x[jj] : 0.0;
-                    be[lane][jj] = (jj < p) ? xb[jj] : 0.0;
-                    if (pub) {
-                        small[L.alpha() + lane * P + jj] = (jj < p) ? x[jj] : 0.0;
-                        small[L.beta() + lane * P + jj] = (jj < p) ? xb[jj] : 0.0;
+                for (int m = 0; m < k; ++m) rk[m] = __shfl_sync(0xffffffffu, l[m], k);
+                if (lane > k && lane < p) {
+                    double sk = l[k];
+#pragma unroll
+                    for (int m = 0; m < k; ++m) sk = fma(-l[m], rk[m], sk);
+                    l[k] = sk * ikk;
+                }
+                if (lane == k) l[k] = ikk;  // 1 / L_kk on the diagonal
+            }
+            PHASE_SUB(9);
+            if (fail) {
+                if (lane == 0) abort_flag = 1;
+            } else {
+                if (lane < P) {
+#pragma unroll
+                    for (int jj = 0; jj < P; ++jj) {
+                        lsm[lane][jj] = l[jj];
+                        if (pub) ctl->lu[lane * P + jj] = l[jj];
+                    }
+                }
+                __syncwarp();
+                double x[P], rhs[P], xb[P];
+                if (lane < p) {
+#pragma unroll
+                    for (int jj = 0; jj < P; ++jj) rhs[jj] = (jj < p) ? -Gm(1, lane, jj) : 0.0;
+                    chol_solve_regs<P>(lsm, p, rhs, x);
+                    PHASE_SUB(10);
+#pragma unroll
+                    for (int jj = 0; jj < P; ++jj) {
+                        double sb = Gm(2, lane, jj);
+#pragma unroll
+                        for (int m = 0; m < P; ++m)
+                            if (m < p) sb = fma(x[m], Gm(3, m, jj), sb);
+                        rhs[jj] = (jj < p) ? -sb : 0.0;
+                    }
+                    chol_solve_regs<P>(lsm, p, rhs, xb);
+                    PHASE_SUB(11);
+#pragma unroll
+                    for (int jj = 0; jj < P; ++jj) {
+                        al[lane][jj] = (jj < p) ? x[jj] : 0.0;
+                        be[lane][jj] = (jj < p) ? xb[jj] : 0.0;
+                        if (pub) {
+                            small[L.alpha() + lane * P + jj] = (jj < p) ? x[jj] : 0.0;
+                            small[L.beta() + lane * P + jj] = (jj < p) ? xb[jj] : 0.0;
+                        }
                     }
                 }
             }
