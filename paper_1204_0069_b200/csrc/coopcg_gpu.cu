@@ -523,7 +523,7 @@ cudaError_t fast_update(coopcg_gpu_ctx* ctx, const double* Q, const double* D, d
 template <int P>
 cudaError_t fast_solve_t(coopcg_gpu_ctx* ctx, int mode) {
     // flat Grams + the reduction scratch (+ solve_cta's five P x (P+1) buffers at P >= 16)
-    const size_t smem = (size_t)(4 * P * P + 1024 + (P >= 16 ? 5 * P * (P + 1) : 0)) * sizeof(double);
+    const size_t smem = (size_t)(4 * P * P + 1024 + (P >= COOPCG_CTA_SOLVE_MIN_P ? 5 * P * (P + 1) : 0)) * sizeof(double);
     static std::once_flag attr_once[kMaxDevices];
     cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once[ctx->device % kMaxDevices], [&] {

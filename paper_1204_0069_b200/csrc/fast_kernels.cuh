@@ -335,7 +335,10 @@ __global__ void __launch_bounds__(256)
 // mode 2: beta only from G0 = R_new^T Q of a residual pass (uses ctl->lu).
 // L L^T x = rhs for lane-owned right-hand sides, L in shared memory with
 // 1 / L_ii stored on its diagonal (no division on the solve's critical path).
-// The step solves on a whole CTA in shared memory (P >= 16, where one warp
+#ifndef COOPCG_CTA_SOLVE_MIN_P
+#define COOPCG_CTA_SOLVE_MIN_P 16
+#endif
+// The step solves on a whole CTA in shared memory (P >= COOPCG_CTA_SOLVE_MIN_P, where one warp
 // holding P-wide register rows spills and serialises: 27 us at P = 16 in the
 // fused kernel, 394 us at P = 32 in fast_solve_kernel, round 2).
 //   M = sym(G0) (identity on the padded rows), SPD guard, right-looking
@@ -512,7 +515,7 @@ __global__ void __launch_bounds__(1024)
     }
     cta_reduce_fixed(partials, nparts, 4 * P * P, 0, 1, nout, flat, red);
     __syncthreads();
-    if constexpr (P >= 16) {
+    if constexpr (P >= COOPCG_CTA_SOLVE_MIN_P) {
         // the whole CTA solves in shared memory (solve_cta); buffers after red[]
         double(*lf)[P + 1] = reinterpret_cast<double(*)[P + 1]>(red + blockDim.x);
         double(*Wb)[P + 1] = lf + P;
@@ -875,7 +878,7 @@ __host__ __device__ constexpr size_t fused_smem_bytes() {
     // C/D: grams (4 P^2) + alpha, beta + 4 update tiles + reductions + the factor
     constexpr size_t a = 3ull * fused_rows_tr<P, RP>() * P;
     constexpr size_t d = 4ull * P * P + 2ull * P * (P + 1) + 4ull * fused_upd_tr<P, RP>() * P + 256 + P * (P + 1);
-    constexpr size_t e = P >= 16 ? 2ull * P * (P + 1) : 0;  // solve_cta's W and Minv
+    constexpr size_t e = P >= COOPCG_CTA_SOLVE_MIN_P ? 2ull * P * (P + 1) : 0;  // solve_cta's W and Minv
     return (a + d + e) * sizeof(double);
 }
 
@@ -1044,7 +1047,7 @@ __global__ void __launch_bounds__(256, 2)
     if (blockIdx.x == 0 && threadIdx.x == 0) t_sub_ = t_prev_;
 #endif
     auto Gm = [&](int gsel, int a, int c) { return flat[(gsel * P + a) * P + c]; };
-    if constexpr (P >= 16) {
+    if constexpr (P >= COOPCG_CTA_SOLVE_MIN_P) {
         double(*Wb)[P + 1] = reinterpret_cast<double(*)[P + 1]>(&lsm[P][0]);
         double(*Mib)[P + 1] = reinterpret_cast<double(*)[P + 1]>(&lsm[2 * P][0]);
         const int rc = solve_cta<P>(flat, p, 0, small + L.nsq_d(), lsm, Wb, Mib, al, be, nred);
