@@ -299,6 +299,8 @@ static int check_guards(const coopcg_gpu_ctx* ctx, std::string& what) {
     return 0;
 }
 
+static void pin_give(double* p, size_t elems);  // the pinned staging cache (below)
+
 static void hh_free(coopcg_gpu_ctx* ctx) {
     gfree(ctx, ctx->hh_V);
     gfree(ctx, ctx->hh_lam);
@@ -872,7 +874,7 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     gfree(ctx, ctx->tr_wall);
     gfree(ctx, ctx->stage);
     for (int q = 0; q < 2; ++q) {
-        if (ctx->pin[q]) cudaFreeHost(ctx->pin[q]);
+        pin_give(ctx->pin[q], ctx->pin_elems);
         gfree(ctx, ctx->dslot[q]);
         if (ctx->pin_ev[q]) cudaEventDestroy(ctx->pin_ev[q]);
     }
@@ -934,9 +936,16 @@ double host_normal(uint64_t key, uint64_t t) {
 
 // memcpy on several host threads (a single core copies ~10 GB/s; the
 // PCIe 5 link and host DRAM take several times that).
+static unsigned copy_threads() {
+    static const unsigned t = [] {
+        const char* e = std::getenv("COOPCG_COPY_THREADS");
+        const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+        return e ? std::max(1u, (unsigned)std::atoi(e)) : std::min(16u, hw);
+    }();
+    return t;
+}
 static void par_memcpy(void* dst, const void* src, size_t bytes) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const unsigned T = bytes >= (size_t(4) << 20) ? std::min(8u, hw) : 1u;
+    const unsigned T = bytes >= (size_t(4) << 20) ? copy_threads() : 1u;
     if (T <= 1) {
         std::memcpy(dst, src, bytes);
         return;
@@ -952,12 +961,53 @@ static void par_memcpy(void* dst, const void* src, size_t bytes) {
     for (auto& x : th) x.join();
 }
 
+// Pinned host staging for A's transfers, cached process-wide: page-locking
+// 2 x 32 MB costs ~70 ms, which a one-shot call (create, set_A, solve,
+// destroy -- the drop-in ccg_solve) would otherwise pay every time.  A
+// mutex-guarded free list of slot buffers (portable pinned memory, any
+// device); contexts take one on first use and give it back on destroy.
+struct PinCache {
+    std::mutex mu;
+    std::vector<std::pair<double*, size_t>> free;  // (buffer, elements)
+};
+static PinCache& pin_cache() {
+    static PinCache c;
+    return c;
+}
+static double* pin_take(size_t elems) {
+    PinCache& c = pin_cache();
+    {
+        std::lock_guard<std::mutex> g(c.mu);
+        for (size_t i = 0; i < c.free.size(); ++i)
+            if (c.free[i].second >= elems) {
+                double* p = c.free[i].first;
+                c.free.erase(c.free.begin() + i);
+                return p;
+            }
+    }
+    double* p = nullptr;
+    if (cudaHostAlloc(&p, sizeof(double) * elems, cudaHostAllocPortable) != cudaSuccess) return nullptr;
+    return p;
+}
+static void pin_give(double* p, size_t elems) {
+    if (!p) return;
+    PinCache& c = pin_cache();
+    std::lock_guard<std::mutex> g(c.mu);
+    if (c.free.size() < 8) c.free.emplace_back(p, elems);  // at most 8 x 32 MB kept
+    else cudaFreeHost(p);
+}
+
 static int ensure_pinned(coopcg_gpu_ctx* ctx) {
     if (ctx->pin[0]) return COOPCG_OK;
-    const size_t slot_bytes = size_t(32) << 20;
+    static const size_t slot_mb = [] {
+        const char* e = std::getenv("COOPCG_PIN_MB");
+        return e ? std::max(1, std::atoi(e)) : 32;
+    }();
+    const size_t slot_bytes = slot_mb << 20;
     ctx->pin_elems = std::max<size_t>(slot_bytes / sizeof(double), (size_t)ctx->n);
     for (int q = 0; q < 2; ++q) {
-        CK(cudaHostAlloc(&ctx->pin[q], sizeof(double) * ctx->pin_elems, cudaHostAllocDefault));
+        ctx->pin[q] = pin_take(ctx->pin_elems);
+        if (!ctx->pin[q]) return fail(ctx, COOPCG_E_CUDA, "cudaHostAlloc of the A staging slot failed");
         CK(gmalloc(ctx, &ctx->dslot[q], sizeof(double) * ctx->pin_elems, "dslot"));
         CK(cudaEventCreateWithFlags(&ctx->pin_ev[q], cudaEventDisableTiming));
     }
