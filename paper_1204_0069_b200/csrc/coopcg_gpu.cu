@@ -458,12 +458,19 @@ size_t fast_ad_smem() {
 // column groups per CTA: P=8 -> 1 (2 DMMA warps), P=16/32 -> 2 (4 DMMA warps)
 template <int P>
 constexpr int fast_wn() { return P >= 16 ? 2 : 1; }
-
-template <int P>
-cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
+// M-tiles (8 rows) per consumer warp.  P >= 16: 4 (WN = 2 already gives four DMMA
+// warps per CTA).  P = 8: 2 when A is small (four DMMA warps per CTA: one warp issues a DMMA
+// only every ~32 cycles, and a launch of a few tens of microseconds is bound by that issue
+// rate, not by HBM -- cfg 1 A.D 29.4 -> 28.1 us), 4 when A streams from HBM for hundreds of
+// microseconds (cfg 2: 315 vs 327 us; fewer warps, less power under sw_power_cap).  The
+// results are bit-identical for any MT (each element's k order is unchanged).
+// COOPCG_FAST_MT8 = 2 / 4 forces one shape.
+constexpr size_t kFastSmallA = (size_t)1 << 26;  // elements of the local A block
+template <int P, int MT>
+cudaError_t fast_ad_mt(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
     constexpr int WN = fast_wn<P>();
     constexpr bool TR = P >= 16;
-    auto kern = ad_fast_kernel<P, WN, TR>;
+    auto kern = ad_fast_kernel<P, WN, TR, MT>;
     static std::once_flag attr_once[kMaxDevices];
     cudaError_t attr_err = cudaSuccess;
     std::call_once(attr_once[ctx->device % kMaxDevices], [&] {
@@ -478,11 +485,24 @@ cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
         ++ctx->launches;
         operand = ctx->dtiles;
     }
-    pdl_launch(kern, dim3(ctx->f_grid), dim3(32 + 64 * WN), fast_ad_smem<P>(), ctx->stream, 
+    pdl_launch(kern, dim3(ctx->f_grid), dim3(32 + 32 * (kFastBR / (8 * MT)) * WN), fast_ad_smem<P>(), ctx->stream, 
         ctx->At, ctx->n, ctx->n_loc, ctx->lay.ntiles, operand, ctx->qpart, ctx->f_kchunks, ctx->f_tpc,
         ctx->f_units, stop, ctx->res_k);
     ++ctx->launches;
     return cudaGetLastError();
+}
+template <int P>
+cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
+    if constexpr (P == 8) {
+#ifdef COOPCG_FAST_MT8
+        return fast_ad_mt<8, COOPCG_FAST_MT8>(ctx, src, stop);
+#else
+        if ((size_t)ctx->n_loc * ctx->n <= kFastSmallA) return fast_ad_mt<8, 2>(ctx, src, stop);
+        return fast_ad_mt<8, 4>(ctx, src, stop);
+#endif
+    } else {
+        return fast_ad_mt<P, 4>(ctx, src, stop);
+    }
 }
 cudaError_t fast_ad(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
     switch (ctx->P) {
@@ -639,25 +659,41 @@ AdConfig pick_ad_config(int n_loc, int P, int sms) {
 // A is re-read by every iteration's A.D; the part of it that fits next to the
 // iteration's other working set (the n x P blocks, the k-chunk partials) can
 // stay in the 126 MB L2 from one iteration to the next.  The resident part is
-// a k-range shared by every panel (the first res_k k-rows, or k-tiles in the
-// fast layout), so every A.D CTA reads the same share of its panel from L2.
-// Budget: COOPCG_L2_RES_MB (0 disables), default kL2ResDefaultMB, split among
-// the contexts sharing a device (`share`).
-constexpr double kL2ResDefaultMB = 0.0;
-double l2_res_budget_mb() {
-    static const double mb = [] {
+// the first res_k k-rows of every panel (exact) or the first res_k k-tiles of
+// every (panel, k-chunk) work unit (fast), so every A.D CTA reads the same
+// share of its stream from L2 and the HBM part is spread over all CTAs.
+// Budget: COOPCG_L2_RES_MB (0 disables), split among the contexts sharing a
+// device (`share`).
+// Default (no COOPCG_L2_RES_MB): fast mode keeps half of L2 for A when the local
+// A block is larger than ~3/4 of L2 (below that all of A stays in L2 anyway) and
+// at most 1 GB (above, the resident share is a few percent of the stream: cfg 2
+// +-1%).  cfg 1 (134 MB, round 2 session 4, tools/l2res_fast.sh): A.D 28.1 us at
+// 0 MB, 24.6 at 64 MB, 24.1 at 80 MB, 28.0 at 112 MB; 25.8k -> 27.1k it/s at
+// 64 MB (the iteration tail wants its own share of L2).  The exact mode's
+// small-n A.D is FP64-issue bound, not HBM bound: off unless asked for.
+double l2_res_budget_mb(const coopcg_gpu_ctx* ctx) {
+    static const double env_mb = [] {
         const char* e = std::getenv("COOPCG_L2_RES_MB");
-        return e ? std::max(0.0, std::atof(e)) : kL2ResDefaultMB;
+        return e ? std::max(0.0, std::atof(e)) : -1.0;
     }();
-    return mb;
+    if (env_mb >= 0.0) return env_mb;
+    if (ctx->arith != COOPCG_ARITH_FAST) return 0.0;
+    int l2 = 0;
+    if (cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, ctx->device) != cudaSuccess || l2 <= 0) return 0.0;
+    const double a_bytes = (double)ctx->n_loc * ctx->n * 8.0;
+    if (a_bytes < 0.75 * l2 || a_bytes > 1e9) return 0.0;
+    return 0.5 * l2 / 1e6;
 }
 void set_l2_residency(coopcg_gpu_ctx* ctx, int share) {
-    const double budget = l2_res_budget_mb() * 1e6 / std::max(1, share);
+    const double budget = l2_res_budget_mb(ctx) * 1e6 / std::max(1, share);
     // bytes of A per unit of res_k: one k-row of every panel (exact) or one
-    // k-tile of every panel (fast)
-    const double unit = ctx->arith == COOPCG_ARITH_FAST ? (double)ctx->npanels * kFastBR * kFastT * 8.0
-                                                         : (double)ctx->npanels * ctx->ad.BR * 8.0;
-    const int units = ctx->arith == COOPCG_ARITH_FAST ? ctx->lay.ntiles : ctx->n;
+    // k-tile of every (panel, k-chunk) work unit (fast: the first res_k tiles
+    // of EVERY unit, so each CTA reads the same share from L2 and the HBM part
+    // is spread over all CTAs -- a CTA's stream is bound by its ring depth)
+    const double unit = ctx->arith == COOPCG_ARITH_FAST
+                            ? (double)ctx->npanels * ctx->f_kchunks * kFastBR * kFastT * 8.0
+                            : (double)ctx->npanels * ctx->ad.BR * 8.0;
+    const int units = ctx->arith == COOPCG_ARITH_FAST ? ctx->f_tpc : ctx->n;
     ctx->res_k = (int)std::min<double>(units, std::floor(budget / unit));
     ctx->res_bytes = (size_t)(ctx->res_k * unit);
 }

@@ -57,21 +57,24 @@ __global__ void __launch_bounds__(256)
 }
 
 // (1) Qpart[c] = A_panel(:, kchunk c) . D(kchunk c, :) for work units
-// (panel, kchunk); persistent CTAs; warp 0 = bulk-copy producer, 2*WN warps
-// consume with m8n8k4 DMMA: warp w covers 32 rows (4 M-tiles) x P/WN
-// columns.  Both operands arrive as contiguous tiles (A: [r][kk], the
+// (panel, kchunk); persistent CTAs; warp 0 = bulk-copy producer, (8/MT)*WN
+// warps consume with m8n8k4 DMMA: warp w covers 8*MT rows (MT M-tiles) x P/WN
+// columns.  MT = 2 at P = 8: four consumer warps per CTA land on the four
+// SM sub-partitions (a CTA's warps map to them by warp index), where two
+// 32-row warps per CTA left the DMMA work of both co-resident CTAs on two
+// of them (cfg 1: the busiest sub-partition's DMMA pipe ~80% active, round 2).  Both operands arrive as contiguous tiles (A: [r][kk], the
 // operand: [col][kk]), one bulk copy each per stage.
 // TR (transposed operand) = true: Dt holds [col][kk] k-tiles (P >= 16);
 // false: Dt is the row-major n x P block itself (P = 8: its 64-byte rows
 // already give conflict-free B fragments), tail rows zero-filled in smem.
-template <int P, int WN, bool TR>
-__global__ void __launch_bounds__(32 + 64 * WN)
+template <int P, int WN, bool TR, int MT = 4>
+__global__ void __launch_bounds__(32 + 32 * (kFastBR / (8 * MT)) * WN)
     ad_fast_kernel(const double* __restrict__ Af, int n, int n_loc, int ntiles, const double* __restrict__ Dt,
                    double* __restrict__ Qpart, int kchunks, int tiles_per_chunk, int nunits,
                    const int* __restrict__ stop, int res_t) {
     static_assert(P % (8 * WN) == 0, "fast contexts pad p to a multiple of 8 per column group");
     constexpr int NT = P / 8 / WN;  // N tiles of 8 columns per warp
-    constexpr int NCW = 2 * WN;     // consumer warps
+    constexpr int NCW = (kFastBR / (8 * MT)) * WN;  // consumer warps
     constexpr int BR = kFastBR, T = kFastT, S = fast_stages<P>();
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);  // S x BR x T
@@ -140,7 +143,7 @@ __global__ void __launch_bounds__(32 + 64 * WN)
                     }
                     mbar_arrive_expect_tx(&full[s], abytes + dbytes);
                     bulk_g2s_evict_first(As + s * BR * T, Af + (static_cast<size_t>(q) * ntiles + t) * BR * T, abytes, &full[s],
-                                         t < res_t ? pol_res : pol);
+                                         (t - t0) < res_t ? pol_res : pol);
                     if (waited) bulk_g2s(Ds + s * P * T, Dt + static_cast<size_t>(t) * P * T, dbytes, &full[s]);
                     else pend_t[it] = t;
                     if (++s == S) {
@@ -156,7 +159,7 @@ __global__ void __launch_bounds__(32 + 64 * WN)
     pdl_wait();
     if (stop != nullptr && *reinterpret_cast<volatile const int*>(stop)) return;
     const int cw = warp - 1;
-    const int rb = cw / WN;          // row block: rows [32 rb, 32 rb + 32)
+    const int rb = cw / WN;          // row block: rows [8 MT rb, 8 MT rb + 8 MT)
     const int cg = cw % WN;          // column group: N tiles [cg*NT, cg*NT + NT)
     const int g = lane >> 2, tg = lane & 3;
     int s = 0;
@@ -164,26 +167,26 @@ __global__ void __launch_bounds__(32 + 64 * WN)
     for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
         const int q = u / kchunks, c = u % kchunks;
         const int t0 = c * tiles_per_chunk, t1 = min(ntiles, t0 + tiles_per_chunk);
-        double acc[4][NT][2];
+        double acc[MT][NT][2];
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt)
+        for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
         for (int t = t0; t < t1; ++t) {
             mbar_wait(&full[s], phase);
-            const double* as = As + s * BR * T + (32 * rb + g) * T + tg;
+            const double* as = As + s * BR * T + (8 * MT * rb + g) * T + tg;
             // B fragment (k = tg, n = g): [col][kk] tiles read like A; row-major [kk][col] otherwise
             const double* ds = TR ? Ds + s * P * T + (8 * NT * cg + g) * T + tg
                                   : Ds + s * P * T + tg * P + 8 * NT * cg + g;
 #pragma unroll
             for (int ks = 0; ks < T / 4; ++ks) {
-                double a[4], bb[NT];
+                double a[MT], bb[NT];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt) a[mt] = as[8 * mt * T + 4 * ks];
+                for (int mt = 0; mt < MT; ++mt) a[mt] = as[8 * mt * T + 4 * ks];
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) bb[nt] = TR ? ds[8 * nt * T + 4 * ks] : ds[4 * ks * P + 8 * nt];
 #pragma unroll
-                for (int mt = 0; mt < 4; ++mt)
+                for (int mt = 0; mt < MT; ++mt)
 #pragma unroll
                     for (int nt = 0; nt < NT; ++nt) dmma884(acc[mt][nt][0], acc[mt][nt][1], a[mt], bb[nt]);
             }
@@ -196,8 +199,8 @@ __global__ void __launch_bounds__(32 + 64 * WN)
         }
         double* qp = Qpart + static_cast<size_t>(c) * n_loc * P;
 #pragma unroll
-        for (int mt = 0; mt < 4; ++mt) {
-            const int il = q * BR + 32 * rb + 8 * mt + g;
+        for (int mt = 0; mt < MT; ++mt) {
+            const int il = q * BR + 8 * MT * rb + 8 * mt + g;
             if (il < n_loc) {
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
