@@ -13,9 +13,10 @@
 // (solvers.hpp:111-115), per-iteration records with the reference's mult
 // counting (workplan.hpp:693-715), final_residual_norms by true
 // recomputation (solvers.hpp:188-210).  In the default exact arithmetic mode
-// the trace is bit-identical to ccg_solve's.  The
-// verification-only options keep_history / x_star (trace.hpp:84-85) are
-// rejected with std::invalid_argument rather than silently ignored.
+// the trace is bit-identical to ccg_solve's, including the
+// verification mode (trace.hpp:84-87): keep_history fills history_x / _r / _d
+// and x_star the per-iteration anorm_errors (one device, not gpu_mccg, which
+// rejects them with std::invalid_argument rather than ignoring them).
 //
 // GpuSolver keeps A resident on the device between solves (SpdMatrix is
 // immutable, dense.hpp:95-96), the common "many right-hand sides" use.
@@ -103,12 +104,20 @@ public:
             throw DimensionError("solver: operand shapes do not match the system matrix");
         if (X0.cols() < 1 || X0.cols() >= n_) throw DimensionError("solver: need 1 <= p < n starting columns");
         if (X0.cols() != p_) throw DimensionError("gpu_ccg: agent count differs from the solver's");
-        // The verification-only fields of SolveOptions (trace.hpp:84-85: history
-        // blocks, A-norm errors against an oracle solution) are not produced by
-        // the device solver; refuse them instead of returning an empty record.
-        if (opts.keep_history || opts.x_star != nullptr)
-            throw std::invalid_argument("gpu_ccg: keep_history / x_star (verification mode) are not supported "
-                                        "on the GPU backend; use ccg_solve for invariant checks");
+        // Verification mode (trace.hpp:84-87: history blocks, A-norm errors against
+        // an oracle solution): coopcg_gpu_set_verification; one device, not mccg.
+        const bool verify = opts.keep_history || opts.x_star != nullptr;
+        if (verify && algo == 1)
+            throw std::invalid_argument("gpu_mccg: keep_history / x_star (verification mode) are not supported "
+                                        "on the GPU backend; use mccg_solve for invariant checks");
+        if (opts.x_star != nullptr && static_cast<int>(opts.x_star->size()) != n_)
+            throw DimensionError("solver: operand shapes do not match the system matrix");
+        if (verify || verify_on_) {
+            const int vrc = coopcg_gpu_set_verification(ctx_, opts.keep_history ? 1 : 0,
+                                                        opts.x_star ? opts.x_star->data() : nullptr);
+            if (vrc != COOPCG_OK) gpu_detail::raise(vrc, gpu_detail::last_error(ctx_));
+            verify_on_ = verify;
+        }
         const int n = n_, p = p_;
         const int max_iters = opts.max_iters >= 0 ? opts.max_iters : 2 * n;  // solvers.hpp:18-23
         const int cap = max_iters > 0 ? max_iters : 1;
@@ -158,6 +167,32 @@ public:
             rec.wall_ns = wall[k];
             t.iterations.push_back(std::move(rec));
         }
+        if (opts.x_star != nullptr && tr.iterations > 0) {  // IterationRecord::anorm_errors (solvers.hpp:131)
+            std::vector<double> an(static_cast<size_t>(tr.iterations) * p);
+            const int arc = coopcg_gpu_get_anorm_errors(ctx_, tr.iterations, an.data());
+            if (arc != COOPCG_OK) gpu_detail::raise(arc, gpu_detail::last_error(ctx_));
+            for (int k = 0; k < tr.iterations; ++k)
+                t.iterations[static_cast<size_t>(k)].anorm_errors.assign(an.begin() + static_cast<size_t>(k) * p,
+                                                                         an.begin() + static_cast<size_t>(k + 1) * p);
+        }
+        if (opts.keep_history) {  // push_history (solvers.hpp:43-50): entry 0 = setup, k + 1 = after iteration k
+            int entries = 0;
+            coopcg_gpu_history_count(ctx_, &entries);
+            std::vector<double> hx(static_cast<size_t>(n) * p), hr(hx.size()), hd(hx.size());
+            auto block_of = [&](const std::vector<double>& v) {
+                DenseBlock<double> blk(n, p);
+                for (int j = 0; j < p; ++j)
+                    for (int i = 0; i < n; ++i) blk(i, j) = v[static_cast<size_t>(j) * n + i];
+                return blk;
+            };
+            for (int e = 0; e < entries; ++e) {
+                const int hrc = coopcg_gpu_get_history(ctx_, e, hx.data(), hr.data(), hd.data());
+                if (hrc != COOPCG_OK) gpu_detail::raise(hrc, gpu_detail::last_error(ctx_));
+                t.history_x.push_back(block_of(hx));
+                t.history_r.push_back(block_of(hr));
+                t.history_d.push_back(block_of(hd));
+            }
+        }
         t.status = gpu_detail::status_of(tr.status);
         t.converged_agent = tr.converged_agent;
         const int na = tr.n_active;
@@ -178,6 +213,7 @@ public:
 private:
     int n_, p_;
     coopcg_gpu_ctx* ctx_ = nullptr;
+    bool verify_on_ = false;
 };
 
 /// mccg_solve's signature plus GPU options (solvers.hpp:338-342).

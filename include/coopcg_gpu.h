@@ -66,8 +66,8 @@ enum coopcg_arith { COOPCG_ARITH_EXACT = 0, COOPCG_ARITH_FAST = 1 };
 enum coopcg_matrix_kind { COOPCG_MATRIX_DIAGDOM = 0, COOPCG_MATRIX_HOUSEHOLDER = 1, COOPCG_MATRIX_RANDOM_SPD = 2 };
 enum coopcg_vector_kind { COOPCG_VEC_UNIFORM = 0, COOPCG_VEC_NORMAL = 1 };
 
-/* SolveOptions<double> (trace.hpp:74-88). keep_history / x_star are not
- * carried by the ABI (verification-only fields of the reference). */
+/* SolveOptions<double> (trace.hpp:74-88).  The verification-only fields
+ * keep_history / x_star are set per context with coopcg_gpu_set_verification. */
 typedef struct {
     double tol;                   /* absolute threshold on ||r_j||_2 (block_cg.hpp:283-289) */
     int max_iters;                /* -1 => 2n (solvers.hpp:18-23) */
@@ -175,6 +175,29 @@ int coopcg_gpu_run(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* t
 /* The drop-in: upload + run + copy-out, host buffers in and out. */
 int coopcg_gpu_solve(coopcg_gpu_ctx* ctx, const double* b, const double* X0_colmajor,
                      const coopcg_opts* opts, coopcg_trace* trace);
+
+/* ---- verification mode: SolveOptions::keep_history / x_star (trace.hpp:84-87) ----
+ * Sticky per context until changed; (0, NULL) turns it off.  Needs one context
+ * holding every row of A (not a multi-device handle or a row shard), whole
+ * solves (coopcg_gpu_run / _solve), and algo 0 or 2 (not mccg_solve).
+ *   keep_history != 0: every solve keeps X_k, R_k, D_k on the device for
+ *     k = 0..iterations (entry 0 = the state after setup, entry k + 1 = after
+ *     iteration k with D = Dnext: push_history, solvers.hpp:43-50, :146);
+ *     3 (max_iters + 1) n P doubles -- the run fails with COOPCG_E_INVALID when
+ *     that exceeds half of the free device memory (set max_iters).
+ *   x_star != NULL (host, n doubles, copied): every iteration also records
+ *     IterationRecord::anorm_errors = ||x_j - x*||_A per agent (block_cg.hpp:316-331,
+ *     dense_ops.hpp:159-196) at the cost of one more A.D; exact mode reproduces
+ *     the reference's values bit for bit; a quadratic form negative beyond
+ *     round-off ends the run with COOPCG_E_SPD_VIOLATION like a_norm's throw. */
+int coopcg_gpu_set_verification(coopcg_gpu_ctx* ctx, int keep_history, const double* x_star);
+/* History entries of the last run (iterations + 1; 0 without keep_history). */
+int coopcg_gpu_history_count(const coopcg_gpu_ctx* ctx, int* entries);
+/* Entry `entry` of trace.history_x / _r / _d, each n x p column-major; NULL skips. */
+int coopcg_gpu_get_history(coopcg_gpu_ctx* ctx, int entry, double* X_colmajor, double* R_colmajor,
+                           double* D_colmajor);
+/* Rows 0..min(capacity, iterations) - 1 of the per-iteration A-norm errors, p per row. */
+int coopcg_gpu_get_anorm_errors(coopcg_gpu_ctx* ctx, int capacity, double* out);
 
 int coopcg_gpu_timing(const coopcg_gpu_ctx* ctx, coopcg_timing* out);
 /* The context's CUDA stream (cudaStream_t), so callers can record events on

@@ -160,17 +160,74 @@ int main() {
         const bool ok = !ref_msg.empty() && ref_msg == gpu_msg;
         std::printf("%-34s %s (\"%s\")\n", "SpdViolationError", ok ? "same exception" : "MISMATCH", gpu_msg.c_str());
         if (!ok) ++failures;
-        // verification-only options are refused, not silently dropped
+        // gpu_mccg refuses the verification-only options instead of dropping them
         bool refused = false;
         SolveOptions<double> oh;
         oh.keep_history = true;
-        try { gpu_ccg(A, b, X0, oh); } catch (const std::invalid_argument&) { refused = true; }
-        std::printf("%-34s %s\n", "keep_history refused", refused ? "invalid_argument" : "MISMATCH");
+        try { gpu_mccg(A, b, X0, oh); } catch (const std::invalid_argument&) { refused = true; }
+        std::printf("%-34s %s\n", "mccg keep_history refused", refused ? "invalid_argument" : "MISMATCH");
         if (!refused) ++failures;
         bool dim = false;
         try { gpu_ccg(A, Vec<double>(n - 1, 1.0), X0, {}); } catch (const DimensionError&) { dim = true; }
         std::printf("%-34s %s\n", "DimensionError", dim ? "same exception" : "MISMATCH");
         if (!dim) ++failures;
+    }
+    // Verification mode (trace.hpp:84-87): history blocks and A-norm errors, bit for bit
+    // (the problem of tests/test_solvers.cpp:227-235, a tolerance run, recompute iterations, cg)
+    {
+        struct VCase { int n, p; double cond; unsigned long long seed; double tol; int max_iters; int recompute; };
+        const VCase vc[] = {{60, 3, 100.0, 41, 1e-300, 15, -1}, {90, 4, 1e3, 5, 1e-9, -1, 4}, {70, 1, 1e2, 9, 1e-10, -1, 1}};
+        for (const auto& c : vc) {
+            ProblemSpec spec;
+            spec.n = c.n;
+            spec.p = c.p;
+            spec.cond = c.cond;
+            spec.seed = c.seed;
+            auto inst = make_problem<double>(spec);
+            const Vec<double> xs = solve_dense(inst.A, inst.b);
+            SolveOptions<double> o;
+            o.tol = c.tol;
+            o.max_iters = c.max_iters;
+            o.recompute_residual_every = c.recompute;
+            o.keep_history = true;
+            o.x_star = &xs;
+            const auto r = ccg_solve(inst.A, inst.b, inst.X0, o);
+            const auto g = gpu_ccg(inst.A, inst.b, inst.X0, o);
+            char name[96];
+            std::snprintf(name, sizeof name, "verify n=%d p=%d", c.n, c.p);
+            compare(name, r, g);
+            bool ok = r.history_x.size() == g.history_x.size() && r.history_r.size() == g.history_r.size() &&
+                      r.history_d.size() == g.history_d.size() &&
+                      g.history_x.size() == static_cast<size_t>(g.iteration_count()) + 1;
+            for (size_t e = 0; ok && e < r.history_x.size(); ++e)
+                ok = r.history_x[e] == g.history_x[e] && r.history_r[e] == g.history_r[e] &&
+                     r.history_d[e] == g.history_d[e];
+            for (int k = 0; ok && k < r.iteration_count(); ++k) {
+                const auto& a = r.iterations[k].anorm_errors;
+                const auto& bb = g.iterations[k].anorm_errors;
+                ok = a.size() == bb.size() && a.size() == static_cast<size_t>(c.p);
+                for (size_t j = 0; ok && j < a.size(); ++j) ok = same(a[j], bb[j]);
+            }
+            std::printf("%-34s entries=%zu  %s\n", "  history + anorm_errors", g.history_x.size(),
+                        ok ? "bit-identical" : "MISMATCH");
+            if (!ok) ++failures;
+            if (c.p == 1) {  // the scalar solver keeps its own history / A-norm record (solvers.hpp:411-415, :489-504)
+                Vec<double> x0(static_cast<size_t>(c.n));
+                for (int i = 0; i < c.n; ++i) x0[static_cast<size_t>(i)] = inst.X0(i, 0);
+                const auto rc = cg_solve(inst.A, inst.b, x0, o);
+                const auto gc = gpu_cg_solve(inst.A, inst.b, x0, o);
+                bool okc = rc.iteration_count() == gc.iteration_count() && rc.history_x.size() == gc.history_x.size();
+                for (size_t e = 0; okc && e < rc.history_x.size(); ++e)
+                    okc = rc.history_x[e] == gc.history_x[e] && rc.history_r[e] == gc.history_r[e] &&
+                          rc.history_d[e] == gc.history_d[e];
+                for (int k = 0; okc && k < rc.iteration_count(); ++k)
+                    okc = rc.iterations[k].anorm_errors.size() == 1 && gc.iterations[k].anorm_errors.size() == 1 &&
+                          same(rc.iterations[k].anorm_errors[0], gc.iterations[k].anorm_errors[0]);
+                std::printf("%-34s entries=%zu  %s\n", "  cg_solve history + anorm", gc.history_x.size(),
+                            okc ? "bit-identical" : "MISMATCH");
+                if (!okc) ++failures;
+            }
+        }
     }
     std::printf("DROPIN %s (%d failures)\n", failures ? "FAIL" : "OK", failures);
     return failures ? 1 : 0;

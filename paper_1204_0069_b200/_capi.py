@@ -67,6 +67,10 @@ SIGNATURES = [
     ("coopcg_gpu_upload", _I, [_VP, _VP, _VP]),
     ("coopcg_gpu_run", _I, [_VP, C.POINTER(coopcg_opts), C.POINTER(coopcg_trace)]),
     ("coopcg_gpu_solve", _I, [_VP, _VP, _VP, C.POINTER(coopcg_opts), C.POINTER(coopcg_trace)]),
+    ("coopcg_gpu_set_verification", _I, [_VP, _I, _VP]),
+    ("coopcg_gpu_history_count", _I, [_VP, C.POINTER(C.c_int)]),
+    ("coopcg_gpu_get_history", _I, [_VP, _I, _VP, _VP, _VP]),
+    ("coopcg_gpu_get_anorm_errors", _I, [_VP, _I, _VP]),
     ("coopcg_gpu_timing", _I, [_VP, C.POINTER(coopcg_timing)]),
     ("coopcg_gpu_stream", _VP, [_VP]),
     ("coopcg_gpu_matvec_block", _I, [_VP, _VP, _VP]),

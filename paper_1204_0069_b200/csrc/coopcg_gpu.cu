@@ -34,6 +34,7 @@
 #include "exact_kernels.cuh"
 #include "gen_kernels.cuh"
 #include "fast_kernels.cuh"
+#include "verify_kernels.cuh"
 
 using namespace coopcg_gpu;
 
@@ -194,6 +195,18 @@ struct coopcg_gpu_ctx {
     double* dslot[2] = {nullptr, nullptr};
     cudaEvent_t pin_ev[2] = {nullptr, nullptr};
     size_t pin_elems = 0;
+
+    // verification mode (SolveOptions::keep_history / x_star, trace.hpp:84-87;
+    // coopcg_gpu_set_verification): history entries of three n x P blocks
+    // (X, R, D; entry 0 after setup, entry k + 1 after iteration k) and one row
+    // of per-agent A-norm errors per iteration
+    bool ver_hist_on = false, ver_xs_on = false;
+    double* ver_hist = nullptr;
+    int ver_hist_cap = 0;      // entries allocated
+    double *ver_xs = nullptr, *ver_E = nullptr, *ver_AE = nullptr, *ver_anorm = nullptr;
+    int ver_anorm_cap = 0;     // rows allocated
+    int* ver_flag = nullptr;   // a_norm's "negative beyond round-off" (dense_ops.hpp:190-191)
+    int ver_iters = -1;        // iterations of the last verification run (-1: none)
 
     AdConfig ad;
     int nparts = 0;
@@ -464,7 +477,8 @@ constexpr int fast_wn() { return P >= 16 ? 2 : 1; }
 // rate, not by HBM -- cfg 1 A.D 29.4 -> 28.1 us), 4 when A streams from HBM for hundreds of
 // microseconds (cfg 2: 315 vs 327 us; fewer warps, less power under sw_power_cap).  The
 // results are bit-identical for any MT (each element's k order is unchanged).
-// COOPCG_FAST_MT8 = 2 / 4 forces one shape.
+// The build macro COOPCG_FAST_MT8 = 2 / 4 or the environment variable
+// COOPCG_FAST_MT = 2 / 4 force one shape.
 constexpr size_t kFastSmallA = (size_t)1 << 26;  // elements of the local A block
 template <int P, int MT>
 cudaError_t fast_ad_mt(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
@@ -497,7 +511,12 @@ cudaError_t fast_ad_t(coopcg_gpu_ctx* ctx, const double* src, const int* stop) {
 #ifdef COOPCG_FAST_MT8
         return fast_ad_mt<8, COOPCG_FAST_MT8>(ctx, src, stop);
 #else
-        if ((size_t)ctx->n_loc * ctx->n <= kFastSmallA) return fast_ad_mt<8, 2>(ctx, src, stop);
+        static const int mt_env = [] {
+            const char* e = std::getenv("COOPCG_FAST_MT");
+            return e ? std::atoi(e) : 0;
+        }();
+        const bool small = mt_env == 2 || (mt_env != 4 && (size_t)ctx->n_loc * ctx->n <= kFastSmallA);
+        if (small) return fast_ad_mt<8, 2>(ctx, src, stop);
         return fast_ad_mt<8, 4>(ctx, src, stop);
 #endif
     } else {
@@ -909,6 +928,12 @@ int destroy_impl(coopcg_gpu_ctx* ctx) {
     gfree(ctx, ctx->tr_minres);
     gfree(ctx, ctx->tr_wall);
     gfree(ctx, ctx->stage);
+    gfree(ctx, ctx->ver_hist);
+    gfree(ctx, ctx->ver_xs);
+    gfree(ctx, ctx->ver_E);
+    gfree(ctx, ctx->ver_AE);
+    gfree(ctx, ctx->ver_anorm);
+    gfree(ctx, ctx->ver_flag);
     for (int q = 0; q < 2; ++q) {
         pin_give(ctx->pin[q], ctx->pin_elems);
         gfree(ctx, ctx->dslot[q]);
@@ -1668,6 +1693,79 @@ static cudaError_t fast_rows_any(coopcg_gpu_ctx* ctx, const double* qpart, int k
     }
 }
 
+// ---- verification mode (keep_history / x_star) --------------------------------
+// Buffers for the coming solve; refuses what the mode does not cover.
+static int ver_begin(coopcg_gpu_ctx* ctx) {
+    ctx->ver_iters = -1;
+    if (!ctx->ver_hist_on && !ctx->ver_xs_on) return COOPCG_OK;
+    if (ctx->algo == 1)
+        return fail(ctx, COOPCG_E_INVALID, "keep_history / x_star are not available with mccg_solve on the GPU");
+    const size_t blk = (size_t)ctx->n * ctx->P;
+    if (ctx->ver_hist_on) {
+        const int entries = ctx->max_iters + 1;
+        if (entries > ctx->ver_hist_cap) {
+            gfree(ctx, ctx->ver_hist);
+            ctx->ver_hist = nullptr;
+            ctx->ver_hist_cap = 0;
+            const size_t bytes = sizeof(double) * 3 * blk * (size_t)entries;
+            size_t free_b = 0, total_b = 0;
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            if (bytes > free_b / 2)
+                return fail(ctx, COOPCG_E_INVALID,
+                            "keep_history: %d entries of three %d x %d blocks need %.1f GB of device memory "
+                            "(set max_iters)", entries, ctx->n, ctx->p, bytes / 1e9);
+            CK(gmalloc(ctx, &ctx->ver_hist, bytes, "ver_hist"));
+            ctx->ver_hist_cap = entries;
+        }
+    }
+    if (ctx->ver_xs_on) {
+        if (!ctx->ver_E) CK(gmalloc(ctx, &ctx->ver_E, sizeof(double) * blk, "ver_E"));
+        if (!ctx->ver_AE) CK(gmalloc(ctx, &ctx->ver_AE, sizeof(double) * blk, "ver_AE"));
+        if (!ctx->ver_flag) CK(gmalloc(ctx, &ctx->ver_flag, sizeof(int), "ver_flag"));
+        const int rows = std::max(ctx->max_iters, 1);
+        if (rows > ctx->ver_anorm_cap) {
+            gfree(ctx, ctx->ver_anorm);
+            ctx->ver_anorm = nullptr;
+            ctx->ver_anorm_cap = 0;
+            CK(gmalloc(ctx, &ctx->ver_anorm, sizeof(double) * (size_t)rows * ctx->p_orig, "ver_anorm"));
+            ctx->ver_anorm_cap = rows;
+        }
+        CK(cudaMemsetAsync(ctx->ver_flag, 0, sizeof(int), ctx->stream));
+    }
+    return COOPCG_OK;
+}
+// History entry `entry` <- (X, R, dir): push_history (solvers.hpp:43-50).  Entries
+// enqueued after a device-side stop copy unchanged blocks and are never read.
+static int ver_snapshot(coopcg_gpu_ctx* ctx, int entry, const double* dir) {
+    if (!ctx->ver_hist_on || entry >= ctx->ver_hist_cap) return COOPCG_OK;
+    const size_t blk = (size_t)ctx->n * ctx->P;
+    double* h = ctx->ver_hist + (size_t)entry * 3 * blk;
+    CK(cudaMemcpyAsync(h, ctx->X, sizeof(double) * blk, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(h + blk, ctx->R, sizeof(double) * blk, cudaMemcpyDeviceToDevice, ctx->stream));
+    CK(cudaMemcpyAsync(h + 2 * blk, dir, sizeof(double) * blk, cudaMemcpyDeviceToDevice, ctx->stream));
+    return COOPCG_OK;
+}
+// Row k of the A-norm errors: ||x_j - x*||_A per agent after iteration k's update
+// (anorm_errors, block_cg.hpp:316-331).  No stop check: the iteration that raises
+// the stop still records (solvers.hpp:131); later launches write unread rows.
+static int ver_anorm(coopcg_gpu_ctx* ctx, int k) {
+    if (!ctx->ver_xs_on || k >= ctx->ver_anorm_cap) return COOPCG_OK;
+    const int n = ctx->n, P = ctx->P;
+    cudaStream_t st = ctx->stream;
+    ver_diff_kernel<<<grid_for((size_t)n * P, 256), 256, 0, st>>>(ctx->X, ctx->ver_xs, ctx->ver_E, n, ctx->p, P);
+    LAUNCHED();
+    if (ctx->arith != COOPCG_ARITH_FAST) {
+        CK(ad_launch(ctx, ctx->ver_E, ctx->ver_AE, nullptr, nullptr));
+    } else {
+        CK(fast_ad(ctx, ctx->ver_E, nullptr));
+        CK(fast_rows(ctx, ctx->ver_AE, nullptr, nullptr, nullptr, nullptr, 1, nullptr));
+    }
+    ver_anorm_kernel<<<1, 256, sizeof(double) * 2 * kVerTile * P, st>>>(
+        ctx->ver_E, ctx->ver_AE, n, ctx->p, P, ctx->ver_anorm + (size_t)k * ctx->p_orig, ctx->ver_flag);
+    LAUNCHED();
+    return COOPCG_OK;
+}
+
 static int begin_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     if (!ctx->a_ready) return fail(ctx, COOPCG_E_STATE, "A not set (coopcg_gpu_set_A / coopcg_gpu_gen_A)");
     if (!ctx->inputs_ready) return fail(ctx, COOPCG_E_STATE, "b / X0 not uploaded");
@@ -1679,6 +1777,7 @@ static int begin_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     ctx->algo = (o.algo == 1 || o.algo == 2) ? o.algo : 0;
     if (ctx->algo == 2 && (ctx->p != 1 || ctx->arith != COOPCG_ARITH_EXACT))
         return fail(ctx, COOPCG_E_INVALID, "steepest descent needs p = 1 and the exact mode");
+    if (int rc = ver_begin(ctx)) return rc;
     ctx->host_err = 0;
     ctx->host_err_msg.clear();
     if (ctx->p != ctx->p_orig)
@@ -1979,6 +2078,32 @@ static int end_impl(coopcg_gpu_ctx* ctx, coopcg_trace* trace) {
                 std::memcpy(trace->final_x + (size_t)ctx->ids[j] * n, xs.data() + (size_t)j * n, sizeof(double) * n);
         }
     }
+    if (ctx->ver_hist_on || ctx->ver_xs_on) {
+        ctx->ver_iters = fin.iterations;
+        // Exact mode forms D' only when the iteration goes on (beta_direction_kernel
+        // returns once an agent has converged); the reference forms Dnext before
+        // end_of_iteration and pushes it (solvers.hpp:146), so the converging
+        // iteration's history entry gets its direction block here: D' = R + D beta^T
+        // with the beta the iteration solved (D' = R for steepest descent).
+        if (ctx->ver_hist_on && ctx->arith != COOPCG_ARITH_FAST && fin.status == 0 && fin.iterations >= 1 &&
+            fin.iterations < ctx->ver_hist_cap) {
+            const int ks = fin.iterations - 1;
+            const size_t blk = (size_t)n * P;
+            const SmallLayout L{P};
+            ver_direction_kernel<<<grid_for(blk, 256), 256, 0, st>>>(
+                ctx->R, ctx->Dblk[ks & 1], ctx->small + L.beta(), ctx->ver_hist + ((size_t)(ks + 1) * 3 + 2) * blk, n, p,
+                P, ctx->algo == 2 ? 1 : 0);
+            CKL();
+            CK(cudaStreamSynchronize(st));
+        }
+        if (ctx->ver_xs_on && ctx->ver_flag) {
+            int flag = 0;
+            CK(cudaMemcpyAsync(&flag, ctx->ver_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (flag)  // dense_ops.hpp:190-191
+                return fail(ctx, COOPCG_E_SPD_VIOLATION, "a_norm: quadratic form negative beyond round-off");
+        }
+    }
     if (ctx->host_err) return fail(ctx, ctx->host_err, "%s", ctx->host_err_msg.c_str());
     if (fin.err == COOPCG_E_SPD_VIOLATION)
         return fail(ctx, COOPCG_E_SPD_VIOLATION, "nonpositive direction energy d^T A d at iteration %d",
@@ -2131,11 +2256,17 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
     if (int rc = each(ctx, X, setup_local)) return rc;
     if (int rc = xrows(ctx, X, COOPCG_BLOCK_R, 0)) return rc;
     if (int rc = each(ctx, X, setup_rest)) return rc;
+    // verification mode (one context holding every row): history entry 0 = the
+    // state after setup; everything stays on the main stream (the A-norm pass
+    // reuses the row-pass partial buffers the side-stream record reads)
+    const bool ver = c0->ver_hist_on || c0->ver_xs_on;
+    if (ver)
+        if (int rc = ver_snapshot(c0, 0, c0->Dblk[0])) return rc;
     if (c0->algo == 1)
         if (int rc = each(ctx, X, mccg_setup)) return rc;
     if (int rc = on0()) return rc;
     CK(cudaEventRecord(c0->ev_loop0, c0->stream));
-    for (coopcg_gpu_ctx* c : X.s) c->rank_async = true;
+    for (coopcg_gpu_ctx* c : X.s) c->rank_async = !ver;
     struct AsyncOff {
         const Exch& X;
         ~AsyncOff() {
@@ -2237,6 +2368,10 @@ static int run_impl(coopcg_gpu_ctx* ctx, const coopcg_opts* opts, coopcg_trace* 
             if (recompute_at(c0, k))
                 if (int rc = xrows(ctx, X, COOPCG_BLOCK_R, k)) return rc;
             if (int rc = each(ctx, X, [&](coopcg_gpu_ctx* c) { return iter_rest(c, k); })) return rc;
+            if (ver) {
+                if (int rc = ver_anorm(c0, k)) return rc;
+                if (int rc = ver_snapshot(c0, k + 1, c0->Dblk[(k + 1) & 1])) return rc;
+            }
         }
         if (int rc = each(ctx, X, join_rank)) return rc;
         if (int rc = on0()) return rc;
@@ -2324,6 +2459,8 @@ int coopcg_gpu_begin(coopcg_gpu_ctx* ctx, const coopcg_opts* opts) {
     if (is_group(ctx))
         return fail(ctx, COOPCG_E_STATE, "a multi-device handle runs whole solves (coopcg_gpu_run / _solve)");
     if (!ctx) return COOPCG_E_INVALID;
+    if (ctx->ver_hist_on || ctx->ver_xs_on)
+        return fail(ctx, COOPCG_E_INVALID, "verification mode (keep_history / x_star) runs whole solves (coopcg_gpu_run)");
     CK(cudaSetDevice(ctx->device));
     return begin_impl(ctx, opts);
 }
@@ -2491,6 +2628,63 @@ int coopcg_gpu_solve(coopcg_gpu_ctx* ctx, const double* b, const double* X0, con
                      coopcg_trace* trace) {
     if (int rc = coopcg_gpu_upload(ctx, b, X0)) return rc;
     return coopcg_gpu_run(ctx, opts, trace);
+}
+
+int coopcg_gpu_set_verification(coopcg_gpu_ctx* ctx, int keep_history, const double* x_star) {
+    if (!ctx) return COOPCG_E_INVALID;
+    if ((keep_history || x_star) && (is_group(ctx) || sharded(ctx) || ctx->nccl))
+        return fail(ctx, COOPCG_E_INVALID,
+                    "verification mode (keep_history / x_star) needs one context holding every row of A");
+    CK(cudaSetDevice(ctx->device));
+    ctx->ver_hist_on = keep_history != 0;
+    ctx->ver_xs_on = x_star != nullptr;
+    ctx->ver_iters = -1;
+    if (x_star) {
+        if (!ctx->ver_xs) CK(gmalloc(ctx, &ctx->ver_xs, sizeof(double) * (size_t)ctx->n, "ver_xs"));
+        CK(cudaMemcpyAsync(ctx->ver_xs, x_star, sizeof(double) * (size_t)ctx->n, cudaMemcpyHostToDevice, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_history_count(const coopcg_gpu_ctx* ctx, int* entries) {
+    if (!ctx || !entries) return COOPCG_E_INVALID;
+    *entries = (ctx->ver_hist_on && ctx->ver_iters >= 0) ? ctx->ver_iters + 1 : 0;
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_get_history(coopcg_gpu_ctx* ctx, int entry, double* X, double* R, double* D) {
+    if (!ctx) return COOPCG_E_INVALID;
+    if (!ctx->ver_hist_on || ctx->ver_iters < 0)
+        return fail(ctx, COOPCG_E_STATE, "no history: run a solve after coopcg_gpu_set_verification(ctx, 1, ...)");
+    if (entry < 0 || entry > ctx->ver_iters || entry >= ctx->ver_hist_cap)
+        return fail(ctx, COOPCG_E_INVALID, "history entry %d outside [0, %d]", entry, ctx->ver_iters);
+    CK(cudaSetDevice(ctx->device));
+    const int n = ctx->n, p = ctx->p_orig, P = ctx->P;
+    const size_t blk = (size_t)n * P;
+    double* outs[3] = {X, R, D};
+    for (int b = 0; b < 3; ++b) {
+        if (!outs[b]) continue;
+        rowmajor_to_colmajor_kernel<<<grid_for((size_t)n * p, 256), 256, 0, ctx->stream>>>(
+            ctx->ver_hist + ((size_t)entry * 3 + b) * blk, ctx->stage, n, p, P);
+        CKL();
+        CK(cudaMemcpyAsync(outs[b], ctx->stage, sizeof(double) * (size_t)n * p, cudaMemcpyDeviceToHost, ctx->stream));
+        CK(cudaStreamSynchronize(ctx->stream));
+    }
+    return COOPCG_OK;
+}
+
+int coopcg_gpu_get_anorm_errors(coopcg_gpu_ctx* ctx, int capacity, double* out) {
+    if (!ctx || !out) return COOPCG_E_INVALID;
+    if (!ctx->ver_xs_on || ctx->ver_iters < 0)
+        return fail(ctx, COOPCG_E_STATE, "no A-norm errors: run a solve after coopcg_gpu_set_verification(ctx, ., x_star)");
+    const int rows = std::min({capacity, ctx->ver_iters, ctx->ver_anorm_cap});
+    if (rows <= 0) return COOPCG_OK;
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpyAsync(out, ctx->ver_anorm, sizeof(double) * (size_t)rows * ctx->p_orig, cudaMemcpyDeviceToHost,
+                       ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    return COOPCG_OK;
 }
 
 int coopcg_gpu_timing(const coopcg_gpu_ctx* ctx, coopcg_timing* out) {

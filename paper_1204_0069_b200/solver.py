@@ -68,6 +68,9 @@ class SolveOptions:
     recompute_residual_every: int = -1
     rank_rel_tol: float = 1e-10
     algo: str = "ccg"  # "ccg" (ccg_solve) | "mccg" (mccg_solve, solvers.hpp:338-342) | "sd" (internal)
+    # verification mode (trace.hpp:86-87): retain X_k, R_k, D_k; record A-norm errors against x_star
+    keep_history: bool = False
+    x_star: Optional[np.ndarray] = None
 
     def to_c(self) -> _capi.coopcg_opts:
         o = _capi.coopcg_opts()
@@ -98,6 +101,7 @@ class IterationRecord:
     mults: int
     mults_per_worker: List[int]
     wall_ns: int
+    anorm_errors: Optional[np.ndarray] = None  # per agent ||x_j - x*||_A when SolveOptions.x_star is set
 
 
 @dataclass
@@ -119,6 +123,10 @@ class SolveTrace:
     minres: np.ndarray = field(default=None)
     wall_ns: np.ndarray = field(default=None)
     exact_rank_checks: int = 0
+    # keep_history: entry 0 is the initial block, entry k + 1 the state after iteration k (trace.hpp:66-70)
+    history_x: List[np.ndarray] = field(default_factory=list)
+    history_r: List[np.ndarray] = field(default_factory=list)
+    history_d: List[np.ndarray] = field(default_factory=list)
 
     def iteration_count(self) -> int:
         return len(self.iterations)
@@ -274,10 +282,45 @@ class GpuContext:
         tr.final_residual_norms = _dp(fres)
         tr.final_x = _dp(fx) if want_x else C.POINTER(C.c_double)()
         co = opts.to_c()
+        self._set_verification(opts)
         rc = _capi.lib().coopcg_gpu_run(self._h, C.byref(co), C.byref(tr))
         _check(self._h, rc)
         _capi.lib().coopcg_gpu_timing(self._h, C.byref(self._timing))
-        return self._make_trace(tr, norms, minres, wall, init, fres, fx, opts, act)
+        t = self._make_trace(tr, norms, minres, wall, init, fres, fx, opts, act)
+        self._read_verification(opts, t)
+        return t
+
+    def _set_verification(self, opts: SolveOptions) -> None:
+        """SolveOptions.keep_history / x_star -> coopcg_gpu_set_verification (sticky per context)."""
+        want = bool(opts.keep_history) or opts.x_star is not None
+        if not want and not getattr(self, "_ver_on", False):
+            return
+        xs = None
+        if opts.x_star is not None:
+            xs = np.ascontiguousarray(opts.x_star, dtype=np.float64)
+            if xs.shape != (self.n,):
+                raise DimensionError("solver: operand shapes do not match the system matrix")
+        _check(self._h, _capi.lib().coopcg_gpu_set_verification(
+            self._h, 1 if opts.keep_history else 0, xs.ctypes.data if xs is not None else None))
+        self._ver_on = want
+
+    def _read_verification(self, opts: SolveOptions, t: "SolveTrace") -> None:
+        L = _capi.lib()
+        n, p, it = self.n, self.p, t.iteration_count()
+        if opts.x_star is not None and it > 0:
+            an = np.zeros((it, p))
+            _check(self._h, L.coopcg_gpu_get_anorm_errors(self._h, it, an.ctypes.data))
+            for rec in t.iterations:
+                rec.anorm_errors = an[rec.k].copy()
+        if opts.keep_history:
+            cnt = C.c_int()
+            _check(self._h, L.coopcg_gpu_history_count(self._h, C.byref(cnt)))
+            for e in range(cnt.value):
+                bufs = [np.zeros((p, n)) for _ in range(3)]
+                _check(self._h, L.coopcg_gpu_get_history(self._h, e, *(b.ctypes.data for b in bufs)))
+                t.history_x.append(bufs[0].T.copy())
+                t.history_r.append(bufs[1].T.copy())
+                t.history_d.append(bufs[2].T.copy())
 
     def run_raw(self, opts: Optional[SolveOptions] = None) -> tuple:
         """One solve through coopcg_gpu_run with reusable trace buffers and no

@@ -79,6 +79,45 @@ def test_fast_fused_iteration_matches_separate_kernels():
             assert np.max(np.linalg.norm(a - b, axis=0) / np.linalg.norm(b, axis=0)) < 1e-12, (key, extra)
 
 
+FAST_BITS_SCRIPT = r"""
+import json, numpy as np, paper_1204_0069_b200 as m
+out = {}
+for n, p in ((700, 8), (1300, 4)):
+    with m.GpuContext(n, p, arith="fast") as ctx:
+        ctx.gen_A("diagdom", n)
+        b = m.gen_rhs(n, "uniform", n); X0 = m.gen_starts(n, p, n)
+        ctx.upload(b, X0)
+        t = ctx.run(m.SolveOptions(tol=0.0, max_iters=25, recompute_residual_every=9))
+        res = ctx.timing()["a_l2_resident_bytes"]
+    out[f"{n}_{p}"] = {"x": t.final_x.tobytes().hex(), "norms": t.residual_norms.tobytes().hex(),
+                       "it": t.iteration_count()}
+    out[f"res_{n}_{p}"] = res
+print(json.dumps(out))
+"""
+
+
+def test_fast_ad_shapes_and_l2_residency_bitwise():
+    """The fast A.D's consumer-warp shape (2 or 4 M-tiles per DMMA warp,
+    COOPCG_FAST_MT) and the L2-resident share of A (COOPCG_L2_RES_MB; evict-last
+    copies of the first k-tiles of every work unit) change scheduling and cache
+    policy only: the fast-mode solve is the same bytes."""
+    def run(extra):
+        env = dict(os.environ, **extra)
+        r = subprocess.run([sys.executable, "-c", FAST_BITS_SCRIPT], cwd=ROOT, env=env, capture_output=True,
+                           text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return json.loads(r.stdout.strip().splitlines()[-1])
+    base = run({"COOPCG_FAST_MT": "4", "COOPCG_L2_RES_MB": "0"})
+    assert base["res_700_8"] == 0 and base["700_8"]["it"] == 25
+    for extra in ({}, {"COOPCG_FAST_MT": "2"}, {"COOPCG_FAST_MT": "2", "COOPCG_L2_RES_MB": "8"},
+                  {"COOPCG_FAST_MT": "4", "COOPCG_L2_RES_MB": "4"}):
+        got = run(extra)
+        if "COOPCG_L2_RES_MB" in extra:
+            assert got["res_700_8"] > 0 and got["res_1300_4"] > 0, extra  # the knob took effect
+        for key in ("700_8", "1300_4"):
+            assert got[key] == base[key], (key, extra)
+
+
 GUARD_SCRIPT = r"""
 import ctypes as C, numpy as np, paper_1204_0069_b200 as m
 from paper_1204_0069_b200 import _capi
