@@ -13,9 +13,11 @@ in and the host final X + trace out, every step; `e2e_oneshot` = the one-shot
 drop-in ccg_solve(A, b, X0) with A itself uploaded from host memory every call
 (what a caller of the reference's ccg_solve does once per system).
 `roofline` describes Q = A.D against the north star's bound
-max(8 n^2 / HBM, 2 n^2 p / FP64).  The line also carries `configs.cfg4` (n =
-131072, p = 32, A = 137 GB on one GPU, 50 fixed iterations), the north star's
-single-GPU target, in both arithmetic modes.
+max(8 n^2 / HBM, 2 n^2 p / FP64).  The metric is quoted "vs n, p", so the line
+also carries `configs`: every other BASELINE config in both arithmetic modes
+-- cfg 4 (n = 131072, p = 32, A = 137 GB on one GPU, 50 fixed iterations: the
+north star's single-GPU target), cfg 3 (n = 65536, p = 16, Householder kappa =
+1e6, 100 iterations), and on one GPU cfg 0 / cfg 1 (solves to 1e-10 ||b||).
 
 --impl reference times the reference's own CPU implementation
 (parallel_ccg, compiled from the unmodified reference headers into
@@ -482,18 +484,29 @@ def run_ours(args, cfg):
         line[other]["unit"] = "iterations/s"
     if big_ok and not args.no_oneshot:
         line["e2e_oneshot"] = _oneshot_e2e(m, torch, cfg, args.arith, max(1, min(args.steps, 3)), args.device)
-    if not args.no_big and cfg.idx != 4:
-        big = Cfg(4)
-        line["configs"] = {"cfg4": {"config": config_dict(big), "modes": {}}}
-        for arith in ("exact", "fast"):
-            r, _ = _measure(m, torch, big, args, arith, args.big_steps, args.warmup, ctx_kw, e2e=True,
-                            clock_dev=clock_dev, barrier=barrier, reduce_max=reduce_max)
-            r["unit"] = "iterations/s"
-            line["configs"]["cfg4"]["modes"][arith] = r
-        line["configs"]["cfg4"]["cpu_reference"] = (
-            "not run by default (137 GB host copy of A; ~50 s per iteration with the reference's 32 threads "
-            "on 16 cores): measured per iteration by tests/test_gpu_full_configs.py "
-            "(profiles/r02_full_config_parity.json)")
+    if not args.no_big:
+        # The metric is quoted "vs n, p": the same line carries every other BASELINE
+        # config, timed the same way in both modes -- the north star's single-GPU
+        # target (cfg 4: n = 131072, p = 32, A = 137 GB) and cfg 3 (n = 65536) with
+        # --big-steps timed solves each, the small configs (cfg 0 / 1) with --steps.
+        line["configs"] = {}
+        for idx in ((0, 1, 3, 4) if big_ok else (3, 4)):  # multi-GPU runs: the sharded configs only
+            if idx == cfg.idx:
+                continue
+            other_cfg = Cfg(idx)
+            obj = {"config": config_dict(other_cfg), "modes": {}}
+            for arith in ("exact", "fast"):
+                r, _ = _measure(m, torch, other_cfg, args, arith, args.big_steps if idx >= 3 else args.steps,
+                                args.warmup, ctx_kw, e2e=True, clock_dev=clock_dev, barrier=barrier,
+                                reduce_max=reduce_max)
+                r["unit"] = "iterations/s"
+                obj["modes"][arith] = r
+            if idx >= 3:
+                obj["cpu_reference"] = (
+                    "not run by bench.py (a 34 / 137 GB host copy of A; 4 / 42 s per iteration with the "
+                    "reference's one thread per agent on 16 cores): measured per iteration by "
+                    "tests/test_gpu_full_configs.py (profiles/r02_full_config_parity.json)")
+            line["configs"][f"cfg{idx}"] = obj
     if not args.no_cpu_baseline and rank == 0:
         runs = cpu_reference_run(cfg, args.cpu_iters)
         walls, kind, cores = runs["parallel"]
@@ -521,8 +534,8 @@ def main():
     ap.add_argument("--device", type=int, default=int(os.environ.get("LOCAL_RANK", "0")))
     ap.add_argument("--cpu-iters", type=int, default=8)
     ap.add_argument("--serial-iters", type=int, default=3, help="reference arm: serial ccg_solve sample (cfg <= 2)")
-    ap.add_argument("--big-steps", type=int, default=2, help="timed 50-iteration solves of the cfg4 object")
-    ap.add_argument("--no-big", action="store_true", help="skip the cfg4 (n = 131072) object")
+    ap.add_argument("--big-steps", type=int, default=2, help="timed solves of the cfg3 / cfg4 objects")
+    ap.add_argument("--no-big", action="store_true", help="skip the other BASELINE configs (the `configs` object)")
     ap.add_argument("--no-oneshot", action="store_true", help="skip the one-shot e2e (A uploaded every call)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the other arithmetic mode")
