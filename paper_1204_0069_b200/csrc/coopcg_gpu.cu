@@ -1169,7 +1169,14 @@ int coopcg_gpu_create_shard(int n, int p, int device, int arith, int row_begin, 
         }();
         const int rg = rg_env > 0 ? std::min(rg_env, kMaxParts)
                                   : ((ctx->P <= 8) ? 128 : (ctx->P == 16 ? 192 : 296));
-        ctx->f_rgrid = std::min(rg, (ctx->n_loc + TR - 1) / TR);
+        // The row-pass grid fixes how the Gram partials are grouped, i.e. the rounding
+        // of every p x p Gram.  On a row shard the Grams are summed over the full
+        // replicated blocks and every shard must get the SAME bits (alpha, beta and
+        // with them the replicated X, R, D must not drift apart between shards -- a
+        // drift of one ulp grows ~100x per iteration once it starts: fast-mode solves
+        // on unequal shards diverged after ~20 iterations, tools/fuzz_parity.py), so
+        // the grid depends on n, not on the shard's own row count.
+        ctx->f_rgrid = std::min(rg, (n + TR - 1) / TR);
         ctx->f_ugrid = std::min(rg, (n + TR - 1) / TR);
         if (ctx->n_loc == n) {
             // single GPU (the fused iteration kernel): the smallest rows-per-thread

@@ -119,6 +119,32 @@ def test_multi_fast_within_tolerance(m, po, n, p, ndev):
     assert rel.max() < 1e-8
 
 
+@pytest.mark.parametrize("n,p,ndev,m_refl,kappa,recompute", [(288, 4, 2, 3, 3.3e3, -1), (288, 4, 3, 3, 3.3e3, -1),
+                                                             (513, 9, 3, 8, 4.5e2, 0)])
+def test_multi_fast_long_run_on_unequal_shards(m, po, n, p, ndev, m_refl, kappa, recompute):
+    """Fast mode over UNEQUAL row shards for hundreds of iterations (a case of
+    tools/fuzz_parity.py): every shard must sum the replicated Grams in the same
+    grouping, or alpha / beta -- and with them the replicated X, R, D -- drift
+    apart between the shards and the solve diverges after ~20 iterations (the
+    row-pass grid used to depend on the shard's own row count)."""
+    A = po.gen_householder(n, m_refl, kappa, 1600630417)
+    b = po.gen_rhs(n, "normal", 1600630417)
+    X0 = po.gen_starts(n, p, 1600630417)
+    tol = 2.4e-10 * po.seq_norm(b)
+    opts = m.SolveOptions(tol=tol, recompute_residual_every=recompute)
+    ref = po.oracle_ccg(A, b, X0, tol=tol, recompute=recompute)
+    one = m.ccg_solve(A, b, X0, opts, m.GpuOptions(arith="fast"))
+    gt = m.ccg_solve(A, b, X0, opts, m.GpuOptions(arith="fast", devices=[0] * ndev))
+    assert ref.status == "converged" and ref.iterations > 60
+    assert str(one.status) == str(gt.status) == "converged"
+    assert abs(gt.iteration_count() - ref.iterations) <= max(4, ref.iterations // 20)
+    assert abs(one.iteration_count() - ref.iterations) <= max(4, ref.iterations // 20)
+    rel = np.linalg.norm(gt.final_x - ref.final_x, axis=0) / np.linalg.norm(ref.final_x, axis=0)
+    assert rel.max() < 10 * kappa * 2.4e-10  # both within kappa * tol of the solution
+    again = m.ccg_solve(A, b, X0, opts, m.GpuOptions(arith="fast", devices=[0] * ndev))
+    assert np.array_equal(again.residual_norms, gt.residual_norms)  # deterministic
+
+
 def test_multi_rejects_bad_splits(m):
     with pytest.raises(m.DimensionError):
         m.GpuContext(3, 1, devices=[0, 0, 0, 0])

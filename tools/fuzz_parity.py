@@ -1,0 +1,176 @@
+#!/usr/bin/env python3
+"""Randomised parity sweep on the GPU box (test infrastructure, not product).
+
+Draws solver cases -- n (biased to the panel / tile / wave boundaries of the
+kernels), p in 1..32, matrix family, stopping rule, residual-recompute policy,
+algorithm (ccg / mccg), one context or 2-3 row shards -- and compares the
+device solve with the compiled reference (oracle/_ref/libccgref.so):
+
+  exact mode: bit for bit (status, iteration count, converged agent, every
+              per-iteration per-agent norm, final X, true final residuals,
+              and the error class when the reference throws);
+  fast mode:  final X within 1e-8 relative when both converge, iteration
+              count within +-2 on the diagonally dominant family, same status.
+
+    python tools/fuzz_parity.py --seconds 300 --seed 1 [--out gpurun_out/fuzz.json]
+
+Every case is reproducible from the printed (seed, index).
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+os.environ.setdefault("OMP_WAIT_POLICY", "passive")
+
+EDGES = [31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 287, 288, 289, 511, 512, 513, 1023, 1024, 1025]
+
+
+def draw_case(rng, multi=False):
+    p = int(rng.choice([1, 2, 3, 4, 5, 7, 8, 9, 12, 15, 16, 17, 24, 31, 32]))
+    kind = rng.choice(["edge", "small", "mid"], p=[0.4, 0.3, 0.3])
+    if kind == "edge":
+        n = int(rng.choice(EDGES)) + int(rng.integers(-1, 2))
+    elif kind == "small":
+        n = int(rng.integers(p + 1, 200))
+    else:
+        n = int(rng.integers(200, 2600))
+    n = max(n, p + 1, 2)
+    matrix = str(rng.choice(["diagdom", "householder", "random_spd"], p=[0.5, 0.3, 0.2]))
+    if matrix == "random_spd" and n > 700:
+        matrix = "diagdom"  # the reference's O(n^3) generator
+    kappa = float(10 ** rng.uniform(0.5, 4.5))
+    m = int(rng.integers(1, 9))
+    fixed = bool(rng.random() < 0.4)
+    max_iters = int(rng.integers(0, 45)) if fixed else -1
+    tol_rel = 0.0 if fixed else float(10 ** rng.uniform(-12, -6))
+    recompute = int(rng.choice([-1, 0, 1, 2, 3, 7, 50]))
+    algo = str(rng.choice(["ccg", "mccg"], p=[0.8, 0.2]))
+    shards = int(rng.choice([1, 1, 2, 3])) if n >= 200 else 1
+    if multi:  # --multi: row shards only, long ill-conditioned runs
+        n = max(n, 200)
+        shards = int(rng.choice([2, 3, 4]))
+        matrix = "householder" if rng.random() < 0.8 else "diagdom"
+        algo = "ccg"
+    degenerate = bool(rng.random() < 0.06) and p > 1
+    return dict(n=n, p=p, matrix=matrix, kappa=kappa, m=m, max_iters=max_iters, tol_rel=tol_rel,
+                recompute=recompute, algo=algo, shards=shards, degenerate=degenerate,
+                seed=int(rng.integers(1, 2**31)))
+
+
+def cost(c):
+    its = c["max_iters"] if c["max_iters"] >= 0 else min(2 * c["n"], 400)
+    return float(c["n"]) ** 2 * c["p"] * max(its, 1)
+
+
+def run_case(m, po, c, arith):
+    n, p = c["n"], c["p"]
+    if c["matrix"] == "diagdom":
+        A = po.gen_diagdom(n, c["seed"])
+        b = po.gen_rhs(n, "uniform", c["seed"])
+    elif c["matrix"] == "householder":
+        A = po.gen_householder(n, c["m"], c["kappa"], c["seed"])
+        b = po.gen_rhs(n, "normal", c["seed"])
+    else:
+        A, b, _ = po.ref_make_problem(n, p, c["kappa"], c["seed"])
+    X0 = po.gen_starts(n, p, c["seed"])
+    if c["degenerate"]:
+        X0[:, -1] = X0[:, 0]  # duplicate start: rank-deficient D0 (ccg: collapse at k = 0; mccg restricts)
+    tol = c["tol_rel"] * po.seq_norm(b)
+    ref = po.ref_solve(A, b, X0, tol=tol, max_iters=c["max_iters"], recompute=c["recompute"], algo=c["algo"])
+    opts = m.SolveOptions(tol=tol, max_iters=c["max_iters"], recompute_residual_every=c["recompute"],
+                          algo=c["algo"])
+    gpu = m.GpuOptions(arith=arith, devices=[0] * c["shards"] if c["shards"] > 1 else None)
+    try:
+        t = m.ccg_solve(A, b, X0, opts, gpu)
+        err = None
+    except m.Error as ex:
+        t, err = None, ex
+    if ref.rc != 0 or err is not None:
+        # the reference threw: same class of failure (pyoracle rc: 2 SPD violation, 3 breakdown)
+        want = {2: m.SpdViolationError, 3: m.NumericalBreakdownError}.get(ref.rc)
+        if arith == "exact":
+            if want is None or not isinstance(err, want):
+                return f"error mismatch: reference rc={ref.rc} ({ref.error!r}), device {err!r}"
+        return None
+    if arith == "exact":
+        if str(t.status) != ref.status or t.iteration_count() != ref.iterations:
+            return f"status/iterations {t.status}/{t.iteration_count()} vs {ref.status}/{ref.iterations}"
+        if t.converged_agent != ref.converged_agent:
+            return "converged agent"
+        if not np.array_equal(t.residual_norms, ref.residual_norms, equal_nan=True):
+            return "per-iteration norms differ"
+        if list(t.active_agents) != list(ref.extra["active_agents"]):
+            return "active agents differ"
+        act = list(t.active_agents)
+        if not np.array_equal(t.final_x, ref.final_x[:, act], equal_nan=True):
+            return "final X differs"
+        if not np.array_equal(t.final_residual_norms, ref.final_residual_norms[act], equal_nan=True):
+            return "final residual norms differ"
+        return None
+    # fast mode (the north star's tolerances); mccg restrictions and rank-collapse exits depend
+    # on rounding-level rank decisions, so only converged ccg runs are held to them -- and only
+    # while the block Krylov space is not exhausted (iterations * p well below n: past that the
+    # direction block loses rank in exact arithmetic and the exit is decided by rounding)
+    if c["algo"] != "ccg" or ref.status != "converged" or ref.iterations * c["p"] > 0.8 * c["n"]:
+        return None
+    if str(t.status) != "converged":
+        return f"fast status {t.status} vs converged"
+    rel = float(np.max(np.linalg.norm(t.final_x - ref.final_x, axis=0) /
+                       np.maximum(np.linalg.norm(ref.final_x, axis=0), 1e-300)))
+    cond = c["kappa"] if c["matrix"] != "diagdom" else 2.0
+    if rel > max(1e-8, 10 * cond * c["tol_rel"]):
+        return f"fast X rel diff {rel:.2e} (cond {cond:.1e}, tol_rel {c['tol_rel']:.1e})"
+    if c["matrix"] == "diagdom" and abs(t.iteration_count() - ref.iterations) > 2:
+        return f"fast iterations {t.iteration_count()} vs {ref.iterations}"
+    return None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--seconds", type=float, default=300.0)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--max-cost", type=float, default=3e9)
+    ap.add_argument("--multi", action="store_true", help="row-sharded cases only (2-4 shards), mostly Householder")
+    ap.add_argument("--out", default="")
+    args = ap.parse_args()
+    import paper_1204_0069_b200 as m
+    import pyoracle as po
+    rng = np.random.default_rng(args.seed)
+    t0 = time.time()
+    done = {"exact": 0, "fast": 0}
+    failures = []
+    idx = 0
+    while time.time() - t0 < args.seconds:
+        c = draw_case(rng, args.multi)
+        idx += 1
+        if cost(c) > args.max_cost:
+            continue
+        for arith in ("exact", "fast"):
+            if arith == "fast" and c["algo"] == "mccg" and c["shards"] > 1:
+                continue
+            try:
+                why = run_case(m, po, c, arith)
+            except Exception as ex:  # a crash is a failure of the case, not of the sweep
+                why = f"exception {type(ex).__name__}: {ex}"
+            done[arith] += 1
+            if why:
+                failures.append({"index": idx, "arith": arith, "case": c, "why": why})
+                print(f"FAIL #{idx} {arith} {c}: {why}", flush=True)
+    res = {"seed": args.seed, "seconds": round(time.time() - t0, 1), "cases_drawn": idx, "solves": done,
+           "failures": failures}
+    print(json.dumps({k: v for k, v in res.items() if k != "failures"}), f"failures={len(failures)}")
+    if args.out:
+        with open(args.out, "w") as f:
+            json.dump(res, f, indent=1)
+    return 1 if failures else 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())
