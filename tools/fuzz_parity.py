@@ -32,9 +32,16 @@ os.environ.setdefault("OMP_WAIT_POLICY", "passive")
 EDGES = [31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 287, 288, 289, 511, 512, 513, 1023, 1024, 1025]
 
 
-def draw_case(rng, multi=False):
+def draw_case(rng, multi=False, large=False):
     p = int(rng.choice([1, 2, 3, 4, 5, 7, 8, 9, 12, 15, 16, 17, 24, 31, 32]))
     kind = rng.choice(["edge", "small", "mid"], p=[0.4, 0.3, 0.3])
+    if large:  # --large: the A.D variants picked above 148 * 64 local rows, a few iterations each
+        p = int(rng.choice([3, 4, 7, 8, 13, 16, 24, 32]))
+        n = int(rng.choice([9471, 9472, 9473, 9600, 10240, 11000, 12289])) + int(rng.integers(-1, 2))
+        return dict(n=n, p=p, matrix=str(rng.choice(["diagdom", "householder"])), kappa=float(10 ** rng.uniform(1, 4)),
+                    m=int(rng.integers(1, 5)), max_iters=int(rng.integers(1, 4)), tol_rel=0.0,
+                    recompute=int(rng.choice([-1, 1, 2])), algo="ccg", shards=int(rng.choice([1, 1, 2])),
+                    degenerate=False, seed=int(rng.integers(1, 2**31)))
     if kind == "edge":
         n = int(rng.choice(EDGES)) + int(rng.integers(-1, 2))
     elif kind == "small":
@@ -132,12 +139,113 @@ def run_case(m, po, c, arith):
     return None
 
 
+def run_session_fast(m, po, rng):
+    """Fast mode: 3-5 solves on one resident context (ccg / mccg, changing options) must
+    each equal, bit for bit, the same solve on a fresh context -- nothing may carry over."""
+    p = int(rng.choice([1, 2, 3, 4, 6, 8, 9, 16, 17, 32]))
+    n = int(rng.integers(max(p + 2, 20), 700))
+    seed = int(rng.integers(1, 2**31))
+    A = po.gen_diagdom(n, seed) if rng.random() < 0.5 else po.gen_householder(
+        n, int(rng.integers(1, 6)), float(10 ** rng.uniform(0.5, 3.0)), seed)
+    shards = int(rng.choice([1, 1, 2, 3])) if n >= 200 else 1
+    gpu = m.GpuOptions(arith="fast", devices=[0] * shards if shards > 1 else None)
+    log = []
+    with m.GpuContext(n, p, arith="fast", devices=gpu.devices) as ctx:
+        ctx.set_A(A)
+        for step in range(int(rng.integers(3, 6))):
+            s2 = int(rng.integers(1, 2**31))
+            b = po.gen_rhs(n, "uniform", s2)
+            X0 = po.gen_starts(n, p, s2)
+            if p > 1 and rng.random() < 0.25:
+                X0[:, -1] = X0[:, 0]
+            fixed = rng.random() < 0.5
+            opts = m.SolveOptions(tol=0.0 if fixed else float(10 ** rng.uniform(-10, -6)) * po.seq_norm(b),
+                                  max_iters=int(rng.integers(0, 70)) if fixed else -1,
+                                  recompute_residual_every=int(rng.choice([-1, 0, 1, 3, 7])),
+                                  algo="mccg" if (rng.random() < 0.3 and shards == 1) else "ccg")
+            log.append(dict(step=step, n=n, p=p, shards=shards, seed=s2, max_iters=opts.max_iters, tol=opts.tol,
+                            rec=opts.recompute_residual_every, algo=opts.algo))
+            res = []
+            for fresh in (False, True):
+                try:
+                    t = m.ccg_solve(A, b, X0, opts, gpu) if fresh else ctx.solve(b, X0, opts)
+                    res.append((str(t.status), t.iteration_count(), t.residual_norms.tobytes(), t.final_x.tobytes()))
+                except m.Error as ex:
+                    res.append((type(ex).__name__, str(ex)))
+            if res[0] != res[1]:
+                return f"{log}: resident {res[0][:2]} vs fresh {res[1][:2]}"
+    return None
+
+
+def run_session(m, po, rng):
+    """3-6 solves on one resident context: new b / X0, ccg / mccg, growing and shrinking
+    max_iters, every recompute policy, verification mode on and off, both arithmetic
+    modes' contexts -- each exact solve bit for bit against the reference."""
+    p = int(rng.choice([1, 2, 3, 4, 6, 8, 9, 16, 17, 32]))
+    n = int(rng.integers(max(p + 2, 20), 500))
+    seed = int(rng.integers(1, 2**31))
+    if rng.random() < 0.5:
+        A = po.gen_diagdom(n, seed)
+    else:
+        A = po.gen_householder(n, int(rng.integers(1, 6)), float(10 ** rng.uniform(0.5, 3.5)), seed)
+    shards = int(rng.choice([1, 1, 1, 2])) if n >= 200 else 1
+    log = []
+    with m.GpuContext(n, p, devices=[0] * shards if shards > 1 else None) as ctx:
+        ctx.set_A(A)
+        for step in range(int(rng.integers(3, 7))):
+            s2 = int(rng.integers(1, 2**31))
+            b = po.gen_rhs(n, "uniform" if rng.random() < 0.5 else "normal", s2)
+            X0 = po.gen_starts(n, p, s2)
+            if p > 1 and rng.random() < 0.25:
+                X0[:, -1] = X0[:, 0]
+            fixed = rng.random() < 0.5
+            max_iters = int(rng.integers(0, 60)) if fixed else -1
+            tol = 0.0 if fixed else float(10 ** rng.uniform(-11, -6)) * po.seq_norm(b)
+            rec = int(rng.choice([-1, 0, 1, 3, 7]))
+            algo = "mccg" if rng.random() < 0.3 else "ccg"
+            verify = shards == 1 and algo == "ccg" and rng.random() < 0.3 and (max_iters >= 0 or n <= 200)
+            xs = np.linalg.solve(A, b) if verify else None
+            log.append(dict(step=step, n=n, p=p, shards=shards, seed=s2, max_iters=max_iters, tol=tol, rec=rec,
+                            algo=algo, verify=bool(verify)))
+            ref = po.ref_solve(A, b, X0, tol=tol, max_iters=max_iters, recompute=rec, algo=algo)
+            opts = m.SolveOptions(tol=tol, max_iters=max_iters, recompute_residual_every=rec, algo=algo,
+                                  keep_history=bool(verify), x_star=xs)
+            try:
+                t = ctx.solve(b, X0, opts)
+                err = None
+            except m.Error as ex:
+                t, err = None, ex
+            if ref.rc != 0 or err is not None:
+                want = {2: m.SpdViolationError, 3: m.NumericalBreakdownError}.get(ref.rc)
+                if want is None or not isinstance(err, want):
+                    return f"{log}: error mismatch: reference rc={ref.rc} ({ref.error!r}), device {err!r}"
+                continue
+            act = list(t.active_agents)
+            ok = (str(t.status) == ref.status and t.iteration_count() == ref.iterations and
+                  np.array_equal(t.residual_norms, ref.residual_norms, equal_nan=True) and
+                  act == list(ref.extra["active_agents"]) and
+                  np.array_equal(t.final_x, ref.final_x[:, act], equal_nan=True) and
+                  np.array_equal(t.final_residual_norms, ref.final_residual_norms[act], equal_nan=True))
+            if not ok:
+                return f"{log}: solve differs from the reference ({t.status}/{t.iteration_count()} vs {ref.status}/{ref.iterations})"
+            if verify:
+                if len(t.history_x) != t.iteration_count() + 1 or not np.array_equal(t.history_x[-1], t.final_x):
+                    return f"{log}: history entries"
+                if t.iteration_count() and t.iterations[-1].anorm_errors is None:
+                    return f"{log}: anorm missing"
+    return None
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seconds", type=float, default=300.0)
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--max-cost", type=float, default=3e9)
     ap.add_argument("--multi", action="store_true", help="row-sharded cases only (2-4 shards), mostly Householder")
+    ap.add_argument("--large", action="store_true", help="n around 9472..12290 (the large-n A.D variants), 1-3 iterations")
+    ap.add_argument("--session", nargs="?", const="exact", default="", choices=["exact", "fast"],
+                    help="several solves with changing options on ONE resident context (state carried between "
+                         "solves): exact against the reference, fast against the same solve on a fresh context")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
     import paper_1204_0069_b200 as m
@@ -148,7 +256,15 @@ def main():
     failures = []
     idx = 0
     while time.time() - t0 < args.seconds:
-        c = draw_case(rng, args.multi)
+        if args.session:
+            idx += 1
+            why = run_session_fast(m, po, rng) if args.session == "fast" else run_session(m, po, rng)
+            done["exact"] += 1
+            if why:
+                failures.append({"index": idx, "arith": "session", "why": why})
+                print(f"FAIL session #{idx}: {why}", flush=True)
+            continue
+        c = draw_case(rng, args.multi, args.large)
         idx += 1
         if cost(c) > args.max_cost:
             continue
