@@ -31,7 +31,7 @@ def m():
     return mod
 
 
-@pytest.mark.parametrize("seed,multi,cases", [(11, False, 60), (12, True, 25)])
+@pytest.mark.parametrize("seed,multi,cases", [(11, False, 300), (12, True, 100)])
 def test_random_cases_match_the_reference(m, po, fz, seed, multi, cases):
     rng = np.random.default_rng(seed)
     ran = 0
@@ -49,9 +49,9 @@ def test_random_cases_match_the_reference(m, po, fz, seed, multi, cases):
 
 def test_random_sessions_on_a_resident_context(m, po, fz):
     rng = np.random.default_rng(13)
-    for _ in range(25):
+    for _ in range(100):
         why = fz.run_session(m, po, rng)
         assert why is None, why
-    for _ in range(15):
+    for _ in range(60):
         why = fz.run_session_fast(m, po, rng)
         assert why is None, why
