@@ -139,6 +139,80 @@ def run_case(m, po, c, arith):
     return None
 
 
+def run_misc(m, po, rng):
+    """The other entry points on random shapes, bit for bit: the scalar solvers against the
+    reference's cg_solve / steepest_descent_solve, the device generators against the oracle's,
+    matvec_block and numerical_rank (certificate and forced-exact paths) against the reference."""
+    what = str(rng.choice(["cg", "sd", "gen", "matvec", "rank"]))
+    seed = int(rng.integers(1, 2**31))
+    if what in ("cg", "sd"):
+        n = int(rng.integers(3, 400))
+        A = po.gen_diagdom(n, seed) if rng.random() < 0.4 else po.gen_householder(
+            n, int(rng.integers(1, 6)), float(10 ** rng.uniform(0.3, 3.5)), seed)
+        b = po.gen_rhs(n, "normal", seed)
+        x0 = po.gen_starts(n, 1, seed)[:, 0] if rng.random() < 0.7 else np.zeros(n)
+        fixed = rng.random() < 0.4
+        mi = int(rng.integers(0, 50)) if fixed else -1
+        tol = 0.0 if fixed else float(10 ** rng.uniform(-11, -5)) * po.seq_norm(b)
+        rec = int(rng.choice([-1, 0, 1, 2, 5]))
+        ref = po.ref_cg(A, b, x0, tol=tol, max_iters=mi, recompute=rec, algo=what)
+        fn = m.cg_solve if what == "cg" else m.steepest_descent_solve
+        try:
+            t = fn(A, b, x0, m.SolveOptions(tol=tol, max_iters=mi, recompute_residual_every=rec))
+        except m.Error as ex:
+            return None if ref.rc != 0 else f"{what} n={n} seed={seed}: device raised {ex!r}"
+        if ref.rc != 0:
+            return f"{what} n={n} seed={seed}: reference raised {ref.error!r}, device did not"
+        ok = (str(t.status) == ref.status and t.iteration_count() == ref.iterations and
+              np.array_equal(t.residual_norms, ref.residual_norms) and np.array_equal(t.final_x, ref.final_x) and
+              np.array_equal(t.final_residual_norms, ref.final_residual_norms))
+        return None if ok else f"{what} n={n} seed={seed} mi={mi} rec={rec}: differs from the reference"
+    p = int(rng.choice([1, 2, 3, 4, 7, 8, 9, 16, 17, 31, 32]))
+    n = max(p + 1, int(rng.choice(EDGES)) + int(rng.integers(-1, 2)) if rng.random() < 0.5 else int(rng.integers(p + 1, 3000)))
+    arith = str(rng.choice(["exact", "fast"]))
+    shards = int(rng.choice([1, 1, 2, 3])) if n >= 200 else 1
+    with m.GpuContext(n, p, arith=arith, devices=[0] * shards if shards > 1 else None) as ctx:
+        if what == "gen":
+            if rng.random() < 0.5:
+                ctx.gen_A("diagdom", seed)
+                want = po.gen_diagdom(n, seed)
+            else:
+                mr, kap = int(rng.integers(1, 9)), float(10 ** rng.uniform(0.3, 6))
+                ctx.gen_A("householder", seed, mr, kap)
+                want = po.gen_householder(n, mr, kap, seed)
+            return None if np.array_equal(ctx.get_A(), want) else f"gen n={n} p={p} {arith} shards={shards} seed={seed}"
+        if what == "matvec":
+            A = po.gen_diagdom(n, seed)
+            ctx.set_A(A)
+            D = np.random.default_rng(seed).uniform(-1, 1, (n, p))
+            Q = ctx.matvec_block(D)
+            ref = np.zeros((p, n))
+            Dc = np.ascontiguousarray(D.T)
+            po.oracle_lib().orc_matvec_block(A.ctypes.data, n, Dc.ctypes.data, p, ref.ctypes.data)
+            if arith == "exact":
+                return None if np.array_equal(Q, ref.T) else f"matvec n={n} p={p} shards={shards} seed={seed}"
+            err = np.max(np.abs(Q - ref.T) / (np.abs(A) @ np.abs(D)))
+            return None if err < 1e-14 else f"fast matvec n={n} p={p} shards={shards} seed={seed}: {err:.1e}"
+        # numerical_rank: full rank, a duplicated / scaled column, a zero column, badly scaled columns
+        if shards > 1:
+            return None
+        g = np.random.default_rng(seed)
+        D = g.standard_normal((n, p)) * 10.0 ** g.integers(-6, 7, size=p)
+        kind = int(g.integers(0, 4))
+        if p > 1 and kind == 1:
+            D[:, -1] = 2.0 * D[:, 0]
+        elif kind == 2:
+            D[:, int(g.integers(0, p))] = 0.0
+        elif p > 2 and kind == 3:
+            D[:, 1] = D[:, 0] + 1e-9 * D[:, 2]
+        want, _ = po.numerical_rank(D, 1e-10, lib="ref")
+        for force in (False, True):
+            got = ctx.numerical_rank(D, 1e-10, force_exact=force)
+            if got != want:
+                return f"rank n={n} p={p} {arith} kind={kind} force={force} seed={seed}: {got} vs {want}"
+    return None
+
+
 def run_session_fast(m, po, rng):
     """Fast mode: 3-5 solves on one resident context (ccg / mccg, changing options) must
     each equal, bit for bit, the same solve on a fresh context -- nothing may carry over."""
@@ -243,6 +317,8 @@ def main():
     ap.add_argument("--max-cost", type=float, default=3e9)
     ap.add_argument("--multi", action="store_true", help="row-sharded cases only (2-4 shards), mostly Householder")
     ap.add_argument("--large", action="store_true", help="n around 9472..12290 (the large-n A.D variants), 1-3 iterations")
+    ap.add_argument("--misc", action="store_true",
+                    help="scalar solvers, device generators, matvec_block, numerical_rank on random shapes")
     ap.add_argument("--session", nargs="?", const="exact", default="", choices=["exact", "fast"],
                     help="several solves with changing options on ONE resident context (state carried between "
                          "solves): exact against the reference, fast against the same solve on a fresh context")
@@ -256,6 +332,17 @@ def main():
     failures = []
     idx = 0
     while time.time() - t0 < args.seconds:
+        if args.misc:
+            idx += 1
+            try:
+                why = run_misc(m, po, rng)
+            except Exception as ex:
+                why = f"exception {type(ex).__name__}: {ex}"
+            done["exact"] += 1
+            if why:
+                failures.append({"index": idx, "arith": "misc", "why": why})
+                print(f"FAIL misc #{idx}: {why}", flush=True)
+            continue
         if args.session:
             idx += 1
             why = run_session_fast(m, po, rng) if args.session == "fast" else run_session(m, po, rng)
