@@ -72,7 +72,7 @@ def draw_case(rng, multi=False, large=False):
 
 
 def cost(c):
-    its = c["max_iters"] if c["max_iters"] >= 0 else min(2 * c["n"], 400)
+    its = c["max_iters"] if c["max_iters"] >= 0 else 2 * c["n"]  # worst case: the run reaches max_iters = 2n
     return float(c["n"]) ** 2 * c["p"] * max(its, 1)
 
 
