@@ -133,6 +133,37 @@ def test_sharded_fast_within_tolerance(po):
         e.close()
 
 
+@pytest.mark.parametrize("n,world", [(257, 2), (385, 2), (386, 3)])
+def test_sharded_fast_long_run_on_unequal_shards(po, n, world):
+    """The phase API on UNEQUAL row shards (129 + 128 rows, 193 + 192, 129 + 129 +
+    128: the old row-pass grids differed between the ranks) for a long fast-mode
+    solve: every rank must hold the same replicated X, R, D bit for bit at the end
+    -- the Gram row pass groups its partial sums by n, not by the shard's own row
+    count (tests/test_gpu_multi.py, profiles/r02_fuzz_parity.txt)."""
+    import paper_1204_0069_b200 as m
+    p, seed = 4, 1600630417
+    A = po.gen_householder(n, 3, 3.3e3, seed)
+    b = po.gen_rhs(n, "normal", seed)
+    X0 = po.gen_starts(n, p, seed)
+    opts = m.SolveOptions(tol=2.4e-10 * po.seq_norm(b))
+    engines = [GpuShardEngine(n, p, r, world, 0, "fast") for r in range(world)]
+    assert len({e.row1 - e.row0 for e in engines}) > 1  # unequal shards
+    for e in engines:
+        e.ctx.set_A(A[e.row0:e.row1])
+        e.ctx.upload(b, X0)
+    traces = lockstep_solve(engines, opts)
+    ref = po.oracle_ccg(A, b, X0, tol=opts.tol)
+    assert ref.status == "converged" and ref.iterations > 60
+    for t in traces:
+        assert str(t.status) == "converged" and abs(t.iteration_count() - ref.iterations) <= max(4, ref.iterations // 20)
+        assert np.array_equal(t.final_x, traces[0].final_x)          # ranks agree bit for bit
+        assert np.array_equal(t.residual_norms, traces[0].residual_norms)
+    rel = np.linalg.norm(traces[0].final_x - ref.final_x, axis=0) / np.linalg.norm(ref.final_x, axis=0)
+    assert rel.max() < 10 * 3.3e3 * 2.4e-10
+    for e in engines:
+        e.close()
+
+
 @pytest.mark.parametrize("name,world", [("mccg_n50_p8", 2), ("mccg_exhaustion_cliff", 3),
                                         ("mccg_duplicate_columns", 2)])
 def test_sharded_mccg_matches_reference(name, world):
