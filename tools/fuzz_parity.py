@@ -29,6 +29,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 os.environ.setdefault("OMP_WAIT_POLICY", "passive")
 
+RANK_SHARE = 0.0  # --rank-share: fraction of the exact sessions run on a rank context (NCCL path)
 EDGES = [31, 32, 33, 63, 64, 65, 127, 128, 129, 255, 256, 257, 287, 288, 289, 511, 512, 513, 1023, 1024, 1025]
 
 
@@ -263,8 +264,10 @@ def run_session(m, po, rng):
     else:
         A = po.gen_householder(n, int(rng.integers(1, 6)), float(10 ** rng.uniform(0.5, 3.5)), seed)
     shards = int(rng.choice([1, 1, 1, 2])) if n >= 200 else 1
+    rank_ctx = shards == 1 and rng.random() < RANK_SHARE  # a rank context (NCCL exchanges, world of one)
     log = []
-    with m.GpuContext(n, p, devices=[0] * shards if shards > 1 else None) as ctx:
+    kw = dict(nccl=(1, 0, m.nccl_unique_id())) if rank_ctx else dict(devices=[0] * shards if shards > 1 else None)
+    with m.GpuContext(n, p, **kw) as ctx:
         ctx.set_A(A)
         for step in range(int(rng.integers(3, 7))):
             s2 = int(rng.integers(1, 2**31))
@@ -277,10 +280,11 @@ def run_session(m, po, rng):
             tol = 0.0 if fixed else float(10 ** rng.uniform(-11, -6)) * po.seq_norm(b)
             rec = int(rng.choice([-1, 0, 1, 3, 7]))
             algo = "mccg" if rng.random() < 0.3 else "ccg"
-            verify = shards == 1 and algo == "ccg" and rng.random() < 0.3 and (max_iters >= 0 or n <= 200)
+            verify = (shards == 1 and not rank_ctx and algo == "ccg" and rng.random() < 0.3 and
+                      (max_iters >= 0 or n <= 200))
             xs = np.linalg.solve(A, b) if verify else None
-            log.append(dict(step=step, n=n, p=p, shards=shards, seed=s2, max_iters=max_iters, tol=tol, rec=rec,
-                            algo=algo, verify=bool(verify)))
+            log.append(dict(step=step, n=n, p=p, shards=shards, rank_ctx=bool(rank_ctx), seed=s2, max_iters=max_iters,
+                            tol=tol, rec=rec, algo=algo, verify=bool(verify)))
             ref = po.ref_solve(A, b, X0, tol=tol, max_iters=max_iters, recompute=rec, algo=algo)
             opts = m.SolveOptions(tol=tol, max_iters=max_iters, recompute_residual_every=rec, algo=algo,
                                   keep_history=bool(verify), x_star=xs)
@@ -317,6 +321,8 @@ def main():
     ap.add_argument("--max-cost", type=float, default=3e9)
     ap.add_argument("--multi", action="store_true", help="row-sharded cases only (2-4 shards), mostly Householder")
     ap.add_argument("--large", action="store_true", help="n around 9472..12290 (the large-n A.D variants), 1-3 iterations")
+    ap.add_argument("--rank-share", type=float, default=0.0,
+                    help="--session: share of the sessions on a coopcg_gpu_create_rank context (world of one)")
     ap.add_argument("--misc", action="store_true",
                     help="scalar solvers, device generators, matvec_block, numerical_rank on random shapes")
     ap.add_argument("--session", nargs="?", const="exact", default="", choices=["exact", "fast"],
@@ -326,6 +332,8 @@ def main():
     args = ap.parse_args()
     import paper_1204_0069_b200 as m
     import pyoracle as po
+    global RANK_SHARE
+    RANK_SHARE = args.rank_share
     rng = np.random.default_rng(args.seed)
     t0 = time.time()
     done = {"exact": 0, "fast": 0}
