@@ -41,8 +41,6 @@ def test_random_cases_match_the_reference(m, po, fz, seed, multi, cases):
             continue
         ran += 1
         for arith in ("exact", "fast"):
-            if arith == "fast" and c["algo"] == "mccg" and c["shards"] > 1:
-                continue
             why = fz.run_case(m, po, c, arith)
             assert why is None, (arith, c, why)
 

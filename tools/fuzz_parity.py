@@ -65,7 +65,7 @@ def draw_case(rng, multi=False, large=False):
         n = max(n, 200)
         shards = int(rng.choice([2, 3, 4]))
         matrix = "householder" if rng.random() < 0.8 else "diagdom"
-        algo = "ccg"
+        algo = "mccg" if rng.random() < 0.25 else "ccg"
     degenerate = bool(rng.random() < 0.06) and p > 1
     return dict(n=n, p=p, matrix=matrix, kappa=kappa, m=m, max_iters=max_iters, tol_rel=tol_rel,
                 recompute=recompute, algo=algo, shards=shards, degenerate=degenerate,
@@ -364,8 +364,6 @@ def main():
         if cost(c) > args.max_cost:
             continue
         for arith in ("exact", "fast"):
-            if arith == "fast" and c["algo"] == "mccg" and c["shards"] > 1:
-                continue
             try:
                 why = run_case(m, po, c, arith)
             except Exception as ex:  # a crash is a failure of the case, not of the sweep
