@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define COOPCG_GPU_ABI_VERSION 1
+#define COOPCG_GPU_ABI_VERSION 2 /* 2: verification mode (set_verification, get_history, get_anorm_errors) */
 #define COOPCG_GPU_MAX_P 32
 
 /* Error codes; map to the reference exception hierarchy (errors.hpp:11-41). */

@@ -1090,7 +1090,7 @@ static int rank_gen_householder(coopcg_gpu_ctx* ctx, uint64_t seed, int m, doubl
 // =============================================================================
 extern "C" {
 
-const char* coopcg_gpu_version(void) { return "coopcg_gpu 1 sm_100a exact+fast"; }
+const char* coopcg_gpu_version(void) { return "coopcg_gpu 2 sm_100a exact+fast"; }
 
 int coopcg_gpu_last_error(const coopcg_gpu_ctx* ctx, char* buf, size_t len) {
     if (!buf || len == 0) return COOPCG_E_INVALID;
